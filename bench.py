@@ -1,0 +1,429 @@
+#!/usr/bin/env python
+"""Benchmark of the 3D-FSR reconstruction hot path on B200.
+
+Headline workload (BASELINE.json configs[1]): closed-form Tikhonov SR, fp64,
+HR 256^3 ellipsoid+texture phantom, Gaussian PSF sigma 1.5 / 13^3, decimation
+2x2x2 -> LR 128^3, 30 dB BSNR, tau (TikhonovConfig::lambda) = 1e-3.
+One step = one TikhonovOperator::solve (reference src/solvers.cpp:48-67).
+
+  value : HR voxels/s, inputs resident in HBM (device-pointer C ABI).
+  e2e   : same metric through the public host-buffer C ABI
+          (vsr_tikhonov_solve: pinned y H2D + solve + x D2H + checks).
+  tv    : ADMM-TV iteration throughput on configs[2] (256^3, d = 64), extra.
+
+Run: python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+For N > 1 (torchrun) every rank solves its own config-1 volume (replicas,
+weak scaling); the slab-sharded path is not part of this line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "HR voxels/s per ADMM-TV iteration and per Tikhonov solve; % of HBM roofline"
+UNIT = "HR voxels/s"
+
+
+def load_peaks():
+    try:
+        return json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except Exception:
+        return {}
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, phys_index: int):
+        self.idx = phys_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "100",
+                 "-i", str(self.idx)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sms, maxs, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sms.append(float(f[1]))
+                maxs.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sms)) if sms else None,
+                "sm_max_mhz": max(maxs) if maxs else None,
+                "reasons": sorted(reasons), "samples": len(sms)}
+
+
+def phys_gpu_index(local: int) -> int:
+    vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+    if vis:
+        try:
+            return int(vis.split(",")[local])
+        except Exception:
+            return local
+    return local
+
+
+# ---------------------------------------------------------------- CPU baseline
+def cpu_baseline(cfg, inp, budget_s: float = 25.0):
+    """Reference CPU path on a bounded sample of the same workload: the
+    reference compiled from its sources (oracle/_ref, FFTW-API shim) when
+    built, else the numpy oracle port.  Single thread (the reference is
+    single-threaded: FFTW without threads, no OpenMP)."""
+    sys.path.insert(0, str(ROOT / "oracle"))
+    ref = None
+    try:
+        import ref_binding  # noqa
+        if ref_binding.available():
+            ref = ref_binding
+    except Exception:
+        ref = None
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    N = cfg.voxels
+    if ref is not None:
+        op = ref.TikhonovOperator(inp.psf, cfg.hr, cfg.rates, cfg.reg, inp.xbar)
+        times = []
+        t_start = time.perf_counter()
+        while not times or (time.perf_counter() - t_start < budget_s and len(times) < 3):
+            t0 = time.perf_counter()
+            op.solve(inp.y)
+            times.append(time.perf_counter() - t0)
+        kind, sample = "reference", (f"reference volsr TikhonovOperator::solve (oracle/_ref, FFTW3-API shim), "
+                                     f"config1 256^3, {len(times)} solves, best")
+    else:
+        import volsr_oracle as O
+        spec = O.DecimationSpec(cfg.hr, cfg.rates)
+        op = O.TikhonovOperator(O.psf_to_spectrum(inp.psf), spec, cfg.reg, inp.xbar)
+        times = []
+        t_start = time.perf_counter()
+        while not times or (time.perf_counter() - t_start < budget_s and len(times) < 3):
+            t0 = time.perf_counter()
+            op.solve(inp.y)
+            times.append(time.perf_counter() - t0)
+        kind, sample = "port", (f"numpy oracle TikhonovOperator.solve, config1 256^3, {len(times)} solves, best")
+    best = min(times)
+    return {"value": N / best, "unit": UNIT, "cores": 1, "kind": kind, "sample": sample,
+            "seconds_per_solve": best}
+
+
+# ---------------------------------------------------------------- reference arm
+def run_reference(args, rank, world):
+    if rank != 0:
+        return 0
+    from paper_2010_15491_b200 import synth
+    cfg = synth.CONFIGS[1]
+    inp = synth.make_inputs(cfg, with_truth=False)
+    sys.path.insert(0, str(ROOT / "oracle"))
+    ref = None
+    try:
+        import ref_binding
+        if ref_binding.available():
+            ref = ref_binding
+    except Exception:
+        ref = None
+    if ref is not None:
+        op = ref.TikhonovOperator(inp.psf, cfg.hr, cfg.rates, cfg.reg, inp.xbar)
+        kind = "reference"
+        sample = "reference volsr TikhonovOperator::solve (oracle/_ref, FFTW3-API shim), config1, 1 thread"
+    else:
+        import volsr_oracle as O
+        spec = O.DecimationSpec(cfg.hr, cfg.rates)
+        op = O.TikhonovOperator(O.psf_to_spectrum(inp.psf), spec, cfg.reg, inp.xbar)
+        kind = "port"
+        sample = "numpy oracle TikhonovOperator.solve, config1, 1 thread"
+    for _ in range(args.warmup):
+        op.solve(inp.y)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        op.solve(inp.y)
+    dt = (time.perf_counter() - t0) / args.steps
+    val = cfg.voxels / dt
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded ellipsoid+texture phantom, BSNR 30 dB)",
+            "config": config_block(cfg),
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": kind, "sample": sample},
+            "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def config_block(cfg):
+    return {"workload": f"config{cfg.idx}: closed-form Tikhonov SR fp64, HR {cfg.hr[0]}x{cfg.hr[1]}x{cfg.hr[2]}"
+                        f" -> LR {cfg.lr[0]}x{cfg.lr[1]}x{cfg.lr[2]} (d={cfg.d}), PSF sigma {cfg.psf_sigma[0]}"
+                        f" {cfg.psf_size[0]}^3, BSNR {cfg.bsnr:g} dB, tau={cfg.reg:g}",
+            "hr": list(cfg.hr), "rates": list(cfg.rates), "step": "TikhonovOperator::solve",
+            "l2": "inputs larger than L2 (Lambda + fft3(xbar) + x_hat = 805 MB per solve)"}
+
+
+# ---------------------------------------------------------------- B200 arm
+STAGE_BYTES = {
+    # algorithmic bytes per launch as multiples of (N, Nl): read + write of the stage
+    "fft_inv_axis3": (32, 0), "fft_inv_axis2": (32, 0), "fft_inv_axis1_c2r": (24, 0),
+    "fft_fwd_axis1_r2c": (24, 0), "fft_fwd_axis2": (32, 0), "fft_fwd_axis3": (32, 0),
+    "tik_fold": (48, 16), "tv_fold": (48, 16), "tv_stencil": (64, 0),
+}
+
+
+def run_b200(args, rank, world, local):
+    import torch
+    from paper_2010_15491_b200 import synth
+    from paper_2010_15491_b200 import volsr as V
+
+    dist = world > 1
+    if dist:
+        import torch.distributed as tdist
+    torch.cuda.set_device(local)
+    cfg = synth.CONFIGS[1]
+    inp = synth.make_inputs(cfg, with_truth=False)
+    N, Nl = cfg.voxels, cfg.voxels // cfg.d
+    ctx = V.Context(local)
+    spec = V.DecimationSpec(cfg.hr, cfg.rates)
+    lam = V.psf_to_spectrum(inp.psf, ctx)
+    lam_d = V.DeviceBuffer(ctx, lam.nbytes)
+    lam_d.upload(lam)
+    xbar_d = V.DeviceBuffer(ctx, inp.xbar.nbytes)
+    xbar_d.upload(inp.xbar)
+    y_d = V.DeviceBuffer(ctx, inp.y.nbytes)
+    y_d.upload(inp.y)
+    x_d = V.DeviceBuffer(ctx, N * 8)
+    op = V.TikhonovDevice(ctx, spec, lam_d, cfg.reg, xbar_d)
+    stream = torch.cuda.ExternalStream(ctx.stream(), device=local)
+
+    def barrier():
+        if dist:
+            tdist.barrier()
+
+    for _ in range(max(args.warmup, 3)):
+        op.solve_d(y_d, x_d)
+    op.check()
+
+    clocks = ClockSampler(phys_gpu_index(local))
+    clocks.start()
+    # keep the GPU under load long enough for the sampler (untimed)
+    t_burn = time.perf_counter()
+    while time.perf_counter() - t_burn < 1.5:
+        for _ in range(20):
+            op.solve_d(y_d, x_d)
+        ctx.synchronize()
+
+    # ---- timed region (device-resident)
+    barrier()
+    torch.cuda.synchronize()
+    ctx.synchronize()
+    V.profile_enable(ctx, True)
+    l0 = V.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        op.solve_d(y_d, x_d)
+    e1.record(stream)
+    e1.synchronize()
+    launches = V.launch_count() - l0
+    stages = V.profile_read(ctx)
+    V.profile_enable(ctx, False)
+    op.check()
+    ctx.synchronize()
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1) / args.steps
+    if dist:
+        t = torch.tensor([ms], device=f"cuda:{local}", dtype=torch.float64)
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = N * world / (ms * 1e-3)
+
+    # ---- end to end through the host-buffer C ABI (pinned buffers)
+    yp = V.PinnedBuffer(inp.y.shape)
+    yp.array[...] = inp.y
+    xp = V.PinnedBuffer(V.shape_of(cfg.hr))
+    for _ in range(2):
+        op.solve_host(yp.array, xp.array)
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        op.solve_host(yp.array, xp.array)
+    e2e_s = (time.perf_counter() - t0) / args.steps
+    if dist:
+        t = torch.tensor([e2e_s], device=f"cuda:{local}", dtype=torch.float64)
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e = {"value": N * world / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(inp.y.nbytes),
+           "d2h_bytes_per_step": int(N * 8), "ms_per_step": e2e_s * 1e3,
+           "api": "vsr_tikhonov_solve (pinned host y, x)"}
+
+    # ---- roofline from the live per-stage events
+    peaks = load_peaks()
+    hbm = peaks.get("hbm_gbs")
+    peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)"
+    if not hbm:
+        hbm, peak_src = 6650.0, "fallback (B200_PROFILING.md)"
+    st_rows = {}
+    for name, (tot_ms, cnt) in stages.items():
+        avg = tot_ms / max(cnt, 1)
+        row = {"avg_us": avg * 1e3, "launches": cnt, "share": tot_ms / (ms * args.steps)}
+        if name in STAGE_BYTES:
+            a, b = STAGE_BYTES[name]
+            byts = a * N + b * Nl
+            row["alg_bytes"] = byts
+            row["gbs"] = byts / (avg * 1e-3) / 1e9
+            row["frac"] = row["gbs"] / hbm
+        st_rows[name] = row
+    timed = {k: v for k, v in st_rows.items() if "alg_bytes" in v}
+    dom = max(timed, key=lambda k: timed[k]["avg_us"] * timed[k]["launches"])
+    d = timed[dom]
+    path_bytes = V.tikhonov_algorithmic_bytes(cfg.hr, cfg.rates)
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": d["gbs"], "peak": hbm, "unit": "GB/s",
+                "frac": d["frac"], "traffic": None, "peak_source": peak_src,
+                "alg_bytes_per_launch": d["alg_bytes"],
+                "path": {"alg_bytes_per_step": path_bytes, "achieved": path_bytes / (ms * 1e-3) / 1e9,
+                         "frac": path_bytes / (ms * 1e-3) / 1e9 / hbm,
+                         "model": "(72 + 40/d) N bytes per Tikhonov solve (SURVEY 8(d))"}}
+    try:
+        prof = json.loads((ROOT / "profiles" / "traffic.json").read_text())
+        if dom in prof:
+            roofline["traffic"] = prof[dom]
+    except Exception:
+        pass
+
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded ellipsoid+texture phantom, BSNR 30 dB; paper volumes proprietary)",
+            "config": config_block(cfg), "roofline": roofline, "e2e": e2e, "gpu_launches": int(launches),
+            "clocks": clk, "stages": st_rows}
+
+    if not args.no_tv:
+        line["tv"] = bench_tv(args, ctx, V, synth, torch, stream, local, hbm)
+    if rank == 0 and world == 1 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline(cfg, inp)
+    op.close()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    return 0
+
+
+def bench_tv(args, ctx, V, synth, torch, stream, local, hbm):
+    """ADMM-TV iteration throughput on configs[2] (256^3, d = 64)."""
+    cfg = synth.CONFIGS[2]
+    inp = synth.make_inputs(cfg, with_truth=False)
+    N = cfg.voxels
+    spec = V.DecimationSpec(cfg.hr, cfg.rates)
+    y_d = V.DeviceBuffer(ctx, inp.y.nbytes)
+    y_d.upload(inp.y)
+    p_d = V.DeviceBuffer(ctx, inp.psf.nbytes)
+    p_d.upload(inp.psf)
+    x0_d = V.DeviceBuffer(ctx, inp.x0.nbytes)
+    x0_d.upload(inp.x0)
+    iters = max(args.steps, 10) + max(args.warmup, 3)
+    tcfg = V.TvAdmmConfig(lambda_=cfg.tv_lambda, mu=cfg.tv_mu, max_iters=iters, rel_tol=0.0,
+                          tau=1e-3 * cfg.tv_mu, init=V.INIT_PROVIDED)
+    tv = V.TvDevice(ctx, spec, y_d, p_d, tcfg, x0_d)
+    tv.iterate(max(args.warmup, 3))
+    ctx.synchronize()
+    V.profile_enable(ctx, True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    k = iters - max(args.warmup, 3)
+    e0.record(stream)
+    tv.iterate(k)
+    e1.record(stream)
+    e1.synchronize()
+    stages = V.profile_read(ctx)
+    V.profile_enable(ctx, False)
+    rep = tv.report()
+    tv.close()
+    ms = e0.elapsed_time(e1) / k
+    path = V.tv_algorithmic_bytes(cfg.hr, cfg.rates)
+    rows = {}
+    for name, (tot, cnt) in stages.items():
+        avg = tot / max(cnt, 1)
+        r = {"avg_us": avg * 1e3, "launches": cnt, "share": tot / (ms * k)}
+        if name in STAGE_BYTES:
+            a, b = STAGE_BYTES[name]
+            byts = a * N + b * (N // cfg.d)
+            r["gbs"] = byts / (avg * 1e-3) / 1e9
+            r["frac"] = r["gbs"] / hbm
+        rows[name] = r
+    return {"workload": "config2: ADMM-TV fp64 256^3 -> 64^3 (d=64), lambda 2e-3, mu 0.05, tau 1e-3*mu",
+            "value": N / (ms * 1e-3), "unit": "HR voxels/s per ADMM-TV iteration", "ms_per_iter": ms,
+            "iters_timed": k, "path_frac": path / (ms * 1e-3) / 1e9 / hbm,
+            "path_model": "(160 + 16/d) N bytes per iteration", "objective_last": rep.objective[-1],
+            "stages": rows}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-tv", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    if world > 1:
+        import torch
+        import torch.distributed as tdist
+        torch.cuda.set_device(local)
+        tdist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    try:
+        return run_b200(args, rank, world, local)
+    finally:
+        if world > 1:
+            import torch.distributed as tdist
+            tdist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    sys.exit(main())

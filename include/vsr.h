@@ -1,0 +1,200 @@
+/* vsr.h — C ABI of the B200-native volsr reconstruction hot path.
+ *
+ * Drop-in boundary for the reference's solver path (arxiv 2010.15491, `volsr`
+ * C++ library under /root/reference/proj).  Every entry point below names the
+ * reference interface it replaces (file:line).  The C++ mirror of the
+ * reference API (include/volsr_b200/volsr.hpp) and the Python mirror
+ * (paper_2010_15491_b200/volsr.py) are thin layers over these calls.
+ *
+ * Conventions
+ *   - dims[3] = {m, n, s}: axis 1 (m) fastest, flat index i + m*j + m*n*k
+ *     (reference include/volsr/volume.hpp:26-45).
+ *   - rates[3] = {dr, dc, ds} (reference include/volsr/operators.hpp:12-27).
+ *   - Real volumes: double[count]; complex volumes: interleaved (re, im)
+ *     double[2*count] (std::complex<double> layout).
+ *   - Functions without a `_d` suffix take HOST pointers (pageable or pinned);
+ *     `_d` variants take DEVICE pointers on the context's device and are
+ *     ordered on the context's stream.
+ *   - No exception crosses this boundary: every function returns a status code
+ *     and vsr_last_error_message() holds the thread's last message.  The C++
+ *     mirror rethrows the reference's exception types by code.
+ */
+#ifndef VSR_H
+#define VSR_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (reference error taxonomy, include/volsr/volume.hpp:12-24) */
+#define VSR_OK 0
+#define VSR_ERR_SHAPE 1        /* volsr::shape_error (std::invalid_argument) */
+#define VSR_ERR_INVALID 2      /* std::invalid_argument (lambda <= 0, mu <= 0, ...) */
+#define VSR_ERR_NUMERIC 3      /* volsr::numeric_error */
+#define VSR_ERR_OUT_OF_RANGE 4 /* std::out_of_range */
+#define VSR_ERR_CUDA 5         /* device / runtime failure (no reference analogue) */
+#define VSR_ERR_INTERNAL 6
+
+typedef struct vsr_ctx vsr_ctx;
+typedef struct vsr_tikhonov vsr_tikhonov;
+typedef struct vsr_folded vsr_folded;
+typedef struct vsr_tv vsr_tv;
+
+const char* vsr_last_error_message(void);
+int vsr_version(void);
+
+/* ---- context: one device, one stream, cached FFT twiddles and scratch */
+int vsr_ctx_create(int device, vsr_ctx** out);
+int vsr_ctx_destroy(vsr_ctx* ctx);
+int vsr_ctx_synchronize(vsr_ctx* ctx);
+void* vsr_ctx_stream(vsr_ctx* ctx); /* cudaStream_t */
+int vsr_ctx_device(vsr_ctx* ctx);
+
+/* pinned host / device memory helpers (for end-to-end staging) */
+int vsr_host_alloc(size_t bytes, void** out);
+int vsr_host_free(void* p);
+int vsr_device_alloc(vsr_ctx* ctx, size_t bytes, void** out);
+int vsr_device_free(vsr_ctx* ctx, void* p);
+int vsr_memcpy_h2d(vsr_ctx* ctx, void* dst_dev, const void* src_host, size_t bytes);
+int vsr_memcpy_d2h(vsr_ctx* ctx, void* dst_host, const void* src_dev, size_t bytes);
+
+/* ---- FFT contract: replaces volsr::fft3 / ifft3 / ifft3_real /
+ *      dft3_unnormalized / fft_counters (include/volsr/fft.hpp:12-31,
+ *      src/fft.cpp:50-111).  Unitary 1/sqrt(N), sign -1 forward. */
+int vsr_fft3(vsr_ctx* ctx, const size_t dims[3], const double* in_c, double* out_c);
+int vsr_fft3_real(vsr_ctx* ctx, const size_t dims[3], const double* in_r, double* out_c);
+int vsr_ifft3(vsr_ctx* ctx, const size_t dims[3], const double* in_c, double* out_c);
+int vsr_ifft3_real(vsr_ctx* ctx, const size_t dims[3], const double* in_c, double* out_r,
+                   double max_rel_imag);
+int vsr_dft3_unnormalized(vsr_ctx* ctx, const size_t dims[3], const double* in_r, double* out_c);
+int vsr_fft_counters(uint64_t* forward, uint64_t* inverse);
+int vsr_reset_fft_counters(void);
+
+/* ---- forward-model operators (include/volsr/operators.hpp:53-87) */
+/* psf_to_spectrum == dft3_unnormalized of the padded PSF (src/operators.cpp:121-123) */
+int vsr_psf_to_spectrum(vsr_ctx* ctx, const size_t dims[3], const double* psf_r, double* lambda_c);
+int vsr_decimate(vsr_ctx* ctx, const size_t hr_dims[3], const size_t rates[3], const double* x,
+                 double* y);                                      /* operators.cpp:133-142 */
+int vsr_decimate_adjoint(vsr_ctx* ctx, const size_t hr_dims[3], const size_t rates[3],
+                         const double* y, double* x);             /* operators.cpp:144-153 */
+int vsr_diff_forward(vsr_ctx* ctx, const size_t dims[3], int axis, const double* x,
+                     double* out);                                /* operators.cpp:191-206 */
+int vsr_diff_adjoint(vsr_ctx* ctx, const size_t dims[3], int axis, const double* x,
+                     double* out);                                /* operators.cpp:208-223 */
+int vsr_blur_apply(vsr_ctx* ctx, const size_t dims[3], const double* x, const double* lambda_c,
+                   int conjugate, double* out);                  /* operators.cpp:125-131 */
+
+/* ---- spectral fold: replaces volsr::FoldedSpectrum / alias_fold / alias_expand /
+ *      gram_diag(_weighted) (include/volsr/spectral.hpp:12-68, src/spectral.cpp:7-142) */
+int vsr_alias_fold(vsr_ctx* ctx, const size_t hr_dims[3], const size_t rates[3],
+                   const double* hr_c, double* lr_c);
+int vsr_alias_expand(vsr_ctx* ctx, const size_t hr_dims[3], const size_t rates[3],
+                     const double* lr_c, double* hr_c);
+int vsr_folded_create(vsr_ctx* ctx, const size_t hr_dims[3], const size_t rates[3],
+                      const double* lambda_c, vsr_folded** out);
+int vsr_folded_destroy(vsr_folded* f);
+int vsr_folded_block_value(vsr_folded* f, size_t br, size_t bc, size_t bs, size_t g,
+                           double out_c[2]);
+int vsr_folded_apply(vsr_folded* f, const double* hr_c, double* lr_c);
+int vsr_folded_apply_adjoint(vsr_folded* f, const double* lr_c, double* hr_c);
+int vsr_folded_apply_weighted(vsr_folded* f, const double* hr_c, const double* hr_w, double* lr_c);
+int vsr_folded_apply_adjoint_weighted(vsr_folded* f, const double* lr_c, const double* hr_w,
+                                      double* hr_c);
+int vsr_folded_gram_diag(vsr_folded* f, double* lr_r);
+int vsr_folded_gram_diag_weighted(vsr_folded* f, const double* hr_w, double* lr_r);
+int vsr_folded_swap_blocks_for_fault_injection(vsr_folded* f);
+
+/* ---- Tikhonov: replaces volsr::TikhonovOperator / tikhonov_fast
+ *      (include/volsr/solvers.hpp:27-47, src/solvers.cpp:36-72).
+ *      ctor: lambda_c = SpectrumDiag (complex HR), reg = TikhonovConfig::lambda,
+ *      xbar = TikhonovConfig::xbar (real HR). */
+int vsr_tikhonov_create(vsr_ctx* ctx, const size_t hr_dims[3], const size_t rates[3],
+                        const double* lambda_c, double reg, const double* xbar_r,
+                        vsr_tikhonov** out);
+int vsr_tikhonov_create_d(vsr_ctx* ctx, const size_t hr_dims[3], const size_t rates[3],
+                          const double* lambda_c_dev, double reg, const double* xbar_r_dev,
+                          vsr_tikhonov** out);
+int vsr_tikhonov_destroy(vsr_tikhonov* t);
+/* solve(): y = LR real (host) -> x = HR real (host).  Exactly one forward and
+ * one inverse 3D transform are counted (test_solvers.cpp:141-157). */
+int vsr_tikhonov_solve(vsr_tikhonov* t, const double* y_r, double* x_r);
+/* device-resident: enqueue on the context stream; errors are sticky and
+ * reported by the next vsr_tikhonov_check (which synchronizes). */
+int vsr_tikhonov_solve_d(vsr_tikhonov* t, const double* y_r_dev, double* x_r_dev);
+int vsr_tikhonov_check(vsr_tikhonov* t);
+int vsr_tikhonov_fast(vsr_ctx* ctx, const size_t hr_dims[3], const size_t rates[3],
+                      const double* y_r, const double* lambda_c, double reg, const double* xbar_r,
+                      double* x_r);
+/* bytes the Tikhonov solve moves per call under the compulsory-traffic model
+ * (SURVEY §8(d)): (72 + 40/d) * N. */
+double vsr_tikhonov_algorithmic_bytes(const size_t hr_dims[3], const size_t rates[3]);
+
+/* ---- TV pieces: replace make_gamma (solvers.hpp:117, solvers.cpp:191-205),
+ *      tv_x_update (:89-91, :245-259), tv_shrink (:100-101, :286-301),
+ *      objective_tv (:111-112, :303-319). */
+int vsr_make_gamma(vsr_ctx* ctx, const size_t hr_dims[3], double tau, double* gamma_r);
+int vsr_tv_x_update(vsr_ctx* ctx, const size_t hr_dims[3], const size_t rates[3],
+                    const double* y_r, const double* lambda_c, double mu,
+                    const double* theta_hat_c, const double* gamma_r, double* x_r);
+int vsr_tv_shrink(vsr_ctx* ctx, size_t count, const double* nu1, const double* nu2,
+                  const double* nu3, double threshold, double* out1, double* out2, double* out3);
+int vsr_objective_tv(vsr_ctx* ctx, const size_t hr_dims[3], const size_t rates[3],
+                     const double* x_r, const double* y_r, const double* lambda_c,
+                     double tv_weight, double* out);
+
+/* ---- ADMM-TV: replaces volsr::admm_tv with TvAdmmConfig / SolveReport
+ *      (include/volsr/solvers.hpp:15-21,72-83,106-107; src/solvers.cpp:321-411). */
+#define VSR_INIT_ZERO 0
+#define VSR_INIT_UPSAMPLED 1
+#define VSR_INIT_PROVIDED 2
+typedef struct vsr_tv_config {
+    double lambda;       /* TV weight (default 0.06) */
+    double mu;           /* ADMM penalty (default 0.1) */
+    size_t max_iters;    /* default 30 */
+    double rel_tol;      /* default 1e-6; 0 = fixed iteration count */
+    int has_tau;         /* 0 -> tau = 1e-8 * mu (solvers.cpp:332) */
+    double tau;
+    int init;            /* VSR_INIT_* */
+    const double* init_volume; /* HR real, when init == VSR_INIT_PROVIDED */
+} vsr_tv_config;
+
+typedef struct vsr_report {
+    size_t iterations;
+    double initial_objective;
+    double seconds;
+    double* objective;       /* caller-owned, capacity >= max_iters */
+    double* primal_residual; /* caller-owned, capacity >= max_iters */
+} vsr_report;
+
+int vsr_admm_tv(vsr_ctx* ctx, const size_t hr_dims[3], const size_t rates[3], const double* y_r,
+                const double* psf_r, const vsr_tv_config* cfg, double* x_r, vsr_report* report);
+
+/* Stepwise ADMM-TV solver over device-resident state (bench / streaming use).
+ * create: precompute (psf -> Lambda, y -> LR spectrum, Gamma tables) and the
+ * iteration-0 state; iterate(k): k iterations enqueued on the stream. */
+int vsr_tv_create_d(vsr_ctx* ctx, const size_t hr_dims[3], const size_t rates[3],
+                    const double* y_r_dev, const double* psf_r_dev, const vsr_tv_config* cfg,
+                    vsr_tv** out);
+int vsr_tv_iterate_d(vsr_tv* h, size_t iters);
+int vsr_tv_x_d(vsr_tv* h, const double** x_dev);
+int vsr_tv_report(vsr_tv* h, vsr_report* report); /* synchronizes */
+int vsr_tv_destroy(vsr_tv* h);
+double vsr_tv_algorithmic_bytes(const size_t hr_dims[3], const size_t rates[3]);
+
+/* ---- instrumentation (bench): kernels launched by this library so far, and
+ *      per-stage CUDA-event durations on the context stream when enabled. */
+int vsr_launch_count(uint64_t* out);
+int vsr_profile_enable(vsr_ctx* ctx, int enable);
+/* Drains the recorded stages (synchronizes on their events).  names is a
+ * max_stages x name_len char array; total_ms / launches per stage name. */
+int vsr_profile_read(vsr_ctx* ctx, int max_stages, char* names, size_t name_len, double* total_ms,
+                     uint64_t* launches, int* n_stages);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* VSR_H */

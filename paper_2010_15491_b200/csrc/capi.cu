@@ -1,0 +1,1297 @@
+// C ABI of the volsr B200 path (include/vsr.h).  Host-side orchestration of
+// the FFT engine (fft.cu), the spectral fold kernels (fold.cu) and the TV
+// stencil (tv.cu); the reference behaviour each entry point reproduces is
+// cited beside it.  Nothing here falls back to the CPU: every numeric step
+// runs in a kernel on the context's device.
+#include <atomic>
+#include <chrono>
+#include <climits>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../../include/vsr.h"
+#include "fft.cuh"
+#include "fold.cuh"
+#include "tv.cuh"
+
+using namespace vsr;
+
+namespace vsr {
+static std::atomic<uint64_t> g_launches{0};
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+// CUDA-event stage profiler owned by a context (see Profiler in vsr_common.cuh).
+class EventProfiler : public Profiler {
+public:
+    struct Rec {
+        std::string name;
+        cudaEvent_t b, e;
+    };
+    void begin(const char* name, cudaStream_t st) override {
+        Rec r{name, take(), take()};
+        VSR_CUDA(cudaEventRecord(r.b, st));
+        open_.push_back(r);
+    }
+    void end(cudaStream_t st) override {
+        Rec r = open_.back();
+        open_.pop_back();
+        VSR_CUDA(cudaEventRecord(r.e, st));
+        done_.push_back(r);
+    }
+    // aggregate (name -> total ms, count); recycles the events
+    std::vector<std::pair<std::string, std::pair<double, uint64_t>>> drain() {
+        std::vector<std::pair<std::string, std::pair<double, uint64_t>>> agg;
+        for (auto& r : done_) {
+            VSR_CUDA(cudaEventSynchronize(r.e));
+            float ms = 0.f;
+            VSR_CUDA(cudaEventElapsedTime(&ms, r.b, r.e));
+            bool found = false;
+            for (auto& a : agg)
+                if (a.first == r.name) {
+                    a.second.first += ms;
+                    a.second.second += 1;
+                    found = true;
+                }
+            if (!found) agg.push_back({r.name, {(double)ms, 1}});
+            pool_.push_back(r.b);
+            pool_.push_back(r.e);
+        }
+        done_.clear();
+        return agg;
+    }
+    ~EventProfiler() override {
+        for (auto& r : done_) {
+            cudaEventDestroy(r.b);
+            cudaEventDestroy(r.e);
+        }
+        for (auto e : pool_) cudaEventDestroy(e);
+    }
+
+private:
+    cudaEvent_t take() {
+        if (!pool_.empty()) {
+            cudaEvent_t e = pool_.back();
+            pool_.pop_back();
+            return e;
+        }
+        cudaEvent_t e;
+        VSR_CUDA(cudaEventCreate(&e));
+        return e;
+    }
+    std::vector<Rec> open_, done_;
+    std::vector<cudaEvent_t> pool_;
+};
+}  // namespace vsr
+
+// ============================================================ errors / state
+namespace {
+
+thread_local std::string g_last_error;
+std::atomic<uint64_t> g_fwd{0}, g_inv{0};  // reference src/fft.cpp:15-16
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return VSR_OK;
+    } catch (const vsr::shape_error& e) {
+        g_last_error = e.what();
+        return VSR_ERR_SHAPE;
+    } catch (const vsr::numeric_error& e) {
+        g_last_error = e.what();
+        return VSR_ERR_NUMERIC;
+    } catch (const std::out_of_range& e) {
+        g_last_error = e.what();
+        return VSR_ERR_OUT_OF_RANGE;
+    } catch (const std::invalid_argument& e) {
+        g_last_error = e.what();
+        return VSR_ERR_INVALID;
+    } catch (const vsr::cuda_error& e) {
+        g_last_error = e.what();
+        return VSR_ERR_CUDA;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return VSR_ERR_INTERNAL;
+    } catch (...) {
+        g_last_error = "unknown error";
+        return VSR_ERR_INTERNAL;
+    }
+}
+
+template <class T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    DevBuf() = default;
+    explicit DevBuf(size_t count) { alloc(count); }
+    void alloc(size_t count) {
+        release();
+        n = count;
+        if (count) VSR_CUDA(cudaMalloc(&p, count * sizeof(T)));
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    ~DevBuf() { release(); }
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr, o.n = 0; }
+    DevBuf& operator=(DevBuf&& o) noexcept {
+        release();
+        p = o.p;
+        n = o.n;
+        o.p = nullptr;
+        o.n = 0;
+        return *this;
+    }
+    size_t bytes() const { return n * sizeof(T); }
+};
+
+Dims to_dims(const size_t d[3]) {
+    if (!d) throw std::invalid_argument("dims pointer is null");
+    Dims r;
+    r.m = d[0];
+    r.n = d[1];
+    r.s = d[2];
+    return r;
+}
+
+// DecimationSpec ctor (src/operators.cpp:8-21).
+struct Spec {
+    Dims hr, lr;
+    int rates[3];
+    size_t rate() const { return (size_t)rates[0] * rates[1] * rates[2]; }
+};
+
+Spec make_spec(const size_t hr_dims[3], const size_t rates[3]) {
+    if (!rates) throw std::invalid_argument("rates pointer is null");
+    const Dims hr = to_dims(hr_dims);
+    static const char* names[3] = {"1 (rows)", "2 (cols)", "3 (slices)"};
+    const size_t ext[3] = {hr.m, hr.n, hr.s};
+    for (int a = 0; a < 3; ++a) {
+        if (rates[a] == 0) throw shape_error(std::string("DecimationSpec: zero rate on axis ") + names[a]);
+        if (ext[a] % rates[a] != 0)
+            throw shape_error("DecimationSpec: rate " + std::to_string(rates[a]) +
+                              " does not divide axis " + names[a] + " of length " +
+                              std::to_string(ext[a]));
+    }
+    Spec s;
+    s.hr = hr;
+    s.lr = Dims{hr.m / rates[0], hr.n / rates[1], hr.s / rates[2]};
+    for (int a = 0; a < 3; ++a) s.rates[a] = (int)rates[a];
+    return s;
+}
+
+void require_nonempty(const Dims& d, const char* where) {
+    if (d.count() == 0) throw shape_error(std::string(where) + ": empty volume");
+}
+
+void require_positive(double v, const char* name) {  // src/solvers.cpp:18-22
+    if (!(v > 0.0))
+        throw std::invalid_argument(std::string(name) + " must be positive, got " + std::to_string(v));
+}
+
+std::vector<double> diff_norm_table(size_t len) {
+    // std::norm({cos(2 pi f/len) - 1, sin(2 pi f/len)}) with exact 0 at DC
+    // (src/operators.cpp:233-240); same libm as the reference build.
+    std::vector<double> t(len);
+    const double two_pi = 2.0 * 3.14159265358979323846;
+    for (size_t f = 0; f < len; ++f) {
+        if (f == 0) {
+            t[f] = 0.0;
+            continue;
+        }
+        const double ang = two_pi * (double)f / (double)len;
+        const double re = std::cos(ang) - 1.0, im = std::sin(ang);
+        t[f] = re * re + im * im;
+    }
+    return t;
+}
+
+// make_gamma validity (src/solvers.cpp:192-201): tau >= 0, every
+// denominator > 0; the smallest denominator is the DC bin, equal to tau.
+void validate_tau(double tau) {
+    if (tau < 0.0) throw std::invalid_argument("make_gamma: tau must be nonnegative");
+    if (!(tau > 0.0))
+        throw numeric_error(
+            "make_gamma: difference-operator gram is singular at the zero frequency (DC); "
+            "a positive tau floor is required");
+}
+
+std::string residue_message(double ratio, double max_rel_imag) {  // src/fft.cpp:90-93
+    return "ifft3_real: imaginary residue " + std::to_string(ratio) + " exceeds " +
+           std::to_string(max_rel_imag) + " (spectral bookkeeping bug?)";
+}
+
+// ---- small kernels local to the ABI layer
+__global__ void residue_status_kernel(const double* __restrict__ partials, long long nblocks,
+                                      double tol, double* __restrict__ status) {
+    __shared__ double red[64];
+    double v[2] = {0.0, 0.0};
+    for (long long i = threadIdx.x; i < nblocks; i += blockDim.x) {
+        v[0] += partials[2 * i];
+        v[1] += partials[2 * i + 1];
+    }
+    block_reduce_sum<2>(v, red);
+    if (threadIdx.x == 0) {
+        const double ratio = v[1] > 0.0 ? sqrt(v[0] / v[1]) : 0.0;
+        status[2] = ratio;
+        if (v[1] > 0.0 && ratio > tol && status[0] == 0.0) {
+            status[0] = 1.0;
+            status[1] = ratio;
+        }
+    }
+}
+
+__global__ void cmul_kernel(long long n, double2* __restrict__ a, const double2* __restrict__ b,
+                            bool conj_b) {
+    const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    const double2 bb = conj_b ? make_double2(b[p].x, -b[p].y) : b[p];
+    a[p] = cmul(a[p], bb);  // operators.cpp:129 xh[p] *= lambda[p]
+}
+
+}  // namespace
+
+// ============================================================ context
+struct vsr_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    DevBuf<double> scal;                // 8 doubles: [0..3] residue status
+    DevBuf<unsigned long long> bad;     // non-finite index slot
+    EventProfiler profiler;
+    bool profiling = false;
+    Profiler* prof() { return profiling ? &profiler : nullptr; }
+    struct Guard {
+        int prev = 0;
+        explicit Guard(int dev) {
+            cudaGetDevice(&prev);
+            if (prev != dev) VSR_CUDA(cudaSetDevice(dev));
+        }
+        ~Guard() {
+            int cur = 0;
+            cudaGetDevice(&cur);
+            if (cur != prev) cudaSetDevice(prev);
+        }
+    };
+};
+
+namespace {
+
+// Run an ifft3_real-style final-pass reduction check synchronously.
+struct ResidueCheck {
+    DevBuf<double> partials;
+    size_t blocks = 0;
+    PassReduce red;
+    ResidueCheck(vsr_ctx* ctx, const Dims& d) {
+        blocks = fft_engine().inverse_final_blocks(d);
+        partials.alloc(2 * std::max<size_t>(blocks, 1));
+        red.partials = partials.p;
+        red.bad_index = ctx->bad.p;
+        VSR_CUDA(cudaMemsetAsync(ctx->scal.p, 0, 8 * sizeof(double), ctx->stream));
+        VSR_CUDA(cudaMemsetAsync(ctx->bad.p, 0xff, sizeof(unsigned long long), ctx->stream));
+    }
+    // returns (violated, ratio) and the non-finite index (ULLONG_MAX = none)
+    void finish(vsr_ctx* ctx, double tol, double* status_out, unsigned long long* bad_out) {
+        residue_status_kernel<<<1, 1024, 0, ctx->stream>>>(partials.p, (long long)blocks, tol,
+                                                           ctx->scal.p);
+        VSR_LAUNCH_CHECK();
+        VSR_CUDA(cudaMemcpyAsync(status_out, ctx->scal.p, 4 * sizeof(double),
+                                 cudaMemcpyDeviceToHost, ctx->stream));
+        VSR_CUDA(cudaMemcpyAsync(bad_out, ctx->bad.p, sizeof(unsigned long long),
+                                 cudaMemcpyDeviceToHost, ctx->stream));
+        VSR_CUDA(cudaStreamSynchronize(ctx->stream));
+    }
+};
+
+void h2d(vsr_ctx* ctx, void* dst, const void* src, size_t bytes) {
+    if (bytes) VSR_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->stream));
+}
+void d2h(vsr_ctx* ctx, void* dst, const void* src, size_t bytes) {
+    if (bytes) VSR_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+}
+void sync(vsr_ctx* ctx) { VSR_CUDA(cudaStreamSynchronize(ctx->stream)); }
+
+void require_ctx(vsr_ctx* ctx) {
+    if (!ctx) throw std::invalid_argument("vsr: null context");
+}
+
+double inv_sqrt_count(const Dims& d) { return 1.0 / std::sqrt((double)d.count()); }
+
+}  // namespace
+
+extern "C" {
+
+const char* vsr_last_error_message(void) { return g_last_error.c_str(); }
+int vsr_version(void) { return 1; }
+
+int vsr_ctx_create(int device, vsr_ctx** out) {
+    return guarded([&] {
+        if (!out) throw std::invalid_argument("vsr_ctx_create: null out");
+        int ndev = 0;
+        VSR_CUDA(cudaGetDeviceCount(&ndev));
+        if (device < 0 || device >= ndev)
+            throw std::invalid_argument("vsr_ctx_create: device " + std::to_string(device) +
+                                        " not present (" + std::to_string(ndev) + " devices)");
+        auto* c = new vsr_ctx();
+        c->device = device;
+        vsr_ctx::Guard g(device);
+        VSR_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        c->scal.alloc(8);
+        c->bad.alloc(1);
+        *out = c;
+    });
+}
+
+int vsr_ctx_destroy(vsr_ctx* ctx) {
+    return guarded([&] {
+        if (!ctx) return;
+        vsr_ctx::Guard g(ctx->device);
+        cudaStreamSynchronize(ctx->stream);
+        ctx->scal.release();
+        ctx->bad.release();
+        cudaStreamDestroy(ctx->stream);
+        delete ctx;
+    });
+}
+
+int vsr_ctx_synchronize(vsr_ctx* ctx) {
+    return guarded([&] {
+        require_ctx(ctx);
+        sync(ctx);
+    });
+}
+
+void* vsr_ctx_stream(vsr_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
+int vsr_ctx_device(vsr_ctx* ctx) { return ctx ? ctx->device : -1; }
+
+int vsr_host_alloc(size_t bytes, void** out) {
+    return guarded([&] { VSR_CUDA(cudaHostAlloc(out, bytes, cudaHostAllocDefault)); });
+}
+int vsr_host_free(void* p) {
+    return guarded([&] { VSR_CUDA(cudaFreeHost(p)); });
+}
+int vsr_device_alloc(vsr_ctx* ctx, size_t bytes, void** out) {
+    return guarded([&] {
+        require_ctx(ctx);
+        vsr_ctx::Guard g(ctx->device);
+        VSR_CUDA(cudaMalloc(out, bytes));
+    });
+}
+int vsr_device_free(vsr_ctx* ctx, void* p) {
+    return guarded([&] {
+        require_ctx(ctx);
+        vsr_ctx::Guard g(ctx->device);
+        VSR_CUDA(cudaFree(p));
+    });
+}
+int vsr_memcpy_h2d(vsr_ctx* ctx, void* dst, const void* src, size_t bytes) {
+    return guarded([&] {
+        require_ctx(ctx);
+        vsr_ctx::Guard g(ctx->device);
+        h2d(ctx, dst, src, bytes);
+        sync(ctx);
+    });
+}
+int vsr_memcpy_d2h(vsr_ctx* ctx, void* dst, const void* src, size_t bytes) {
+    return guarded([&] {
+        require_ctx(ctx);
+        vsr_ctx::Guard g(ctx->device);
+        d2h(ctx, dst, src, bytes);
+        sync(ctx);
+    });
+}
+
+// ============================================================ FFT contract
+// src/fft.cpp:66-101
+static void fft_host(vsr_ctx* ctx, const size_t dims[3], const void* in, bool real_in, double* out,
+                     double scale_override) {
+    require_ctx(ctx);
+    const Dims d = to_dims(dims);
+    require_nonempty(d, "fft3");
+    vsr_ctx::Guard g(ctx->device);
+    DevBuf<double2> buf(d.count());
+    DevBuf<double> rin;
+    if (real_in) {
+        rin.alloc(d.count());
+        h2d(ctx, rin.p, in, rin.bytes());
+        fft_engine().forward3(d, rin.p, IN_REAL, buf.p, scale_override, ctx->stream);
+    } else {
+        h2d(ctx, buf.p, in, buf.bytes());
+        fft_engine().forward3(d, buf.p, IN_COMPLEX, buf.p, scale_override, ctx->stream);
+    }
+    ++g_fwd;
+    d2h(ctx, out, buf.p, buf.bytes());
+    sync(ctx);
+}
+
+int vsr_fft3(vsr_ctx* ctx, const size_t dims[3], const double* in_c, double* out_c) {
+    return guarded([&] { fft_host(ctx, dims, in_c, false, out_c, inv_sqrt_count(to_dims(dims))); });
+}
+int vsr_fft3_real(vsr_ctx* ctx, const size_t dims[3], const double* in_r, double* out_c) {
+    return guarded([&] { fft_host(ctx, dims, in_r, true, out_c, inv_sqrt_count(to_dims(dims))); });
+}
+int vsr_dft3_unnormalized(vsr_ctx* ctx, const size_t dims[3], const double* in_r, double* out_c) {
+    return guarded([&] { fft_host(ctx, dims, in_r, true, out_c, 1.0); });
+}
+int vsr_psf_to_spectrum(vsr_ctx* ctx, const size_t dims[3], const double* psf_r, double* lambda_c) {
+    return vsr_dft3_unnormalized(ctx, dims, psf_r, lambda_c);
+}
+
+int vsr_ifft3(vsr_ctx* ctx, const size_t dims[3], const double* in_c, double* out_c) {
+    return guarded([&] {
+        require_ctx(ctx);
+        const Dims d = to_dims(dims);
+        require_nonempty(d, "fft3");
+        vsr_ctx::Guard g(ctx->device);
+        DevBuf<double2> buf(d.count());
+        h2d(ctx, buf.p, in_c, buf.bytes());
+        fft_engine().inverse3(d, buf.p, buf.p, OUT_COMPLEX, inv_sqrt_count(d), nullptr, ctx->stream);
+        ++g_inv;
+        d2h(ctx, out_c, buf.p, buf.bytes());
+        sync(ctx);
+    });
+}
+
+int vsr_ifft3_real(vsr_ctx* ctx, const size_t dims[3], const double* in_c, double* out_r,
+                   double max_rel_imag) {
+    return guarded([&] {
+        require_ctx(ctx);
+        const Dims d = to_dims(dims);
+        require_nonempty(d, "fft3");
+        vsr_ctx::Guard g(ctx->device);
+        DevBuf<double2> buf(d.count());
+        DevBuf<double> xr(d.count());
+        h2d(ctx, buf.p, in_c, buf.bytes());
+        ResidueCheck rc(ctx, d);
+        fft_engine().inverse3(d, buf.p, xr.p, OUT_REAL, inv_sqrt_count(d), &rc.red, ctx->stream);
+        ++g_inv;
+        double status[4];
+        unsigned long long bad;
+        rc.finish(ctx, max_rel_imag, status, &bad);
+        if (status[0] != 0.0) throw numeric_error(residue_message(status[1], max_rel_imag));
+        d2h(ctx, out_r, xr.p, xr.bytes());
+        sync(ctx);
+    });
+}
+
+int vsr_fft_counters(uint64_t* forward, uint64_t* inverse) {
+    if (forward) *forward = g_fwd.load(std::memory_order_relaxed);
+    if (inverse) *inverse = g_inv.load(std::memory_order_relaxed);
+    return VSR_OK;
+}
+int vsr_reset_fft_counters(void) {
+    g_fwd.store(0);
+    g_inv.store(0);
+    return VSR_OK;
+}
+
+// ============================================================ operators
+int vsr_decimate(vsr_ctx* ctx, const size_t hr_dims[3], const size_t rates[3], const double* x,
+                 double* y) {
+    return guarded([&] {
+        require_ctx(ctx);
+        const Spec sp = make_spec(hr_dims, rates);
+        vsr_ctx::Guard g(ctx->device);
+        DevBuf<double> dx(sp.hr.count()), dy(sp.lr.count());
+        h2d(ctx, dx.p, x, dx.bytes());
+        launch_decimate(sp.hr, sp.rates, dx.p, dy.p, ctx->stream);
+        d2h(ctx, y, dy.p, dy.bytes());
+        sync(ctx);
+    });
+}
+
+int vsr_decimate_adjoint(vsr_ctx* ctx, const size_t hr_dims[3], const size_t rates[3],
+                         const double* y, double* x) {
+    return guarded([&] {
+        require_ctx(ctx);
+        const Spec sp = make_spec(hr_dims, rates);
+        vsr_ctx::Guard g(ctx->device);
+        DevBuf<double> dx(sp.hr.count()), dy(sp.lr.count());
+        h2d(ctx, dy.p, y, dy.bytes());
+        launch_decimate_adjoint(sp.hr, sp.rates, dy.p, dx.p, 1.0, ctx->stream);
+        d2h(ctx, x, dx.p, dx.bytes());
+        sync(ctx);
+    });
+}
+
+static int diff_host(vsr_ctx* ctx, const size_t dims[3], int axis, const double* x, double* out,
+                     bool adjoint) {
+    return guarded([&] {
+        require_ctx(ctx);
+        const Dims d = to_dims(dims);
+        if (axis < 0 || axis > 2) throw std::invalid_argument("diff: axis must be 0, 1 or 2");
+        vsr_ctx::Guard g(ctx->device);
+        DevBuf<double> dx(d.count()), dout(d.count());
+        h2d(ctx, dx.p, x, dx.bytes());
+        launch_diff(d, axis, adjoint, dx.p, dout.p, ctx->stream);
+        d2h(ctx, out, dout.p, dout.bytes());
+        sync(ctx);
+    });
+}
+int vsr_diff_forward(vsr_ctx* ctx, const size_t dims[3], int axis, const double* x, double* out) {
+    return diff_host(ctx, dims, axis, x, out, false);
+}
+int vsr_diff_adjoint(vsr_ctx* ctx, const size_t dims[3], int axis, const double* x, double* out) {
+    return diff_host(ctx, dims, axis, x, out, true);
+}
+
+int vsr_blur_apply(vsr_ctx* ctx, const size_t dims[3], const double* x, const double* lambda_c,
+                   int conjugate, double* out) {
+    return guarded([&] {
+        require_ctx(ctx);
+        const Dims d = to_dims(dims);
+        require_nonempty(d, "fft3");
+        vsr_ctx::Guard g(ctx->device);
+        DevBuf<double> dx(d.count());
+        DevBuf<double2> W(d.count()), lam(d.count());
+        h2d(ctx, dx.p, x, dx.bytes());
+        h2d(ctx, lam.p, lambda_c, lam.bytes());
+        fft_engine().forward3(d, dx.p, IN_REAL, W.p, inv_sqrt_count(d), ctx->stream);
+        ++g_fwd;
+        cmul_kernel<<<(unsigned)((d.count() + 255) / 256), 256, 0, ctx->stream>>>(
+            (long long)d.count(), W.p, lam.p, conjugate != 0);
+        VSR_LAUNCH_CHECK();
+        ResidueCheck rc(ctx, d);
+        fft_engine().inverse3(d, W.p, dx.p, OUT_REAL, inv_sqrt_count(d), &rc.red, ctx->stream);
+        ++g_inv;
+        double status[4];
+        unsigned long long bad;
+        rc.finish(ctx, 1e-8, status, &bad);
+        if (status[0] != 0.0) throw numeric_error(residue_message(status[1], 1e-8));
+        d2h(ctx, out, dx.p, dx.bytes());
+        sync(ctx);
+    });
+}
+
+// ============================================================ spectral fold
+int vsr_alias_fold(vsr_ctx* ctx, const size_t hr_dims[3], const size_t rates[3],
+                   const double* hr_c, double* lr_c) {
+    return guarded([&] {
+        require_ctx(ctx);
+        const Spec sp = make_spec(hr_dims, rates);
+        vsr_ctx::Guard g(ctx->device);
+        const FoldGeom G = make_geom(sp.hr, sp.rates);
+        DevBuf<double2> hi(sp.hr.count()), lo(sp.lr.count());
+        h2d(ctx, hi.p, hr_c, hi.bytes());
+        launch_fold_apply(G, nullptr, nullptr, hi.p, lo.p, ctx->stream);
+        d2h(ctx, lr_c, lo.p, lo.bytes());
+        sync(ctx);
+    });
+}
+
+int vsr_alias_expand(vsr_ctx* ctx, const size_t hr_dims[3], const size_t rates[3],
+                     const double* lr_c, double* hr_c) {
+    return guarded([&] {
+        require_ctx(ctx);
+        const Spec sp = make_spec(hr_dims, rates);
+        vsr_ctx::Guard g(ctx->device);
+        const FoldGeom G = make_geom(sp.hr, sp.rates);
+        DevBuf<double2> hi(sp.hr.count()), lo(sp.lr.count());
+        h2d(ctx, lo.p, lr_c, lo.bytes());
+        launch_fold_adjoint(G, nullptr, nullptr, lo.p, hi.p, ctx->stream);
+        d2h(ctx, hr_c, hi.p, hi.bytes());
+        sync(ctx);
+    });
+}
+
+struct vsr_folded {
+    vsr_ctx* ctx;
+    Spec sp;
+    FoldGeom G;
+    DevBuf<double2> lam;
+};
+
+int vsr_folded_create(vsr_ctx* ctx, const size_t hr_dims[3], const size_t rates[3],
+                      const double* lambda_c, vsr_folded** out) {
+    return guarded([&] {
+        require_ctx(ctx);
+        const Spec sp = make_spec(hr_dims, rates);
+        vsr_ctx::Guard g(ctx->device);
+        auto* f = new vsr_folded();
+        f->ctx = ctx;
+        f->sp = sp;
+        f->G = make_geom(sp.hr, sp.rates);
+        f->lam.alloc(sp.hr.count());
+        h2d(ctx, f->lam.p, lambda_c, f->lam.bytes());
+        sync(ctx);
+        *out = f;
+    });
+}
+
+int vsr_folded_destroy(vsr_folded* f) {
+    return guarded([&] {
+        if (!f) return;
+        vsr_ctx::Guard g(f->ctx->device);
+        delete f;
+    });
+}
+
+int vsr_folded_block_value(vsr_folded* f, size_t br, size_t bc, size_t bs, size_t gi,
+                           double out_c[2]) {
+    return guarded([&] {
+        if (br >= (size_t)f->sp.rates[0] || bc >= (size_t)f->sp.rates[1] ||
+            bs >= (size_t)f->sp.rates[2] || gi >= f->sp.lr.count())
+            throw std::out_of_range("FoldedSpectrum::block_value: block offset out of range");
+        vsr_ctx::Guard g(f->ctx->device);
+        const Dims& lr = f->sp.lr;
+        const size_t g1 = gi % lr.m, g2 = (gi / lr.m) % lr.n, g3 = gi / (lr.m * lr.n);
+        const size_t hr = (g1 + br * lr.m) + f->sp.hr.m * ((g2 + bc * lr.n) + f->sp.hr.n * (g3 + bs * lr.s));
+        d2h(f->ctx, out_c, f->lam.p + hr, sizeof(double2));
+        sync(f->ctx);
+    });
+}
+
+static int folded_apply_host(vsr_folded* f, const double* in_c, const double* w, double* out_c,
+                             bool adjoint) {
+    return guarded([&] {
+        vsr_ctx* ctx = f->ctx;
+        vsr_ctx::Guard g(ctx->device);
+        DevBuf<double2> hi(f->sp.hr.count()), lo(f->sp.lr.count());
+        DevBuf<double> dw;
+        if (w) {
+            dw.alloc(f->sp.hr.count());
+            h2d(ctx, dw.p, w, dw.bytes());
+        }
+        if (!adjoint) {
+            h2d(ctx, hi.p, in_c, hi.bytes());
+            launch_fold_apply(f->G, f->lam.p, dw.p, hi.p, lo.p, ctx->stream);
+            d2h(ctx, out_c, lo.p, lo.bytes());
+        } else {
+            h2d(ctx, lo.p, in_c, lo.bytes());
+            launch_fold_adjoint(f->G, f->lam.p, dw.p, lo.p, hi.p, ctx->stream);
+            d2h(ctx, out_c, hi.p, hi.bytes());
+        }
+        sync(ctx);
+    });
+}
+int vsr_folded_apply(vsr_folded* f, const double* hr_c, double* lr_c) {
+    return folded_apply_host(f, hr_c, nullptr, lr_c, false);
+}
+int vsr_folded_apply_adjoint(vsr_folded* f, const double* lr_c, double* hr_c) {
+    return folded_apply_host(f, lr_c, nullptr, hr_c, true);
+}
+int vsr_folded_apply_weighted(vsr_folded* f, const double* hr_c, const double* hr_w, double* lr_c) {
+    return folded_apply_host(f, hr_c, hr_w, lr_c, false);
+}
+int vsr_folded_apply_adjoint_weighted(vsr_folded* f, const double* lr_c, const double* hr_w,
+                                      double* hr_c) {
+    return folded_apply_host(f, lr_c, hr_w, hr_c, true);
+}
+
+static int gram_host(vsr_folded* f, const double* w, double* lr_r) {
+    return guarded([&] {
+        vsr_ctx* ctx = f->ctx;
+        vsr_ctx::Guard g(ctx->device);
+        DevBuf<double> lo(f->sp.lr.count()), dw;
+        if (w) {
+            dw.alloc(f->sp.hr.count());
+            h2d(ctx, dw.p, w, dw.bytes());
+        }
+        launch_gram(f->G, f->lam.p, dw.p, lo.p, ctx->stream);
+        d2h(ctx, lr_r, lo.p, lo.bytes());
+        sync(ctx);
+    });
+}
+int vsr_folded_gram_diag(vsr_folded* f, double* lr_r) { return gram_host(f, nullptr, lr_r); }
+int vsr_folded_gram_diag_weighted(vsr_folded* f, const double* hr_w, double* lr_r) {
+    return gram_host(f, hr_w, lr_r);
+}
+int vsr_folded_swap_blocks_for_fault_injection(vsr_folded* f) {
+    return guarded([&] {
+        if (f->sp.rate() < 2) return;  // spectral.cpp:116
+        vsr_ctx::Guard g(f->ctx->device);
+        launch_swap_blocks(f->G, f->lam.p, f->ctx->stream);
+        sync(f->ctx);
+    });
+}
+
+// ============================================================ Tikhonov
+// TikhonovOperator (src/solvers.cpp:36-67).  Device state: Lambda (16N),
+// X̄ = fft3(xbar) (16N), x̂ work (16N), LR spectrum of y, y and x staging.
+struct vsr_tikhonov {
+    vsr_ctx* ctx = nullptr;
+    Spec sp;
+    FoldGeom G;
+    double reg = 0.0;
+    DevBuf<double2> lam, xbh, Yl, xh;
+    DevBuf<double> y, x;
+    DevBuf<double> partials, status;  // status: [violated, ratio, last ratio, pad]
+    DevBuf<unsigned long long> bad;
+    size_t res_blocks = 0;
+};
+
+static void tik_reset_status(vsr_tikhonov* t) {
+    VSR_CUDA(cudaMemsetAsync(t->status.p, 0, 4 * sizeof(double), t->ctx->stream));
+    VSR_CUDA(cudaMemsetAsync(t->bad.p, 0xff, sizeof(unsigned long long), t->ctx->stream));
+}
+
+static vsr_tikhonov* tik_new(vsr_ctx* ctx, const size_t hr_dims[3], const size_t rates[3],
+                             double reg) {
+    require_ctx(ctx);
+    const Spec sp = make_spec(hr_dims, rates);
+    require_positive(reg, "lambda");  // solvers.cpp:39
+    require_nonempty(sp.hr, "fft3");
+    auto* t = new vsr_tikhonov();
+    t->ctx = ctx;
+    t->sp = sp;
+    t->G = make_geom(sp.hr, sp.rates);
+    t->reg = reg;
+    const size_t N = sp.hr.count(), Nl = sp.lr.count();
+    t->lam.alloc(N);
+    t->xbh.alloc(N);
+    t->xh.alloc(N);
+    t->Yl.alloc(Nl);
+    t->y.alloc(Nl);
+    t->x.alloc(N);
+    t->res_blocks = fft_engine().inverse_final_blocks(sp.hr);
+    t->partials.alloc(2 * std::max<size_t>(t->res_blocks, 1));
+    t->status.alloc(4);
+    t->bad.alloc(1);
+    tik_reset_status(t);
+    return t;
+}
+
+int vsr_tikhonov_create(vsr_ctx* ctx, const size_t hr_dims[3], const size_t rates[3],
+                        const double* lambda_c, double reg, const double* xbar_r,
+                        vsr_tikhonov** out) {
+    return guarded([&] {
+        require_ctx(ctx);
+        vsr_ctx::Guard g(ctx->device);
+        vsr_tikhonov* t = tik_new(ctx, hr_dims, rates, reg);
+        try {
+            h2d(ctx, t->lam.p, lambda_c, t->lam.bytes());
+            h2d(ctx, t->x.p, xbar_r, t->x.bytes());
+            // xbar_hat_ = fft3(cfg.xbar)   (solvers.cpp:45)
+            fft_engine().forward3(t->sp.hr, t->x.p, IN_REAL, t->xbh.p, inv_sqrt_count(t->sp.hr),
+                                  ctx->stream);
+            ++g_fwd;
+            sync(ctx);
+        } catch (...) {
+            delete t;
+            throw;
+        }
+        *out = t;
+    });
+}
+
+int vsr_tikhonov_create_d(vsr_ctx* ctx, const size_t hr_dims[3], const size_t rates[3],
+                          const double* lambda_c_dev, double reg, const double* xbar_r_dev,
+                          vsr_tikhonov** out) {
+    return guarded([&] {
+        require_ctx(ctx);
+        vsr_ctx::Guard g(ctx->device);
+        vsr_tikhonov* t = tik_new(ctx, hr_dims, rates, reg);
+        try {
+            VSR_CUDA(cudaMemcpyAsync(t->lam.p, lambda_c_dev, t->lam.bytes(),
+                                     cudaMemcpyDeviceToDevice, ctx->stream));
+            fft_engine().forward3(t->sp.hr, xbar_r_dev, IN_REAL, t->xbh.p,
+                                  inv_sqrt_count(t->sp.hr), ctx->stream);
+            ++g_fwd;
+            sync(ctx);
+        } catch (...) {
+            delete t;
+            throw;
+        }
+        *out = t;
+    });
+}
+
+int vsr_tikhonov_destroy(vsr_tikhonov* t) {
+    return guarded([&] {
+        if (!t) return;
+        vsr_ctx::Guard g(t->ctx->device);
+        cudaStreamSynchronize(t->ctx->stream);
+        delete t;
+    });
+}
+
+// Enqueue one solve: LR FFT of y (== F D^H y up to the alias replication and
+// 1/sqrt(d)) -> fused fold -> inverse FFT to real x with
+// the residue / finiteness reductions.
+static void tik_enqueue(vsr_tikhonov* t, const double* y_dev, double* x_dev) {
+    cudaStream_t st = t->ctx->stream;
+    Profiler* prof = t->ctx->prof();
+    {
+        ProfScope ps(prof, "lr_fft3", st);
+        fft_engine().forward3(t->sp.lr, y_dev, IN_REAL, t->Yl.p, inv_sqrt_count(t->sp.lr), st);
+    }
+    ++g_fwd;  // the one forward transform of solve() (solvers.cpp:52)
+    {
+        ProfScope ps(prof, "tik_fold", st);
+        launch_tik_fold(t->G, t->Yl.p, t->lam.p, t->xbh.p, t->xh.p, t->reg, st);
+    }
+    PassReduce red{t->partials.p, t->bad.p};
+    fft_engine().inverse3(t->sp.hr, t->xh.p, x_dev, OUT_REAL, inv_sqrt_count(t->sp.hr), &red, st,
+                          prof);
+    ++g_inv;  // the one inverse transform (solvers.cpp:64)
+    {
+        ProfScope ps(prof, "residue_status", st);
+        residue_status_kernel<<<1, 1024, 0, st>>>(t->partials.p, (long long)t->res_blocks, 1e-8,
+                                                  t->status.p);
+        VSR_LAUNCH_CHECK();
+    }
+}
+
+static void tik_check(vsr_tikhonov* t) {
+    double status[4];
+    unsigned long long bad = 0;
+    d2h(t->ctx, status, t->status.p, sizeof(status));
+    d2h(t->ctx, &bad, t->bad.p, sizeof(bad));
+    sync(t->ctx);
+    if (status[0] != 0.0 || bad != ULLONG_MAX) {
+        tik_reset_status(t);
+        sync(t->ctx);
+        if (status[0] != 0.0) throw numeric_error(residue_message(status[1], 1e-8));
+        throw numeric_error("tikhonov_fast: non-finite value at flat index " + std::to_string(bad));
+    }
+}
+
+int vsr_tikhonov_solve(vsr_tikhonov* t, const double* y_r, double* x_r) {
+    return guarded([&] {
+        if (!t) throw std::invalid_argument("vsr_tikhonov_solve: null operator");
+        vsr_ctx::Guard g(t->ctx->device);
+        h2d(t->ctx, t->y.p, y_r, t->y.bytes());
+        tik_enqueue(t, t->y.p, t->x.p);
+        d2h(t->ctx, x_r, t->x.p, t->x.bytes());
+        tik_check(t);
+    });
+}
+
+int vsr_tikhonov_solve_d(vsr_tikhonov* t, const double* y_dev, double* x_dev) {
+    return guarded([&] {
+        if (!t) throw std::invalid_argument("vsr_tikhonov_solve_d: null operator");
+        vsr_ctx::Guard g(t->ctx->device);
+        tik_enqueue(t, y_dev, x_dev);
+    });
+}
+
+int vsr_tikhonov_check(vsr_tikhonov* t) {
+    return guarded([&] {
+        vsr_ctx::Guard g(t->ctx->device);
+        tik_check(t);
+    });
+}
+
+int vsr_tikhonov_fast(vsr_ctx* ctx, const size_t hr_dims[3], const size_t rates[3],
+                      const double* y_r, const double* lambda_c, double reg, const double* xbar_r,
+                      double* x_r) {
+    vsr_tikhonov* t = nullptr;
+    int rc = vsr_tikhonov_create(ctx, hr_dims, rates, lambda_c, reg, xbar_r, &t);
+    if (rc != VSR_OK) return rc;
+    rc = vsr_tikhonov_solve(t, y_r, x_r);
+    std::string msg = g_last_error;
+    vsr_tikhonov_destroy(t);
+    g_last_error = msg;
+    return rc;
+}
+
+double vsr_tikhonov_algorithmic_bytes(const size_t hr_dims[3], const size_t rates[3]) {
+    const double N = (double)hr_dims[0] * hr_dims[1] * hr_dims[2];
+    const double d = (double)rates[0] * rates[1] * rates[2];
+    return (72.0 + 40.0 / d) * N;
+}
+
+// ============================================================ TV pieces
+int vsr_make_gamma(vsr_ctx* ctx, const size_t hr_dims[3], double tau, double* gamma_r) {
+    return guarded([&] {
+        require_ctx(ctx);
+        const Dims d = to_dims(hr_dims);
+        validate_tau(tau);
+        vsr_ctx::Guard g(ctx->device);
+        const auto nr = diff_norm_table(d.m), nc = diff_norm_table(d.n), ns = diff_norm_table(d.s);
+        DevBuf<double> dr(d.m), dc(d.n), ds(d.s), out(d.count());
+        h2d(ctx, dr.p, nr.data(), dr.bytes());
+        h2d(ctx, dc.p, nc.data(), dc.bytes());
+        h2d(ctx, ds.p, ns.data(), ds.bytes());
+        launch_gamma(d, dr.p, dc.p, ds.p, tau, out.p, ctx->stream);
+        d2h(ctx, gamma_r, out.p, out.bytes());
+        sync(ctx);
+    });
+}
+
+int vsr_tv_x_update(vsr_ctx* ctx, const size_t hr_dims[3], const size_t rates[3],
+                    const double* y_r, const double* lambda_c, double mu,
+                    const double* theta_hat_c, const double* gamma_r, double* x_r) {
+    return guarded([&] {
+        require_ctx(ctx);
+        const Spec sp = make_spec(hr_dims, rates);
+        require_positive(mu, "mu");  // solvers.cpp:248
+        const size_t N = sp.hr.count(), Nl = sp.lr.count();
+        // require_gamma_valid (solvers.cpp:209-216)
+        for (size_t p = 0; p < N; ++p)
+            if (!(gamma_r[p] > 0.0) || !std::isfinite(gamma_r[p]))
+                throw numeric_error(
+                    "tv_x_update: gamma must be strictly positive and finite everywhere; entry " +
+                    std::to_string(p) +
+                    " is not (unfloored DC singularity of the difference gram?)");
+        vsr_ctx::Guard g(ctx->device);
+        const FoldGeom G = make_geom(sp.hr, sp.rates);
+        DevBuf<double> dy(Nl), gam(N), x(N);
+        DevBuf<double2> Yl(Nl), lam(N), W(N);
+        h2d(ctx, dy.p, y_r, dy.bytes());
+        h2d(ctx, lam.p, lambda_c, lam.bytes());
+        h2d(ctx, W.p, theta_hat_c, W.bytes());
+        h2d(ctx, gam.p, gamma_r, gam.bytes());
+        fft_engine().forward3(sp.lr, dy.p, IN_REAL, Yl.p, inv_sqrt_count(sp.lr), ctx->stream);
+        ++g_fwd;
+        GammaTables tabs{nullptr, nullptr, nullptr, 0.0};
+        launch_tv_fold(G, Yl.p, lam.p, W.p, W.p, gam.p, tabs, mu, nullptr, ctx->stream);
+        ResidueCheck rc(ctx, sp.hr);
+        fft_engine().inverse3(sp.hr, W.p, x.p, OUT_REAL, inv_sqrt_count(sp.hr), &rc.red, ctx->stream);
+        ++g_inv;
+        double status[4];
+        unsigned long long bad;
+        rc.finish(ctx, 1e-8, status, &bad);
+        if (status[0] != 0.0) throw numeric_error(residue_message(status[1], 1e-8));
+        d2h(ctx, x_r, x.p, x.bytes());
+        sync(ctx);
+    });
+}
+
+int vsr_tv_shrink(vsr_ctx* ctx, size_t count, const double* nu1, const double* nu2,
+                  const double* nu3, double threshold, double* out1, double* out2, double* out3) {
+    return guarded([&] {
+        require_ctx(ctx);
+        if (threshold < 0.0) throw std::invalid_argument("tv_shrink: threshold must be >= 0");
+        if (count == 0) return;
+        vsr_ctx::Guard g(ctx->device);
+        DevBuf<double> a(count), b(count), c(count), o1(count), o2(count), o3(count);
+        h2d(ctx, a.p, nu1, a.bytes());
+        h2d(ctx, b.p, nu2, b.bytes());
+        h2d(ctx, c.p, nu3, c.bytes());
+        launch_shrink(count, a.p, b.p, c.p, threshold, o1.p, o2.p, o3.p, ctx->stream);
+        d2h(ctx, out1, o1.p, o1.bytes());
+        d2h(ctx, out2, o2.p, o2.bytes());
+        d2h(ctx, out3, o3.p, o3.bytes());
+        sync(ctx);
+    });
+}
+
+int vsr_objective_tv(vsr_ctx* ctx, const size_t hr_dims[3], const size_t rates[3],
+                     const double* x_r, const double* y_r, const double* lambda_c,
+                     double tv_weight, double* out) {
+    return guarded([&] {
+        require_ctx(ctx);
+        const Spec sp = make_spec(hr_dims, rates);
+        require_nonempty(sp.hr, "fft3");
+        vsr_ctx::Guard g(ctx->device);
+        const FoldGeom G = make_geom(sp.hr, sp.rates);
+        const size_t N = sp.hr.count(), Nl = sp.lr.count();
+        DevBuf<double> dx(N), dy(Nl);
+        DevBuf<double2> lam(N), W(N), Yl(Nl);
+        h2d(ctx, dx.p, x_r, dx.bytes());
+        h2d(ctx, dy.p, y_r, dy.bytes());
+        h2d(ctx, lam.p, lambda_c, lam.bytes());
+        cudaStream_t st = ctx->stream;
+        // data term by LR Parseval: ||y - D H x||^2 = ||F_l y - (1/sqrt d) fold(Lambda x̂)||^2
+        fft_engine().forward3(sp.lr, dy.p, IN_REAL, Yl.p, inv_sqrt_count(sp.lr), st);
+        fft_engine().forward3(sp.hr, dx.p, IN_REAL, W.p, inv_sqrt_count(sp.hr), st);
+        g_fwd += 2;
+        const size_t fb = tv_fold_blocks(G), tb = tv_norm_blocks(sp.hr);
+        DevBuf<double> fitp(fb), tvp(tb), res(2);
+        launch_fit_partials(G, Yl.p, lam.p, W.p, fitp.p, st);
+        launch_tv_norm(sp.hr, dx.p, tvp.p, st);
+        launch_finalize_sum(fitp.p, 1, 1, fb, res.p, st);
+        launch_finalize_sum(tvp.p, 1, 1, tb, res.p + 1, st);
+        double h[2];
+        d2h(ctx, h, res.p, sizeof(h));
+        sync(ctx);
+        *out = 0.5 * h[0] + tv_weight * h[1];  // solvers.cpp:318
+    });
+}
+
+// ============================================================ ADMM-TV
+// admm_tv (src/solvers.cpp:321-411).  State per iteration: theta (8N),
+// dual (24N, ping-pong), x (8N), spectral work (16N), Lambda (16N).
+struct vsr_tv {
+    vsr_ctx* ctx = nullptr;
+    Spec sp;
+    FoldGeom G;
+    double lambda = 0, mu = 0, rel_tol = 0, tau = 0;
+    size_t max_iters = 0;
+    DevBuf<double2> lam, Yl, W;
+    DevBuf<double> x, xprev, theta, dualA, dualB;
+    DevBuf<double> tnr, tnc, tns;
+    DevBuf<double> fitp, stp, resp;
+    DevBuf<unsigned long long> bad;
+    DevBuf<double> obj, res, rel, status, init_obj;
+    size_t fit_blocks = 0, st_blocks = 0, res_blocks = 0;
+    size_t iters_done = 0;
+    bool dual_in_a = true;
+    bool stopped = false;
+    std::chrono::steady_clock::time_point t0;
+};
+
+static void tv_validate(const vsr_tv_config* cfg) {
+    if (!cfg) throw std::invalid_argument("admm_tv: null config");
+    require_positive(cfg->lambda, "lambda");  // solvers.cpp:323-326
+    require_positive(cfg->mu, "mu");
+    if (cfg->max_iters < 1) throw std::invalid_argument("admm_tv: max_iters must be >= 1");
+}
+
+static vsr_tv* tv_build(vsr_ctx* ctx, const Spec& sp, const double* y_dev, const double* psf_dev,
+                        const vsr_tv_config* cfg, const double* init_dev) {
+    auto t0 = std::chrono::steady_clock::now();
+    auto* h = new vsr_tv();
+    try {
+        h->ctx = ctx;
+        h->sp = sp;
+        h->t0 = t0;
+        h->G = make_geom(sp.hr, sp.rates);
+        h->lambda = cfg->lambda;
+        h->mu = cfg->mu;
+        h->rel_tol = cfg->rel_tol;
+        h->max_iters = cfg->max_iters;
+        h->tau = cfg->has_tau ? cfg->tau : 1e-8 * cfg->mu;  // solvers.cpp:332
+        validate_tau(h->tau);
+        const Dims& hr = sp.hr;
+        const size_t N = hr.count(), Nl = sp.lr.count();
+        cudaStream_t st = ctx->stream;
+        h->lam.alloc(N);
+        h->Yl.alloc(Nl);
+        h->W.alloc(N);
+        h->x.alloc(N);
+        if (h->rel_tol > 0.0) h->xprev.alloc(N);
+        h->theta.alloc(N);
+        h->dualA.alloc(3 * N);
+        h->dualB.alloc(3 * N);
+        const auto nr = diff_norm_table(hr.m), nc = diff_norm_table(hr.n), ns = diff_norm_table(hr.s);
+        h->tnr.alloc(hr.m);
+        h->tnc.alloc(hr.n);
+        h->tns.alloc(hr.s);
+        h2d(ctx, h->tnr.p, nr.data(), h->tnr.bytes());
+        h2d(ctx, h->tnc.p, nc.data(), h->tnc.bytes());
+        h2d(ctx, h->tns.p, ns.data(), h->tns.bytes());
+        h->fit_blocks = tv_fold_blocks(h->G);
+        h->st_blocks = stencil_geom(hr).blocks();
+        h->res_blocks = fft_engine().inverse_final_blocks(hr);
+        h->fitp.alloc(std::max<size_t>(h->fit_blocks, 1));
+        h->stp.alloc(kStencilVals * h->st_blocks);
+        h->resp.alloc(2 * std::max<size_t>(h->res_blocks, 1));
+        h->bad.alloc(1);
+        h->obj.alloc(h->max_iters);
+        h->res.alloc(h->max_iters);
+        h->rel.alloc(h->max_iters);
+        h->status.alloc(4);
+        h->init_obj.alloc(1);
+        const double st_init[4] = {-1.0, 0.0, 0.0, 0.0};
+        h2d(ctx, h->status.p, st_init, sizeof(st_init));
+        VSR_CUDA(cudaMemsetAsync(h->bad.p, 0xff, sizeof(unsigned long long), st));
+
+        // precompute (solvers.cpp:336-344): Lambda = DFT(psf); LR spectrum of y
+        fft_engine().forward3(hr, psf_dev, IN_REAL, h->lam.p, 1.0, st);
+        fft_engine().forward3(sp.lr, y_dev, IN_REAL, h->Yl.p, inv_sqrt_count(sp.lr), st);
+        g_fwd += 2;
+        // init (solvers.cpp:346-354)
+        if (cfg->init == VSR_INIT_ZERO) {
+            VSR_CUDA(cudaMemsetAsync(h->x.p, 0, h->x.bytes(), st));
+        } else if (cfg->init == VSR_INIT_UPSAMPLED) {
+            launch_nn_upsample(hr, sp.rates, y_dev, h->x.p, st);
+        } else if (cfg->init == VSR_INIT_PROVIDED) {
+            if (!init_dev) throw shape_error("admm_tv: init volume: dims mismatch");
+            VSR_CUDA(cudaMemcpyAsync(h->x.p, init_dev, h->x.bytes(), cudaMemcpyDeviceToDevice, st));
+        } else {
+            throw std::invalid_argument("admm_tv: unknown init mode");
+        }
+        // u0 = L x0, dual0 = 0 (:356-358) -> theta for iteration 1; TV(x0)
+        launch_tv_stencil(hr, true, h->x.p, nullptr, h->dualA.p, h->theta.p, h->lambda / h->mu,
+                          nullptr, h->stp.p, st);
+        // initial objective (:361): data term by LR Parseval from fft3(x0)
+        fft_engine().forward3(hr, h->x.p, IN_REAL, h->W.p, inv_sqrt_count(hr), st);
+        ++g_fwd;
+        launch_fit_partials(h->G, h->Yl.p, h->lam.p, h->W.p, h->fitp.p, st);
+        TvIterScalars sc{h->obj.p, h->res.p, h->rel.p, h->status.p};
+        launch_tv_finalize(0, h->fitp.p, h->fit_blocks, h->stp.p, h->st_blocks, nullptr, 0,
+                           h->lambda, 1e-8, sc, h->init_obj.p, st);
+    } catch (...) {
+        delete h;
+        throw;
+    }
+    return h;
+}
+
+static void tv_step(vsr_tv* h) {
+    cudaStream_t st = h->ctx->stream;
+    const Dims& hr = h->sp.hr;
+    const double s = inv_sqrt_count(hr);
+    // theta_hat = fft3(theta); k_hat = data_hat + mu theta_hat (:374-375), folded x-update (:376)
+    Profiler* prof = h->ctx->prof();
+    fft_engine().forward3(hr, h->theta.p, IN_REAL, h->W.p, s, st, prof);
+    GammaTables tabs{h->tnr.p, h->tnc.p, h->tns.p, h->tau};
+    {
+        ProfScope ps(prof, "tv_fold", st);
+        launch_tv_fold(h->G, h->Yl.p, h->lam.p, h->W.p, h->W.p, nullptr, tabs, h->mu, h->fitp.p, st);
+    }
+    if (h->rel_tol > 0.0) std::swap(h->x, h->xprev);  // x_prev = x (:364)
+    PassReduce red{h->resp.p, h->bad.p};
+    fft_engine().inverse3(hr, h->W.p, h->x.p, OUT_REAL, s, &red, st, prof);
+    g_fwd += 1;
+    g_inv += 1;
+    double* din = h->dual_in_a ? h->dualA.p : h->dualB.p;
+    double* dout = h->dual_in_a ? h->dualB.p : h->dualA.p;
+    // shrink / dual / residual (:379-393) and theta for the next iteration (:367-373)
+    {
+        ProfScope ps(prof, "tv_stencil", st);
+        launch_tv_stencil(hr, false, h->x.p, din, dout, h->theta.p, h->lambda / h->mu,
+                          h->rel_tol > 0.0 ? h->xprev.p : nullptr, h->stp.p, st);
+    }
+    h->dual_in_a = !h->dual_in_a;
+    TvIterScalars sc{h->obj.p, h->res.p, h->rel.p, h->status.p};
+    {
+        ProfScope ps(prof, "tv_finalize", st);
+        launch_tv_finalize((int)h->iters_done, h->fitp.p, h->fit_blocks, h->stp.p, h->st_blocks,
+                           h->resp.p, h->res_blocks, h->lambda, 1e-8, sc, nullptr, st);
+    }
+    ++h->iters_done;
+}
+
+static void tv_iterate(vsr_tv* h, size_t iters) {
+    for (size_t k = 0; k < iters && !h->stopped && h->iters_done < h->max_iters; ++k) {
+        tv_step(h);
+        if (h->rel_tol > 0.0) {  // stop test (:405) needs the scalar now
+            double rc = 0.0;
+            d2h(h->ctx, &rc, h->rel.p + (h->iters_done - 1), sizeof(double));
+            sync(h->ctx);
+            if (rc < h->rel_tol) h->stopped = true;
+        }
+    }
+}
+
+static void tv_fill_report(vsr_tv* h, vsr_report* rep, const char* where) {
+    double status[4];
+    unsigned long long bad = 0;
+    d2h(h->ctx, status, h->status.p, sizeof(status));
+    d2h(h->ctx, &bad, h->bad.p, sizeof(bad));
+    double init_obj = 0.0;
+    d2h(h->ctx, &init_obj, h->init_obj.p, sizeof(double));
+    sync(h->ctx);
+    if (status[0] >= 0.0) throw numeric_error(residue_message(status[1], 1e-8));
+    if (bad != ULLONG_MAX)
+        throw numeric_error(std::string(where) + ": non-finite value at flat index " + std::to_string(bad));
+    if (rep) {
+        rep->iterations = h->iters_done;
+        rep->initial_objective = init_obj;
+        if (rep->objective) d2h(h->ctx, rep->objective, h->obj.p, h->iters_done * sizeof(double));
+        if (rep->primal_residual)
+            d2h(h->ctx, rep->primal_residual, h->res.p, h->iters_done * sizeof(double));
+        sync(h->ctx);
+        rep->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - h->t0).count();
+    }
+}
+
+int vsr_admm_tv(vsr_ctx* ctx, const size_t hr_dims[3], const size_t rates[3], const double* y_r,
+                const double* psf_r, const vsr_tv_config* cfg, double* x_r, vsr_report* report) {
+    return guarded([&] {
+        require_ctx(ctx);
+        const Spec sp = make_spec(hr_dims, rates);
+        tv_validate(cfg);
+        require_nonempty(sp.hr, "fft3");
+        vsr_ctx::Guard g(ctx->device);
+        const size_t N = sp.hr.count(), Nl = sp.lr.count();
+        DevBuf<double> dy(Nl), dpsf(N), dinit;
+        h2d(ctx, dy.p, y_r, dy.bytes());
+        h2d(ctx, dpsf.p, psf_r, dpsf.bytes());
+        if (cfg->init == VSR_INIT_PROVIDED) {
+            if (!cfg->init_volume) throw shape_error("admm_tv: init volume: dims mismatch");
+            dinit.alloc(N);
+            h2d(ctx, dinit.p, cfg->init_volume, dinit.bytes());
+        }
+        vsr_tv* h = tv_build(ctx, sp, dy.p, dpsf.p, cfg, dinit.p);
+        try {
+            tv_iterate(h, h->max_iters);
+            tv_fill_report(h, report, "admm_tv");
+            d2h(ctx, x_r, h->x.p, h->x.bytes());
+            sync(ctx);
+            if (report) report->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - h->t0).count();
+        } catch (...) {
+            delete h;
+            throw;
+        }
+        delete h;
+    });
+}
+
+int vsr_tv_create_d(vsr_ctx* ctx, const size_t hr_dims[3], const size_t rates[3],
+                    const double* y_r_dev, const double* psf_r_dev, const vsr_tv_config* cfg,
+                    vsr_tv** out) {
+    return guarded([&] {
+        require_ctx(ctx);
+        const Spec sp = make_spec(hr_dims, rates);
+        tv_validate(cfg);
+        require_nonempty(sp.hr, "fft3");
+        vsr_ctx::Guard g(ctx->device);
+        *out = tv_build(ctx, sp, y_r_dev, psf_r_dev, cfg, cfg->init_volume);
+    });
+}
+
+int vsr_tv_iterate_d(vsr_tv* h, size_t iters) {
+    return guarded([&] {
+        vsr_ctx::Guard g(h->ctx->device);
+        tv_iterate(h, iters);
+    });
+}
+
+int vsr_tv_x_d(vsr_tv* h, const double** x_dev) {
+    return guarded([&] { *x_dev = h->x.p; });
+}
+
+int vsr_tv_report(vsr_tv* h, vsr_report* report) {
+    return guarded([&] {
+        vsr_ctx::Guard g(h->ctx->device);
+        tv_fill_report(h, report, "admm_tv");
+    });
+}
+
+int vsr_tv_destroy(vsr_tv* h) {
+    return guarded([&] {
+        if (!h) return;
+        vsr_ctx::Guard g(h->ctx->device);
+        cudaStreamSynchronize(h->ctx->stream);
+        delete h;
+    });
+}
+
+int vsr_launch_count(uint64_t* out) {
+    if (out) *out = g_launches.load(std::memory_order_relaxed);
+    return VSR_OK;
+}
+
+int vsr_profile_enable(vsr_ctx* ctx, int enable) {
+    return guarded([&] {
+        require_ctx(ctx);
+        ctx->profiling = enable != 0;
+    });
+}
+
+int vsr_profile_read(vsr_ctx* ctx, int max_stages, char* names, size_t name_len, double* total_ms,
+                     uint64_t* launches, int* n_stages) {
+    return guarded([&] {
+        require_ctx(ctx);
+        vsr_ctx::Guard g(ctx->device);
+        auto agg = ctx->profiler.drain();
+        int n = 0;
+        for (auto& a : agg) {
+            if (n >= max_stages) break;
+            std::strncpy(names + (size_t)n * name_len, a.first.c_str(), name_len - 1);
+            names[(size_t)n * name_len + name_len - 1] = 0;
+            total_ms[n] = a.second.first;
+            launches[n] = a.second.second;
+            ++n;
+        }
+        *n_stages = n;
+    });
+}
+
+double vsr_tv_algorithmic_bytes(const size_t hr_dims[3], const size_t rates[3]) {
+    const double N = (double)hr_dims[0] * hr_dims[1] * hr_dims[2];
+    const double d = (double)rates[0] * rates[1] * rates[2];
+    return (160.0 + 16.0 / d) * N;
+}
+
+}  // extern "C"

@@ -1,0 +1,539 @@
+// fp64 3D FFT engine, sm_100a.  See fft.cuh for the design summary.
+//
+// Reference semantics reproduced (proj/src/fft.cpp):
+//   * forward = sign -1 (FFTW_FORWARD), inverse = sign +1 (:57,67,76);
+//   * axis 1 (m) is the fastest-varying (FFTW's last dimension, :32-38);
+//   * unitary scaling 1/sqrt(N) applied after the transform (:68-69,77-78);
+//   * ifft3_real reduces sum(imag^2) and sum(|z|^2) for the residue check (:84-93).
+#include <climits>
+#include <cmath>
+
+#include "fft.cuh"
+
+namespace vsr {
+namespace {
+
+// ------------------------------------------------------------ register DFTs
+__device__ constexpr double kC8[8] = {1.0,
+                                               0.9807852804032304,
+                                               0.9238795325112867,
+                                               0.8314696123025452,
+                                               0.7071067811865476,
+                                               0.5555702330196022,
+                                               0.3826834323650898,
+                                               0.19509032201612828};
+
+// exp(-+2 pi i k / 32) * v, k in [0, 16); k is a compile-time constant after
+// unrolling so every branch below folds away.
+template <bool INV>
+__device__ __forceinline__ double2 twiddle32(double2 v, int k) {
+    if (k == 0) return v;
+    if (k == 8) return INV ? make_double2(-v.y, v.x) : make_double2(v.y, -v.x);
+    double c, s;  // cos, sin of 2*pi*k/32
+    if (k < 8) {
+        c = kC8[k];
+        s = kC8[8 - k];
+    } else {
+        c = -kC8[16 - k];
+        s = kC8[k - 8];
+    }
+    // forward: v * (c - i s); inverse: v * (c + i s)
+    if (INV) return make_double2(v.x * c - v.y * s, v.y * c + v.x * s);
+    return make_double2(v.x * c + v.y * s, v.y * c - v.x * s);
+}
+
+template <int R>
+__host__ __device__ constexpr int bitrev(int i) {
+    int r = 0;
+    for (int b = 1; b < R; b <<= 1) {
+        r = (r << 1) | (i & 1);
+        i >>= 1;
+    }
+    return r;
+}
+
+// In-register radix-R DFT (R = 1..32, power of two), natural order in/out.
+template <int R, bool INV>
+__device__ __forceinline__ void dft_reg(double2* a) {
+    if constexpr (R > 1) {
+    double2 b[R];
+#pragma unroll
+    for (int i = 0; i < R; ++i) b[bitrev<R>(i)] = a[i];
+#pragma unroll
+    for (int h = 1; h < R; h <<= 1) {
+#pragma unroll
+        for (int i = 0; i < R; i += 2 * h) {
+#pragma unroll
+            for (int j = 0; j < h; ++j) {
+                const double2 u = b[i + j];
+                const double2 t = twiddle32<INV>(b[i + j + h], j * (16 / h));
+                b[i + j] = cadd(u, t);
+                b[i + j + h] = csub(u, t);
+            }
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < R; ++i) a[i] = b[i];
+    }
+}
+
+__host__ __device__ constexpr int ilog2(int v) { return v <= 1 ? 0 : 1 + ilog2(v >> 1); }
+
+// ------------------------------------------------------------ pass kernel
+// Kernel shape: a CTA owns NL = TG * T lines of length L.  Each line is served
+// by P = L / R threads, each holding R elements in registers.
+//   CONTIG = true : axis 1; lines are contiguous, lanes run along a line.
+//   CONTIG = false: strided axis; a tile is T consecutive inner indices, lanes
+//                   run across the tile so HBM rows are T * 16 B.
+// Stockham stages: k = log_R(L) radix-R stages, then an optional final radix
+// RL < R stage (each thread then does R / RL butterflies).
+template <int L, int R, int T, int TG, bool CONTIG>
+struct PassShape {
+    static constexpr int P = L / R;
+    static constexpr int NL = TG * T;
+    static constexpr int THREADS = NL * P;
+    static constexpr int LOGL = ilog2(L), LOGR = ilog2(R);
+    static constexpr int K = LOGL / LOGR;                // full radix-R stages
+    static constexpr int RL = 1 << (LOGL - K * LOGR);   // final small radix (1 = none)
+    static constexpr int NSTAGE = K + (RL > 1 ? 1 : 0);
+    static constexpr int LPAD = CONTIG ? (L + L / R) : L;  // smem line pitch (contig)
+    static constexpr int SMEM_ELEMS = NSTAGE > 1 ? NL * LPAD : 0;
+    __device__ static __forceinline__ int sidx(int ls, int q) {
+        if constexpr (CONTIG)
+            return ls * LPAD + q + q / R;
+        else
+            return (ls / T) * (L * T) + q * T + (ls % T);
+    }
+};
+
+template <int L, int R, int T, int TG, bool CONTIG, bool INV, int IK, int OK>
+__global__ void __launch_bounds__(PassShape<L, R, T, TG, CONTIG>::THREADS)
+    fft_pass_kernel(const void* in_, void* out_, long long S,
+                    long long nlines_or_tiles, const double2* __restrict__ tw, double scale,
+                    double* __restrict__ partials, unsigned long long* __restrict__ bad_index) {
+    using Sh = PassShape<L, R, T, TG, CONTIG>;
+    constexpr int P = Sh::P;
+    extern __shared__ double2 sm[];
+
+    const int tid = threadIdx.x;
+    int ls, t;  // line slot in CTA, thread index within its line
+    long long base;
+    long long estride;
+    bool active;
+    if constexpr (CONTIG) {
+        ls = tid / P;
+        t = tid % P;
+        const long long line = (long long)blockIdx.x * Sh::NL + ls;
+        active = line < nlines_or_tiles;
+        base = line * L;
+        estride = 1;
+    } else {
+        const int g = tid / (T * P);
+        const int rem = tid % (T * P);
+        const int lt = rem % T;
+        t = rem / T;
+        ls = g * T + lt;
+        const long long tile = (long long)blockIdx.x * TG + g;
+        active = tile < nlines_or_tiles;
+        const long long tiles_per_o = S / T;
+        const long long o = active ? tile / tiles_per_o : 0;
+        const long long p0 = active ? (tile % tiles_per_o) * T : 0;
+        base = p0 + lt + S * (long long)L * o;
+        estride = S;
+    }
+
+    double2 v[R];
+    // ---- load: first stage (radix R, Ns = 1) reads q = t + P * r
+    if (active) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const long long off = base + estride * (long long)(t + P * r);
+            if constexpr (IK == IN_REAL) {
+                v[r] = make_double2(reinterpret_cast<const double*>(in_)[off], 0.0);
+            } else {
+                v[r] = reinterpret_cast<const double2*>(in_)[off];
+            }
+        }
+    } else {
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[r] = make_double2(0.0, 0.0);
+    }
+
+    int Ns = 1;
+#pragma unroll
+    for (int stage = 0; stage < Sh::NSTAGE; ++stage) {
+        const bool last = stage == Sh::NSTAGE - 1;
+        const int RS = (stage < Sh::K) ? R : Sh::RL;
+        const int NB = R / RS;  // butterflies per thread
+        // -- twiddle + butterfly for each of this thread's butterflies
+#pragma unroll
+        for (int vv = 0; vv < NB; ++vv) {
+            const int u = t + P * vv;
+            const int k = u & (Ns - 1);
+            if (stage > 0) {
+                const int tstride = L / (Ns * RS);
+#pragma unroll
+                for (int r = 1; r < R; ++r) {
+                    if (r < RS) {
+                        const double2 w = __ldg(tw + ((r * k * tstride) & (L - 1)));
+                        const double2 a = v[vv * RS + r];
+                        v[vv * RS + r] = INV ? cmulc(w, a) : cmul(w, a);
+                    }
+                }
+            }
+            if (RS == R)
+                dft_reg<R, INV>(v);
+            else if (RS == Sh::RL)
+                dft_reg<(Sh::RL > 1 ? Sh::RL : 1), INV>(v + vv * RS);
+        }
+        if (!last) {
+            // -- Stockham store to smem, then gather next stage inputs
+#pragma unroll
+            for (int vv = 0; vv < NB; ++vv) {
+                const int u = t + P * vv;
+                const int k = u & (Ns - 1);
+                const int ob = (u - k) * RS + k;
+#pragma unroll
+                for (int r = 0; r < R; ++r)
+                    if (r < RS) sm[Sh::sidx(ls, ob + r * Ns)] = v[vv * RS + r];
+            }
+            __syncthreads();
+            Ns *= RS;
+            const int RSn = (stage + 1 < Sh::K) ? R : Sh::RL;
+            const int NBn = R / RSn;
+#pragma unroll
+            for (int vv = 0; vv < NBn; ++vv) {
+                const int u = t + P * vv;
+#pragma unroll
+                for (int r = 0; r < R; ++r)
+                    if (r < RSn) v[vv * RSn + r] = sm[Sh::sidx(ls, u + (L / RSn) * r)];
+            }
+            __syncthreads();
+        } else {
+            Ns *= RS;
+        }
+    }
+
+    // ---- store: last stage wrote q = u + (L / RS_last) * r, u = t + P * vv
+    constexpr int RSL = (Sh::RL > 1) ? Sh::RL : R;
+    constexpr int NBL = R / RSL;
+    double acc_im = 0.0, acc_tot = 0.0;
+    if (active) {
+#pragma unroll
+        for (int vv = 0; vv < NBL; ++vv) {
+#pragma unroll
+            for (int r = 0; r < RSL; ++r) {
+                const int q = t + P * vv + (L / RSL) * r;
+                const long long off = base + estride * (long long)q;
+                double2 z = cscale(v[vv * RSL + r], scale);
+                if constexpr (OK == OUT_REAL) {
+                    acc_im += z.y * z.y;
+                    acc_tot += z.x * z.x + z.y * z.y;
+                    reinterpret_cast<double*>(out_)[off] = z.x;
+                    if (!isfinite(z.x)) atomicMin(bad_index, (unsigned long long)off);
+                } else {
+                    reinterpret_cast<double2*>(out_)[off] = z;
+                }
+            }
+        }
+    }
+    if constexpr (OK == OUT_REAL) {
+        __shared__ double red[64];
+        double vals[2] = {acc_im, acc_tot};
+        block_reduce_sum<2>(vals, red);
+        if (tid == 0) {
+            partials[2 * blockIdx.x] = vals[0];
+            partials[2 * blockIdx.x + 1] = vals[1];
+        }
+    }
+}
+
+// ------------------------------------------------------------ generic DFT
+// Direct O(L) per output DFT along one axis for any L (non powers of two,
+// L = 1, and strided shapes the tiled kernel cannot cover).  One thread per
+// output element.
+template <bool INV, int IK, int OK>
+__global__ void __launch_bounds__(256)
+    dft_direct_kernel(const void* __restrict__ in_, void* __restrict__ out_, long long S,
+                      long long L, long long total, const double2* __restrict__ tw,
+                      double scale, double* __restrict__ partials,
+                      unsigned long long* __restrict__ bad_index) {
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    double acc_im = 0.0, acc_tot = 0.0;
+    if (e < total) {
+        const long long p = e % S;
+        const long long q = (e / S) % L;
+        const long long o = e / (S * L);
+        const long long base = p + S * L * o;
+        double2 acc = make_double2(0.0, 0.0);
+        long long idx = 0;  // (j * q) mod L
+        for (long long j = 0; j < L; ++j) {
+            double2 x;
+            if constexpr (IK == IN_REAL)
+                x = make_double2(reinterpret_cast<const double*>(in_)[base + S * j], 0.0);
+            else
+                x = reinterpret_cast<const double2*>(in_)[base + S * j];
+            const double2 w = tw[idx];
+            const double2 prod = INV ? cmulc(w, x) : cmul(w, x);
+            acc = cadd(acc, prod);
+            idx += q;
+            if (idx >= L) idx -= L;
+        }
+        acc = cscale(acc, scale);
+        if constexpr (OK == OUT_REAL) {
+            acc_im = acc.y * acc.y;
+            acc_tot = acc.x * acc.x + acc.y * acc.y;
+            reinterpret_cast<double*>(out_)[e] = acc.x;
+            if (!isfinite(acc.x)) atomicMin(bad_index, (unsigned long long)e);
+        } else {
+            reinterpret_cast<double2*>(out_)[e] = acc;
+        }
+    }
+    if constexpr (OK == OUT_REAL) {
+        __shared__ double red[64];
+        double vals[2] = {acc_im, acc_tot};
+        block_reduce_sum<2>(vals, red);
+        if (threadIdx.x == 0) {
+            partials[2 * blockIdx.x] = vals[0];
+            partials[2 * blockIdx.x + 1] = vals[1];
+        }
+    }
+}
+
+// ------------------------------------------------------------ dispatch
+template <int L>
+struct LCfg {
+    static constexpr int R = L < 16 ? L : 16;
+    static constexpr int P = L / R;
+    // strided tile width and tiles per CTA (>= 128 threads per CTA)
+    static constexpr int TS = L >= 1024 ? 4 : 8;
+    static constexpr int TGS = (TS * P) >= 128 ? 1 : (128 / (TS * P));
+    // contiguous: lines per CTA
+    static constexpr int TGC = P >= 128 ? 1 : (128 / P);
+};
+
+struct Launch {
+    dim3 grid, block;
+    size_t smem;
+};
+
+template <int L, bool CONTIG>
+Launch pass_geometry(long long S, long long lines_or_tiles) {
+    using C = LCfg<L>;
+    constexpr int T = CONTIG ? 1 : C::TS;
+    constexpr int TG = CONTIG ? C::TGC : C::TGS;
+    using Sh = PassShape<L, C::R, T, TG, CONTIG>;
+    Launch g;
+    g.block = dim3(Sh::THREADS);
+    g.grid = dim3((unsigned)((lines_or_tiles + TG - 1) / TG));
+    g.smem = (size_t)Sh::SMEM_ELEMS * sizeof(double2);
+    return g;
+}
+
+template <int L, bool CONTIG, bool INV, int IK, int OK>
+void launch_pass(long long S, long long units, const void* in, void* out, const double2* tw,
+                 double scale, const PassReduce* red, cudaStream_t st) {
+    using C = LCfg<L>;
+    constexpr int T = CONTIG ? 1 : C::TS;
+    constexpr int TG = CONTIG ? C::TGC : C::TGS;
+    auto kern = fft_pass_kernel<L, C::R, T, TG, CONTIG, INV, IK, OK>;
+    Launch g = pass_geometry<L, CONTIG>(S, units);
+    if (g.smem > 48 * 1024) {
+        VSR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)g.smem));
+    }
+    kern<<<g.grid, g.block, g.smem, st>>>(in, out, S, units, tw, scale,
+                                          red ? red->partials : nullptr,
+                                          red ? red->bad_index : nullptr);
+    VSR_LAUNCH_CHECK();
+}
+
+template <bool CONTIG, bool INV, int IK, int OK>
+bool dispatch_L(size_t L, long long S, long long units, const void* in, void* out,
+                const double2* tw, double scale, const PassReduce* red, cudaStream_t st) {
+    switch (L) {
+#define VSR_CASE(LL)                                                                       \
+    case LL:                                                                               \
+        launch_pass<LL, CONTIG, INV, IK, OK>(S, units, in, out, tw, scale, red, st);       \
+        return true;
+        VSR_CASE(2)
+        VSR_CASE(4)
+        VSR_CASE(8)
+        VSR_CASE(16)
+        VSR_CASE(32)
+        VSR_CASE(64)
+        VSR_CASE(128)
+        VSR_CASE(256)
+        VSR_CASE(512)
+        VSR_CASE(1024)
+        VSR_CASE(2048)
+#undef VSR_CASE
+        default:
+            return false;
+    }
+}
+
+template <bool CONTIG>
+long long pass_units(size_t L, long long S, long long total) {
+    if (CONTIG) return total / (long long)L;
+    const size_t TS = L >= 1024 ? 4 : 8;
+    return total / ((long long)TS * (long long)L);  // tiles of TS whole lines
+}
+
+size_t blocks_for(size_t L, bool contig, long long units) {
+    size_t P = L < 16 ? 1 : L / 16;
+    size_t TS = L >= 1024 ? 4 : 8;
+    size_t tg;
+    if (contig)
+        tg = P >= 128 ? 1 : 128 / P;
+    else
+        tg = (TS * P) >= 128 ? 1 : 128 / (TS * P);
+    return (size_t)((units + (long long)tg - 1) / (long long)tg);
+}
+
+bool tiled_ok(size_t L, int axis, long long S) {
+    if (L < 2 || L > 2048 || !is_pow2(L)) return false;
+    if (axis == 0) return true;
+    const long long TS = L >= 1024 ? 4 : 8;
+    return S % TS == 0;
+}
+
+}  // namespace
+
+FftEngine& fft_engine() {
+    static FftEngine eng;
+    return eng;
+}
+
+const double2* FftEngine::twiddles(size_t L) {
+    int dev = 0;
+    VSR_CUDA(cudaGetDevice(&dev));
+    const size_t key = ((size_t)dev << 40) | L;
+    std::lock_guard<std::mutex> lock(mu_);
+    auto it = tw_.find(key);
+    if (it != tw_.end()) return it->second;
+    std::vector<double2> h(L);
+    for (size_t j = 0; j < L; ++j) {
+        // long double argument reduction keeps every entry correctly rounded
+        // for the table sizes used here.
+        const long double ang = 2.0L * 3.141592653589793238462643383279502884L *
+                                (long double)j / (long double)L;
+        h[j] = make_double2((double)cosl(ang), (double)-sinl(ang));
+    }
+    double2* d = nullptr;
+    VSR_CUDA(cudaMalloc(&d, L * sizeof(double2)));
+    VSR_CUDA(cudaMemcpy(d, h.data(), L * sizeof(double2), cudaMemcpyHostToDevice));
+    tw_[key] = d;
+    return d;
+}
+
+static void axis_geometry(const Dims& d, int axis, long long& S, long long& L, long long& total) {
+    total = (long long)d.count();
+    L = (long long)d.len(axis);
+    S = axis == 0 ? 1 : (axis == 1 ? (long long)d.m : (long long)(d.m * d.n));
+}
+
+size_t FftEngine::pass_blocks(const Dims& d, int axis) const {
+    long long S, L, total;
+    axis_geometry(d, axis, S, L, total);
+    if (tiled_ok((size_t)L, axis, S)) {
+        const long long units = axis == 0 ? pass_units<true>(L, S, total)
+                                          : pass_units<false>(L, S, total);
+        return blocks_for((size_t)L, axis == 0, units);
+    }
+    return (size_t)((total + 255) / 256);
+}
+
+void FftEngine::axis_pass(const Dims& d, int axis, bool inverse, const void* in, InKind ik,
+                          void* out, OutKind ok, double scale, const PassReduce* red,
+                          cudaStream_t st) {
+    long long S, L, total;
+    axis_geometry(d, axis, S, L, total);
+    if (total == 0) return;
+    const double2* tw = twiddles((size_t)L);
+    if (tiled_ok((size_t)L, axis, S)) {
+        bool done = false;
+        if (axis == 0) {
+            const long long units = pass_units<true>(L, S, total);
+            if (!inverse) {
+                if (ik == IN_REAL && ok == OUT_COMPLEX)
+                    done = dispatch_L<true, false, IN_REAL, OUT_COMPLEX>(L, S, units, in, out, tw, scale, red, st);
+                else if (ik == IN_COMPLEX && ok == OUT_COMPLEX)
+                    done = dispatch_L<true, false, IN_COMPLEX, OUT_COMPLEX>(L, S, units, in, out, tw, scale, red, st);
+            } else {
+                if (ik == IN_COMPLEX && ok == OUT_REAL)
+                    done = dispatch_L<true, true, IN_COMPLEX, OUT_REAL>(L, S, units, in, out, tw, scale, red, st);
+                else if (ik == IN_COMPLEX && ok == OUT_COMPLEX)
+                    done = dispatch_L<true, true, IN_COMPLEX, OUT_COMPLEX>(L, S, units, in, out, tw, scale, red, st);
+            }
+        } else if (ik == IN_COMPLEX && ok == OUT_COMPLEX) {
+            const long long units = pass_units<false>(L, S, total);
+            done = inverse ? dispatch_L<false, true, IN_COMPLEX, OUT_COMPLEX>(L, S, units, in, out, tw, scale, red, st)
+                           : dispatch_L<false, false, IN_COMPLEX, OUT_COMPLEX>(L, S, units, in, out, tw, scale, red, st);
+        }
+        if (done) return;
+    }
+    // Generic direct DFT.  Out-of-place only: stage through a temporary when
+    // the caller asked for an in-place pass.
+    void* dst = out;
+    void* tmp = nullptr;
+    const size_t out_bytes = (size_t)total * (ok == OUT_REAL ? sizeof(double) : sizeof(double2));
+    if (in == out) {
+        VSR_CUDA(cudaMallocAsync(&tmp, out_bytes, st));
+        dst = tmp;
+    }
+    const unsigned blocks = (unsigned)((total + 255) / 256);
+    double* part = red ? red->partials : nullptr;
+    unsigned long long* bad = red ? red->bad_index : nullptr;
+#define VSR_DIRECT(INV, IK, OK) \
+    dft_direct_kernel<INV, IK, OK><<<blocks, 256, 0, st>>>(in, dst, S, L, total, tw, scale, part, bad)
+    if (!inverse) {
+        if (ik == IN_REAL && ok == OUT_COMPLEX) VSR_DIRECT(false, IN_REAL, OUT_COMPLEX);
+        else if (ik == IN_COMPLEX && ok == OUT_COMPLEX) VSR_DIRECT(false, IN_COMPLEX, OUT_COMPLEX);
+        else throw std::logic_error("fft: unsupported forward pass kinds");
+    } else {
+        if (ik == IN_COMPLEX && ok == OUT_REAL) VSR_DIRECT(true, IN_COMPLEX, OUT_REAL);
+        else if (ik == IN_COMPLEX && ok == OUT_COMPLEX) VSR_DIRECT(true, IN_COMPLEX, OUT_COMPLEX);
+        else throw std::logic_error("fft: unsupported inverse pass kinds");
+    }
+#undef VSR_DIRECT
+    VSR_LAUNCH_CHECK();
+    if (tmp) {
+        VSR_CUDA(cudaMemcpyAsync(out, tmp, out_bytes, cudaMemcpyDeviceToDevice, st));
+        VSR_CUDA(cudaFreeAsync(tmp, st));
+    }
+}
+
+void FftEngine::forward3(const Dims& d, const void* in, InKind ik, double2* out, double scale,
+                         cudaStream_t st, Profiler* prof) {
+    {
+        ProfScope ps(prof, ik == IN_REAL ? "fft_fwd_axis1_r2c" : "fft_fwd_axis1", st);
+        axis_pass(d, 0, false, in, ik, out, OUT_COMPLEX, 1.0, nullptr, st);
+    }
+    {
+        ProfScope ps(prof, "fft_fwd_axis2", st);
+        axis_pass(d, 1, false, out, IN_COMPLEX, out, OUT_COMPLEX, 1.0, nullptr, st);
+    }
+    {
+        ProfScope ps(prof, "fft_fwd_axis3", st);
+        axis_pass(d, 2, false, out, IN_COMPLEX, out, OUT_COMPLEX, scale, nullptr, st);
+    }
+}
+
+void FftEngine::inverse3(const Dims& d, double2* in, void* out, OutKind ok, double scale,
+                         const PassReduce* red, cudaStream_t st, Profiler* prof) {
+    {
+        ProfScope ps(prof, "fft_inv_axis3", st);
+        axis_pass(d, 2, true, in, IN_COMPLEX, in, OUT_COMPLEX, 1.0, nullptr, st);
+    }
+    {
+        ProfScope ps(prof, "fft_inv_axis2", st);
+        axis_pass(d, 1, true, in, IN_COMPLEX, in, OUT_COMPLEX, 1.0, nullptr, st);
+    }
+    {
+        ProfScope ps(prof, ok == OUT_REAL ? "fft_inv_axis1_c2r" : "fft_inv_axis1", st);
+        axis_pass(d, 0, true, in, IN_COMPLEX, out, ok, scale, red, st);
+    }
+}
+
+}  // namespace vsr

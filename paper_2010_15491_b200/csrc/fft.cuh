@@ -1,0 +1,64 @@
+// Hand-written fp64 3D FFT engine for sm_100a (replaces FFTW3 in the
+// reference: proj/src/fft.cpp:21-101).
+//
+// A 3D transform is three axis passes.  Each pass is one kernel that moves a
+// tile of whole lines HBM -> registers, runs a Stockham radix-16/8/4/2
+// decomposition with warp-local register butterflies and shared-memory
+// exchanges between stages, and writes the tile back (in place or out of
+// place).  Axis 1 is contiguous (lines laid out back to back); axes 2 and 3
+// are strided and tiled T consecutive inner indices wide, so every HBM row
+// segment is T*16 bytes (128 B for T = 8).
+#pragma once
+
+#include <map>
+#include <mutex>
+#include <vector>
+
+#include "vsr_common.cuh"
+
+namespace vsr {
+
+enum InKind { IN_COMPLEX = 0, IN_REAL = 1 };
+enum OutKind { OUT_COMPLEX = 0, OUT_REAL = 1 };
+
+// Deterministic reduction slots written by a pass with OUT_REAL: per-block
+// partial sums of (imag^2, |z|^2) and the minimum flat index of a non-finite
+// real output (reference ifft3_real src/fft.cpp:84-93 and require_finite
+// src/volume.cpp:31-36).
+struct PassReduce {
+    double* partials = nullptr;               // 2 doubles per block
+    unsigned long long* bad_index = nullptr;  // atomicMin target (init ULLONG_MAX)
+};
+
+class FftEngine {
+public:
+    // Device twiddle table exp(-2*pi*i*j/L), j in [0, L), cached per L.
+    const double2* twiddles(size_t L);
+
+    // Number of thread blocks a pass launches (for sizing PassReduce partials).
+    size_t pass_blocks(const Dims& d, int axis) const;
+
+    // One pass along `axis` (0 = m, 1 = n, 2 = s).  in/out may alias (in-place).
+    // The result of the pass is multiplied by `scale`.
+    void axis_pass(const Dims& d, int axis, bool inverse, const void* in, InKind ik, void* out,
+                   OutKind ok, double scale, const PassReduce* red, cudaStream_t st);
+
+    // Forward 3D: pass order 1,2,3; first pass in -> out, then in place on out.
+    void forward3(const Dims& d, const void* in, InKind ik, double2* out, double scale,
+                  cudaStream_t st, Profiler* prof = nullptr);
+    // Inverse 3D: pass order 3,2,1; passes 3,2 run IN PLACE on `in` (clobbered),
+    // pass 1 writes `out` (complex or real + reduction).
+    void inverse3(const Dims& d, double2* in, void* out, OutKind ok, double scale,
+                  const PassReduce* red, cudaStream_t st, Profiler* prof = nullptr);
+
+    // Blocks of the final (axis-1) pass of inverse3.
+    size_t inverse_final_blocks(const Dims& d) const { return pass_blocks(d, 0); }
+
+private:
+    std::mutex mu_;
+    std::map<size_t, double2*> tw_;
+};
+
+FftEngine& fft_engine();
+
+}  // namespace vsr

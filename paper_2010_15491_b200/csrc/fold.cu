@@ -1,0 +1,404 @@
+// Spectral fold kernels.  One thread per LR frequency g; the d aliases of g
+// are visited in b_lin order (b_r fastest), which is the reference's
+// summation order (spectral.cpp:67-75: out[g] += block * v, b ascending).
+// For d <= 8 the per-alias operands stay in registers (one HBM read per
+// alias); for larger d a second sweep re-reads them (L2-resident: the CTA's
+// alias footprint is a few tens of KB).
+#include "fold.cuh"
+
+namespace vsr {
+
+FoldGeom make_geom(const Dims& hr, const int rates[3]) {
+    FoldGeom G;
+    G.m = (long long)hr.m;
+    G.n = (long long)hr.n;
+    G.s = (long long)hr.s;
+    G.dr = rates[0];
+    G.dc = rates[1];
+    G.ds = rates[2];
+    G.ml = G.m / G.dr;
+    G.nl = G.n / G.dc;
+    G.sl = G.s / G.ds;
+    G.d = G.dr * G.dc * G.ds;
+    return G;
+}
+
+namespace {
+
+constexpr int kFoldThreads = 128;
+
+struct LrPos {
+    long long g1, g2, g3;
+};
+
+__device__ __forceinline__ LrPos lr_pos(const FoldGeom& G, long long g) {
+    LrPos p;
+    p.g1 = g % G.ml;
+    const long long r = g / G.ml;
+    p.g2 = r % G.nl;
+    p.g3 = r / G.nl;
+    return p;
+}
+
+__device__ __forceinline__ long long alias_index(const FoldGeom& G, const LrPos& p, int b,
+                                                 long long* f1, long long* f2, long long* f3) {
+    const int br = b % G.dr;
+    const int bc = (b / G.dr) % G.dc;
+    const int bs = b / (G.dr * G.dc);
+    *f1 = p.g1 + br * G.ml;
+    *f2 = p.g2 + bc * G.nl;
+    *f3 = p.g3 + bs * G.sl;
+    return *f1 + G.m * (*f2 + G.n * *f3);
+}
+
+// ---------------------------------------------------------------- Tikhonov
+// k_b   = conj(L_b) * (Yl[g]/sqrt d) + (2 reg) * X̄_b        (solvers.cpp:53-54)
+// w     = (sum_b L_b k_b) / (sum_b |L_b|^2 + 2 reg d)     (:56-57, ctor :42-44)
+// x̂_b  = (k_b - conj(L_b) w) * (1/(2 reg))                (:58-62)
+template <int DC>
+__global__ void __launch_bounds__(kFoldThreads)
+    tik_fold_kernel(FoldGeom G, const double2* __restrict__ Yl, const double2* __restrict__ lam,
+                    const double2* __restrict__ xbh, double2* __restrict__ xh, double reg2,
+                    double shift, double inv2l, double invsqrtd) {
+    const long long Nl = G.ml * G.nl * G.sl;
+    const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= Nl) return;
+    const LrPos p = lr_pos(G, g);
+    const double2 yv = cscale(Yl[g], invsqrtd);
+    double2 S = make_double2(0.0, 0.0);
+    double gram = 0.0;
+    const int d = DC > 0 ? DC : G.d;
+    if constexpr (DC > 0) {
+        double2 Lc[DC], kc[DC];
+        long long fi[DC];
+#pragma unroll
+        for (int b = 0; b < DC; ++b) {
+            long long f1, f2, f3;
+            fi[b] = alias_index(G, p, b, &f1, &f2, &f3);
+            Lc[b] = __ldg(lam + fi[b]);
+        }
+#pragma unroll
+        for (int b = 0; b < DC; ++b) {
+            const double2 X = __ldg(xbh + fi[b]);
+            kc[b] = cadd(cmulc(Lc[b], yv), cscale(X, reg2));
+            S = cadd(S, cmul(Lc[b], kc[b]));
+            gram += cnorm(Lc[b]);
+        }
+        const double den = gram + shift;
+        const double2 w = make_double2(S.x / den, S.y / den);
+#pragma unroll
+        for (int b = 0; b < DC; ++b)
+            xh[fi[b]] = cscale(csub(kc[b], cmulc(Lc[b], w)), inv2l);
+    } else {
+        for (int b = 0; b < d; ++b) {
+            long long f1, f2, f3;
+            const long long f = alias_index(G, p, b, &f1, &f2, &f3);
+            const double2 L = __ldg(lam + f);
+            const double2 k = cadd(cmulc(L, yv), cscale(__ldg(xbh + f), reg2));
+            S = cadd(S, cmul(L, k));
+            gram += cnorm(L);
+        }
+        const double den = gram + shift;
+        const double2 w = make_double2(S.x / den, S.y / den);
+        for (int b = 0; b < d; ++b) {
+            long long f1, f2, f3;
+            const long long f = alias_index(G, p, b, &f1, &f2, &f3);
+            const double2 L = __ldg(lam + f);
+            const double2 k = cadd(cmulc(L, yv), cscale(__ldg(xbh + f), reg2));
+            xh[f] = cscale(csub(k, cmulc(L, w)), inv2l);
+        }
+    }
+}
+
+// ---------------------------------------------------------------- TV
+// k_b = conj(L_b) Yl/sqrt d + mu θ̂_b            (solvers.cpp:342-344,375)
+// ĝ_b = Γ_b k_b                                  (:223)
+// w   = (sum_b L_b ĝ_b) / (sum_b Γ_b|L_b|^2 + mu d)   (:225-226, :235-241)
+// x̂_b = (ĝ_b - (Γ_b conj(L_b)) w) / mu          (:227-231, spectral.cpp:110)
+template <int DC, bool GTAB, bool FIT>
+__global__ void __launch_bounds__(kFoldThreads)
+    tv_fold_kernel(FoldGeom G, const double2* __restrict__ Yl, const double2* __restrict__ lam,
+                   const double2* th, double2* xh, const double* __restrict__ gam,
+                   GammaTables tabs, double mu, double inv_mu, double shift, double invsqrtd,
+                   double* __restrict__ fit_partials) {
+    const long long Nl = G.ml * G.nl * G.sl;
+    const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    double fit = 0.0;
+    if (g < Nl) {
+        const LrPos p = lr_pos(G, g);
+        const double2 yraw = Yl[g];
+        const double2 yv = cscale(yraw, invsqrtd);
+        double2 S = make_double2(0.0, 0.0);
+        double gram = 0.0;
+        double2 acc = make_double2(0.0, 0.0);
+        auto gamma_at = [&](long long f, long long f1, long long f2, long long f3) -> double {
+            if constexpr (GTAB)
+                return 1.0 / (((__ldg(tabs.nr + f1) + __ldg(tabs.nc + f2)) + __ldg(tabs.ns + f3)) +
+                              tabs.tau);
+            else
+                return __ldg(gam + f);
+        };
+        if constexpr (DC > 0) {
+            double2 Lc[DC], gc[DC];
+            double Gm[DC];
+            long long fi[DC];
+#pragma unroll
+            for (int b = 0; b < DC; ++b) {
+                long long f1, f2, f3;
+                fi[b] = alias_index(G, p, b, &f1, &f2, &f3);
+                Lc[b] = __ldg(lam + fi[b]);
+                Gm[b] = gamma_at(fi[b], f1, f2, f3);
+            }
+#pragma unroll
+            for (int b = 0; b < DC; ++b) {
+                const double2 T = th[fi[b]];
+                const double2 k = cadd(cmulc(Lc[b], yv), cscale(T, mu));
+                gc[b] = cscale(k, Gm[b]);
+                S = cadd(S, cmul(Lc[b], gc[b]));
+                gram += Gm[b] * cnorm(Lc[b]);
+            }
+            const double den = gram + shift;
+            const double2 w = make_double2(S.x / den, S.y / den);
+#pragma unroll
+            for (int b = 0; b < DC; ++b) {
+                const double2 corr = cmul(make_double2(Gm[b] * Lc[b].x, -(Gm[b] * Lc[b].y)), w);
+                const double2 x = cscale(csub(gc[b], corr), inv_mu);
+                xh[fi[b]] = x;
+                if constexpr (FIT) acc = cadd(acc, cmul(Lc[b], x));
+            }
+        } else {
+            const int d = G.d;
+            for (int b = 0; b < d; ++b) {
+                long long f1, f2, f3;
+                const long long f = alias_index(G, p, b, &f1, &f2, &f3);
+                const double2 L = __ldg(lam + f);
+                const double Gb = gamma_at(f, f1, f2, f3);
+                const double2 k = cadd(cmulc(L, yv), cscale(th[f], mu));
+                const double2 gb = cscale(k, Gb);
+                S = cadd(S, cmul(L, gb));
+                gram += Gb * cnorm(L);
+            }
+            const double den = gram + shift;
+            const double2 w = make_double2(S.x / den, S.y / den);
+            for (int b = 0; b < d; ++b) {
+                long long f1, f2, f3;
+                const long long f = alias_index(G, p, b, &f1, &f2, &f3);
+                const double2 L = __ldg(lam + f);
+                const double Gb = gamma_at(f, f1, f2, f3);
+                const double2 k = cadd(cmulc(L, yv), cscale(th[f], mu));
+                const double2 gb = cscale(k, Gb);
+                const double2 corr = cmul(make_double2(Gb * L.x, -(Gb * L.y)), w);
+                const double2 x = cscale(csub(gb, corr), inv_mu);
+                xh[f] = x;
+                if constexpr (FIT) acc = cadd(acc, cmul(L, x));
+            }
+        }
+        if constexpr (FIT) {
+            const double2 r = csub(yraw, cscale(acc, invsqrtd));
+            fit = cnorm(r);
+        }
+    }
+    if constexpr (FIT) {
+        __shared__ double red[32];
+        double v[1] = {fit};
+        block_reduce_sum<1>(v, red);
+        if (threadIdx.x == 0) fit_partials[blockIdx.x] = v[0];
+    }
+}
+
+__global__ void __launch_bounds__(kFoldThreads)
+    fit_kernel(FoldGeom G, const double2* __restrict__ Yl, const double2* __restrict__ lam,
+               const double2* __restrict__ xh, double invsqrtd, double* __restrict__ partials) {
+    const long long Nl = G.ml * G.nl * G.sl;
+    const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    double fit = 0.0;
+    if (g < Nl) {
+        const LrPos p = lr_pos(G, g);
+        double2 acc = make_double2(0.0, 0.0);
+        for (int b = 0; b < G.d; ++b) {
+            long long f1, f2, f3;
+            const long long f = alias_index(G, p, b, &f1, &f2, &f3);
+            acc = cadd(acc, cmul(__ldg(lam + f), __ldg(xh + f)));
+        }
+        fit = cnorm(csub(Yl[g], cscale(acc, invsqrtd)));
+    }
+    __shared__ double red[32];
+    double v[1] = {fit};
+    block_reduce_sum<1>(v, red);
+    if (threadIdx.x == 0) partials[blockIdx.x] = v[0];
+}
+
+// ---------------------------------------------------------------- primitives
+__global__ void fold_apply_kernel(FoldGeom G, const double2* __restrict__ lam,
+                                  const double* __restrict__ wts, const double2* __restrict__ in,
+                                  double2* __restrict__ out) {
+    const long long Nl = G.ml * G.nl * G.sl;
+    const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= Nl) return;
+    const LrPos p = lr_pos(G, g);
+    double2 acc = make_double2(0.0, 0.0);
+    for (int b = 0; b < G.d; ++b) {
+        long long f1, f2, f3;
+        const long long f = alias_index(G, p, b, &f1, &f2, &f3);
+        double2 coef = lam ? lam[f] : make_double2(1.0, 0.0);
+        if (wts) coef = cscale(coef, wts[f]);  // (block * w) * v  (spectral.cpp:97)
+        acc = cadd(acc, lam || wts ? cmul(coef, in[f]) : in[f]);
+    }
+    out[g] = acc;
+}
+
+__global__ void fold_adjoint_kernel(FoldGeom G, const double2* __restrict__ lam,
+                                    const double* __restrict__ wts,
+                                    const double2* __restrict__ in, double2* __restrict__ out) {
+    const long long N = G.m * G.n * G.s;
+    const long long f = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (f >= N) return;
+    const long long f1 = f % G.m, f2 = (f / G.m) % G.n, f3 = f / (G.m * G.n);
+    const long long g = (f1 % G.ml) + G.ml * ((f2 % G.nl) + G.nl * (f3 % G.sl));
+    double2 v = in[g];
+    if (lam) {
+        double2 c = make_double2(lam[f].x, -lam[f].y);
+        if (wts) c = cscale(c, wts[f]);  // (w * conj(block)) * lr  (spectral.cpp:110)
+        v = cmul(c, v);
+    }
+    out[f] = v;
+}
+
+__global__ void gram_kernel(FoldGeom G, const double2* __restrict__ lam,
+                            const double* __restrict__ wts, double* __restrict__ out) {
+    const long long Nl = G.ml * G.nl * G.sl;
+    const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= Nl) return;
+    const LrPos p = lr_pos(G, g);
+    double acc = 0.0;
+    for (int b = 0; b < G.d; ++b) {
+        long long f1, f2, f3;
+        const long long f = alias_index(G, p, b, &f1, &f2, &f3);
+        const double nrm = cnorm(lam[f]);
+        acc += wts ? wts[f] * nrm : nrm;
+    }
+    out[g] = acc;
+}
+
+__global__ void swap_blocks_kernel(FoldGeom G, double2* lam) {
+    const long long Nl = G.ml * G.nl * G.sl;
+    const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= Nl) return;
+    const LrPos p = lr_pos(G, g);
+    long long f1, f2, f3;
+    const long long a = alias_index(G, p, 0, &f1, &f2, &f3);
+    const long long b = alias_index(G, p, 1, &f1, &f2, &f3);
+    const double2 t = lam[a];
+    lam[a] = lam[b];
+    lam[b] = t;
+}
+
+__global__ void __launch_bounds__(1024)
+    finalize_sum_kernel(const double* __restrict__ partials, int stride, int nvals,
+                        long long nblocks, double* __restrict__ out) {
+    __shared__ double red[32 * 4];
+    double v[4] = {0.0, 0.0, 0.0, 0.0};
+    for (long long i = threadIdx.x; i < nblocks; i += blockDim.x)
+        for (int k = 0; k < nvals; ++k) v[k] += partials[i * stride + k];
+    block_reduce_sum<4>(v, red);
+    if (threadIdx.x == 0)
+        for (int k = 0; k < nvals; ++k) out[k] = v[k];
+}
+
+unsigned lr_blocks(const FoldGeom& G) {
+    const long long Nl = G.ml * G.nl * G.sl;
+    return (unsigned)((Nl + kFoldThreads - 1) / kFoldThreads);
+}
+
+}  // namespace
+
+void launch_tik_fold(const FoldGeom& G, const double2* Yl, const double2* lam, const double2* xbh,
+                     double2* xh, double reg, cudaStream_t st) {
+    const double reg2 = 2.0 * reg;
+    const double shift = 2.0 * reg * (double)G.d;  // solvers.cpp:43
+    const double inv2l = 1.0 / (2.0 * reg);         // solvers.cpp:59
+    const double invsqrtd = 1.0 / std::sqrt((double)G.d);
+    const unsigned blocks = lr_blocks(G);
+#define VSR_TIK(DCV) \
+    tik_fold_kernel<DCV><<<blocks, kFoldThreads, 0, st>>>(G, Yl, lam, xbh, xh, reg2, shift, inv2l, invsqrtd)
+    switch (G.d) {
+        case 1: VSR_TIK(1); break;
+        case 2: VSR_TIK(2); break;
+        case 4: VSR_TIK(4); break;
+        case 8: VSR_TIK(8); break;
+        default: VSR_TIK(0); break;
+    }
+#undef VSR_TIK
+    VSR_LAUNCH_CHECK();
+}
+
+size_t tv_fold_blocks(const FoldGeom& G) { return lr_blocks(G); }
+
+void launch_tv_fold(const FoldGeom& G, const double2* Yl, const double2* lam, const double2* th,
+                    double2* xh, const double* gam, const GammaTables& tabs, double mu,
+                    double* fit_partials, cudaStream_t st) {
+    const double inv_mu = 1.0 / mu;                     // solvers.cpp:230
+    const double shift = mu * (double)G.d;              // solvers.cpp:238
+    const double invsqrtd = 1.0 / std::sqrt((double)G.d);
+    const unsigned blocks = lr_blocks(G);
+    const bool gtab = gam == nullptr;
+    const bool fit = fit_partials != nullptr;
+#define VSR_TV(DCV, GT, FT)                                                                  \
+    tv_fold_kernel<DCV, GT, FT><<<blocks, kFoldThreads, 0, st>>>(G, Yl, lam, th, xh, gam, tabs, \
+                                                                 mu, inv_mu, shift, invsqrtd,   \
+                                                                 fit_partials)
+#define VSR_TV_D(DCV)                           \
+    if (gtab && fit) VSR_TV(DCV, true, true);   \
+    else if (gtab) VSR_TV(DCV, true, false);    \
+    else if (fit) VSR_TV(DCV, false, true);     \
+    else VSR_TV(DCV, false, false);
+    switch (G.d) {
+        case 1: VSR_TV_D(1); break;
+        case 2: VSR_TV_D(2); break;
+        case 4: VSR_TV_D(4); break;
+        case 8: VSR_TV_D(8); break;
+        default: VSR_TV_D(0); break;
+    }
+#undef VSR_TV_D
+#undef VSR_TV
+    VSR_LAUNCH_CHECK();
+}
+
+void launch_fit_partials(const FoldGeom& G, const double2* Yl, const double2* lam,
+                         const double2* xh, double* fit_partials, cudaStream_t st) {
+    fit_kernel<<<lr_blocks(G), kFoldThreads, 0, st>>>(G, Yl, lam, xh,
+                                                      1.0 / std::sqrt((double)G.d), fit_partials);
+    VSR_LAUNCH_CHECK();
+}
+
+void launch_fold_apply(const FoldGeom& G, const double2* lam, const double* weights,
+                       const double2* hr_in, double2* lr_out, cudaStream_t st) {
+    fold_apply_kernel<<<lr_blocks(G), kFoldThreads, 0, st>>>(G, lam, weights, hr_in, lr_out);
+    VSR_LAUNCH_CHECK();
+}
+
+void launch_fold_adjoint(const FoldGeom& G, const double2* lam, const double* weights,
+                         const double2* lr_in, double2* hr_out, cudaStream_t st) {
+    const long long N = G.m * G.n * G.s;
+    fold_adjoint_kernel<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(G, lam, weights, lr_in, hr_out);
+    VSR_LAUNCH_CHECK();
+}
+
+void launch_gram(const FoldGeom& G, const double2* lam, const double* weights, double* lr_out,
+                 cudaStream_t st) {
+    gram_kernel<<<lr_blocks(G), kFoldThreads, 0, st>>>(G, lam, weights, lr_out);
+    VSR_LAUNCH_CHECK();
+}
+
+void launch_swap_blocks(const FoldGeom& G, double2* lam, cudaStream_t st) {
+    swap_blocks_kernel<<<lr_blocks(G), kFoldThreads, 0, st>>>(G, lam);
+    VSR_LAUNCH_CHECK();
+}
+
+void launch_finalize_sum(const double* partials, int stride, int nvals, size_t nblocks,
+                         double* out, cudaStream_t st) {
+    finalize_sum_kernel<<<1, 1024, 0, st>>>(partials, stride, nvals, (long long)nblocks, out);
+    VSR_LAUNCH_CHECK();
+}
+
+}  // namespace vsr

@@ -1,0 +1,433 @@
+// ADMM-TV spatial kernels (see tv.cuh).
+//
+// The fused stencil marches a 32 x 8 column of voxels through a chunk of KC
+// planes along axis 3 ("2.5D"): two x planes (with a one-voxel periodic halo)
+// live in shared memory, rho_x / rho_y of the current plane are exchanged
+// through shared memory for the divergence, and rho_z of the previous plane
+// stays in a register.  Every HBM byte of x, dual, dual' and theta is touched
+// once per iteration (halo re-reads hit L2).
+#include "tv.cuh"
+
+namespace vsr {
+namespace {
+
+constexpr int TX = 32, TY = 8, STH = TX * TY;
+
+__device__ __forceinline__ int wrapi(long long v, long long len) {
+    while (v < 0) v += len;
+    while (v >= len) v -= len;
+    return (int)v;
+}
+
+struct Shrunk {
+    double u0, u1, u2, dn0, dn1, dn2, r0, r1, r2;
+};
+
+// solvers.cpp:286-301 (factor = mag > t ? 1 - t/mag : 0) and :387-390.
+__device__ __forceinline__ Shrunk shrink_point(double l0, double l1, double l2, double d0, double d1,
+                                               double d2, double thr) {
+    Shrunk o;
+    const double n0 = l0 + d0, n1 = l1 + d1, n2 = l2 + d2;
+    const double mag = sqrt(n0 * n0 + n1 * n1 + n2 * n2);
+    const double f = mag > thr ? 1.0 - thr / mag : 0.0;
+    o.u0 = f * n0;
+    o.u1 = f * n1;
+    o.u2 = f * n2;
+    o.dn0 = n0 - o.u0;
+    o.dn1 = n1 - o.u1;
+    o.dn2 = n2 - o.u2;
+    o.r0 = o.u0 - o.dn0;
+    o.r1 = o.u1 - o.dn1;
+    o.r2 = o.u2 - o.dn2;
+    return o;
+}
+
+template <bool INIT, bool RELCHG>
+__global__ void __launch_bounds__(STH)
+    tv_stencil_kernel(int m, int n, int s, int KC, const double* __restrict__ x,
+                      const double* __restrict__ dual_in, double* __restrict__ dual_out,
+                      double* __restrict__ theta, double thr, const double* __restrict__ xprev,
+                      double* __restrict__ partials) {
+    __shared__ double xs[2][TY + 2][TX + 2];
+    __shared__ double rx[TY][TX + 1];
+    __shared__ double ry[TY + 1][TX];
+    __shared__ double red[32 * 4];
+
+    const int tid = threadIdx.x;
+    const int tx = tid % TX, ty = tid / TX;
+    const int i0 = blockIdx.x * TX, j0 = blockIdx.y * TY;
+    const int k0 = blockIdx.z * KC;
+    const int k1 = min(k0 + KC, s);
+    const long long plane = (long long)m * n;
+    const long long N = plane * s;
+    const int gi = i0 + tx, gj = j0 + ty;
+    const bool valid = gi < m && gj < n;
+    const long long col = valid ? (long long)gi + (long long)m * gj : 0;
+
+    auto load_plane = [&](int buf, int kz) {
+        const long long zoff = plane * wrapi(kz, s);
+        for (int e = tid; e < (TY + 2) * (TX + 2); e += STH) {
+            const int jj = e / (TX + 2) - 1, ii = e % (TX + 2) - 1;
+            const int gx = wrapi((long long)i0 + ii, m), gy = wrapi((long long)j0 + jj, n);
+            xs[buf][jj + 1][ii + 1] = __ldg(x + gx + (long long)m * gy + zoff);
+        }
+    };
+
+    double acc_res = 0.0, acc_tv = 0.0, acc_dx = 0.0, acc_xp = 0.0;
+    double rz_prev = 0.0;
+
+    load_plane(0, k0 - 1);
+    load_plane(1, k0);
+    for (int k = k0 - 1; k < k1; ++k) {
+        const int bc = (k - k0 + 1) & 1, bn = bc ^ 1;
+        const bool warm = k < k0;
+        if (!warm) {
+            load_plane(bn, k + 1);
+        }
+        __syncthreads();
+        const long long zoff = plane * wrapi(k, s);
+
+        // ---- interior point
+        {
+            const double xc = xs[bc][ty + 1][tx + 1];
+            const double l0 = xs[bc][ty + 1][tx + 2] - xc;
+            const double l1 = xs[bc][ty + 2][tx + 1] - xc;
+            const double l2 = xs[bn][ty + 1][tx + 1] - xc;
+            double r0, r1, r2;
+            if constexpr (INIT) {
+                r0 = l0;
+                r1 = l1;
+                r2 = l2;
+                if (!warm && valid) {
+                    const long long idx = col + zoff;
+                    dual_out[idx] = 0.0;
+                    dual_out[N + idx] = 0.0;
+                    dual_out[2 * N + idx] = 0.0;
+                    acc_tv += sqrt(l0 * l0 + l1 * l1 + l2 * l2);
+                }
+            } else {
+                const long long idx = col + zoff;
+                double d0 = 0.0, d1 = 0.0, d2 = 0.0;
+                if (valid) {
+                    d0 = __ldg(dual_in + idx);
+                    d1 = __ldg(dual_in + N + idx);
+                    d2 = __ldg(dual_in + 2 * N + idx);
+                }
+                const Shrunk o = shrink_point(l0, l1, l2, d0, d1, d2, thr);
+                r0 = o.r0;
+                r1 = o.r1;
+                r2 = o.r2;
+                if (!warm && valid) {
+                    dual_out[idx] = o.dn0;
+                    dual_out[N + idx] = o.dn1;
+                    dual_out[2 * N + idx] = o.dn2;
+                    const double e0 = l0 - o.u0, e1 = l1 - o.u1, e2 = l2 - o.u2;
+                    acc_res += e0 * e0 + e1 * e1 + e2 * e2;
+                    acc_tv += sqrt(l0 * l0 + l1 * l1 + l2 * l2);
+                }
+            }
+            if constexpr (RELCHG) {
+                if (!warm && valid) {
+                    const double xp = __ldg(xprev + col + zoff);
+                    const double dd = xc - xp;
+                    acc_dx += dd * dd;
+                    acc_xp += xp * xp;
+                }
+            }
+            rx[ty][tx + 1] = r0;
+            ry[ty + 1][tx] = r1;
+            // r2 is this plane's rho_z; theta needs rho_z of the previous plane
+            if (!warm) {
+                // halo points: rho_x at ii = -1 (jj = tid < TY), rho_y at jj = -1 (ii = tid - TY)
+                if (tid < TY + TX) {
+                    int ii, jj;
+                    if (tid < TY) {
+                        ii = -1;
+                        jj = tid;
+                    } else {
+                        ii = tid - TY;
+                        jj = -1;
+                    }
+                    const double hc = xs[bc][jj + 1][ii + 1];
+                    const double h0 = xs[bc][jj + 1][ii + 2] - hc;
+                    const double h1 = xs[bc][jj + 2][ii + 1] - hc;
+                    const double h2 = xs[bn][jj + 1][ii + 1] - hc;
+                    double q0, q1;
+                    if constexpr (INIT) {
+                        q0 = h0;
+                        q1 = h1;
+                    } else {
+                        const long long hidx = (long long)wrapi((long long)i0 + ii, m) +
+                                               (long long)m * wrapi((long long)j0 + jj, n) + zoff;
+                        const Shrunk o = shrink_point(h0, h1, h2, __ldg(dual_in + hidx),
+                                                      __ldg(dual_in + N + hidx),
+                                                      __ldg(dual_in + 2 * N + hidx), thr);
+                        q0 = o.r0;
+                        q1 = o.r1;
+                    }
+                    if (tid < TY)
+                        rx[jj][0] = q0;
+                    else
+                        ry[0][ii] = q1;
+                }
+            }
+            __syncthreads();
+            if (!warm && valid) {
+                // diff_adjoint sum in axis order (solvers.cpp:367-373): ((adj_x) + adj_y) + adj_z
+                const double ax = rx[ty][tx] - rx[ty][tx + 1];
+                const double ay = ry[ty][tx] - ry[ty + 1][tx];
+                const double az = rz_prev - r2;
+                theta[col + zoff] = (ax + ay) + az;
+            }
+            rz_prev = r2;
+        }
+        __syncthreads();
+    }
+
+    double v[4] = {acc_res, acc_tv, acc_dx, acc_xp};
+    block_reduce_sum<4>(v, red);
+    if (tid == 0) {
+        const size_t b = blockIdx.x + (size_t)gridDim.x * (blockIdx.y + (size_t)gridDim.y * blockIdx.z);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) partials[b * 4 + q] = v[q];
+    }
+}
+
+// Sum `nvals` interleaved per-block partials in a fixed order.
+__device__ void fixed_sum(const double* p, int stride, int nvals, long long nblocks, double* out,
+                          double* red) {
+    double v[4] = {0.0, 0.0, 0.0, 0.0};
+    for (long long i = threadIdx.x; i < nblocks; i += blockDim.x)
+        for (int k = 0; k < nvals; ++k) v[k] += p[i * stride + k];
+    block_reduce_sum<4>(v, red);
+    __syncthreads();
+    if (threadIdx.x == 0)
+        for (int k = 0; k < nvals; ++k) out[k] = v[k];
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(1024)
+    tv_finalize_kernel(int iter, const double* fitp, long long fitn, const double* stp,
+                       long long stn, const double* resp, long long resn, double tv_weight,
+                       double max_rel_imag, TvIterScalars sc, double* init_obj) {
+    __shared__ double red[32 * 4];
+    __shared__ double vals[12];
+    fixed_sum(fitp, 1, 1, fitn, vals + 0, red);
+    fixed_sum(stp, 4, 4, stn, vals + 4, red);
+    if (resp) fixed_sum(resp, 2, 2, resn, vals + 8, red);
+    if (threadIdx.x == 0) {
+        const double fit = vals[0];
+        const double resid = vals[4], tv = vals[5], dx2 = vals[6], xp2 = vals[7];
+        const double obj = 0.5 * fit + tv_weight * tv;  // solvers.cpp:401, :318
+        if (init_obj) {
+            *init_obj = obj;
+        } else {
+            sc.objective[iter] = obj;
+            sc.primal_residual[iter] = sqrt(resid);
+            sc.rel_change[iter] = sqrt(dx2) / fmax(sqrt(xp2), 1e-300);
+            if (resp) {
+                const double im2 = vals[8], tot2 = vals[9];
+                const double ratio = tot2 > 0.0 ? sqrt(im2 / tot2) : 0.0;
+                sc.status[2] = ratio;
+                if (tot2 > 0.0 && ratio > max_rel_imag && sc.status[0] < 0.0) {
+                    sc.status[0] = (double)iter;
+                    sc.status[1] = ratio;
+                }
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------- elementwise
+__global__ void decimate_kernel(long long m, long long n, int dr, int dc, int ds, long long ml,
+                                long long nl, long long Nl, const double* __restrict__ x,
+                                double* __restrict__ y) {
+    const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= Nl) return;
+    const long long i = g % ml, j = (g / ml) % nl, k = g / (ml * nl);
+    y[g] = x[i * dr + m * (j * dc + n * (k * ds))];
+}
+
+__global__ void decimate_adjoint_kernel(long long m, long long n, int dr, int dc, int ds,
+                                        long long N, double scale, const double* __restrict__ y,
+                                        long long ml, long long nl, double* __restrict__ x) {
+    const long long f = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (f >= N) return;
+    const long long i = f % m, j = (f / m) % n, k = f / (m * n);
+    double v = 0.0;
+    if (i % dr == 0 && j % dc == 0 && k % ds == 0) v = y[i / dr + ml * (j / dc + nl * (k / ds))] * scale;
+    x[f] = v;
+}
+
+__global__ void nn_upsample_kernel(long long m, long long n, int dr, int dc, int ds, long long N,
+                                   const double* __restrict__ y, long long ml, long long nl,
+                                   double* __restrict__ x) {
+    const long long f = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (f >= N) return;
+    const long long i = f % m, j = (f / m) % n, k = f / (m * n);
+    x[f] = y[i / dr + ml * (j / dc + nl * (k / ds))];
+}
+
+__global__ void diff_kernel(long long m, long long n, long long s, int axis, bool adjoint,
+                            const double* __restrict__ x, double* __restrict__ out) {
+    const long long N = m * n * s;
+    const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= N) return;
+    const long long i = p % m, j = (p / m) % n, k = p / (m * n);
+    const long long pos = axis == 0 ? i : (axis == 1 ? j : k);
+    const long long len = axis == 0 ? m : (axis == 1 ? n : s);
+    const long long stride = axis == 0 ? 1 : (axis == 1 ? m : m * n);
+    long long q;
+    if (!adjoint)
+        q = (pos + 1 == len) ? p - (len - 1) * stride : p + stride;  // operators.cpp:201-203
+    else
+        q = (pos == 0) ? p + (len - 1) * stride : p - stride;  // operators.cpp:218-220
+    out[p] = x[q] - x[p];
+}
+
+__global__ void shrink_kernel(long long count, const double* __restrict__ a,
+                              const double* __restrict__ b, const double* __restrict__ c,
+                              double thr, double* __restrict__ o1, double* __restrict__ o2,
+                              double* __restrict__ o3) {
+    const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= count) return;
+    const double n0 = a[p], n1 = b[p], n2 = c[p];
+    const double mag = sqrt(n0 * n0 + n1 * n1 + n2 * n2);
+    const double f = mag > thr ? 1.0 - thr / mag : 0.0;
+    o1[p] = f * n0;
+    o2[p] = f * n1;
+    o3[p] = f * n2;
+}
+
+__global__ void gamma_kernel(long long m, long long n, long long N, const double* __restrict__ nr,
+                             const double* __restrict__ nc, const double* __restrict__ ns,
+                             double tau, double* __restrict__ g) {
+    const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= N) return;
+    const long long i = p % m, j = (p / m) % n, k = p / (m * n);
+    g[p] = 1.0 / (((nr[i] + nc[j]) + ns[k]) + tau);  // solvers.cpp:196-202
+}
+
+__global__ void tv_norm_kernel(long long m, long long n, long long s, const double* __restrict__ x,
+                               double* __restrict__ partials) {
+    __shared__ double red[32];
+    const long long N = m * n * s;
+    const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    double acc = 0.0;
+    if (p < N) {
+        const long long i = p % m, j = (p / m) % n, k = p / (m * n);
+        const double xc = x[p];
+        const double g0 = x[(i + 1 == m) ? p - (m - 1) : p + 1] - xc;
+        const double g1 = x[(j + 1 == n) ? p - (n - 1) * m : p + m] - xc;
+        const double g2 = x[(k + 1 == s) ? p - (s - 1) * m * n : p + m * n] - xc;
+        acc = sqrt(g0 * g0 + g1 * g1 + g2 * g2);
+    }
+    double v[1] = {acc};
+    block_reduce_sum<1>(v, red);
+    if (threadIdx.x == 0) partials[blockIdx.x] = v[0];
+}
+
+unsigned blocks256(long long n) { return (unsigned)((n + 255) / 256); }
+
+}  // namespace
+
+StencilGeom stencil_geom(const Dims& d) {
+    StencilGeom g;
+    const unsigned gx = (unsigned)((d.m + TX - 1) / TX), gy = (unsigned)((d.n + TY - 1) / TY);
+    // chunk so that the grid has >= ~16 waves of 148 SMs when possible
+    const long long tiles = (long long)gx * gy;
+    int kc = 16;
+    while (kc > 4 && tiles * (((long long)d.s + kc - 1) / kc) < 148 * 16) kc >>= 1;
+    g.kc = kc;
+    g.grid = dim3(gx, gy, (unsigned)((d.s + kc - 1) / kc));
+    return g;
+}
+
+void launch_tv_stencil(const Dims& d, bool init, const double* x, const double* dual_in,
+                       double* dual_out, double* theta, double thr, const double* xprev,
+                       double* partials, cudaStream_t st) {
+    const StencilGeom g = stencil_geom(d);
+    const int m = (int)d.m, n = (int)d.n, s = (int)d.s;
+    if (init) {
+        tv_stencil_kernel<true, false><<<g.grid, STH, 0, st>>>(m, n, s, g.kc, x, dual_in, dual_out,
+                                                              theta, thr, xprev, partials);
+    } else if (xprev) {
+        tv_stencil_kernel<false, true><<<g.grid, STH, 0, st>>>(m, n, s, g.kc, x, dual_in, dual_out,
+                                                              theta, thr, xprev, partials);
+    } else {
+        tv_stencil_kernel<false, false><<<g.grid, STH, 0, st>>>(m, n, s, g.kc, x, dual_in, dual_out,
+                                                               theta, thr, xprev, partials);
+    }
+    VSR_LAUNCH_CHECK();
+}
+
+void launch_tv_finalize(int iter, const double* fit_partials, size_t fit_blocks,
+                        const double* st_partials, size_t st_blocks, const double* res_partials,
+                        size_t res_blocks, double tv_weight, double max_rel_imag,
+                        TvIterScalars sc, double* init_objective_out, cudaStream_t st) {
+    tv_finalize_kernel<<<1, 1024, 0, st>>>(iter, fit_partials, (long long)fit_blocks, st_partials,
+                                           (long long)st_blocks, res_partials,
+                                           (long long)res_blocks, tv_weight, max_rel_imag, sc,
+                                           init_objective_out);
+    VSR_LAUNCH_CHECK();
+}
+
+void launch_decimate(const Dims& hr, const int rates[3], const double* x, double* y,
+                     cudaStream_t st) {
+    const long long ml = hr.m / rates[0], nl = hr.n / rates[1], sl = hr.s / rates[2];
+    const long long Nl = ml * nl * sl;
+    decimate_kernel<<<blocks256(Nl), 256, 0, st>>>((long long)hr.m, (long long)hr.n, rates[0],
+                                                   rates[1], rates[2], ml, nl, Nl, x, y);
+    VSR_LAUNCH_CHECK();
+}
+
+void launch_decimate_adjoint(const Dims& hr, const int rates[3], const double* y, double* x,
+                             double scale, cudaStream_t st) {
+    const long long N = (long long)hr.count();
+    decimate_adjoint_kernel<<<blocks256(N), 256, 0, st>>>(
+        (long long)hr.m, (long long)hr.n, rates[0], rates[1], rates[2], N, scale, y,
+        (long long)(hr.m / rates[0]), (long long)(hr.n / rates[1]), x);
+    VSR_LAUNCH_CHECK();
+}
+
+void launch_nn_upsample(const Dims& hr, const int rates[3], const double* y, double* x,
+                        cudaStream_t st) {
+    const long long N = (long long)hr.count();
+    nn_upsample_kernel<<<blocks256(N), 256, 0, st>>>((long long)hr.m, (long long)hr.n, rates[0],
+                                                     rates[1], rates[2], N, y,
+                                                     (long long)(hr.m / rates[0]),
+                                                     (long long)(hr.n / rates[1]), x);
+    VSR_LAUNCH_CHECK();
+}
+
+void launch_diff(const Dims& d, int axis, bool adjoint, const double* x, double* out,
+                 cudaStream_t st) {
+    diff_kernel<<<blocks256((long long)d.count()), 256, 0, st>>>(
+        (long long)d.m, (long long)d.n, (long long)d.s, axis, adjoint, x, out);
+    VSR_LAUNCH_CHECK();
+}
+
+void launch_shrink(size_t count, const double* nu1, const double* nu2, const double* nu3,
+                   double thr, double* o1, double* o2, double* o3, cudaStream_t st) {
+    shrink_kernel<<<blocks256((long long)count), 256, 0, st>>>((long long)count, nu1, nu2, nu3, thr,
+                                                              o1, o2, o3);
+    VSR_LAUNCH_CHECK();
+}
+
+void launch_gamma(const Dims& d, const double* nr, const double* nc, const double* ns, double tau,
+                  double* gamma, cudaStream_t st) {
+    const long long N = (long long)d.count();
+    gamma_kernel<<<blocks256(N), 256, 0, st>>>((long long)d.m, (long long)d.n, N, nr, nc, ns, tau,
+                                               gamma);
+    VSR_LAUNCH_CHECK();
+}
+
+size_t tv_norm_blocks(const Dims& d) { return blocks256((long long)d.count()); }
+
+void launch_tv_norm(const Dims& d, const double* x, double* partials, cudaStream_t st) {
+    tv_norm_kernel<<<blocks256((long long)d.count()), 256, 0, st>>>(
+        (long long)d.m, (long long)d.n, (long long)d.s, x, partials);
+    VSR_LAUNCH_CHECK();
+}
+
+}  // namespace vsr

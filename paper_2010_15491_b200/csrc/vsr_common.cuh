@@ -1,0 +1,118 @@
+// Common device/host utilities for the volsr B200 path.
+// Layout contract (reference include/volsr/volume.hpp:26-45): a volume with
+// dims (m, n, s) is stored lexicographically, axis 1 (m) fastest; complex
+// values are interleaved (re, im) doubles, i.e. double2.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstddef>
+#include <stdexcept>
+#include <string>
+
+namespace vsr {
+
+// Error taxonomy mirrored from the reference (volume.hpp:12-24) plus a device
+// failure class.  The C ABI maps each to a status code (include/vsr.h).
+struct shape_error : std::invalid_argument {
+    using std::invalid_argument::invalid_argument;
+};
+struct numeric_error : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct cuda_error : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+#define VSR_CUDA(call)                                                                   \
+    do {                                                                                 \
+        cudaError_t e_ = (call);                                                         \
+        if (e_ != cudaSuccess)                                                           \
+            throw ::vsr::cuda_error(std::string("CUDA error ") + cudaGetErrorString(e_) + \
+                                    " at " __FILE__ ":" + std::to_string(__LINE__));     \
+    } while (0)
+
+// Every kernel launch site is followed by VSR_LAUNCH_CHECK(), which also
+// counts the launch (reported through vsr_launch_count for the bench).
+void note_launch();
+#define VSR_LAUNCH_CHECK()               \
+    do {                                 \
+        VSR_CUDA(cudaGetLastError());    \
+        ::vsr::note_launch();            \
+    } while (0)
+
+// Optional per-stage CUDA-event profiler (bench roofline): stages record an
+// event pair on the launching stream; durations are read after a sync.
+struct Profiler {
+    virtual ~Profiler() = default;
+    virtual void begin(const char* name, cudaStream_t st) = 0;
+    virtual void end(cudaStream_t st) = 0;
+};
+struct ProfScope {
+    Profiler* p;
+    cudaStream_t st;
+    ProfScope(Profiler* prof, const char* name, cudaStream_t s) : p(prof), st(s) {
+        if (p) p->begin(name, st);
+    }
+    ~ProfScope() {
+        if (p) p->end(st);
+    }
+};
+
+struct Dims {
+    size_t m = 0, n = 0, s = 0;
+    size_t count() const { return m * n * s; }
+    bool operator==(const Dims& o) const { return m == o.m && n == o.n && s == o.s; }
+    size_t len(int axis) const { return axis == 0 ? m : (axis == 1 ? n : s); }
+};
+
+inline std::string to_string(const Dims& d) {
+    return std::to_string(d.m) + "x" + std::to_string(d.n) + "x" + std::to_string(d.s);
+}
+
+inline bool is_pow2(size_t v) { return v && !(v & (v - 1)); }
+
+// ---------------------------------------------------------------- complex ops
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+    return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+// conj(a) * b
+__device__ __forceinline__ double2 cmulc(double2 a, double2 b) {
+    return make_double2(a.x * b.x + a.y * b.y, a.x * b.y - a.y * b.x);
+}
+__device__ __forceinline__ double2 cscale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
+__device__ __forceinline__ double cnorm(double2 a) { return a.x * a.x + a.y * a.y; }
+
+// ------------------------------------------------- deterministic block reduce
+// Fixed-order tree: warp shuffle tree, then warp 0 reduces the per-warp sums in
+// warp order.  Same launch geometry => bit-identical result run to run.
+template <int NV>
+__device__ __forceinline__ void block_reduce_sum(double (&v)[NV], double* smem /* >= 32*NV */) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) v[k] += __shfl_down_sync(0xffffffffu, v[k], off);
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nwarps = (blockDim.x + 31) >> 5;
+    __syncthreads();
+    if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < NV; ++k) smem[warp * NV + k] = v[k];
+    }
+    __syncthreads();
+    if (warp == 0) {
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+            double t = lane < nwarps ? smem[lane * NV + k] : 0.0;
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) t += __shfl_down_sync(0xffffffffu, t, off);
+            v[k] = t;
+        }
+    }
+}
+
+}  // namespace vsr

@@ -1,0 +1,374 @@
+"""GPU parity: the CUDA path (through the C ABI, include/vsr.h) against the CPU
+oracle on identical seeded inputs.  fp64 tolerance: relative L2 <= 1e-10
+(BASELINE.json north_star), unless a reference test states a looser bound."""
+import math
+
+import numpy as np
+import pytest
+
+from conftest import random_psf, random_spectrum, random_volume, rel_err
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-10
+
+ODD_EVEN = [(5, 3, 7), (4, 6, 2), (8, 8, 8), (1, 9, 4), (1, 1, 1), (3, 1, 1), (12, 10, 8), (6, 4, 4)]
+POW2 = [(2, 2, 2), (4, 4, 4), (16, 8, 4), (32, 32, 32), (64, 64, 64), (128, 8, 16), (2048, 2, 4),
+        (1024, 4, 2), (8, 1024, 2), (4, 2, 2048), (512, 16, 4), (256, 256, 4), (64, 32, 128)]
+
+
+# ------------------------------------------------------------------ FFT engine
+@pytest.mark.parametrize("d", ODD_EVEN + POW2)
+def test_fft3_complex_vs_numpy(V, O, d):
+    rng = np.random.default_rng(hash(d) % 2 ** 32)
+    x = random_spectrum(d, rng)
+    assert rel_err(V.fft3(x), O.fft3(x)) < 1e-13
+    assert rel_err(V.ifft3(x), O.ifft3(x)) < 1e-13
+
+
+@pytest.mark.parametrize("d", ODD_EVEN + POW2)
+def test_fft3_real_and_ifft3_real(V, O, d):
+    rng = np.random.default_rng(1 + hash(d) % 2 ** 31)
+    x = random_volume(d, rng)
+    xh = V.fft3(x)
+    assert rel_err(xh, O.fft3(x)) < 1e-13
+    back = V.ifft3_real(xh)
+    assert rel_err(back, x) < 1e-13
+    assert rel_err(V.dft3_unnormalized(x), O.dft3_unnormalized(x)) < 1e-13
+
+
+def test_fft3_constant_dc(V):
+    """test_volume.cpp:44-50."""
+    d = (4, 3, 5)
+    sp = V.fft3(np.full((5, 3, 4), 0.75))
+    assert abs(sp.reshape(-1)[0] - 0.75 * math.sqrt(60)) < 1e-12
+    assert np.all(np.abs(sp.reshape(-1)[1:]) < 1e-12)
+
+
+def test_fft3_dense_dft(V, O):
+    """test_volume.cpp:71-81 (sign, scale, axis order)."""
+    rng = np.random.default_rng(11)
+    d = (4, 3, 2)
+    x = random_volume(d, rng)
+    assert np.max(np.abs(V.fft3(x).reshape(-1) - O.build_dense_dft(d) @ x.reshape(-1))) < 1e-12
+
+
+def test_ifft3_real_rejects_nonhermitian(V):
+    """test_volume.cpp:83-87."""
+    rng = np.random.default_rng(3)
+    with pytest.raises(V.NumericError, match="imaginary residue"):
+        V.ifft3_real(random_spectrum((4, 4, 4), rng), 1e-8)
+    with pytest.raises(V.NumericError):
+        V.ifft3_real(random_spectrum((64, 32, 16), rng), 1e-8)
+
+
+def test_fft_empty_volume_rejected(V):
+    with pytest.raises(V.ShapeError):
+        V.fft3(np.zeros((0, 4, 4)))
+
+
+# ------------------------------------------------------------------ operators
+@pytest.mark.parametrize("hr,rates", [((8, 8, 8), (2, 2, 2)), ((6, 4, 8), (3, 2, 4)), ((5, 3, 7), (5, 1, 7))])
+def test_decimate_ops(V, O, hr, rates):
+    rng = np.random.default_rng(6)
+    spec = V.DecimationSpec(hr, rates)
+    ospec = O.DecimationSpec(hr, rates)
+    x = random_volume(hr, rng)
+    y = random_volume(spec.lr, rng)
+    assert np.array_equal(V.decimate(x, spec), O.decimate(x, ospec))
+    assert np.array_equal(V.decimate_adjoint(y, spec), O.decimate_adjoint(y, ospec))
+
+
+@pytest.mark.parametrize("d", [(5, 4, 3), (32, 8, 16), (1, 7, 2)])
+@pytest.mark.parametrize("axis", [0, 1, 2])
+def test_diff_ops_bit_exact(V, O, d, axis):
+    rng = np.random.default_rng(8)
+    x = random_volume(d, rng)
+    assert np.array_equal(V.diff_forward(x, axis), O.diff_forward(x, axis))
+    assert np.array_equal(V.diff_adjoint(x, axis), O.diff_adjoint(x, axis))
+
+
+def test_blur_apply(V, O):
+    rng = np.random.default_rng(9)
+    d = (16, 12, 8)
+    psf = random_psf(d, 3, rng)
+    x = random_volume(d, rng)
+    lam = O.psf_to_spectrum(psf)
+    assert rel_err(V.psf_to_spectrum(psf), lam) < 1e-13
+    assert rel_err(V.blur_apply(x, lam), O.blur_apply(x, lam)) < TOL
+    assert rel_err(V.blur_apply(x, lam, True), O.blur_apply(x, lam, True)) < TOL
+
+
+# ------------------------------------------------------------------ spectral fold
+@pytest.mark.parametrize("hr,rates", [((4, 4, 2), (2, 2, 1)), ((6, 4, 4), (3, 2, 2)), ((16, 16, 16), (4, 4, 4)),
+                                      ((32, 16, 8), (2, 2, 4)), ((3, 4, 5), (1, 1, 1))])
+def test_fold_primitives(V, O, hr, rates):
+    rng = np.random.default_rng(12)
+    spec, ospec = V.DecimationSpec(hr, rates), O.DecimationSpec(hr, rates)
+    v = random_spectrum(hr, rng)
+    lam = random_spectrum(hr, rng)
+    w = random_spectrum(spec.lr, rng)
+    gw = rng.uniform(0.1, 1.0, V.shape_of(hr))
+    assert rel_err(V.alias_fold(v, spec), O.alias_fold(v, ospec)) < 1e-15
+    assert np.array_equal(V.alias_expand(w, spec), O.alias_expand(w, ospec))
+    f, of = V.FoldedSpectrum(lam, spec), O.FoldedSpectrum(lam, ospec)
+    assert rel_err(f.apply(v), of.apply(v)) < 1e-14
+    assert rel_err(f.apply_adjoint(w), of.apply_adjoint(w)) < 1e-15
+    assert rel_err(f.apply_weighted(v, gw), of.apply_weighted(v, gw)) < 1e-14
+    assert rel_err(f.apply_adjoint_weighted(w, gw), of.apply_adjoint_weighted(w, gw)) < 1e-15
+    assert rel_err(V.gram_diag(f), O.gram_diag(of)) < 1e-14
+    assert rel_err(V.gram_diag_weighted(f, gw), O.gram_diag_weighted(of, gw)) < 1e-14
+    if spec.rate() >= 2:
+        assert f.block_value(1, 0, 0, 0) == of.block_value(1, 0, 0, 0) or rates[0] == 1
+        a = f.apply(v)
+        f.swap_blocks_for_fault_injection()
+        assert rel_err(f.apply(v), a) > 1e-3
+    with pytest.raises(IndexError):
+        f.block_value(rates[0], 0, 0, 0)
+
+
+# ------------------------------------------------------------------ Tikhonov
+TIK_CASES = [((8, 8, 8), (2, 2, 2)), ((6, 4, 4), (3, 2, 1)), ((4, 6, 4), (2, 3, 2)), ((8, 4, 4), (2, 1, 2)),
+             ((12, 10, 8), (2, 2, 2)), ((32, 32, 32), (4, 4, 4)), ((64, 32, 16), (2, 2, 4)),
+             ((16, 16, 16), (1, 1, 1)), ((64, 64, 64), (8, 8, 8)), ((20, 12, 6), (5, 3, 2))]
+
+
+@pytest.mark.parametrize("dims,rates", TIK_CASES)
+def test_tikhonov_vs_oracle(V, O, dims, rates):
+    rng = np.random.default_rng(3)
+    spec, ospec = V.DecimationSpec(dims, rates), O.DecimationSpec(dims, rates)
+    psf = random_psf(dims, 3, rng)
+    lam = O.psf_to_spectrum(psf)
+    reg = 0.02 + 0.2 * rng.uniform()
+    xbar = random_volume(dims, rng)
+    y = random_volume(spec.lr, rng)
+    got = V.tikhonov_fast(y, lam, spec, V.TikhonovConfig(reg, xbar))
+    want = O.tikhonov_fast(y, lam, ospec, reg, xbar)
+    assert rel_err(got, want) < TOL
+
+
+def test_tikhonov_identity_formula(V):
+    """test_solvers.cpp:55-69."""
+    rng = np.random.default_rng(1)
+    d = (4, 4, 4)
+    spec = V.DecimationSpec(d, (1, 1, 1))
+    xbar = random_volume(d, rng)
+    y = random_volume(d, rng)
+    x = V.tikhonov_fast(y, np.ones((4, 4, 4), complex), spec, V.TikhonovConfig(0.35, xbar))
+    want = (y + 0.7 * xbar) / 1.7
+    assert np.max(np.abs(x - want) / np.abs(want)) < 1e-12
+
+
+def test_tikhonov_huge_lambda(V, O):
+    rng = np.random.default_rng(2)
+    d = (8, 8, 8)
+    spec = V.DecimationSpec(d, (2, 2, 2))
+    lam = O.psf_to_spectrum(random_psf(d, 3, rng))
+    xbar = random_volume(d, rng)
+    x = V.tikhonov_fast(random_volume(spec.lr, rng), lam, spec, V.TikhonovConfig(1e6, xbar))
+    assert rel_err(x, xbar) < 1e-4
+
+
+def test_tikhonov_errors(V):
+    d = (4, 4, 4)
+    spec = V.DecimationSpec(d, (1, 1, 1))
+    with pytest.raises(ValueError, match="lambda must be positive"):
+        V.TikhonovOperator(np.ones((4, 4, 4), complex), spec, V.TikhonovConfig(0.0, np.zeros((4, 4, 4))))
+    op = V.TikhonovOperator(np.ones((4, 4, 4), complex), spec, V.TikhonovConfig(0.1, np.zeros((4, 4, 4))))
+    with pytest.raises(V.ShapeError):
+        op.solve(np.zeros((2, 4, 4)))
+    with pytest.raises(V.ShapeError, match="does not divide"):
+        V.DecimationSpec((4, 5, 4), (2, 2, 2))
+
+
+def test_tikhonov_nonfinite_detected(V):
+    d = (8, 8, 8)
+    spec = V.DecimationSpec(d, (2, 2, 2))
+    op = V.TikhonovOperator(np.ones((8, 8, 8), complex), spec, V.TikhonovConfig(0.1, np.zeros((8, 8, 8))))
+    y = np.zeros((4, 4, 4))
+    y[1, 2, 3] = np.nan
+    with pytest.raises(V.NumericError, match="non-finite"):
+        op.solve(y)
+    # operator stays usable after an error
+    assert np.all(np.isfinite(op.solve(np.ones((4, 4, 4)))))
+
+
+def test_tikhonov_fft_budget(V, O):
+    """test_solvers.cpp:141-157: 1 forward + 1 inverse transform per solve."""
+    rng = np.random.default_rng(5)
+    d = (8, 8, 8)
+    spec = V.DecimationSpec(d, (2, 2, 2))
+    op = V.TikhonovOperator(O.psf_to_spectrum(random_psf(d, 3, rng)), spec,
+                            V.TikhonovConfig(0.1, random_volume(d, rng)))
+    V.reset_fft_counters()
+    op.solve(random_volume(spec.lr, rng))
+    assert V.fft_counters() == {"forward": 1, "inverse": 1}
+
+
+def test_tikhonov_deterministic(V, O):
+    """test_cli.cpp:237-268: byte-identical outputs run to run."""
+    rng = np.random.default_rng(6)
+    d = (64, 64, 64)
+    spec = V.DecimationSpec(d, (2, 2, 2))
+    op = V.TikhonovOperator(O.psf_to_spectrum(random_psf(d, 5, rng)), spec,
+                            V.TikhonovConfig(1e-3, random_volume(d, rng)))
+    y = random_volume(spec.lr, rng)
+    a, b = op.solve(y), op.solve(y)
+    assert a.tobytes() == b.tobytes()
+
+
+# ------------------------------------------------------------------ TV pieces
+@pytest.mark.parametrize("d", [(4, 4, 4), (16, 8, 32), (5, 3, 7)])
+def test_make_gamma(V, O, d):
+    assert np.array_equal(V.make_gamma(d, 1e-3), O.make_gamma(d, 1e-3))
+
+
+def test_make_gamma_errors(V):
+    with pytest.raises(V.NumericError, match="zero frequency"):
+        V.make_gamma((4, 4, 4), 0.0)
+    with pytest.raises(ValueError):
+        V.make_gamma((4, 4, 4), -1.0)
+
+
+def test_tv_shrink(V, O):
+    rng = np.random.default_rng(9)
+    d = (16, 8, 4)
+    nu = [random_volume(d, rng) for _ in range(3)]
+    nu[0][0, 0, 0] = nu[1][0, 0, 0] = nu[2][0, 0, 0] = 0.0
+    got, want = V.tv_shrink(*nu, 0.4), O.tv_shrink(*nu, 0.4)
+    for g, w in zip(got, want):
+        assert np.max(np.abs(g - w)) < 1e-15
+    one = lambda v: np.full((1, 1, 1), v)
+    out = V.tv_shrink(one(3.0), one(0.0), one(0.0), 1.0)
+    assert abs(out[0][0, 0, 0] - 2.0) < 1e-12
+    with pytest.raises(ValueError):
+        V.tv_shrink(one(1.0), one(0.0), one(0.0), -0.5)
+
+
+@pytest.mark.parametrize("dims,rates,tau", [((8, 8, 8), (2, 2, 2), 1e-6), ((16, 16, 16), (4, 4, 4), 1e-3),
+                                            ((32, 16, 8), (2, 2, 4), 1e-3), ((6, 4, 4), (1, 1, 1), 1e-2),
+                                            ((12, 10, 8), (2, 2, 2), 1e-3)])
+def test_tv_x_update_vs_oracle(V, O, dims, rates, tau):
+    rng = np.random.default_rng(11)
+    spec, ospec = V.DecimationSpec(dims, rates), O.DecimationSpec(dims, rates)
+    lam = O.psf_to_spectrum(random_psf(dims, 3, rng))
+    mu = 0.7
+    g = O.make_gamma(dims, tau)
+    y = random_volume(spec.lr, rng)
+    th = O.fft3(_theta(O, dims, rng))
+    got = V.tv_x_update(y, V.FoldedSpectrum(lam, spec), lam, spec, mu, th, g)
+    want = O.tv_x_update(y, O.FoldedSpectrum(lam, ospec), lam, ospec, mu, th, g)
+    assert rel_err(got, want) < TOL
+
+
+def test_tv_x_update_rejects_bad_gamma(V, O):
+    d = (4, 4, 4)
+    spec = V.DecimationSpec(d, (2, 2, 2))
+    lam = O.psf_to_spectrum(O.make_gaussian_psf((3, 3, 3), (1, 1, 1), d))
+    g = O.make_gamma(d, 1e-8)
+    g[0, 0, 0] = 0.0
+    with pytest.raises(V.NumericError, match="gamma must be strictly positive"):
+        V.tv_x_update(np.zeros((2, 2, 2)), V.FoldedSpectrum(lam, spec), lam, spec, 1.0,
+                      np.zeros((4, 4, 4), complex), g)
+
+
+def _theta(O, d, rng):
+    th = np.zeros(O.shape_of(d))
+    for a in range(3):
+        th = th + O.diff_adjoint(random_volume(d, rng), a)
+    return th
+
+
+def test_objective_tv(V, O):
+    rng = np.random.default_rng(13)
+    for d, rates in [((6, 4, 4), (2, 2, 2)), ((32, 16, 8), (4, 2, 2))]:
+        spec, ospec = V.DecimationSpec(d, rates), O.DecimationSpec(d, rates)
+        lam = O.psf_to_spectrum(random_psf(d, 3, rng))
+        x = random_volume(d, rng)
+        y = random_volume(spec.lr, rng)
+        got = V.objective_tv(x, y, lam, spec, 0.3)
+        want = O.objective_tv(x, y, lam, ospec, 0.3)
+        assert abs(got - want) / abs(want) < 1e-12
+
+
+# ------------------------------------------------------------------ ADMM-TV
+TV_CASES = [((8, 8, 8), (2, 2, 2), 6), ((16, 16, 16), (4, 4, 4), 10), ((32, 32, 16), (2, 2, 4), 8),
+            ((12, 10, 8), (2, 2, 2), 5), ((64, 64, 64), (4, 4, 4), 12), ((40, 24, 16), (2, 2, 2), 5)]
+
+
+@pytest.mark.parametrize("dims,rates,iters", TV_CASES)
+def test_admm_tv_vs_oracle(V, O, dims, rates, iters):
+    """Parity protocol: explicit tau = 1e-3 * mu, rel_tol = 0."""
+    rng = np.random.default_rng(21)
+    spec, ospec = V.DecimationSpec(dims, rates), O.DecimationSpec(dims, rates)
+    psf = O.make_gaussian_psf(tuple(min(5, x - (1 - x % 2)) for x in dims), (1.5, 1.5, 1.5), dims)
+    y = random_volume(spec.lr, rng, 0.0, 1.0)
+    mu, lam_tv = 0.05, 2e-3
+    for init, x0 in [(V.INIT_ZERO, None), (V.INIT_UPSAMPLED, None),
+                     (V.INIT_PROVIDED, random_volume(dims, rng, 0.0, 1.0))]:
+        cfg = V.TvAdmmConfig(lambda_=lam_tv, mu=mu, max_iters=iters, rel_tol=0.0, tau=1e-3 * mu,
+                             init=init, init_volume=x0)
+        got, rep = V.admm_tv(y, psf, spec, cfg)
+        want, orep = O.admm_tv(y, psf, ospec, lam_tv=lam_tv, mu=mu, max_iters=iters, rel_tol=0.0,
+                               tau=1e-3 * mu, init=init, init_volume=x0)
+        assert rel_err(got, want) < TOL
+        assert rep.iterations == orep.iterations == iters
+        assert abs(rep.initial_objective - orep.initial_objective) <= 1e-10 * abs(orep.initial_objective)
+        assert rel_err(rep.objective, orep.objective) < 1e-10
+        assert rel_err(rep.primal_residual, orep.primal_residual) < 1e-9
+
+
+def test_admm_tv_rel_tol_stop(V, O):
+    rng = np.random.default_rng(22)
+    d = (16, 16, 16)
+    spec, ospec = V.DecimationSpec(d, (2, 2, 2)), O.DecimationSpec(d, (2, 2, 2))
+    psf = O.make_gaussian_psf((5, 5, 5), (1.0, 1.0, 1.0), d)
+    y = random_volume(spec.lr, rng, 0.0, 1.0)
+    cfg = V.TvAdmmConfig(lambda_=2e-3, mu=0.05, max_iters=200, rel_tol=1e-3, tau=5e-5)
+    got, rep = V.admm_tv(y, psf, spec, cfg)
+    want, orep = O.admm_tv(y, psf, ospec, lam_tv=2e-3, mu=0.05, max_iters=200, rel_tol=1e-3, tau=5e-5)
+    assert rep.iterations == orep.iterations < 200
+    assert rel_err(got, want) < TOL
+
+
+def test_admm_tv_default_tau_dc_split(V, O):
+    """At the reference default tau = 1e-8 mu the DC bin is ill-conditioned
+    (SURVEY Appendix B): the mean-free part must still match to 1e-10; the
+    mean is reported against the eps/(tau mu d) amplification bound."""
+    rng = np.random.default_rng(23)
+    d = (32, 32, 32)
+    spec, ospec = V.DecimationSpec(d, (4, 4, 4)), O.DecimationSpec(d, (4, 4, 4))
+    psf = O.make_gaussian_psf((5, 5, 5), (1.5, 1.5, 1.5), d)
+    y = random_volume(spec.lr, rng, 0.0, 1.0)
+    got, _ = V.admm_tv(y, psf, spec, V.TvAdmmConfig(lambda_=2e-3, mu=0.05, max_iters=5, rel_tol=0.0))
+    want, _ = O.admm_tv(y, psf, ospec, lam_tv=2e-3, mu=0.05, max_iters=5, rel_tol=0.0)
+    assert rel_err(got - got.mean(), want - want.mean()) < TOL
+    bound = 1e-16 / (1e-8 * 0.05 * 0.05 * 64) * 100
+    assert abs(got.mean() - want.mean()) / abs(want.mean()) < bound
+
+
+def test_admm_tv_validates(V):
+    d = (8, 8, 8)
+    spec = V.DecimationSpec(d, (2, 2, 2))
+    psf = V.make_gaussian_psf((3, 3, 3), (1, 1, 1), d)
+    y = np.full((4, 4, 4), 0.5)
+    V.admm_tv(y, psf, spec, V.TvAdmmConfig(max_iters=2, init=V.INIT_UPSAMPLED))
+    with pytest.raises(V.ShapeError):
+        V.admm_tv(y, psf, spec, V.TvAdmmConfig(max_iters=2, init=V.INIT_PROVIDED, init_volume=np.zeros((4, 4, 4))))
+    for bad in (V.TvAdmmConfig(lambda_=-1.0), V.TvAdmmConfig(mu=0.0), V.TvAdmmConfig(max_iters=0)):
+        with pytest.raises(ValueError):
+            V.admm_tv(y, psf, spec, bad)
+    with pytest.raises(V.NumericError, match="zero frequency"):
+        V.admm_tv(y, psf, spec, V.TvAdmmConfig(max_iters=2, tau=0.0))
+
+
+def test_admm_tv_deterministic(V):
+    rng = np.random.default_rng(24)
+    d = (32, 32, 32)
+    spec = V.DecimationSpec(d, (2, 2, 2))
+    psf = V.make_gaussian_psf((5, 5, 5), (1.5, 1.5, 1.5), d)
+    y = random_volume(spec.lr, rng, 0.0, 1.0)
+    cfg = V.TvAdmmConfig(lambda_=2e-3, mu=0.05, max_iters=6, rel_tol=0.0)
+    a, ra = V.admm_tv(y, psf, spec, cfg)
+    b, rb = V.admm_tv(y, psf, spec, cfg)
+    assert a.tobytes() == b.tobytes()
+    assert ra.objective == rb.objective and ra.primal_residual == rb.primal_residual
