@@ -7,6 +7,7 @@
 #include <chrono>
 #include <climits>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <utility>
@@ -15,6 +16,7 @@
 #include "../../include/vsr.h"
 #include "fft.cuh"
 #include "fold.cuh"
+#include "fused.cuh"
 #include "tv.cuh"
 
 using namespace vsr;
@@ -322,6 +324,15 @@ void require_ctx(vsr_ctx* ctx) {
 }
 
 double inv_sqrt_count(const Dims& d) { return 1.0 / std::sqrt((double)d.count()); }
+
+// Fused fold + axis-3 FFT kernels unless disabled (VSR_NO_FUSE=1, for A/B runs).
+bool use_fused(const FoldGeom& G) {
+    static const bool off = [] {
+        const char* e = std::getenv("VSR_NO_FUSE");
+        return e && e[0] == '1';
+    }();
+    return !off && fused_axis3_ok(G);
+}
 
 }  // namespace
 
@@ -822,13 +833,22 @@ static void tik_enqueue(vsr_tikhonov* t, const double* y_dev, double* x_dev) {
         fft_engine().forward3(t->sp.lr, y_dev, IN_REAL, t->Yl.p, inv_sqrt_count(t->sp.lr), st);
     }
     ++g_fwd;  // the one forward transform of solve() (solvers.cpp:52)
-    {
-        ProfScope ps(prof, "tik_fold", st);
-        launch_tik_fold(t->G, t->Yl.p, t->lam.p, t->xbh.p, t->xh.p, t->reg, st);
-    }
     PassReduce red{t->partials.p, t->bad.p};
-    fft_engine().inverse3(t->sp.hr, t->xh.p, x_dev, OUT_REAL, inv_sqrt_count(t->sp.hr), &red, st,
-                          prof);
+    if (use_fused(t->G)) {
+        {
+            ProfScope ps(prof, "tik_fold_ifft_axis3", st);
+            launch_tik_fold_ifft3(t->G, t->Yl.p, t->lam.p, t->xbh.p, t->xh.p, t->reg, st);
+        }
+        fft_engine().inverse21(t->sp.hr, t->xh.p, x_dev, OUT_REAL, inv_sqrt_count(t->sp.hr), &red,
+                               st, prof);
+    } else {
+        {
+            ProfScope ps(prof, "tik_fold", st);
+            launch_tik_fold(t->G, t->Yl.p, t->lam.p, t->xbh.p, t->xh.p, t->reg, st);
+        }
+        fft_engine().inverse3(t->sp.hr, t->xh.p, x_dev, OUT_REAL, inv_sqrt_count(t->sp.hr), &red,
+                              st, prof);
+    }
     ++g_inv;  // the one inverse transform (solvers.cpp:64)
     {
         ProfScope ps(prof, "residue_status", st);
@@ -993,7 +1013,7 @@ int vsr_objective_tv(vsr_ctx* ctx, const size_t hr_dims[3], const size_t rates[3
         fft_engine().forward3(sp.lr, dy.p, IN_REAL, Yl.p, inv_sqrt_count(sp.lr), st);
         fft_engine().forward3(sp.hr, dx.p, IN_REAL, W.p, inv_sqrt_count(sp.hr), st);
         g_fwd += 2;
-        const size_t fb = tv_fold_blocks(G), tb = tv_norm_blocks(sp.hr);
+        const size_t fb = fit_blocks(G), tb = tv_norm_blocks(sp.hr);
         DevBuf<double> fitp(fb), tvp(tb), res(2);
         launch_fit_partials(G, Yl.p, lam.p, W.p, fitp.p, st);
         launch_tv_norm(sp.hr, dx.p, tvp.p, st);
@@ -1071,7 +1091,8 @@ static vsr_tv* tv_build(vsr_ctx* ctx, const Spec& sp, const double* y_dev, const
         h->fit_blocks = tv_fold_blocks(h->G);
         h->st_blocks = stencil_geom(hr).blocks();
         h->res_blocks = fft_engine().inverse_final_blocks(hr);
-        h->fitp.alloc(std::max<size_t>(h->fit_blocks, 1));
+        h->fitp.alloc(std::max<size_t>(
+            std::max(std::max(h->fit_blocks, fit_blocks(h->G)), tv_sandwich_blocks(h->G)), 1));
         h->stp.alloc(kStencilVals * h->st_blocks);
         h->resp.alloc(2 * std::max<size_t>(h->res_blocks, 1));
         h->bad.alloc(1);
@@ -1107,7 +1128,7 @@ static vsr_tv* tv_build(vsr_ctx* ctx, const Spec& sp, const double* y_dev, const
         ++g_fwd;
         launch_fit_partials(h->G, h->Yl.p, h->lam.p, h->W.p, h->fitp.p, st);
         TvIterScalars sc{h->obj.p, h->res.p, h->rel.p, h->status.p};
-        launch_tv_finalize(0, h->fitp.p, h->fit_blocks, h->stp.p, h->st_blocks, nullptr, 0,
+        launch_tv_finalize(0, h->fitp.p, fit_blocks(h->G), h->stp.p, h->st_blocks, nullptr, 0,
                            h->lambda, 1e-8, sc, h->init_obj.p, st);
     } catch (...) {
         delete h;
@@ -1122,15 +1143,23 @@ static void tv_step(vsr_tv* h) {
     const double s = inv_sqrt_count(hr);
     // theta_hat = fft3(theta); k_hat = data_hat + mu theta_hat (:374-375), folded x-update (:376)
     Profiler* prof = h->ctx->prof();
-    fft_engine().forward3(hr, h->theta.p, IN_REAL, h->W.p, s, st, prof);
     GammaTables tabs{h->tnr.p, h->tnc.p, h->tns.p, h->tau};
-    {
+    const bool fused = use_fused(h->G);
+    if (fused) {
+        fft_engine().forward12(hr, h->theta.p, IN_REAL, h->W.p, st, prof);
+        ProfScope ps(prof, "tv_fft3_fold_ifft3", st);
+        launch_tv_sandwich(h->G, h->Yl.p, h->lam.p, h->W.p, tabs, h->mu, s, h->fitp.p, st);
+    } else {
+        fft_engine().forward3(hr, h->theta.p, IN_REAL, h->W.p, s, st, prof);
         ProfScope ps(prof, "tv_fold", st);
         launch_tv_fold(h->G, h->Yl.p, h->lam.p, h->W.p, h->W.p, nullptr, tabs, h->mu, h->fitp.p, st);
     }
     if (h->rel_tol > 0.0) std::swap(h->x, h->xprev);  // x_prev = x (:364)
     PassReduce red{h->resp.p, h->bad.p};
-    fft_engine().inverse3(hr, h->W.p, h->x.p, OUT_REAL, s, &red, st, prof);
+    if (fused)
+        fft_engine().inverse21(hr, h->W.p, h->x.p, OUT_REAL, s, &red, st, prof);
+    else
+        fft_engine().inverse3(hr, h->W.p, h->x.p, OUT_REAL, s, &red, st, prof);
     g_fwd += 1;
     g_inv += 1;
     double* din = h->dual_in_a ? h->dualA.p : h->dualB.p;
@@ -1145,7 +1174,8 @@ static void tv_step(vsr_tv* h) {
     TvIterScalars sc{h->obj.p, h->res.p, h->rel.p, h->status.p};
     {
         ProfScope ps(prof, "tv_finalize", st);
-        launch_tv_finalize((int)h->iters_done, h->fitp.p, h->fit_blocks, h->stp.p, h->st_blocks,
+        launch_tv_finalize((int)h->iters_done, h->fitp.p, fused ? tv_sandwich_blocks(h->G) : h->fit_blocks,
+                       h->stp.p, h->st_blocks,
                            h->resp.p, h->res_blocks, h->lambda, 1e-8, sc, nullptr, st);
     }
     ++h->iters_done;

@@ -9,75 +9,12 @@
 #include <cmath>
 
 #include "fft.cuh"
+#include "fft_core.cuh"
 
 namespace vsr {
 namespace {
 
-// ------------------------------------------------------------ register DFTs
-__device__ constexpr double kC8[8] = {1.0,
-                                               0.9807852804032304,
-                                               0.9238795325112867,
-                                               0.8314696123025452,
-                                               0.7071067811865476,
-                                               0.5555702330196022,
-                                               0.3826834323650898,
-                                               0.19509032201612828};
-
-// exp(-+2 pi i k / 32) * v, k in [0, 16); k is a compile-time constant after
-// unrolling so every branch below folds away.
-template <bool INV>
-__device__ __forceinline__ double2 twiddle32(double2 v, int k) {
-    if (k == 0) return v;
-    if (k == 8) return INV ? make_double2(-v.y, v.x) : make_double2(v.y, -v.x);
-    double c, s;  // cos, sin of 2*pi*k/32
-    if (k < 8) {
-        c = kC8[k];
-        s = kC8[8 - k];
-    } else {
-        c = -kC8[16 - k];
-        s = kC8[k - 8];
-    }
-    // forward: v * (c - i s); inverse: v * (c + i s)
-    if (INV) return make_double2(v.x * c - v.y * s, v.y * c + v.x * s);
-    return make_double2(v.x * c + v.y * s, v.y * c - v.x * s);
-}
-
-template <int R>
-__host__ __device__ constexpr int bitrev(int i) {
-    int r = 0;
-    for (int b = 1; b < R; b <<= 1) {
-        r = (r << 1) | (i & 1);
-        i >>= 1;
-    }
-    return r;
-}
-
-// In-register radix-R DFT (R = 1..32, power of two), natural order in/out.
-template <int R, bool INV>
-__device__ __forceinline__ void dft_reg(double2* a) {
-    if constexpr (R > 1) {
-    double2 b[R];
-#pragma unroll
-    for (int i = 0; i < R; ++i) b[bitrev<R>(i)] = a[i];
-#pragma unroll
-    for (int h = 1; h < R; h <<= 1) {
-#pragma unroll
-        for (int i = 0; i < R; i += 2 * h) {
-#pragma unroll
-            for (int j = 0; j < h; ++j) {
-                const double2 u = b[i + j];
-                const double2 t = twiddle32<INV>(b[i + j + h], j * (16 / h));
-                b[i + j] = cadd(u, t);
-                b[i + j + h] = csub(u, t);
-            }
-        }
-    }
-#pragma unroll
-    for (int i = 0; i < R; ++i) a[i] = b[i];
-    }
-}
-
-__host__ __device__ constexpr int ilog2(int v) { return v <= 1 ? 0 : 1 + ilog2(v >> 1); }
+using fftc::ilog2;
 
 // ------------------------------------------------------------ pass kernel
 // Kernel shape: a CTA owns NL = TG * T lines of length L.  Each line is served
@@ -159,81 +96,23 @@ __global__ void __launch_bounds__(PassShape<L, R, T, TG, CONTIG>::THREADS)
         for (int r = 0; r < R; ++r) v[r] = make_double2(0.0, 0.0);
     }
 
-    int Ns = 1;
-#pragma unroll
-    for (int stage = 0; stage < Sh::NSTAGE; ++stage) {
-        const bool last = stage == Sh::NSTAGE - 1;
-        const int RS = (stage < Sh::K) ? R : Sh::RL;
-        const int NB = R / RS;  // butterflies per thread
-        // -- twiddle + butterfly for each of this thread's butterflies
-#pragma unroll
-        for (int vv = 0; vv < NB; ++vv) {
-            const int u = t + P * vv;
-            const int k = u & (Ns - 1);
-            if (stage > 0) {
-                const int tstride = L / (Ns * RS);
-#pragma unroll
-                for (int r = 1; r < R; ++r) {
-                    if (r < RS) {
-                        const double2 w = __ldg(tw + ((r * k * tstride) & (L - 1)));
-                        const double2 a = v[vv * RS + r];
-                        v[vv * RS + r] = INV ? cmulc(w, a) : cmul(w, a);
-                    }
-                }
-            }
-            if (RS == R)
-                dft_reg<R, INV>(v);
-            else if (RS == Sh::RL)
-                dft_reg<(Sh::RL > 1 ? Sh::RL : 1), INV>(v + vv * RS);
-        }
-        if (!last) {
-            // -- Stockham store to smem, then gather next stage inputs
-#pragma unroll
-            for (int vv = 0; vv < NB; ++vv) {
-                const int u = t + P * vv;
-                const int k = u & (Ns - 1);
-                const int ob = (u - k) * RS + k;
-#pragma unroll
-                for (int r = 0; r < R; ++r)
-                    if (r < RS) sm[Sh::sidx(ls, ob + r * Ns)] = v[vv * RS + r];
-            }
-            __syncthreads();
-            Ns *= RS;
-            const int RSn = (stage + 1 < Sh::K) ? R : Sh::RL;
-            const int NBn = R / RSn;
-#pragma unroll
-            for (int vv = 0; vv < NBn; ++vv) {
-                const int u = t + P * vv;
-#pragma unroll
-                for (int r = 0; r < R; ++r)
-                    if (r < RSn) v[vv * RSn + r] = sm[Sh::sidx(ls, u + (L / RSn) * r)];
-            }
-            __syncthreads();
-        } else {
-            Ns *= RS;
-        }
-    }
+    fftc::stockham<L, INV>(v, t, sm, [&](int q) { return Sh::sidx(ls, q); }, tw);
 
-    // ---- store: last stage wrote q = u + (L / RS_last) * r, u = t + P * vv
-    constexpr int RSL = (Sh::RL > 1) ? Sh::RL : R;
-    constexpr int NBL = R / RSL;
+    // ---- store (output order: slot j holds line position Plan<L>::out_q(t, j))
     double acc_im = 0.0, acc_tot = 0.0;
     if (active) {
 #pragma unroll
-        for (int vv = 0; vv < NBL; ++vv) {
-#pragma unroll
-            for (int r = 0; r < RSL; ++r) {
-                const int q = t + P * vv + (L / RSL) * r;
-                const long long off = base + estride * (long long)q;
-                double2 z = cscale(v[vv * RSL + r], scale);
-                if constexpr (OK == OUT_REAL) {
-                    acc_im += z.y * z.y;
-                    acc_tot += z.x * z.x + z.y * z.y;
-                    reinterpret_cast<double*>(out_)[off] = z.x;
-                    if (!isfinite(z.x)) atomicMin(bad_index, (unsigned long long)off);
-                } else {
-                    reinterpret_cast<double2*>(out_)[off] = z;
-                }
+        for (int j = 0; j < R; ++j) {
+            const int q = fftc::Plan<L>::out_q(t, j);
+            const long long off = base + estride * (long long)q;
+            const double2 z = cscale(v[j], scale);
+            if constexpr (OK == OUT_REAL) {
+                acc_im += z.y * z.y;
+                acc_tot += z.x * z.x + z.y * z.y;
+                reinterpret_cast<double*>(out_)[off] = z.x;
+                if (!isfinite(z.x)) atomicMin(bad_index, (unsigned long long)off);
+            } else {
+                reinterpret_cast<double2*>(out_)[off] = z;
             }
         }
     }
@@ -466,10 +345,19 @@ void FftEngine::axis_pass(const Dims& d, int axis, bool inverse, const void* in,
                 else if (ik == IN_COMPLEX && ok == OUT_COMPLEX)
                     done = dispatch_L<true, true, IN_COMPLEX, OUT_COMPLEX>(L, S, units, in, out, tw, scale, red, st);
             }
-        } else if (ik == IN_COMPLEX && ok == OUT_COMPLEX) {
+        } else {
             const long long units = pass_units<false>(L, S, total);
-            done = inverse ? dispatch_L<false, true, IN_COMPLEX, OUT_COMPLEX>(L, S, units, in, out, tw, scale, red, st)
-                           : dispatch_L<false, false, IN_COMPLEX, OUT_COMPLEX>(L, S, units, in, out, tw, scale, red, st);
+            if (!inverse) {
+                if (ik == IN_COMPLEX && ok == OUT_COMPLEX)
+                    done = dispatch_L<false, false, IN_COMPLEX, OUT_COMPLEX>(L, S, units, in, out, tw, scale, red, st);
+                else if (ik == IN_REAL && ok == OUT_COMPLEX)
+                    done = dispatch_L<false, false, IN_REAL, OUT_COMPLEX>(L, S, units, in, out, tw, scale, red, st);
+            } else {
+                if (ik == IN_COMPLEX && ok == OUT_COMPLEX)
+                    done = dispatch_L<false, true, IN_COMPLEX, OUT_COMPLEX>(L, S, units, in, out, tw, scale, red, st);
+                else if (ik == IN_COMPLEX && ok == OUT_REAL)
+                    done = dispatch_L<false, true, IN_COMPLEX, OUT_REAL>(L, S, units, in, out, tw, scale, red, st);
+            }
         }
         if (done) return;
     }
@@ -533,6 +421,30 @@ void FftEngine::inverse3(const Dims& d, double2* in, void* out, OutKind ok, doub
     {
         ProfScope ps(prof, ok == OUT_REAL ? "fft_inv_axis1_c2r" : "fft_inv_axis1", st);
         axis_pass(d, 0, true, in, IN_COMPLEX, out, ok, scale, red, st);
+    }
+}
+
+void FftEngine::inverse21(const Dims& d, double2* in, void* out, OutKind ok, double scale,
+                          const PassReduce* red, cudaStream_t st, Profiler* prof) {
+    {
+        ProfScope ps(prof, "fft_inv_axis2", st);
+        axis_pass(d, 1, true, in, IN_COMPLEX, in, OUT_COMPLEX, 1.0, nullptr, st);
+    }
+    {
+        ProfScope ps(prof, ok == OUT_REAL ? "fft_inv_axis1_c2r" : "fft_inv_axis1", st);
+        axis_pass(d, 0, true, in, IN_COMPLEX, out, ok, scale, red, st);
+    }
+}
+
+void FftEngine::forward12(const Dims& d, const void* in, InKind ik, double2* out, cudaStream_t st,
+                          Profiler* prof) {
+    {
+        ProfScope ps(prof, ik == IN_REAL ? "fft_fwd_axis1_r2c" : "fft_fwd_axis1", st);
+        axis_pass(d, 0, false, in, ik, out, OUT_COMPLEX, 1.0, nullptr, st);
+    }
+    {
+        ProfScope ps(prof, "fft_fwd_axis2", st);
+        axis_pass(d, 1, false, out, IN_COMPLEX, out, OUT_COMPLEX, 1.0, nullptr, st);
     }
 }
 

@@ -51,6 +51,14 @@ public:
     void inverse3(const Dims& d, double2* in, void* out, OutKind ok, double scale,
                   const PassReduce* red, cudaStream_t st, Profiler* prof = nullptr);
 
+    // Inverse passes 2 then 1 only (axis 3 already done, e.g. by a fused
+    // fold kernel): axis 2 in place on `in`, axis 1 writes `out`.
+    void inverse21(const Dims& d, double2* in, void* out, OutKind ok, double scale,
+                   const PassReduce* red, cudaStream_t st, Profiler* prof = nullptr);
+    // Forward passes 1 then 2 only (axis 3 left to a fused kernel).
+    void forward12(const Dims& d, const void* in, InKind ik, double2* out, cudaStream_t st,
+                   Profiler* prof = nullptr);
+
     // Blocks of the final (axis-1) pass of inverse3.
     size_t inverse_final_blocks(const Dims& d) const { return pass_blocks(d, 0); }
 

@@ -206,6 +206,92 @@ __global__ void __launch_bounds__(kFoldThreads)
     }
 }
 
+// Large-d TV fold: a CTA owns 32 consecutive LR frequencies x BG alias groups;
+// each thread keeps AP = d / BG aliases in registers (one HBM read each).
+// Partial sums over a group are combined in fixed group order through shared
+// memory, so results are deterministic (the association differs from the
+// reference's single running sum only at rounding level).
+template <int BG, int AP, bool GTAB, bool FIT>
+__global__ void __launch_bounds__(32 * BG)
+    tv_fold_grouped_kernel(FoldGeom G, const double2* __restrict__ Yl, const double2* __restrict__ lam,
+                           const double2* th, double2* xh, const double* __restrict__ gam,
+                           GammaTables tabs, double mu, double inv_mu, double shift, double invsqrtd,
+                           double* __restrict__ fit_partials) {
+    __shared__ double2 sS[BG][32];
+    __shared__ double sG[BG][32];
+    __shared__ double red[32];
+    const long long Nl = G.ml * G.nl * G.sl;
+    const int lane = threadIdx.x & 31, grp = threadIdx.x >> 5;
+    const long long g = (long long)blockIdx.x * 32 + lane;
+    const bool ok = g < Nl;
+    const LrPos p = lr_pos(G, ok ? g : 0);
+    const double2 yraw = ok ? Yl[g] : make_double2(0.0, 0.0);
+    const double2 yv = cscale(yraw, invsqrtd);
+    double2 Lc[AP], gc[AP];
+    double Gm[AP];
+    long long fi[AP];
+    double2 S = make_double2(0.0, 0.0);
+    double gram = 0.0;
+#pragma unroll
+    for (int a = 0; a < AP; ++a) {
+        long long f1, f2, f3;
+        fi[a] = alias_index(G, p, grp * AP + a, &f1, &f2, &f3);
+        if (ok) {
+            Lc[a] = __ldg(lam + fi[a]);
+            if constexpr (GTAB)
+                Gm[a] = 1.0 / (((__ldg(tabs.nr + f1) + __ldg(tabs.nc + f2)) + __ldg(tabs.ns + f3)) + tabs.tau);
+            else
+                Gm[a] = __ldg(gam + fi[a]);
+        } else {
+            Lc[a] = make_double2(0.0, 0.0);
+            Gm[a] = 0.0;
+        }
+    }
+#pragma unroll
+    for (int a = 0; a < AP; ++a) {
+        const double2 T = ok ? th[fi[a]] : make_double2(0.0, 0.0);
+        const double2 k = cadd(cmulc(Lc[a], yv), cscale(T, mu));
+        gc[a] = cscale(k, Gm[a]);
+        S = cadd(S, cmul(Lc[a], gc[a]));
+        gram += Gm[a] * cnorm(Lc[a]);
+    }
+    sS[grp][lane] = S;
+    sG[grp][lane] = gram;
+    __syncthreads();
+    double2 St = sS[0][lane];
+    double Gt = sG[0][lane];
+#pragma unroll
+    for (int b = 1; b < BG; ++b) {
+        St = cadd(St, sS[b][lane]);
+        Gt += sG[b][lane];
+    }
+    const double den = Gt + shift;
+    const double2 w = make_double2(St.x / den, St.y / den);
+    double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int a = 0; a < AP; ++a) {
+        const double2 corr = cmul(make_double2(Gm[a] * Lc[a].x, -(Gm[a] * Lc[a].y)), w);
+        const double2 xv = cscale(csub(gc[a], corr), inv_mu);
+        if (ok) xh[fi[a]] = xv;
+        if constexpr (FIT) acc = cadd(acc, cmul(Lc[a], xv));
+    }
+    if constexpr (FIT) {
+        __syncthreads();
+        sS[grp][lane] = acc;
+        __syncthreads();
+        double fit = 0.0;
+        if (grp == 0 && ok) {
+            double2 At = sS[0][lane];
+#pragma unroll
+            for (int b = 1; b < BG; ++b) At = cadd(At, sS[b][lane]);
+            fit = cnorm(csub(yraw, cscale(At, invsqrtd)));
+        }
+        double v[1] = {fit};
+        block_reduce_sum<1>(v, red);
+        if (threadIdx.x == 0) fit_partials[blockIdx.x] = v[0];
+    }
+}
+
 __global__ void __launch_bounds__(kFoldThreads)
     fit_kernel(FoldGeom G, const double2* __restrict__ Yl, const double2* __restrict__ lam,
                const double2* __restrict__ xh, double invsqrtd, double* __restrict__ partials) {
@@ -332,7 +418,10 @@ void launch_tik_fold(const FoldGeom& G, const double2* Yl, const double2* lam, c
     VSR_LAUNCH_CHECK();
 }
 
-size_t tv_fold_blocks(const FoldGeom& G) { return lr_blocks(G); }
+
+
+size_t tv_fold_blocks_for(const FoldGeom& G);
+size_t tv_fold_blocks(const FoldGeom& G) { return tv_fold_blocks_for(G); }
 
 void launch_tv_fold(const FoldGeom& G, const double2* Yl, const double2* lam, const double2* th,
                     double2* xh, const double* gam, const GammaTables& tabs, double mu,
@@ -352,17 +441,40 @@ void launch_tv_fold(const FoldGeom& G, const double2* Yl, const double2* lam, co
     else if (gtab) VSR_TV(DCV, true, false);    \
     else if (fit) VSR_TV(DCV, false, true);     \
     else VSR_TV(DCV, false, false);
+    const long long Nl = G.ml * G.nl * G.sl;
+    const unsigned gblocks = (unsigned)((Nl + 31) / 32);
+#define VSR_TVG(BG, GT, FT)                                                                          \
+    tv_fold_grouped_kernel<BG, 8, GT, FT><<<gblocks, 32 * BG, 0, st>>>(G, Yl, lam, th, xh, gam, tabs, mu, \
+                                                                        inv_mu, shift, invsqrtd, fit_partials)
+#define VSR_TVG_B(BG)                            \
+    if (gtab && fit) VSR_TVG(BG, true, true);    \
+    else if (gtab) VSR_TVG(BG, true, false);     \
+    else if (fit) VSR_TVG(BG, false, true);      \
+    else VSR_TVG(BG, false, false);
     switch (G.d) {
         case 1: VSR_TV_D(1); break;
         case 2: VSR_TV_D(2); break;
         case 4: VSR_TV_D(4); break;
         case 8: VSR_TV_D(8); break;
+        case 16: VSR_TVG_B(2); break;
+        case 32: VSR_TVG_B(4); break;
+        case 64: VSR_TVG_B(8); break;
         default: VSR_TV_D(0); break;
     }
+#undef VSR_TVG_B
+#undef VSR_TVG
 #undef VSR_TV_D
 #undef VSR_TV
     VSR_LAUNCH_CHECK();
 }
+
+size_t tv_fold_blocks_for(const FoldGeom& G) {
+    const long long Nl = G.ml * G.nl * G.sl;
+    if (G.d == 16 || G.d == 32 || G.d == 64) return (size_t)((Nl + 31) / 32);
+    return lr_blocks(G);
+}
+
+size_t fit_blocks(const FoldGeom& G) { return lr_blocks(G); }
 
 void launch_fit_partials(const FoldGeom& G, const double2* Yl, const double2* lam,
                          const double2* xh, double* fit_partials, cudaStream_t st) {

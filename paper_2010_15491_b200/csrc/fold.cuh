@@ -43,6 +43,7 @@ void launch_tv_fold(const FoldGeom& G, const double2* Yl, const double2* lam, co
                     double* fit_partials, cudaStream_t st);
 
 // ---- data fit only: per-block partials of ||Yl - (1/sqrt d) sum_b Lambda_b Xh_b||^2
+size_t fit_blocks(const FoldGeom& G);
 void launch_fit_partials(const FoldGeom& G, const double2* Yl, const double2* lam,
                          const double2* xh, double* fit_partials, cudaStream_t st);
 

@@ -1,0 +1,34 @@
+// Fused spectral-fold + axis-3 FFT kernels.
+//
+// The d aliases of an LR frequency g = (g1, g2, g3) sit at HR frequencies
+// (g1 + br ml, g2 + bc nl, g3 + bs sl).  A CTA owns T consecutive g1 x one g2
+// and the A = dr*dc axis-3 lines through their (br, bc) aliases, full length
+// s: the bs aliases of every g3 then lie in one thread's registers and the
+// (br, bc) aliases in lanes of one warp.  So the fold needs no extra HBM pass:
+//   Tikhonov: x̂ = fold(Lambda, X̄, Ŷ) -> inverse axis-3 FFT        (one pass)
+//   TV      : W -> forward axis-3 FFT -> fold -> inverse axis-3 FFT (one pass)
+#pragma once
+
+#include "fold.cuh"
+
+namespace vsr {
+
+// Whether the fused kernels cover this geometry (otherwise callers use the
+// separate fold + axis-pass kernels).
+bool fused_axis3_ok(const FoldGeom& G);
+
+// out = IFFT_axis3(x̂) (unscaled) with x̂ from TikhonovOperator::solve's fold
+// (solvers.cpp:53-62).  out must not alias lam / xbh.
+void launch_tik_fold_ifft3(const FoldGeom& G, const double2* Yl, const double2* lam,
+                           const double2* xbh, double2* out, double reg, cudaStream_t st);
+
+// In place on W (spectrum after forward axes 1,2): forward axis-3 FFT scaled
+// by fwd_scale, TV x-update fold (solvers.cpp:219-233 with k̂ = data_hat +
+// mu theta_hat), inverse axis-3 FFT (unscaled).  fit_partials: one double per
+// block (||y - D H x||^2 by LR Parseval), sized by tv_sandwich_blocks().
+size_t tv_sandwich_blocks(const FoldGeom& G);
+void launch_tv_sandwich(const FoldGeom& G, const double2* Yl, const double2* lam, double2* W,
+                        const GammaTables& tabs, double mu, double fwd_scale, double* fit_partials,
+                        cudaStream_t st);
+
+}  // namespace vsr

@@ -42,15 +42,39 @@ __device__ __forceinline__ Shrunk shrink_point(double l0, double l1, double l2, 
     return o;
 }
 
+__device__ __forceinline__ void cp_async8(double* smem_dst, const double* gsrc) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem_dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+constexpr int XW = TX + 2, XH = TY + 2;  // x plane with halo [-1, TX] x [-1, TY]
+constexpr int DW = TX + 1, DH = TY + 1;  // dual plane with low halo [-1, TX) x [-1, TY)
+constexpr int NSLOT = 4;                  // plane ring: compute k, k+1; in flight k+2, k+3
+
+__host__ __device__ constexpr size_t stencil_smem_doubles(bool init) {
+    return (size_t)NSLOT * XH * XW + (init ? 0 : (size_t)NSLOT * 3 * DH * DW) + TY * (TX + 1) +
+           (TY + 1) * TX;
+}
+
+// cp.async-pipelined march along axis 3: the x plane (with halo) and the three
+// dual planes (with low halo) of z = k+3 are requested while plane k is
+// computed, so one kernel keeps ~3 planes of loads in flight per CTA.
 template <bool INIT, bool RELCHG>
 __global__ void __launch_bounds__(STH)
     tv_stencil_kernel(int m, int n, int s, int KC, const double* __restrict__ x,
                       const double* __restrict__ dual_in, double* __restrict__ dual_out,
                       double* __restrict__ theta, double thr, const double* __restrict__ xprev,
                       double* __restrict__ partials) {
-    __shared__ double xs[2][TY + 2][TX + 2];
-    __shared__ double rx[TY][TX + 1];
-    __shared__ double ry[TY + 1][TX];
+    extern __shared__ double sm[];
+    double* xs = sm;                                            // [NSLOT][XH][XW]
+    double* ds = xs + NSLOT * XH * XW;                          // [NSLOT][3][DH][DW]
+    double* rx = ds + (INIT ? 0 : NSLOT * 3 * DH * DW);         // [TY][TX+1]
+    double* ry = rx + TY * (TX + 1);                            // [TY+1][TX]
     __shared__ double red[32 * 4];
 
     const int tid = threadIdx.x;
@@ -64,125 +88,137 @@ __global__ void __launch_bounds__(STH)
     const bool valid = gi < m && gj < n;
     const long long col = valid ? (long long)gi + (long long)m * gj : 0;
 
-    auto load_plane = [&](int buf, int kz) {
-        const long long zoff = plane * wrapi(kz, s);
-        for (int e = tid; e < (TY + 2) * (TX + 2); e += STH) {
-            const int jj = e / (TX + 2) - 1, ii = e % (TX + 2) - 1;
-            const int gx = wrapi((long long)i0 + ii, m), gy = wrapi((long long)j0 + jj, n);
-            xs[buf][jj + 1][ii + 1] = __ldg(x + gx + (long long)m * gy + zoff);
+    // per-thread load assignments (independent of z): 2 x elements, 2 dual elements
+    long long xo[2], dof[2];
+    bool xa[2], da[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+        const int e = tid + q * STH;
+        xa[q] = e < XH * XW;
+        const int jj = (xa[q] ? e : 0) / XW - 1, ii = (xa[q] ? e : 0) % XW - 1;
+        xo[q] = (long long)wrapi((long long)i0 + ii, m) + (long long)m * wrapi((long long)j0 + jj, n);
+        da[q] = e < DH * DW;
+        const int dj = (da[q] ? e : 0) / DW - 1, di = (da[q] ? e : 0) % DW - 1;
+        dof[q] = (long long)wrapi((long long)i0 + di, m) + (long long)m * wrapi((long long)j0 + dj, n);
+    }
+    auto issue = [&](int z) {
+        const int slot = (z - (k0 - 1)) & (NSLOT - 1);
+        const long long zoff = plane * wrapi(z, s);
+        double* xsl = xs + slot * XH * XW;
+#pragma unroll
+        for (int q = 0; q < 2; ++q)
+            if (xa[q]) cp_async8(xsl + tid + q * STH, x + xo[q] + zoff);
+        if (!INIT && z < k1) {
+            double* dsl = ds + slot * 3 * DH * DW;
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+#pragma unroll
+                for (int q = 0; q < 2; ++q)
+                    if (da[q]) cp_async8(dsl + c * DH * DW + tid + q * STH, dual_in + c * N + dof[q] + zoff);
         }
+        cp_async_commit();
     };
 
     double acc_res = 0.0, acc_tv = 0.0, acc_dx = 0.0, acc_xp = 0.0;
     double rz_prev = 0.0;
 
-    load_plane(0, k0 - 1);
-    load_plane(1, k0);
+    issue(k0 - 1);
+    issue(k0);
+    issue(k0 + 1);
     for (int k = k0 - 1; k < k1; ++k) {
-        const int bc = (k - k0 + 1) & 1, bn = bc ^ 1;
-        const bool warm = k < k0;
-        if (!warm) {
-            load_plane(bn, k + 1);
-        }
+        if (k + 3 <= k1)
+            issue(k + 3);
+        else
+            cp_async_commit();
+        cp_async_wait<2>();
         __syncthreads();
+        const bool warm = k < k0;
+        const int sc = (k - (k0 - 1)) & (NSLOT - 1), sn = (sc + 1) & (NSLOT - 1);
+        const double* X0 = xs + sc * XH * XW;
+        const double* X1 = xs + sn * XH * XW;
+        const double* D0 = ds + sc * 3 * DH * DW;
         const long long zoff = plane * wrapi(k, s);
 
-        // ---- interior point
-        {
-            const double xc = xs[bc][ty + 1][tx + 1];
-            const double l0 = xs[bc][ty + 1][tx + 2] - xc;
-            const double l1 = xs[bc][ty + 2][tx + 1] - xc;
-            const double l2 = xs[bn][ty + 1][tx + 1] - xc;
-            double r0, r1, r2;
-            if constexpr (INIT) {
-                r0 = l0;
-                r1 = l1;
-                r2 = l2;
-                if (!warm && valid) {
-                    const long long idx = col + zoff;
-                    dual_out[idx] = 0.0;
-                    dual_out[N + idx] = 0.0;
-                    dual_out[2 * N + idx] = 0.0;
-                    acc_tv += sqrt(l0 * l0 + l1 * l1 + l2 * l2);
-                }
-            } else {
-                const long long idx = col + zoff;
-                double d0 = 0.0, d1 = 0.0, d2 = 0.0;
-                if (valid) {
-                    d0 = __ldg(dual_in + idx);
-                    d1 = __ldg(dual_in + N + idx);
-                    d2 = __ldg(dual_in + 2 * N + idx);
-                }
-                const Shrunk o = shrink_point(l0, l1, l2, d0, d1, d2, thr);
-                r0 = o.r0;
-                r1 = o.r1;
-                r2 = o.r2;
-                if (!warm && valid) {
-                    dual_out[idx] = o.dn0;
-                    dual_out[N + idx] = o.dn1;
-                    dual_out[2 * N + idx] = o.dn2;
-                    const double e0 = l0 - o.u0, e1 = l1 - o.u1, e2 = l2 - o.u2;
-                    acc_res += e0 * e0 + e1 * e1 + e2 * e2;
-                    acc_tv += sqrt(l0 * l0 + l1 * l1 + l2 * l2);
-                }
-            }
-            if constexpr (RELCHG) {
-                if (!warm && valid) {
-                    const double xp = __ldg(xprev + col + zoff);
-                    const double dd = xc - xp;
-                    acc_dx += dd * dd;
-                    acc_xp += xp * xp;
-                }
-            }
-            rx[ty][tx + 1] = r0;
-            ry[ty + 1][tx] = r1;
-            // r2 is this plane's rho_z; theta needs rho_z of the previous plane
-            if (!warm) {
-                // halo points: rho_x at ii = -1 (jj = tid < TY), rho_y at jj = -1 (ii = tid - TY)
-                if (tid < TY + TX) {
-                    int ii, jj;
-                    if (tid < TY) {
-                        ii = -1;
-                        jj = tid;
-                    } else {
-                        ii = tid - TY;
-                        jj = -1;
-                    }
-                    const double hc = xs[bc][jj + 1][ii + 1];
-                    const double h0 = xs[bc][jj + 1][ii + 2] - hc;
-                    const double h1 = xs[bc][jj + 2][ii + 1] - hc;
-                    const double h2 = xs[bn][jj + 1][ii + 1] - hc;
-                    double q0, q1;
-                    if constexpr (INIT) {
-                        q0 = h0;
-                        q1 = h1;
-                    } else {
-                        const long long hidx = (long long)wrapi((long long)i0 + ii, m) +
-                                               (long long)m * wrapi((long long)j0 + jj, n) + zoff;
-                        const Shrunk o = shrink_point(h0, h1, h2, __ldg(dual_in + hidx),
-                                                      __ldg(dual_in + N + hidx),
-                                                      __ldg(dual_in + 2 * N + hidx), thr);
-                        q0 = o.r0;
-                        q1 = o.r1;
-                    }
-                    if (tid < TY)
-                        rx[jj][0] = q0;
-                    else
-                        ry[0][ii] = q1;
-                }
-            }
-            __syncthreads();
+        // ---- interior point (tx, ty)
+        const double xc = X0[(ty + 1) * XW + tx + 1];
+        const double l0 = X0[(ty + 1) * XW + tx + 2] - xc;
+        const double l1 = X0[(ty + 2) * XW + tx + 1] - xc;
+        const double l2 = X1[(ty + 1) * XW + tx + 1] - xc;
+        double r0, r1, r2;
+        if constexpr (INIT) {
+            r0 = l0;
+            r1 = l1;
+            r2 = l2;
             if (!warm && valid) {
-                // diff_adjoint sum in axis order (solvers.cpp:367-373): ((adj_x) + adj_y) + adj_z
-                const double ax = rx[ty][tx] - rx[ty][tx + 1];
-                const double ay = ry[ty][tx] - ry[ty + 1][tx];
-                const double az = rz_prev - r2;
-                theta[col + zoff] = (ax + ay) + az;
+                const long long idx = col + zoff;
+                dual_out[idx] = 0.0;
+                dual_out[N + idx] = 0.0;
+                dual_out[2 * N + idx] = 0.0;
+                acc_tv += sqrt(l0 * l0 + l1 * l1 + l2 * l2);
             }
-            rz_prev = r2;
+        } else {
+            const int di = (ty + 1) * DW + tx + 1;
+            const Shrunk o = shrink_point(l0, l1, l2, D0[di], D0[DH * DW + di], D0[2 * DH * DW + di], thr);
+            r0 = o.r0;
+            r1 = o.r1;
+            r2 = o.r2;
+            if (!warm && valid) {
+                const long long idx = col + zoff;
+                dual_out[idx] = o.dn0;
+                dual_out[N + idx] = o.dn1;
+                dual_out[2 * N + idx] = o.dn2;
+                const double e0 = l0 - o.u0, e1 = l1 - o.u1, e2 = l2 - o.u2;
+                acc_res += e0 * e0 + e1 * e1 + e2 * e2;
+                acc_tv += sqrt(l0 * l0 + l1 * l1 + l2 * l2);
+            }
+        }
+        if constexpr (RELCHG) {
+            if (!warm && valid) {
+                const double xp = __ldg(xprev + col + zoff);
+                const double dd = xc - xp;
+                acc_dx += dd * dd;
+                acc_xp += xp * xp;
+            }
+        }
+        if (!warm) {
+            rx[ty * (TX + 1) + tx + 1] = r0;
+            ry[(ty + 1) * TX + tx] = r1;
+            // halo: rho_x at ii = -1 (jj = tid < TY), rho_y at jj = -1 (ii = tid - TY)
+            if (tid < TY + TX) {
+                const int ii = tid < TY ? -1 : tid - TY;
+                const int jj = tid < TY ? tid : -1;
+                const double hc = X0[(jj + 1) * XW + ii + 1];
+                const double h0 = X0[(jj + 1) * XW + ii + 2] - hc;
+                const double h1 = X0[(jj + 2) * XW + ii + 1] - hc;
+                const double h2 = X1[(jj + 1) * XW + ii + 1] - hc;
+                double q0, q1;
+                if constexpr (INIT) {
+                    q0 = h0;
+                    q1 = h1;
+                } else {
+                    const int hi = (jj + 1) * DW + ii + 1;
+                    const Shrunk o =
+                        shrink_point(h0, h1, h2, D0[hi], D0[DH * DW + hi], D0[2 * DH * DW + hi], thr);
+                    q0 = o.r0;
+                    q1 = o.r1;
+                }
+                if (tid < TY)
+                    rx[jj * (TX + 1)] = q0;
+                else
+                    ry[ii] = q1;
+            }
         }
         __syncthreads();
+        if (!warm && valid) {
+            // diff_adjoint sum in axis order (solvers.cpp:367-373): ((adj_x) + adj_y) + adj_z
+            const double ax = rx[ty * (TX + 1) + tx] - rx[ty * (TX + 1) + tx + 1];
+            const double ay = ry[ty * TX + tx] - ry[(ty + 1) * TX + tx];
+            const double az = rz_prev - r2;
+            theta[col + zoff] = (ax + ay) + az;
+        }
+        rz_prev = r2;
     }
+    cp_async_wait<0>();
 
     double v[4] = {acc_res, acc_tv, acc_dx, acc_xp};
     block_reduce_sum<4>(v, red);
@@ -348,15 +384,16 @@ void launch_tv_stencil(const Dims& d, bool init, const double* x, const double* 
                        double* partials, cudaStream_t st) {
     const StencilGeom g = stencil_geom(d);
     const int m = (int)d.m, n = (int)d.n, s = (int)d.s;
+    const size_t smem = stencil_smem_doubles(init) * sizeof(double);
     if (init) {
-        tv_stencil_kernel<true, false><<<g.grid, STH, 0, st>>>(m, n, s, g.kc, x, dual_in, dual_out,
-                                                              theta, thr, xprev, partials);
+        tv_stencil_kernel<true, false><<<g.grid, STH, smem, st>>>(m, n, s, g.kc, x, dual_in, dual_out,
+                                                                  theta, thr, xprev, partials);
     } else if (xprev) {
-        tv_stencil_kernel<false, true><<<g.grid, STH, 0, st>>>(m, n, s, g.kc, x, dual_in, dual_out,
-                                                              theta, thr, xprev, partials);
+        tv_stencil_kernel<false, true><<<g.grid, STH, smem, st>>>(m, n, s, g.kc, x, dual_in, dual_out,
+                                                                  theta, thr, xprev, partials);
     } else {
-        tv_stencil_kernel<false, false><<<g.grid, STH, 0, st>>>(m, n, s, g.kc, x, dual_in, dual_out,
-                                                               theta, thr, xprev, partials);
+        tv_stencil_kernel<false, false><<<g.grid, STH, smem, st>>>(m, n, s, g.kc, x, dual_in, dual_out,
+                                                                   theta, thr, xprev, partials);
     }
     VSR_LAUNCH_CHECK();
 }

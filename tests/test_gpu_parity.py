@@ -129,7 +129,10 @@ def test_fold_primitives(V, O, hr, rates):
 # ------------------------------------------------------------------ Tikhonov
 TIK_CASES = [((8, 8, 8), (2, 2, 2)), ((6, 4, 4), (3, 2, 1)), ((4, 6, 4), (2, 3, 2)), ((8, 4, 4), (2, 1, 2)),
              ((12, 10, 8), (2, 2, 2)), ((32, 32, 32), (4, 4, 4)), ((64, 32, 16), (2, 2, 4)),
-             ((16, 16, 16), (1, 1, 1)), ((64, 64, 64), (8, 8, 8)), ((20, 12, 6), (5, 3, 2))]
+             ((16, 16, 16), (1, 1, 1)), ((64, 64, 64), (8, 8, 8)), ((20, 12, 6), (5, 3, 2)),
+             # geometries served by the fused fold + axis-3 FFT kernel
+             ((128, 64, 256), (2, 2, 2)), ((64, 32, 128), (2, 2, 4)), ((32, 64, 64), (4, 4, 4)),
+             ((64, 64, 1024), (2, 2, 2)), ((16, 16, 32), (1, 1, 1))]
 
 
 @pytest.mark.parametrize("dims,rates", TIK_CASES)
@@ -292,7 +295,8 @@ def test_objective_tv(V, O):
 
 # ------------------------------------------------------------------ ADMM-TV
 TV_CASES = [((8, 8, 8), (2, 2, 2), 6), ((16, 16, 16), (4, 4, 4), 10), ((32, 32, 16), (2, 2, 4), 8),
-            ((12, 10, 8), (2, 2, 2), 5), ((64, 64, 64), (4, 4, 4), 12), ((40, 24, 16), (2, 2, 2), 5)]
+            ((12, 10, 8), (2, 2, 2), 5), ((64, 64, 64), (4, 4, 4), 12), ((40, 24, 16), (2, 2, 2), 5),
+            ((32, 32, 64), (2, 2, 4), 6), ((64, 32, 128), (2, 2, 2), 4), ((32, 32, 32), (1, 1, 1), 4)]
 
 
 @pytest.mark.parametrize("dims,rates,iters", TV_CASES)
