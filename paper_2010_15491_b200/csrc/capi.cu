@@ -17,6 +17,7 @@
 #include "fft.cuh"
 #include "fold.cuh"
 #include "fused.cuh"
+#include "chain.cuh"
 #include "tv.cuh"
 
 using namespace vsr;
@@ -326,6 +327,16 @@ void require_ctx(vsr_ctx* ctx) {
 double inv_sqrt_count(const Dims& d) { return 1.0 / std::sqrt((double)d.count()); }
 
 // Fused fold + axis-3 FFT kernels unless disabled (VSR_NO_FUSE=1, for A/B runs).
+// Chained in-plane passes (chain.cuh): opt-in (VSR_CHAIN=1) until they beat
+// two plain passes (measured r01: 201 us vs 173 us at 256^3).
+bool use_chain() {
+    static const bool on = [] {
+        const char* e = std::getenv("VSR_CHAIN");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
+
 bool use_fused(const FoldGeom& G) {
     static const bool off = [] {
         const char* e = std::getenv("VSR_NO_FUSE");
@@ -735,6 +746,9 @@ struct vsr_tikhonov {
     DevBuf<double> partials, status;  // status: [violated, ratio, last ratio, pad]
     DevBuf<unsigned long long> bad;
     size_t res_blocks = 0;
+    ChainPlan chain;                  // chained inverse axes 2 -> 1 (L2 ring)
+    DevBuf<double2> ring;
+    DevBuf<int> chain_ctr;
 };
 
 static void tik_reset_status(vsr_tikhonov* t) {
@@ -761,6 +775,14 @@ static vsr_tikhonov* tik_new(vsr_ctx* ctx, const size_t hr_dims[3], const size_t
     t->y.alloc(Nl);
     t->x.alloc(N);
     t->res_blocks = fft_engine().inverse_final_blocks(sp.hr);
+    if (use_chain() && use_fused(t->G)) {
+        t->chain = chain_plan(sp.hr);
+        if (t->chain.ok) {
+            t->ring.alloc(t->chain.scratch_elems);
+            t->chain_ctr.alloc(1 + 2 * t->chain.chunks);
+            t->res_blocks = std::max(t->res_blocks, t->chain.b_total());
+        }
+    }
     t->partials.alloc(2 * std::max<size_t>(t->res_blocks, 1));
     t->status.alloc(4);
     t->bad.alloc(1);
@@ -839,8 +861,14 @@ static void tik_enqueue(vsr_tikhonov* t, const double* y_dev, double* x_dev) {
             ProfScope ps(prof, "tik_fold_ifft_axis3", st);
             launch_tik_fold_ifft3(t->G, t->Yl.p, t->lam.p, t->xbh.p, t->xh.p, t->reg, st);
         }
-        fft_engine().inverse21(t->sp.hr, t->xh.p, x_dev, OUT_REAL, inv_sqrt_count(t->sp.hr), &red,
-                               st, prof);
+        if (t->chain.ok) {
+            ProfScope ps(prof, "chain_inv_axis2_axis1_c2r", st);
+            ChainWork w{t->ring.p, t->chain_ctr.p};
+            launch_chain_inverse(t->sp.hr, t->chain, w, t->xh.p, x_dev, inv_sqrt_count(t->sp.hr), red, st);
+        } else {
+            fft_engine().inverse21(t->sp.hr, t->xh.p, x_dev, OUT_REAL, inv_sqrt_count(t->sp.hr), &red,
+                                   st, prof);
+        }
     } else {
         {
             ProfScope ps(prof, "tik_fold", st);
@@ -852,8 +880,9 @@ static void tik_enqueue(vsr_tikhonov* t, const double* y_dev, double* x_dev) {
     ++g_inv;  // the one inverse transform (solvers.cpp:64)
     {
         ProfScope ps(prof, "residue_status", st);
-        residue_status_kernel<<<1, 1024, 0, st>>>(t->partials.p, (long long)t->res_blocks, 1e-8,
-                                                  t->status.p);
+        const size_t nres = (use_fused(t->G) && t->chain.ok) ? t->chain.b_total()
+                                                               : fft_engine().inverse_final_blocks(t->sp.hr);
+        residue_status_kernel<<<1, 1024, 0, st>>>(t->partials.p, (long long)nres, 1e-8, t->status.p);
         VSR_LAUNCH_CHECK();
     }
 }
@@ -1042,6 +1071,9 @@ struct vsr_tv {
     DevBuf<unsigned long long> bad;
     DevBuf<double> obj, res, rel, status, init_obj;
     size_t fit_blocks = 0, st_blocks = 0, res_blocks = 0;
+    ChainPlan chain;
+    DevBuf<double2> ring;
+    DevBuf<int> chain_ctr;
     size_t iters_done = 0;
     bool dual_in_a = true;
     bool stopped = false;
@@ -1091,6 +1123,14 @@ static vsr_tv* tv_build(vsr_ctx* ctx, const Spec& sp, const double* y_dev, const
         h->fit_blocks = tv_fold_blocks(h->G);
         h->st_blocks = stencil_geom(hr).blocks();
         h->res_blocks = fft_engine().inverse_final_blocks(hr);
+        if (use_chain() && use_fused(h->G)) {
+            h->chain = chain_plan(hr);
+            if (h->chain.ok) {
+                h->ring.alloc(h->chain.scratch_elems);
+                h->chain_ctr.alloc(1 + 2 * h->chain.chunks);
+                h->res_blocks = h->chain.b_total();
+            }
+        }
         h->fitp.alloc(std::max<size_t>(
             std::max(std::max(h->fit_blocks, fit_blocks(h->G)), tv_sandwich_blocks(h->G)), 1));
         h->stp.alloc(kStencilVals * h->st_blocks);
@@ -1145,8 +1185,14 @@ static void tv_step(vsr_tv* h) {
     Profiler* prof = h->ctx->prof();
     GammaTables tabs{h->tnr.p, h->tnc.p, h->tns.p, h->tau};
     const bool fused = use_fused(h->G);
+    ChainWork cw{h->ring.p, h->chain_ctr.p};
     if (fused) {
-        fft_engine().forward12(hr, h->theta.p, IN_REAL, h->W.p, st, prof);
+        if (h->chain.ok) {
+            ProfScope ps(prof, "chain_fwd_axis1_r2c_axis2", st);
+            launch_chain_forward(hr, h->chain, cw, h->theta.p, h->W.p, st);
+        } else {
+            fft_engine().forward12(hr, h->theta.p, IN_REAL, h->W.p, st, prof);
+        }
         ProfScope ps(prof, "tv_fft3_fold_ifft3", st);
         launch_tv_sandwich(h->G, h->Yl.p, h->lam.p, h->W.p, tabs, h->mu, s, h->fitp.p, st);
     } else {
@@ -1156,7 +1202,10 @@ static void tv_step(vsr_tv* h) {
     }
     if (h->rel_tol > 0.0) std::swap(h->x, h->xprev);  // x_prev = x (:364)
     PassReduce red{h->resp.p, h->bad.p};
-    if (fused)
+    if (fused && h->chain.ok) {
+        ProfScope ps(prof, "chain_inv_axis2_axis1_c2r", st);
+        launch_chain_inverse(hr, h->chain, cw, h->W.p, h->x.p, s, red, st);
+    } else if (fused)
         fft_engine().inverse21(hr, h->W.p, h->x.p, OUT_REAL, s, &red, st, prof);
     else
         fft_engine().inverse3(hr, h->W.p, h->x.p, OUT_REAL, s, &red, st, prof);

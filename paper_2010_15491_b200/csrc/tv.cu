@@ -229,6 +229,206 @@ __global__ void __launch_bounds__(STH)
     }
 }
 
+// ---------------------------------------------------------------- fast path
+// Same march, for even m: planes move as aligned 16-byte pairs staged through
+// registers one step ahead (x plane k+2 and dual plane k+1 are in flight while
+// plane k is computed), all per-thread load offsets are computed once, and
+// the plane pointer advances incrementally.  ~4x fewer issued instructions
+// than the element-wise cp.async variant above.
+constexpr int FXW = TX + 4;                 // x row in smem: columns i0-2 .. i0+33
+constexpr int FDW = TX + 2;                 // dual row: columns i0-2 .. i0+31
+constexpr int FXH = TY + 2, FDH = TY + 1;   // x rows j0-1 .. j0+TY; dual rows j0-1 .. j0+TY-1
+constexpr int FXP = FXH * (FXW / 2);        // 180 x pairs per plane
+constexpr int FDP = FDH * (FDW / 2);        // 153 dual pairs per component
+constexpr int FXS = FXH * FXW, FDS = 3 * FDH * FDW;
+
+__host__ __device__ constexpr size_t fast_smem_doubles() {
+    return (size_t)3 * FXS + 2 * FDS + TY * (TX + 1) + (TY + 1) * TX;
+}
+
+template <bool INIT, bool RELCHG>
+__global__ void __launch_bounds__(STH)
+    tv_stencil_fast_kernel(int m, int n, int s, int KC, const double* __restrict__ x,
+                           const double* __restrict__ dual_in, double* __restrict__ dual_out,
+                           double* __restrict__ theta, double thr, const double* __restrict__ xprev,
+                           double* __restrict__ partials) {
+    extern __shared__ double sm[];
+    double* xs = sm;                 // [3][FXH][FXW]
+    double* ds = xs + 3 * FXS;       // [2][3][FDH][FDW]
+    double* rx = ds + 2 * FDS;       // [TY][TX+1]
+    double* ry = rx + TY * (TX + 1); // [TY+1][TX]
+    __shared__ double red[32 * 4];
+
+    const int tid = threadIdx.x;
+    const int tx = tid % TX, ty = tid / TX;
+    const int i0 = blockIdx.x * TX, j0 = blockIdx.y * TY;
+    const int k0 = blockIdx.z * KC;
+    const int k1 = min(k0 + KC, s);
+    const long long plane = (long long)m * n;
+    const long long N = plane * s;
+    const bool valid = (i0 + tx) < m && (j0 + ty) < n;
+    const int col = valid ? (i0 + tx) + m * (j0 + ty) : 0;
+
+    auto wrap = [](int v, int len) {
+        v %= len;
+        return v < 0 ? v + len : v;
+    };
+    // load assignments: one x pair (tid < FXP), up to two dual pairs
+    const bool xa = tid < FXP;
+    int xoff = 0, xsm = 0;
+    if (xa) {
+        const int row = tid / (FXW / 2), pc = tid % (FXW / 2);
+        xoff = wrap(i0 - 2 + 2 * pc, m) + m * wrap(j0 - 1 + row, n);
+        xsm = row * FXW + 2 * pc;
+    }
+    bool da[2];
+    long long doff[2];
+    int dsm[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+        const int e = tid + q * STH;
+        da[q] = !INIT && e < 3 * FDP;
+        const int c = da[q] ? e / FDP : 0, rem = da[q] ? e % FDP : 0;
+        const int row = rem / (FDW / 2), pc = rem % (FDW / 2);
+        doff[q] = (long long)c * N + wrap(i0 - 2 + 2 * pc, m) + (long long)m * wrap(j0 - 1 + row, n);
+        dsm[q] = c * FDH * FDW + row * FDW + 2 * pc;
+    }
+    // z only leaves [0, s) by one plane at a chunk edge (z = -1 or z = s)
+    auto zoff = [&](int z) { return plane * (long long)(z < 0 ? z + s : (z >= s ? z - s : z)); };
+
+    double2 rxv = make_double2(0.0, 0.0), rdv[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
+    auto load_x = [&](int z) {
+        if (xa) rxv = __ldg(reinterpret_cast<const double2*>(x + zoff(z) + xoff));
+    };
+    auto load_d = [&](int z) {
+        const long long zo = zoff(z);
+#pragma unroll
+        for (int q = 0; q < 2; ++q)
+            if (da[q]) rdv[q] = __ldg(reinterpret_cast<const double2*>(dual_in + zo + doff[q]));
+    };
+    auto store_x = [&](int z) {
+        if (xa) *reinterpret_cast<double2*>(xs + ((z - k0 + 1) % 3) * FXS + xsm) = rxv;
+    };
+    auto store_d = [&](int z) {
+#pragma unroll
+        for (int q = 0; q < 2; ++q)
+            if (da[q]) *reinterpret_cast<double2*>(ds + ((z - k0 + 1) & 1) * FDS + dsm[q]) = rdv[q];
+    };
+
+    // prologue: x(k0-1), x(k0), dual(k0-1) resident; x(k0+1), dual(k0) in registers
+    load_x(k0 - 1);
+    if (!INIT) load_d(k0 - 1);
+    store_x(k0 - 1);
+    if (!INIT) store_d(k0 - 1);
+    load_x(k0);
+    store_x(k0);
+    if (k0 + 1 <= k1) load_x(k0 + 1);
+    if (!INIT && k0 < k1) load_d(k0);
+
+    double acc_res = 0.0, acc_tv = 0.0, acc_dx = 0.0, acc_xp = 0.0;
+    double rz_prev = 0.0;
+    for (int k = k0 - 1; k < k1; ++k) {
+        // registers -> smem for step k+1, then request the next planes
+        if (k + 2 <= k1) store_x(k + 2);
+        if (!INIT && k + 1 <= k1 - 1) store_d(k + 1);
+        if (k + 3 <= k1) load_x(k + 3);
+        if (!INIT && k + 2 <= k1 - 1) load_d(k + 2);
+        __syncthreads();
+        const bool warm = k < k0;
+        const double* X0 = xs + ((k - k0 + 1) % 3) * FXS;
+        const double* X1 = xs + ((k - k0 + 2) % 3) * FXS;
+        const double* D0 = ds + ((k - k0 + 1) & 1) * FDS;
+        const long long zo = zoff(k);
+
+        const int xi = (ty + 1) * FXW + tx + 2;
+        const double xc = X0[xi];
+        const double l0 = X0[xi + 1] - xc;
+        const double l1 = X0[xi + FXW] - xc;
+        const double l2 = X1[xi] - xc;
+        double r0, r1, r2;
+        if constexpr (INIT) {
+            r0 = l0;
+            r1 = l1;
+            r2 = l2;
+            if (!warm && valid) {
+                const long long idx = col + zo;
+                dual_out[idx] = 0.0;
+                dual_out[N + idx] = 0.0;
+                dual_out[2 * N + idx] = 0.0;
+                acc_tv += sqrt(l0 * l0 + l1 * l1 + l2 * l2);
+            }
+        } else {
+            const int di = (ty + 1) * FDW + tx + 2;
+            const Shrunk o = shrink_point(l0, l1, l2, D0[di], D0[FDH * FDW + di], D0[2 * FDH * FDW + di], thr);
+            r0 = o.r0;
+            r1 = o.r1;
+            r2 = o.r2;
+            if (!warm && valid) {
+                const long long idx = col + zo;
+                dual_out[idx] = o.dn0;
+                dual_out[N + idx] = o.dn1;
+                dual_out[2 * N + idx] = o.dn2;
+                const double e0 = l0 - o.u0, e1 = l1 - o.u1, e2 = l2 - o.u2;
+                acc_res += e0 * e0 + e1 * e1 + e2 * e2;
+                acc_tv += sqrt(l0 * l0 + l1 * l1 + l2 * l2);
+            }
+        }
+        if constexpr (RELCHG) {
+            if (!warm && valid) {
+                const double xp = __ldg(xprev + col + zo);
+                const double dd = xc - xp;
+                acc_dx += dd * dd;
+                acc_xp += xp * xp;
+            }
+        }
+        if (!warm) {
+            rx[ty * (TX + 1) + tx + 1] = r0;
+            ry[(ty + 1) * TX + tx] = r1;
+            if (tid < TY + TX) {  // halo: rho_x at ii = -1, rho_y at jj = -1
+                const int ii = tid < TY ? -1 : tid - TY;
+                const int jj = tid < TY ? tid : -1;
+                const int hx = (jj + 1) * FXW + ii + 2;
+                const double hc = X0[hx];
+                const double h0 = X0[hx + 1] - hc;
+                const double h1 = X0[hx + FXW] - hc;
+                const double h2 = X1[hx] - hc;
+                double q0, q1;
+                if constexpr (INIT) {
+                    q0 = h0;
+                    q1 = h1;
+                } else {
+                    const int hd = (jj + 1) * FDW + ii + 2;
+                    const Shrunk o =
+                        shrink_point(h0, h1, h2, D0[hd], D0[FDH * FDW + hd], D0[2 * FDH * FDW + hd], thr);
+                    q0 = o.r0;
+                    q1 = o.r1;
+                }
+                if (tid < TY)
+                    rx[jj * (TX + 1)] = q0;
+                else
+                    ry[ii] = q1;
+            }
+        }
+        __syncthreads();
+        if (!warm && valid) {
+            // diff_adjoint sum in axis order (solvers.cpp:367-373): ((adj_x) + adj_y) + adj_z
+            const double ax = rx[ty * (TX + 1) + tx] - rx[ty * (TX + 1) + tx + 1];
+            const double ay = ry[ty * TX + tx] - ry[(ty + 1) * TX + tx];
+            const double az = rz_prev - r2;
+            theta[col + zo] = (ax + ay) + az;
+        }
+        rz_prev = r2;
+    }
+
+    double v[4] = {acc_res, acc_tv, acc_dx, acc_xp};
+    block_reduce_sum<4>(v, red);
+    if (tid == 0) {
+        const size_t b = blockIdx.x + (size_t)gridDim.x * (blockIdx.y + (size_t)gridDim.y * blockIdx.z);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) partials[b * 4 + q] = v[q];
+    }
+}
+
 // Sum `nvals` interleaved per-block partials in a fixed order.
 __device__ void fixed_sum(const double* p, int stride, int nvals, long long nblocks, double* out,
                           double* red) {
@@ -384,6 +584,21 @@ void launch_tv_stencil(const Dims& d, bool init, const double* x, const double* 
                        double* partials, cudaStream_t st) {
     const StencilGeom g = stencil_geom(d);
     const int m = (int)d.m, n = (int)d.n, s = (int)d.s;
+    if (m % 2 == 0) {
+        const size_t smem = fast_smem_doubles() * sizeof(double);
+#define VSR_FAST(I, R)                                                                               \
+    tv_stencil_fast_kernel<I, R><<<g.grid, STH, smem, st>>>(m, n, s, g.kc, x, dual_in, dual_out, theta, \
+                                                            thr, xprev, partials)
+        if (init)
+            VSR_FAST(true, false);
+        else if (xprev)
+            VSR_FAST(false, true);
+        else
+            VSR_FAST(false, false);
+#undef VSR_FAST
+        VSR_LAUNCH_CHECK();
+        return;
+    }
     const size_t smem = stencil_smem_doubles(init) * sizeof(double);
     if (init) {
         tv_stencil_kernel<true, false><<<g.grid, STH, smem, st>>>(m, n, s, g.kc, x, dual_in, dual_out,
