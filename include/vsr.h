@@ -184,6 +184,36 @@ int vsr_tv_report(vsr_tv* h, vsr_report* report); /* synchronizes */
 int vsr_tv_destroy(vsr_tv* h);
 double vsr_tv_algorithmic_bytes(const size_t hr_dims[3], const size_t rates[3]);
 
+/* ---- slab-decomposed distributed path; per-rank device stages.
+ *      A rank holds z-slab p (s/P planes) of spatial volumes and, spectrally,
+ *      the alias-closed row set {g2 + bc*nl : g2 in [p nl/P, (p+1) nl/P)} in
+ *      the local layout [f3][jl][f1] (dims m x n/P x s).  The host exchanges
+ *      (all-to-all, halos, scalar gathers) between these calls
+ *      (paper_2010_15491_b200/dist.py).  All pointers are device pointers on
+ *      the context's device; work is ordered on the context stream. */
+int vsr_fft3_d(vsr_ctx* ctx, const size_t dims[3], const double* in, int in_real, double* out_c,
+               double scale);
+int vsr_slab_fwd_xy_pack_d(vsr_ctx* ctx, const size_t hr_dims[3], const size_t rates[3], int P,
+                           const double* in, int in_real, double* work_c, double* send_c);
+int vsr_slab_axis3_d(vsr_ctx* ctx, const size_t hr_dims[3], const size_t rates[3], int P, double* W,
+                     int inverse, double scale);
+int vsr_slab_lr_slice_d(vsr_ctx* ctx, const size_t hr_dims[3], const size_t rates[3], int P, int rank,
+                        const double* Yl_full, double* Yl_loc);
+int vsr_slab_tik_fold_d(vsr_ctx* ctx, const size_t hr_dims[3], const size_t rates[3], int P,
+                        const double* Yl_loc, const double* lam_loc, const double* xbh_loc, double reg,
+                        double* W_out);
+int vsr_slab_tv_fold_d(vsr_ctx* ctx, const size_t hr_dims[3], const size_t rates[3], int P, int rank,
+                       const double* Yl_loc, const double* lam_loc, double* W, double mu, double tau,
+                       double fwd_scale, double* fit_out);
+int vsr_slab_unpack_inv_xy_d(vsr_ctx* ctx, const size_t hr_dims[3], const size_t rates[3], int P,
+                             const double* recv_c, double* work_c, double* out_real, double scale,
+                             double* sums_out, unsigned long long* bad_out);
+int vsr_slab_tv_stencil_d(vsr_ctx* ctx, const size_t hr_dims[3], const size_t rates[3], int P, int init,
+                          const double* x_ext, const double* dual_in_ext, double* dual_out_ext,
+                          double* theta, double thr, double* sums_out);
+int vsr_slab_fit_d(vsr_ctx* ctx, const size_t hr_dims[3], const size_t rates[3], int P,
+                   const double* Yl_loc, const double* lam_loc, const double* xh_loc, double* fit_out);
+
 /* ---- instrumentation (bench): kernels launched by this library so far, and
  *      per-stage CUDA-event durations on the context stream when enabled. */
 int vsr_launch_count(uint64_t* out);

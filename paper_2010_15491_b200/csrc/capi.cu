@@ -9,6 +9,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <string>
 #include <utility>
 #include <vector>
@@ -346,6 +347,19 @@ bool use_fused(const FoldGeom& G) {
 }
 
 }  // namespace
+
+// hooks for the other C-ABI translation units (dist.cu)
+namespace vsr_capi {
+cudaStream_t stream_of(vsr_ctx* ctx) {
+    if (!ctx) throw std::invalid_argument("vsr: null context");
+    return ctx->stream;
+}
+int device_of(vsr_ctx* ctx) {
+    if (!ctx) throw std::invalid_argument("vsr: null context");
+    return ctx->device;
+}
+int guard_call(const std::function<void()>& f) { return guarded(f); }
+}  // namespace vsr_capi
 
 extern "C" {
 

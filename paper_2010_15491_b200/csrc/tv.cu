@@ -251,7 +251,7 @@ __global__ void __launch_bounds__(STH)
     tv_stencil_fast_kernel(int m, int n, int s, int KC, const double* __restrict__ x,
                            const double* __restrict__ dual_in, double* __restrict__ dual_out,
                            double* __restrict__ theta, double thr, const double* __restrict__ xprev,
-                           double* __restrict__ partials) {
+                           double* __restrict__ partials, int halo, long long dsi, long long dso) {
     extern __shared__ double sm[];
     double* xs = sm;                 // [3][FXH][FXW]
     double* ds = xs + 3 * FXS;       // [2][3][FDH][FDW]
@@ -290,11 +290,15 @@ __global__ void __launch_bounds__(STH)
         da[q] = !INIT && e < 3 * FDP;
         const int c = da[q] ? e / FDP : 0, rem = da[q] ? e % FDP : 0;
         const int row = rem / (FDW / 2), pc = rem % (FDW / 2);
-        doff[q] = (long long)c * N + wrap(i0 - 2 + 2 * pc, m) + (long long)m * wrap(j0 - 1 + row, n);
+        doff[q] = (long long)c * dsi + wrap(i0 - 2 + 2 * pc, m) + (long long)m * wrap(j0 - 1 + row, n);
         dsm[q] = c * FDH * FDW + row * FDW + 2 * pc;
     }
-    // z only leaves [0, s) by one plane at a chunk edge (z = -1 or z = s)
-    auto zoff = [&](int z) { return plane * (long long)(z < 0 ? z + s : (z >= s ? z - s : z)); };
+    // z only leaves [0, s) by one plane at a chunk edge (z = -1 or z = s): periodic
+    // wrap on a whole volume, or explicit halo planes (x, dual_in pre-offset by
+    // one plane) on a slab of a distributed volume
+    auto zoff = [&](int z) {
+        return plane * (long long)(halo ? z : (z < 0 ? z + s : (z >= s ? z - s : z)));
+    };
 
     double2 rxv = make_double2(0.0, 0.0), rdv[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
     auto load_x = [&](int z) {
@@ -353,8 +357,8 @@ __global__ void __launch_bounds__(STH)
             if (!warm && valid) {
                 const long long idx = col + zo;
                 dual_out[idx] = 0.0;
-                dual_out[N + idx] = 0.0;
-                dual_out[2 * N + idx] = 0.0;
+                dual_out[dso + idx] = 0.0;
+                dual_out[2 * dso + idx] = 0.0;
                 acc_tv += sqrt(l0 * l0 + l1 * l1 + l2 * l2);
             }
         } else {
@@ -366,8 +370,8 @@ __global__ void __launch_bounds__(STH)
             if (!warm && valid) {
                 const long long idx = col + zo;
                 dual_out[idx] = o.dn0;
-                dual_out[N + idx] = o.dn1;
-                dual_out[2 * N + idx] = o.dn2;
+                dual_out[dso + idx] = o.dn1;
+                dual_out[2 * dso + idx] = o.dn2;
                 const double e0 = l0 - o.u0, e1 = l1 - o.u1, e2 = l2 - o.u2;
                 acc_res += e0 * e0 + e1 * e1 + e2 * e2;
                 acc_tv += sqrt(l0 * l0 + l1 * l1 + l2 * l2);
@@ -586,9 +590,10 @@ void launch_tv_stencil(const Dims& d, bool init, const double* x, const double* 
     const int m = (int)d.m, n = (int)d.n, s = (int)d.s;
     if (m % 2 == 0) {
         const size_t smem = fast_smem_doubles() * sizeof(double);
+        const long long N = (long long)d.count();
 #define VSR_FAST(I, R)                                                                               \
     tv_stencil_fast_kernel<I, R><<<g.grid, STH, smem, st>>>(m, n, s, g.kc, x, dual_in, dual_out, theta, \
-                                                            thr, xprev, partials)
+                                                            thr, xprev, partials, 0, N, N)
         if (init)
             VSR_FAST(true, false);
         else if (xprev)
@@ -679,6 +684,28 @@ size_t tv_norm_blocks(const Dims& d) { return blocks256((long long)d.count()); }
 void launch_tv_norm(const Dims& d, const double* x, double* partials, cudaStream_t st) {
     tv_norm_kernel<<<blocks256((long long)d.count()), 256, 0, st>>>(
         (long long)d.m, (long long)d.n, (long long)d.s, x, partials);
+    VSR_LAUNCH_CHECK();
+}
+
+void launch_tv_stencil_slab(const Dims& slab, bool init, const double* x_ext, const double* dual_in_ext,
+                            double* dual_out_ext, double* theta, double thr, double* partials,
+                            cudaStream_t st) {
+    if (slab.m % 2 != 0) throw std::invalid_argument("slab stencil: axis 1 must be even");
+    const StencilGeom g = stencil_geom(slab);
+    const int m = (int)slab.m, n = (int)slab.n, s = (int)slab.s;
+    const long long plane = (long long)m * n;
+    const long long dstride = plane * (s + 1);  // components of the halo-extended dual arrays
+    const size_t smem = fast_smem_doubles() * sizeof(double);
+    // x_ext planes: [z0-1, slab, z1] -> pass plane 0 of the slab; dual ext: [z0-1, slab]
+    const double* x0 = x_ext + plane;
+    const double* d0 = dual_in_ext ? dual_in_ext + plane : nullptr;
+    double* o0 = dual_out_ext + plane;
+    if (init)
+        tv_stencil_fast_kernel<true, false><<<g.grid, STH, smem, st>>>(m, n, s, g.kc, x0, d0, o0, theta, thr,
+                                                                       nullptr, partials, 1, dstride, dstride);
+    else
+        tv_stencil_fast_kernel<false, false><<<g.grid, STH, smem, st>>>(m, n, s, g.kc, x0, d0, o0, theta, thr,
+                                                                        nullptr, partials, 1, dstride, dstride);
     VSR_LAUNCH_CHECK();
 }
 

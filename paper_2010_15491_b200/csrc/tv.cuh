@@ -28,6 +28,14 @@ void launch_tv_stencil(const Dims& d, bool init, const double* x, const double* 
                        double* dual_out, double* theta, double thr, const double* xprev,
                        double* partials, cudaStream_t st);
 
+// Slab of a z-distributed volume: x_ext has the slab's planes plus one halo
+// plane on each side ([z0-1, slab..., z1]); dual ext arrays hold 3 components
+// of (slab planes + 1) with the low halo plane first.  Writes dual_out_ext's
+// slab planes and theta (slab planes).  axis 1 must be even.
+void launch_tv_stencil_slab(const Dims& slab, bool init, const double* x_ext, const double* dual_in_ext,
+                            double* dual_out_ext, double* theta, double thr, double* partials,
+                            cudaStream_t st);
+
 // Per-iteration scalar reduction for admm_tv (fixed order, single CTA):
 // report[iter] objective / primal residual / rel change, residue check.
 struct TvIterScalars {
