@@ -650,6 +650,19 @@ def tv_algorithmic_bytes(hr_dims, rates) -> float:
     return float(_lib.vsr_tv_algorithmic_bytes(_dims_arr(hr_dims), _dims_arr(rates)))
 
 
+# ---------------------------------------------------------------- slab stages (dist.py)
+_sig("vsr_fft3_d", [_vp, _szp, _vp, C.c_int, _vp, C.c_double])
+_sig("vsr_slab_fwd_xy_pack_d", [_vp, _szp, _szp, C.c_int, _vp, C.c_int, _vp, _vp])
+_sig("vsr_slab_axis3_d", [_vp, _szp, _szp, C.c_int, _vp, C.c_int, C.c_double])
+_sig("vsr_slab_lr_slice_d", [_vp, _szp, _szp, C.c_int, C.c_int, _vp, _vp])
+_sig("vsr_slab_tik_fold_d", [_vp, _szp, _szp, C.c_int, _vp, _vp, _vp, C.c_double, _vp])
+_sig("vsr_slab_tv_fold_d", [_vp, _szp, _szp, C.c_int, C.c_int, _vp, _vp, _vp, C.c_double, C.c_double,
+                            C.c_double, _vp])
+_sig("vsr_slab_unpack_inv_xy_d", [_vp, _szp, _szp, C.c_int, _vp, _vp, _vp, C.c_double, _vp, _vp])
+_sig("vsr_slab_tv_stencil_d", [_vp, _szp, _szp, C.c_int, C.c_int, _vp, _vp, _vp, _vp, C.c_double, _vp])
+_sig("vsr_slab_fit_d", [_vp, _szp, _szp, C.c_int, _vp, _vp, _vp, _vp])
+
+
 # ---------------------------------------------------------------- instrumentation
 _sig("vsr_launch_count", [C.POINTER(C.c_uint64)])
 _sig("vsr_profile_enable", [_vp, C.c_int])
