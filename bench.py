@@ -345,6 +345,8 @@ def run_b200(args, rank, world, local):
 
     if not args.no_tv:
         line["tv"] = bench_tv(args, ctx, V, synth, torch, stream, local, hbm)
+    if world > 1 or args.sharded:
+        line["sharded"] = bench_sharded(args, ctx, V, synth, torch, rank, world, local)
     if rank == 0 and world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(cfg, inp)
     op.close()
@@ -401,6 +403,54 @@ def bench_tv(args, ctx, V, synth, torch, stream, local, hbm):
             "stages": rows}
 
 
+def bench_sharded(args, ctx, V, synth, torch, rank, world, local):
+    """configs[3] ADMM-TV (512x512x256, d = (2,2,4)) slab-decomposed over all
+    ranks: NCCL all-to-all transposes + ring halos (paper_2010_15491_b200/dist.py).
+    Seeded random data of the config's shapes (values do not change the work)."""
+    import torch.distributed as tdist
+    from paper_2010_15491_b200 import dist as D
+    cfg = synth.CONFIGS[3]
+    hr, rates = cfg.hr, cfg.rates
+    m, n, s = hr
+    psf = synth.make_gaussian_psf(cfg.psf_size, cfg.psf_sigma, hr)
+    g = D.SlabGeometry(hr, rates, world)
+    dev = torch.device("cuda", local)
+    gen = torch.Generator(device=dev).manual_seed(1234 + rank)
+    sz = g.sz
+    psf_slab = torch.from_numpy(np.ascontiguousarray(psf[rank * sz:(rank + 1) * sz])).reshape(-1).to(dev)
+    gy = torch.Generator(device=dev).manual_seed(99)
+    y = torch.rand(g.sl * g.nl * g.ml, generator=gy, device=dev, dtype=torch.float64)
+    x0 = torch.rand(g.slab_elems, generator=gen, device=dev, dtype=torch.float64)
+    dist_on = tdist.is_available() and tdist.is_initialized()
+    ex = D.TorchExchange() if dist_on else D.LocalExchange(1)
+    st = D.GpuStages({rank if dist_on else 0: ctx})
+    r0 = rank if dist_on else 0
+    tv = D.SlabADMMTV(st, ex, hr, rates, {r0: psf_slab}, {r0: y}, {r0: x0}, cfg.tv_lambda, cfg.tv_mu,
+                      tau=1e-3 * cfg.tv_mu)
+    tv.iterate(2)
+    k = max(3, min(args.steps, 10))
+    if dist_on:
+        tdist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    tv.iterate(k)
+    e1.record()
+    e1.synchronize()
+    ms = e0.elapsed_time(e1) / k
+    if dist_on:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        ms = float(t.item())
+    N = g.N
+    a2a = 2 * 16 * (N // world) * (world - 1) / world
+    return {"workload": "config3: ADMM-TV fp64 512x512x256 -> 256x256x64 (d=2,2,4), slab-sharded over "
+                        f"{world} GPU(s): NCCL all-to-all FFT transposes + ring halos",
+            "value": N / (ms * 1e-3), "unit": "HR voxels/s per ADMM-TV iteration", "ms_per_iter": ms,
+            "iters_timed": k, "scaling": "strong", "alltoall_bytes_per_rank_per_iter": a2a,
+            "note": "host-orchestrated stages (python), exchanges synchronous"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -409,6 +459,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-tv", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--sharded", action="store_true", help="also time the slab-sharded config-3 path at N=1")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     rank = int(os.environ.get("RANK", "0"))

@@ -1,0 +1,484 @@
+// volsr_b200/volsr.hpp — header-only C++ mirror of the reference `volsr`
+// solver API (include/volsr/{volume,fft,operators,spectral,solvers}.hpp under
+// /root/reference/proj) over the C ABI in vsr.h.  Same namespace, type and
+// function names, argument meaning and exception types, so callers written
+// against the reference compile unchanged against this header and link
+// libvsr_b200.so instead of the CPU library.
+//
+// Every numeric step runs on the GPU (one process-wide context on device
+// VSR_DEVICE, default 0); there is no CPU fallback.
+#pragma once
+
+#include <array>
+#include <cmath>
+#include <complex>
+#include <cstdint>
+#include <cstdlib>
+#include <optional>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../vsr.h"
+
+namespace volsr {
+
+// ------------------------------------------------------------- volume.hpp:12-104
+struct shape_error : std::invalid_argument {
+    using std::invalid_argument::invalid_argument;
+};
+struct numeric_error : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct io_error : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+struct Dims3 {
+    std::size_t m = 0, n = 0, s = 0;
+    std::size_t count() const { return m * n * s; }
+    bool operator==(const Dims3&) const = default;
+};
+
+inline std::string to_string(const Dims3& d) {
+    return std::to_string(d.m) + "x" + std::to_string(d.n) + "x" + std::to_string(d.s);
+}
+
+inline std::size_t lex_index(std::size_t i, std::size_t j, std::size_t k, const Dims3& d) {
+    if (i >= d.m || j >= d.n || k >= d.s)
+        throw std::out_of_range("lex_index: voxel (" + std::to_string(i) + "," + std::to_string(j) + "," +
+                                std::to_string(k) + ") outside grid " + to_string(d));
+    return i + d.m * j + d.m * d.n * k;
+}
+
+class Volume3D {
+public:
+    Volume3D() = default;
+    explicit Volume3D(const Dims3& dims, double fill = 0.0) : dims_(dims), data_(dims.count(), fill) {}
+    Volume3D(const Dims3& dims, std::vector<double> data) : dims_(dims), data_(std::move(data)) {
+        if (data_.size() != dims_.count())
+            throw shape_error("Volume3D: data length " + std::to_string(data_.size()) +
+                              " does not match dims " + to_string(dims_));
+    }
+    const Dims3& dims() const { return dims_; }
+    std::size_t size() const { return data_.size(); }
+    double operator[](std::size_t p) const { return data_[p]; }
+    double& operator[](std::size_t p) { return data_[p]; }
+    double at(std::size_t i, std::size_t j, std::size_t k) const { return data_[lex_index(i, j, k, dims_)]; }
+    double& at(std::size_t i, std::size_t j, std::size_t k) { return data_[lex_index(i, j, k, dims_)]; }
+    const std::vector<double>& data() const { return data_; }
+    std::vector<double>& data() { return data_; }
+
+private:
+    Dims3 dims_;
+    std::vector<double> data_;
+};
+
+class ComplexVolume3D {
+public:
+    using value_type = std::complex<double>;
+    ComplexVolume3D() = default;
+    explicit ComplexVolume3D(const Dims3& dims, value_type fill = {}) : dims_(dims), data_(dims.count(), fill) {}
+    ComplexVolume3D(const Dims3& dims, std::vector<value_type> data) : dims_(dims), data_(std::move(data)) {
+        if (data_.size() != dims_.count())
+            throw shape_error("ComplexVolume3D: data length " + std::to_string(data_.size()) +
+                              " does not match dims " + to_string(dims_));
+    }
+    const Dims3& dims() const { return dims_; }
+    std::size_t size() const { return data_.size(); }
+    value_type operator[](std::size_t p) const { return data_[p]; }
+    value_type& operator[](std::size_t p) { return data_[p]; }
+    const std::vector<value_type>& data() const { return data_; }
+    std::vector<value_type>& data() { return data_; }
+
+private:
+    Dims3 dims_;
+    std::vector<value_type> data_;
+};
+
+inline void require_same_dims(const Dims3& a, const Dims3& b, const char* where) {
+    if (!(a == b)) throw shape_error(std::string(where) + ": dims mismatch, " + to_string(a) + " vs " + to_string(b));
+}
+
+// ------------------------------------------------------------- C ABI plumbing
+namespace detail {
+inline vsr_ctx* ctx() {
+    static vsr_ctx* c = [] {
+        vsr_ctx* p = nullptr;
+        const char* e = std::getenv("VSR_DEVICE");
+        const int rc = vsr_ctx_create(e ? std::atoi(e) : 0, &p);
+        if (rc != VSR_OK) throw std::runtime_error(vsr_last_error_message());
+        return p;
+    }();
+    return c;
+}
+inline void check(int rc) {
+    if (rc == VSR_OK) return;
+    const std::string m = vsr_last_error_message();
+    switch (rc) {
+        case VSR_ERR_SHAPE: throw shape_error(m);
+        case VSR_ERR_INVALID: throw std::invalid_argument(m);
+        case VSR_ERR_NUMERIC: throw numeric_error(m);
+        case VSR_ERR_OUT_OF_RANGE: throw std::out_of_range(m);
+        default: throw std::runtime_error(m);
+    }
+}
+struct D3 {
+    std::size_t v[3];
+    explicit D3(const Dims3& d) : v{d.m, d.n, d.s} {}
+};
+inline const double* cp(const ComplexVolume3D& v) { return reinterpret_cast<const double*>(v.data().data()); }
+inline double* cp(ComplexVolume3D& v) { return reinterpret_cast<double*>(v.data().data()); }
+}  // namespace detail
+
+// ------------------------------------------------------------- fft.hpp:12-31
+inline ComplexVolume3D fft3(const Volume3D& v) {
+    ComplexVolume3D out(v.dims());
+    detail::check(vsr_fft3_real(detail::ctx(), detail::D3(v.dims()).v, v.data().data(), detail::cp(out)));
+    return out;
+}
+inline ComplexVolume3D fft3(const ComplexVolume3D& v) {
+    ComplexVolume3D out(v.dims());
+    detail::check(vsr_fft3(detail::ctx(), detail::D3(v.dims()).v, detail::cp(v), detail::cp(out)));
+    return out;
+}
+inline ComplexVolume3D ifft3(const ComplexVolume3D& v) {
+    ComplexVolume3D out(v.dims());
+    detail::check(vsr_ifft3(detail::ctx(), detail::D3(v.dims()).v, detail::cp(v), detail::cp(out)));
+    return out;
+}
+inline Volume3D ifft3_real(const ComplexVolume3D& v, double max_rel_imag = 1e-8) {
+    Volume3D out(v.dims());
+    detail::check(vsr_ifft3_real(detail::ctx(), detail::D3(v.dims()).v, detail::cp(v), out.data().data(),
+                                 max_rel_imag));
+    return out;
+}
+inline ComplexVolume3D dft3_unnormalized(const Volume3D& v) {
+    ComplexVolume3D out(v.dims());
+    detail::check(vsr_dft3_unnormalized(detail::ctx(), detail::D3(v.dims()).v, v.data().data(), detail::cp(out)));
+    return out;
+}
+struct FftCounters {
+    std::uint64_t forward = 0, inverse = 0;
+};
+inline FftCounters fft_counters() {
+    FftCounters c;
+    uint64_t f = 0, i = 0;
+    vsr_fft_counters(&f, &i);
+    c.forward = f;
+    c.inverse = i;
+    return c;
+}
+inline void reset_fft_counters() { vsr_reset_fft_counters(); }
+
+// ------------------------------------------------------------- operators.hpp:12-87
+class DecimationSpec {
+public:
+    DecimationSpec(const Dims3& hr, std::array<std::size_t, 3> rates) : hr_(hr), rates_(rates) {
+        const char* names[3] = {"1 (rows)", "2 (cols)", "3 (slices)"};
+        const std::size_t ext[3] = {hr.m, hr.n, hr.s};
+        for (int a = 0; a < 3; ++a) {
+            if (rates[a] == 0) throw shape_error(std::string("DecimationSpec: zero rate on axis ") + names[a]);
+            if (ext[a] % rates[a] != 0)
+                throw shape_error("DecimationSpec: rate " + std::to_string(rates[a]) + " does not divide axis " +
+                                  names[a] + " of length " + std::to_string(ext[a]));
+        }
+        lr_ = {hr.m / rates[0], hr.n / rates[1], hr.s / rates[2]};
+    }
+    const Dims3& hr() const { return hr_; }
+    const Dims3& lr() const { return lr_; }
+    std::size_t dr() const { return rates_[0]; }
+    std::size_t dc() const { return rates_[1]; }
+    std::size_t ds() const { return rates_[2]; }
+    std::size_t rate() const { return rates_[0] * rates_[1] * rates_[2]; }
+    const std::size_t* rates_ptr() const { return rates_.data(); }
+
+private:
+    Dims3 hr_, lr_;
+    std::array<std::size_t, 3> rates_;
+};
+
+struct SpectrumDiag {
+    ComplexVolume3D values;
+    const Dims3& dims() const { return values.dims(); }
+};
+
+// PSF description and host-side construction (operators.cpp:23-119; setup, not hot path)
+struct PsfSpec {
+    std::array<std::size_t, 3> size{1, 1, 1};
+    std::array<double, 3> sigma{0.0, 0.0, 0.0};
+    std::vector<double> weights;
+    static PsfSpec gaussian(std::array<std::size_t, 3> size, std::array<double, 3> sigma) {
+        PsfSpec s;
+        s.size = size;
+        s.sigma = sigma;
+        return s;
+    }
+    static PsfSpec explicit_kernel(std::array<std::size_t, 3> size, std::vector<double> w) {
+        if (w.size() != size[0] * size[1] * size[2])
+            throw std::invalid_argument("PsfSpec: weight count does not match kernel size");
+        double sum = 0.0;
+        for (double v : w) {
+            if (!(v >= 0.0)) throw std::invalid_argument("PsfSpec: weights must be nonnegative");
+            sum += v;
+        }
+        if (sum <= 0.0) throw std::invalid_argument("PsfSpec: weights must not all be zero");
+        for (double& v : w) v /= sum;
+        PsfSpec s;
+        s.size = size;
+        s.weights = std::move(w);
+        return s;
+    }
+};
+
+inline Volume3D make_gaussian_psf(const PsfSpec& spec, const Dims3& hr) {
+    const std::size_t ext[3] = {hr.m, hr.n, hr.s};
+    for (int a = 0; a < 3; ++a) {
+        if (spec.size[a] % 2 == 0)
+            throw std::invalid_argument("make_gaussian_psf: kernel size must be odd on axis " + std::to_string(a + 1));
+        if (spec.size[a] > ext[a])
+            throw std::invalid_argument("make_gaussian_psf: kernel size " + std::to_string(spec.size[a]) +
+                                        " exceeds volume axis " + std::to_string(a + 1) + " of length " +
+                                        std::to_string(ext[a]));
+    }
+    const std::size_t kr = spec.size[0], kc = spec.size[1], ks = spec.size[2];
+    std::vector<double> k(kr * kc * ks);
+    if (!spec.weights.empty()) {
+        k = spec.weights;
+    } else {
+        auto g1 = [](std::size_t n, double sg) {
+            std::vector<double> w(n);
+            const long h = (long)(n / 2);
+            for (long t = -h; t <= h; ++t)
+                w[(std::size_t)(t + h)] = sg <= 0.0 ? (t == 0 ? 1.0 : 0.0) : std::exp(-0.5 * (t / sg) * (t / sg));
+            return w;
+        };
+        const auto wr = g1(kr, spec.sigma[0]), wc = g1(kc, spec.sigma[1]), ws = g1(ks, spec.sigma[2]);
+        double sum = 0.0;
+        for (std::size_t c = 0; c < ks; ++c)
+            for (std::size_t b = 0; b < kc; ++b)
+                for (std::size_t a = 0; a < kr; ++a) sum += (k[a + kr * b + kr * kc * c] = wr[a] * wc[b] * ws[c]);
+        for (double& v : k) v /= sum;
+    }
+    Volume3D psf(hr);
+    for (std::size_t c = 0; c < ks; ++c)
+        for (std::size_t b = 0; b < kc; ++b)
+            for (std::size_t a = 0; a < kr; ++a) {
+                const std::size_t i = (std::size_t)(((long)a - (long)(kr / 2) + (long)hr.m) % (long)hr.m);
+                const std::size_t j = (std::size_t)(((long)b - (long)(kc / 2) + (long)hr.n) % (long)hr.n);
+                const std::size_t l = (std::size_t)(((long)c - (long)(ks / 2) + (long)hr.s) % (long)hr.s);
+                psf.at(i, j, l) += k[a + kr * b + kr * kc * c];
+            }
+    return psf;
+}
+
+inline SpectrumDiag psf_to_spectrum(const Volume3D& psf) { return SpectrumDiag{dft3_unnormalized(psf)}; }
+
+inline Volume3D blur_apply(const Volume3D& x, const SpectrumDiag& lambda, bool conjugate = false) {
+    require_same_dims(x.dims(), lambda.dims(), "blur_apply");
+    Volume3D out(x.dims());
+    detail::check(vsr_blur_apply(detail::ctx(), detail::D3(x.dims()).v, x.data().data(), detail::cp(lambda.values),
+                                 conjugate ? 1 : 0, out.data().data()));
+    return out;
+}
+inline Volume3D decimate(const Volume3D& x, const DecimationSpec& spec) {
+    require_same_dims(x.dims(), spec.hr(), "decimate");
+    Volume3D y(spec.lr());
+    detail::check(vsr_decimate(detail::ctx(), detail::D3(spec.hr()).v, spec.rates_ptr(), x.data().data(),
+                               y.data().data()));
+    return y;
+}
+inline Volume3D decimate_adjoint(const Volume3D& y, const DecimationSpec& spec) {
+    require_same_dims(y.dims(), spec.lr(), "decimate_adjoint");
+    Volume3D x(spec.hr());
+    detail::check(vsr_decimate_adjoint(detail::ctx(), detail::D3(spec.hr()).v, spec.rates_ptr(), y.data().data(),
+                                       x.data().data()));
+    return x;
+}
+inline Volume3D zero_fill_upsample(const Volume3D& y, const DecimationSpec& spec) {
+    Volume3D x = decimate_adjoint(y, spec);
+    const double d = static_cast<double>(spec.rate());
+    for (auto& v : x.data()) v *= d;
+    return x;
+}
+
+enum class Axis { Rows = 0, Cols = 1, Slices = 2 };
+inline Volume3D diff_forward(const Volume3D& x, Axis a) {
+    Volume3D out(x.dims());
+    detail::check(vsr_diff_forward(detail::ctx(), detail::D3(x.dims()).v, (int)a, x.data().data(), out.data().data()));
+    return out;
+}
+inline Volume3D diff_adjoint(const Volume3D& x, Axis a) {
+    Volume3D out(x.dims());
+    detail::check(vsr_diff_adjoint(detail::ctx(), detail::D3(x.dims()).v, (int)a, x.data().data(), out.data().data()));
+    return out;
+}
+
+// ------------------------------------------------------------- spectral.hpp:21-68
+class FoldedSpectrum {
+public:
+    FoldedSpectrum(const SpectrumDiag& lambda, const DecimationSpec& spec) : spec_(spec) {
+        require_same_dims(lambda.dims(), spec.hr(), "FoldedSpectrum");
+        detail::check(vsr_folded_create(detail::ctx(), detail::D3(spec.hr()).v, spec.rates_ptr(),
+                                        detail::cp(lambda.values), &h_));
+    }
+    FoldedSpectrum(const FoldedSpectrum&) = delete;
+    FoldedSpectrum& operator=(const FoldedSpectrum&) = delete;
+    ~FoldedSpectrum() { vsr_folded_destroy(h_); }
+    const DecimationSpec& spec() const { return spec_; }
+    std::complex<double> block_value(std::size_t br, std::size_t bc, std::size_t bs, std::size_t g) const {
+        double v[2];
+        detail::check(vsr_folded_block_value(h_, br, bc, bs, g, v));
+        return {v[0], v[1]};
+    }
+    ComplexVolume3D apply(const ComplexVolume3D& hr) const {
+        require_same_dims(hr.dims(), spec_.hr(), "FoldedSpectrum::apply");
+        ComplexVolume3D out(spec_.lr());
+        detail::check(vsr_folded_apply(h_, detail::cp(hr), detail::cp(out)));
+        return out;
+    }
+    ComplexVolume3D apply_adjoint(const ComplexVolume3D& lr) const {
+        require_same_dims(lr.dims(), spec_.lr(), "FoldedSpectrum::apply_adjoint");
+        ComplexVolume3D out(spec_.hr());
+        detail::check(vsr_folded_apply_adjoint(h_, detail::cp(lr), detail::cp(out)));
+        return out;
+    }
+    void swap_blocks_for_fault_injection() { detail::check(vsr_folded_swap_blocks_for_fault_injection(h_)); }
+    vsr_folded* handle() const { return h_; }
+
+private:
+    DecimationSpec spec_;
+    vsr_folded* h_ = nullptr;
+};
+
+inline Volume3D gram_diag(const FoldedSpectrum& f) {
+    Volume3D out(f.spec().lr());
+    detail::check(vsr_folded_gram_diag(f.handle(), out.data().data()));
+    return out;
+}
+
+// ------------------------------------------------------------- solvers.hpp:10-117
+struct TikhonovConfig {
+    double lambda = 0.01;
+    Volume3D xbar;
+};
+
+struct SolveReport {
+    std::size_t iterations = 0;
+    double initial_objective = 0.0;
+    std::vector<double> objective;
+    std::vector<double> primal_residual;
+    double seconds = 0.0;
+};
+
+class TikhonovOperator {
+public:
+    TikhonovOperator(const SpectrumDiag& lambda, const DecimationSpec& spec, const TikhonovConfig& cfg)
+        : spec_(spec) {
+        if (!(cfg.lambda > 0.0))
+            throw std::invalid_argument("lambda must be positive, got " + std::to_string(cfg.lambda));
+        require_same_dims(lambda.dims(), spec.hr(), "TikhonovOperator");
+        require_same_dims(cfg.xbar.dims(), spec.hr(), "TikhonovOperator: xbar");
+        detail::check(vsr_tikhonov_create(detail::ctx(), detail::D3(spec.hr()).v, spec.rates_ptr(),
+                                          detail::cp(lambda.values), cfg.lambda, cfg.xbar.data().data(), &h_));
+    }
+    TikhonovOperator(const TikhonovOperator&) = delete;
+    TikhonovOperator& operator=(const TikhonovOperator&) = delete;
+    ~TikhonovOperator() { vsr_tikhonov_destroy(h_); }
+    Volume3D solve(const Volume3D& y) const {
+        require_same_dims(y.dims(), spec_.lr(), "TikhonovOperator::solve");
+        Volume3D x(spec_.hr());
+        detail::check(vsr_tikhonov_solve(h_, y.data().data(), x.data().data()));
+        return x;
+    }
+    const DecimationSpec& spec() const { return spec_; }
+
+private:
+    DecimationSpec spec_;
+    vsr_tikhonov* h_ = nullptr;
+};
+
+inline Volume3D tikhonov_fast(const Volume3D& y, const SpectrumDiag& lambda, const DecimationSpec& spec,
+                              const TikhonovConfig& cfg) {
+    return TikhonovOperator(lambda, spec, cfg).solve(y);
+}
+
+struct TvAdmmConfig {
+    double lambda = 0.06;
+    double mu = 0.1;
+    std::size_t max_iters = 30;
+    double rel_tol = 1e-6;
+    std::optional<double> tau;
+    enum class Init { Zero, UpsampledObservation, Provided };
+    Init init = Init::Zero;
+    Volume3D init_volume;
+};
+
+inline Volume3D make_gamma(const Dims3& hr, double tau) {
+    Volume3D g(hr);
+    detail::check(vsr_make_gamma(detail::ctx(), detail::D3(hr).v, tau, g.data().data()));
+    return g;
+}
+
+inline Volume3D tv_x_update(const Volume3D& y, const FoldedSpectrum&, const SpectrumDiag& lambda,
+                            const DecimationSpec& spec, double mu, const ComplexVolume3D& theta_hat,
+                            const Volume3D& gamma) {
+    if (!(mu > 0.0)) throw std::invalid_argument("mu must be positive, got " + std::to_string(mu));
+    require_same_dims(y.dims(), spec.lr(), "tv_x_update");
+    require_same_dims(theta_hat.dims(), spec.hr(), "tv_x_update: theta_hat");
+    require_same_dims(gamma.dims(), spec.hr(), "tv_x_update: gamma");
+    Volume3D x(spec.hr());
+    detail::check(vsr_tv_x_update(detail::ctx(), detail::D3(spec.hr()).v, spec.rates_ptr(), y.data().data(),
+                                  detail::cp(lambda.values), mu, detail::cp(theta_hat), gamma.data().data(),
+                                  x.data().data()));
+    return x;
+}
+
+inline std::array<Volume3D, 3> tv_shrink(const Volume3D& a, const Volume3D& b, const Volume3D& c, double t) {
+    require_same_dims(a.dims(), b.dims(), "tv_shrink");
+    require_same_dims(a.dims(), c.dims(), "tv_shrink");
+    std::array<Volume3D, 3> o{Volume3D(a.dims()), Volume3D(a.dims()), Volume3D(a.dims())};
+    detail::check(vsr_tv_shrink(detail::ctx(), a.size(), a.data().data(), b.data().data(), c.data().data(), t,
+                                o[0].data().data(), o[1].data().data(), o[2].data().data()));
+    return o;
+}
+
+inline double objective_tv(const Volume3D& x, const Volume3D& y, const SpectrumDiag& lambda,
+                           const DecimationSpec& spec, double w) {
+    require_same_dims(x.dims(), spec.hr(), "objective_tv");
+    require_same_dims(y.dims(), spec.lr(), "objective_tv");
+    double out = 0.0;
+    detail::check(vsr_objective_tv(detail::ctx(), detail::D3(spec.hr()).v, spec.rates_ptr(), x.data().data(),
+                                   y.data().data(), detail::cp(lambda.values), w, &out));
+    return out;
+}
+
+inline std::pair<Volume3D, SolveReport> admm_tv(const Volume3D& y, const Volume3D& psf, const DecimationSpec& spec,
+                                                const TvAdmmConfig& cfg) {
+    if (!(cfg.lambda > 0.0)) throw std::invalid_argument("lambda must be positive, got " + std::to_string(cfg.lambda));
+    if (!(cfg.mu > 0.0)) throw std::invalid_argument("mu must be positive, got " + std::to_string(cfg.mu));
+    if (cfg.max_iters < 1) throw std::invalid_argument("admm_tv: max_iters must be >= 1");
+    require_same_dims(y.dims(), spec.lr(), "admm_tv");
+    require_same_dims(psf.dims(), spec.hr(), "admm_tv: psf");
+    if (cfg.init == TvAdmmConfig::Init::Provided)
+        require_same_dims(cfg.init_volume.dims(), spec.hr(), "admm_tv: init volume");
+    vsr_tv_config c{cfg.lambda, cfg.mu, cfg.max_iters, cfg.rel_tol, cfg.tau.has_value() ? 1 : 0,
+                    cfg.tau.value_or(0.0), static_cast<int>(cfg.init),
+                    cfg.init == TvAdmmConfig::Init::Provided ? cfg.init_volume.data().data() : nullptr};
+    SolveReport rep;
+    rep.objective.resize(cfg.max_iters);
+    rep.primal_residual.resize(cfg.max_iters);
+    vsr_report vr{0, 0.0, 0.0, rep.objective.data(), rep.primal_residual.data()};
+    Volume3D x(spec.hr());
+    detail::check(vsr_admm_tv(detail::ctx(), detail::D3(spec.hr()).v, spec.rates_ptr(), y.data().data(),
+                              psf.data().data(), &c, x.data().data(), &vr));
+    rep.iterations = vr.iterations;
+    rep.initial_objective = vr.initial_objective;
+    rep.seconds = vr.seconds;
+    rep.objective.resize(vr.iterations);
+    rep.primal_residual.resize(vr.iterations);
+    return {std::move(x), std::move(rep)};
+}
+
+}  // namespace volsr
