@@ -209,6 +209,8 @@ STAGE_BYTES = {
     "tik_fold": (48, 16), "tv_fold": (48, 16), "tv_stencil": (64, 0),
     # fused kernels: Lambda (+ X̄ or W) in, spectrum out (+ LR spectrum of y)
     "tik_fold_ifft_axis3": (48, 16), "tv_fft3_fold_ifft3": (48, 16),
+    "tik_fold_ifft_axis1": (48, 16), "tv_fft1_fold_ifft1": (48, 16),
+    "fft_inv_axis3_c2r": (24, 0), "fft_fwd_axis3_r2c": (24, 0),
     # chained in-plane passes: one HBM read of the input, one write of the output
     "chain_inv_axis2_axis1_c2r": (24, 0), "chain_fwd_axis1_r2c_axis2": (24, 0),
 }

@@ -338,6 +338,27 @@ bool use_chain() {
     return on;
 }
 
+// Which pass the fold is fused with: 1 (contiguous rows), 3 (strided lines) or
+// 0 (none).  Measured at 256^3 (r01): Tikhonov fold+axis3 220 us vs
+// fold+axis1 285 us; TV sandwich on axis 1 358 us vs axis 3 470 us.  So the
+// default is axis 3 for Tikhonov and axis 1 for TV (VSR_FUSE_AXIS overrides).
+int fuse_axis(const FoldGeom& G, int dflt) {
+    static const int env = [] {
+        const char* e = std::getenv("VSR_FUSE_AXIS");
+        return e ? std::atoi(e) : -1;
+    }();
+    const int pref = env >= 0 ? env : dflt;
+    static const bool off = [] {
+        const char* e = std::getenv("VSR_NO_FUSE");
+        return e && e[0] == '1';
+    }();
+    if (off || pref == 0) return 0;
+    if (pref == 1 && fused_axis1_ok(G)) return 1;
+    if (fused_axis3_ok(G)) return 3;
+    if (fused_axis1_ok(G)) return 1;
+    return 0;
+}
+
 bool use_fused(const FoldGeom& G) {
     static const bool off = [] {
         const char* e = std::getenv("VSR_NO_FUSE");
@@ -788,7 +809,7 @@ static vsr_tikhonov* tik_new(vsr_ctx* ctx, const size_t hr_dims[3], const size_t
     t->Yl.alloc(Nl);
     t->y.alloc(Nl);
     t->x.alloc(N);
-    t->res_blocks = fft_engine().inverse_final_blocks(sp.hr);
+    t->res_blocks = std::max(fft_engine().inverse_final_blocks(sp.hr), fft_engine().pass_blocks(sp.hr, 2));
     if (use_chain() && use_fused(t->G)) {
         t->chain = chain_plan(sp.hr);
         if (t->chain.ok) {
@@ -870,7 +891,22 @@ static void tik_enqueue(vsr_tikhonov* t, const double* y_dev, double* x_dev) {
     }
     ++g_fwd;  // the one forward transform of solve() (solvers.cpp:52)
     PassReduce red{t->partials.p, t->bad.p};
-    if (use_fused(t->G)) {
+    if (fuse_axis(t->G, 3) == 1) {
+        // fold + inverse axis 1 (contiguous rows), then axis 2, then axis 3 -> real x
+        {
+            ProfScope ps(prof, "tik_fold_ifft_axis1", st);
+            launch_tik_fold_ifft1(t->G, t->Yl.p, t->lam.p, t->xbh.p, t->xh.p, t->reg, st);
+        }
+        {
+            ProfScope ps(prof, "fft_inv_axis2", st);
+            fft_engine().axis_pass(t->sp.hr, 1, true, t->xh.p, IN_COMPLEX, t->xh.p, OUT_COMPLEX, 1.0, nullptr, st);
+        }
+        {
+            ProfScope ps(prof, "fft_inv_axis3_c2r", st);
+            fft_engine().axis_pass(t->sp.hr, 2, true, t->xh.p, IN_COMPLEX, x_dev, OUT_REAL,
+                                   inv_sqrt_count(t->sp.hr), &red, st);
+        }
+    } else if (use_fused(t->G)) {
         {
             ProfScope ps(prof, "tik_fold_ifft_axis3", st);
             launch_tik_fold_ifft3(t->G, t->Yl.p, t->lam.p, t->xbh.p, t->xh.p, t->reg, st);
@@ -894,7 +930,8 @@ static void tik_enqueue(vsr_tikhonov* t, const double* y_dev, double* x_dev) {
     ++g_inv;  // the one inverse transform (solvers.cpp:64)
     {
         ProfScope ps(prof, "residue_status", st);
-        const size_t nres = (use_fused(t->G) && t->chain.ok) ? t->chain.b_total()
+        const size_t nres = fuse_axis(t->G, 3) == 1 ? fft_engine().pass_blocks(t->sp.hr, 2)
+                            : (use_fused(t->G) && t->chain.ok) ? t->chain.b_total()
                                                                : fft_engine().inverse_final_blocks(t->sp.hr);
         residue_status_kernel<<<1, 1024, 0, st>>>(t->partials.p, (long long)nres, 1e-8, t->status.p);
         VSR_LAUNCH_CHECK();
@@ -1146,9 +1183,11 @@ static vsr_tv* tv_build(vsr_ctx* ctx, const Spec& sp, const double* y_dev, const
             }
         }
         h->fitp.alloc(std::max<size_t>(
-            std::max(std::max(h->fit_blocks, fit_blocks(h->G)), tv_sandwich_blocks(h->G)), 1));
+            std::max(std::max(std::max(h->fit_blocks, fit_blocks(h->G)), tv_sandwich_blocks(h->G)),
+                     tv_sandwich1_blocks(h->G)),
+            1));
         h->stp.alloc(kStencilVals * h->st_blocks);
-        h->resp.alloc(2 * std::max<size_t>(h->res_blocks, 1));
+        h->resp.alloc(2 * std::max<size_t>(std::max(h->res_blocks, fft_engine().pass_blocks(hr, 2)), 1));
         h->bad.alloc(1);
         h->obj.alloc(h->max_iters);
         h->res.alloc(h->max_iters);
@@ -1200,7 +1239,19 @@ static void tv_step(vsr_tv* h) {
     GammaTables tabs{h->tnr.p, h->tnc.p, h->tns.p, h->tau};
     const bool fused = use_fused(h->G);
     ChainWork cw{h->ring.p, h->chain_ctr.p};
-    if (fused) {
+    const bool a1 = fuse_axis(h->G, 1) == 1;
+    if (a1) {
+        {
+            ProfScope ps(prof, "fft_fwd_axis3_r2c", st);
+            fft_engine().axis_pass(hr, 2, false, h->theta.p, IN_REAL, h->W.p, OUT_COMPLEX, 1.0, nullptr, st);
+        }
+        {
+            ProfScope ps(prof, "fft_fwd_axis2", st);
+            fft_engine().axis_pass(hr, 1, false, h->W.p, IN_COMPLEX, h->W.p, OUT_COMPLEX, 1.0, nullptr, st);
+        }
+        ProfScope ps(prof, "tv_fft1_fold_ifft1", st);
+        launch_tv_sandwich1(h->G, h->Yl.p, h->lam.p, h->W.p, tabs, h->mu, s, h->fitp.p, st);
+    } else if (fused) {
         if (h->chain.ok) {
             ProfScope ps(prof, "chain_fwd_axis1_r2c_axis2", st);
             launch_chain_forward(hr, h->chain, cw, h->theta.p, h->W.p, st);
@@ -1216,7 +1267,14 @@ static void tv_step(vsr_tv* h) {
     }
     if (h->rel_tol > 0.0) std::swap(h->x, h->xprev);  // x_prev = x (:364)
     PassReduce red{h->resp.p, h->bad.p};
-    if (fused && h->chain.ok) {
+    if (a1) {
+        {
+            ProfScope ps(prof, "fft_inv_axis2", st);
+            fft_engine().axis_pass(hr, 1, true, h->W.p, IN_COMPLEX, h->W.p, OUT_COMPLEX, 1.0, nullptr, st);
+        }
+        ProfScope ps(prof, "fft_inv_axis3_c2r", st);
+        fft_engine().axis_pass(hr, 2, true, h->W.p, IN_COMPLEX, h->x.p, OUT_REAL, s, &red, st);
+    } else if (fused && h->chain.ok) {
         ProfScope ps(prof, "chain_inv_axis2_axis1_c2r", st);
         launch_chain_inverse(hr, h->chain, cw, h->W.p, h->x.p, s, red, st);
     } else if (fused)
@@ -1237,9 +1295,11 @@ static void tv_step(vsr_tv* h) {
     TvIterScalars sc{h->obj.p, h->res.p, h->rel.p, h->status.p};
     {
         ProfScope ps(prof, "tv_finalize", st);
-        launch_tv_finalize((int)h->iters_done, h->fitp.p, fused ? tv_sandwich_blocks(h->G) : h->fit_blocks,
-                       h->stp.p, h->st_blocks,
-                           h->resp.p, h->res_blocks, h->lambda, 1e-8, sc, nullptr, st);
+        launch_tv_finalize((int)h->iters_done, h->fitp.p,
+                           a1 ? tv_sandwich1_blocks(h->G) : (fused ? tv_sandwich_blocks(h->G) : h->fit_blocks),
+                           h->stp.p, h->st_blocks, h->resp.p,
+                           a1 ? fft_engine().pass_blocks(hr, 2) : h->res_blocks, h->lambda, 1e-8, sc, nullptr,
+                           st);
     }
     ++h->iters_done;
 }

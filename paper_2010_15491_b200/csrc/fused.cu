@@ -3,12 +3,17 @@
 #include "fft_core.cuh"
 #include "fused.cuh"
 
+#include <cstdlib>
+
 namespace vsr {
 namespace {
 
 // CTA shape for line length L and A alias lines: T consecutive g1 per tile,
 // capped so the exchange buffer (T*A lines of L complex) is <= 64 KB.
 constexpr int FR = 8;  // values per thread in the fused kernels (register budget)
+#ifndef VSR_FUSED_TMAX
+#define VSR_FUSED_TMAX 8
+#endif
 
 template <int L, int A>
 struct FShape {
@@ -16,7 +21,7 @@ struct FShape {
     static constexpr int TMAX = (4096 / (L * A)) > 0 ? (4096 / (L * A)) : 1;
     // the A alias lanes of one (g1, t) must sit in one warp: T * A <= 32
     static constexpr int TW = (32 / A) > 0 ? (32 / A) : 1;
-    static constexpr int T0 = TMAX > 8 ? 8 : TMAX;
+    static constexpr int T0 = TMAX > VSR_FUSED_TMAX ? VSR_FUSED_TMAX : TMAX;
     static constexpr int T = T0 > TW ? TW : T0;
     static constexpr int NLN = T * A;               // lines per CTA
     static constexpr int THREADS = NLN * P;
@@ -149,6 +154,270 @@ __global__ void __launch_bounds__(FShape<L, A>::THREADS, (512 / FShape<L, A>::TH
     }
 }
 
+// ---------------------------------------------------------------- Tikhonov v2
+// Same fold + inverse axis-3 FFT with the register profile of the plain
+// strided pass (16 values per thread, 128-thread CTAs, ~5 CTAs/SM): Lambda is
+// parked in this thread's own slots of the FFT exchange buffer while the fold
+// runs (same thread writes and reads them, so no barrier), and the buffer is
+// reused by the transform afterwards.
+template <int L, int A, int DS, int T>
+__global__ void __launch_bounds__(T * A * (L / 16), (512 / (T * A * (L / 16))) > 0 ? 512 / (T * A * (L / 16)) : 1)
+    tik_fold_ax3_v2_kernel(FoldGeom G, const double2* __restrict__ Yl, const double2* __restrict__ lam,
+                           const double2* __restrict__ xbh, double2* __restrict__ out, double reg2, double shift,
+                           double inv2l, double invsqrtd, const double2* __restrict__ tw) {
+    using Pl = fftc::Plan<L, 16>;
+    constexpr int R = Pl::R, P = Pl::P, NLN = T * A, RD = R / DS;
+    static_assert(R % DS == 0, "ds must divide 16");
+    extern __shared__ double2 sm[];
+    const int tid = threadIdx.x;
+    const int ln = tid % NLN, t = tid / NLN;
+    const int ti = ln % T, a = ln / T;
+    const int br = a % G.dr, bc = a / G.dr;
+    const long long tpr = G.ml / T;
+    const long long g1 = (blockIdx.x % tpr) * T + ti, g2 = blockIdx.x / tpr;
+    const long long f1 = g1 + br * G.ml, f2 = g2 + bc * G.nl;
+    const long long base = f1 + G.m * f2, stride = G.m * G.n;
+    auto sidx = [&](int q) { return q * NLN + ln; };
+    double2 v[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const long long off = base + stride * (t + P * r);
+        v[r] = __ldg(xbh + off);
+        sm[sidx(t + P * r)] = __ldg(lam + off);
+    }
+    const double2* Yrow = Yl + g1 + G.ml * g2;
+    const long long Ystride = G.ml * G.nl;
+#pragma unroll
+    for (int rr = 0; rr < RD; ++rr) {
+        const double2 yv = cscale(__ldg(Yrow + Ystride * (t + P * rr)), invsqrtd);
+        double Sx = 0.0, Sy = 0.0, gram = 0.0;
+#pragma unroll
+        for (int bs = 0; bs < DS; ++bs) {
+            const int r = rr + RD * bs;
+            const double2 Lr = sm[sidx(t + P * r)];
+            v[r] = cadd(cmulc(Lr, yv), cscale(v[r], reg2));  // k (solvers.cpp:53-54)
+            gram += cnorm(Lr);
+            const double2 pr = cmul(Lr, v[r]);
+            Sx += pr.x;
+            Sy += pr.y;
+        }
+        Sx = lanes_sum<T, A>(Sx);
+        Sy = lanes_sum<T, A>(Sy);
+        gram = lanes_sum<T, A>(gram);
+        const double den = gram + shift;
+        const double2 w = make_double2(Sx / den, Sy / den);
+#pragma unroll
+        for (int bs = 0; bs < DS; ++bs) {
+            const int r = rr + RD * bs;
+            const double2 Lr = sm[sidx(t + P * r)];
+            v[r] = cscale(csub(v[r], cmulc(Lr, w)), inv2l);  // x̂ (solvers.cpp:60-62)
+        }
+    }
+    __syncthreads();  // the exchange buffer changes hands
+    fftc::stockham<L, true, decltype(sidx), 16>(v, t, sm, sidx, tw);
+#pragma unroll
+    for (int j = 0; j < R; ++j) out[base + stride * Pl::out_q(t, j)] = v[j];
+}
+
+template <int L, int A, int DS, int T>
+void launch_tik_v2(const FoldGeom& G, const double2* Yl, const double2* lam, const double2* xbh, double2* out,
+                   double reg, cudaStream_t st) {
+    auto kern = tik_fold_ax3_v2_kernel<L, A, DS, T>;
+    const int threads = T * A * (L / 16);
+    const size_t smem = (size_t)T * A * L * sizeof(double2);
+    if (smem > 48 * 1024)
+        VSR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const unsigned grid = (unsigned)((G.ml / T) * G.nl);
+    kern<<<grid, threads, smem, st>>>(G, Yl, lam, xbh, out, 2.0 * reg, 2.0 * reg * (double)G.d, 1.0 / (2.0 * reg),
+                                      1.0 / std::sqrt((double)G.d), fft_engine().twiddles((size_t)L));
+    VSR_LAUNCH_CHECK();
+}
+
+bool dispatch_tik_v2(const FoldGeom& G, const double2* Yl, const double2* lam, const double2* xbh, double2* out,
+                     double reg, cudaStream_t st) {
+    const int A = G.dr * G.dc;
+    static const int vt = [] {
+        const char* e = std::getenv("VSR_TIK_V2_T");
+        return e ? std::atoi(e) : 2;
+    }();
+    if (A == 4 && G.ds == 2 && G.ml % 2 == 0) {
+        switch (G.s) {
+            case 256:
+                if (vt == 8 && G.ml % 8 == 0) launch_tik_v2<256, 4, 2, 8>(G, Yl, lam, xbh, out, reg, st);
+                else if (vt == 4 && G.ml % 4 == 0) launch_tik_v2<256, 4, 2, 4>(G, Yl, lam, xbh, out, reg, st);
+                else launch_tik_v2<256, 4, 2, 2>(G, Yl, lam, xbh, out, reg, st);
+                return true;
+            case 512: launch_tik_v2<512, 4, 2, 2>(G, Yl, lam, xbh, out, reg, st); return true;
+            case 1024: launch_tik_v2<1024, 4, 2, 2>(G, Yl, lam, xbh, out, reg, st); return true;
+            default: return false;
+        }
+    }
+    return false;
+}
+
+// ---------------------------------------------------------------- fold + axis 1
+// The fold fused with the contiguous axis-1 pass.  A CTA owns T consecutive
+// g2 x the A = dc*ds alias rows (g2 + bc nl, g3 + bs sl) of one g3, full rows
+// of length m: the br aliases of every g1 sit in one thread (positions q and
+// q + br*ml, ml a multiple of P) and the (bc, bs) aliases in adjacent lanes,
+// and every HBM access is a 128-byte-plus row segment.
+//   TV = false: Tikhonov fold (solvers.cpp:53-62) -> inverse axis-1 FFT -> out
+//   TV = true : W -> forward axis-1 FFT (scaled) -> TV fold (:219-233) -> inverse
+//               axis-1 FFT -> W (in place), + LR-Parseval data-fit partials
+// Lambda waits in the thread's own slots of the exchange buffer during the fold.
+template <int L, int A, int DR, int T, bool TV, bool FIT>
+__global__ void __launch_bounds__(T * A * (L / 16), (512 / (T * A * (L / 16))) > 0 ? 512 / (T * A * (L / 16)) : 1)
+    fold_axis1_kernel(FoldGeom G, const double2* __restrict__ Yl, const double2* __restrict__ lam,
+                      const double2* __restrict__ xbh, double2* W, double2* out, GammaTables tabs, double cA,
+                      double shift, double inv_scale, double invsqrtd, double fwd_scale,
+                      const double2* __restrict__ tw, double* __restrict__ fit_partials) {
+    using Pl = fftc::Plan<L, 16>;
+    constexpr int R = Pl::R, P = Pl::P, NLN = T * A;
+    constexpr int RD = R / DR;  // r = rr + RD * br: alias br of g1 = t + P rr
+    static_assert(R % DR == 0, "dr must divide 16");
+    extern __shared__ double2 sm[];
+    const int tid = threadIdx.x;
+    const int ln = tid % NLN, t = tid / NLN;
+    const int a = ln % A, ti = ln / A;
+    const int bc = a % G.dc, bs = a / G.dc;
+    const long long ng2 = G.nl / T;
+    const long long g2 = (blockIdx.x % ng2) * T + ti, g3 = blockIdx.x / ng2;
+    const long long f2 = g2 + bc * G.nl, f3 = g3 + bs * G.sl;
+    const long long rowb = G.m * (f2 + G.n * f3);
+    // line-interleaved: a quarter-warp (8 lines at one position) is one 128-B row
+    auto sidx = [&](int q) { return q * NLN + ln; };
+    double2 v[R];
+    if constexpr (TV) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[r] = W[rowb + t + P * r];
+        fftc::stockham<L, false, decltype(sidx), 16>(v, t, sm, sidx, tw);
+        fftc::to_natural<L, 16>(v);
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[r] = cscale(v[r], fwd_scale);
+        __syncthreads();  // exchange buffer reused for Lambda below
+    } else {
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[r] = __ldg(xbh + rowb + t + P * r);
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) sm[sidx(t + P * r)] = __ldg(lam + rowb + t + P * r);
+    double base_g = 0.0;
+    if constexpr (TV) base_g = __ldg(tabs.nc + f2) + __ldg(tabs.ns + f3);
+    const double2* Yrow = Yl + G.ml * (g2 + G.nl * g3);
+    double fit = 0.0;
+#pragma unroll
+    for (int rr = 0; rr < RD; ++rr) {
+        const double2 yraw = __ldg(Yrow + t + P * rr);
+        const double2 yv = cscale(yraw, invsqrtd);
+        double Gg[DR];
+        double Sx = 0.0, Sy = 0.0, gram = 0.0;
+#pragma unroll
+        for (int br = 0; br < DR; ++br) {
+            const int r = rr + RD * br;
+            const double2 Lr = sm[sidx(t + P * r)];
+            if constexpr (TV) {
+                Gg[br] = 1.0 / ((__ldg(tabs.nr + (t + P * r)) + base_g) + tabs.tau);
+                v[r] = cscale(cadd(cmulc(Lr, yv), cscale(v[r], cA)), Gg[br]);
+                gram += Gg[br] * cnorm(Lr);
+            } else {
+                v[r] = cadd(cmulc(Lr, yv), cscale(v[r], cA));
+                gram += cnorm(Lr);
+            }
+            const double2 pr = cmul(Lr, v[r]);
+            Sx += pr.x;
+            Sy += pr.y;
+        }
+        Sx = lanes_sum<1, A>(Sx);
+        Sy = lanes_sum<1, A>(Sy);
+        gram = lanes_sum<1, A>(gram);
+        const double den = gram + shift;
+        const double2 w = make_double2(Sx / den, Sy / den);
+        double ax = 0.0, ay = 0.0;
+#pragma unroll
+        for (int br = 0; br < DR; ++br) {
+            const int r = rr + RD * br;
+            const double2 Lr = sm[sidx(t + P * r)];
+            double2 c;
+            if constexpr (TV)
+                c = cmul(make_double2(Gg[br] * Lr.x, -(Gg[br] * Lr.y)), w);
+            else
+                c = cmulc(Lr, w);
+            v[r] = cscale(csub(v[r], c), inv_scale);
+            if constexpr (FIT) {
+                const double2 pr = cmul(Lr, v[r]);
+                ax += pr.x;
+                ay += pr.y;
+            }
+        }
+        if constexpr (FIT) {
+            ax = lanes_sum<1, A>(ax);
+            ay = lanes_sum<1, A>(ay);
+            if (a == 0) {
+                const double rx = yraw.x - invsqrtd * ax, ry = yraw.y - invsqrtd * ay;
+                fit += rx * rx + ry * ry;
+            }
+        }
+    }
+    __syncthreads();
+    fftc::stockham<L, true, decltype(sidx), 16>(v, t, sm, sidx, tw);
+    double2* dst = TV ? W : out;
+#pragma unroll
+    for (int j = 0; j < R; ++j) dst[rowb + Pl::out_q(t, j)] = v[j];
+    if constexpr (FIT) {
+        __shared__ double red[32];
+        double vv[1] = {fit};
+        block_reduce_sum<1>(vv, red);
+        if (tid == 0) fit_partials[blockIdx.x] = vv[0];
+    }
+}
+
+template <int L, int A, int DR>
+struct A1Shape {
+    static constexpr int T0 = 32 / A > 0 ? 32 / A : 1;          // NLN <= 32 (alias lanes in a warp)
+    static constexpr int TT = (T0 * A * (L / 16)) > 256 ? (256 / (A * (L / 16)) > 0 ? 256 / (A * (L / 16)) : 1) : T0;
+    static constexpr int T = TT > 2 ? 2 : TT;                    // 2 consecutive g2 per tile
+    static constexpr int THREADS = T * A * (L / 16);
+    static constexpr size_t SMEM = (size_t)T * A * L * sizeof(double2);
+};
+
+template <int L, int A, int DR, bool TV, bool FIT>
+void launch_a1(const FoldGeom& G, const double2* Yl, const double2* lam, const double2* xbh, double2* W,
+               double2* out, const GammaTables& tabs, double cA, double shift, double inv_scale, double fwd_scale,
+               double* fit, cudaStream_t st) {
+    using Sh = A1Shape<L, A, DR>;
+    auto kern = fold_axis1_kernel<L, A, DR, Sh::T, TV, FIT>;
+    if (Sh::SMEM > 48 * 1024)
+        VSR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Sh::SMEM));
+    const unsigned grid = (unsigned)((G.nl / Sh::T) * G.sl);
+    kern<<<grid, Sh::THREADS, Sh::SMEM, st>>>(G, Yl, lam, xbh, W, out, tabs, cA, shift, inv_scale,
+                                              1.0 / std::sqrt((double)G.d), fwd_scale,
+                                              fft_engine().twiddles((size_t)L), fit);
+    VSR_LAUNCH_CHECK();
+}
+
+// (L = m, A = dc*ds, DR = dr) triples served by fold_axis1_kernel
+#define VSR_A1_TABLE(X)                                                                 \
+    X(64, 4, 2) X(128, 4, 2) X(256, 4, 2) X(512, 4, 2) X(1024, 4, 2)                      \
+    X(64, 8, 2) X(128, 8, 2) X(256, 8, 2) X(512, 8, 2) X(1024, 8, 2)                      \
+    X(64, 16, 4) X(128, 16, 4) X(256, 16, 4) X(512, 16, 4)                               \
+    X(64, 1, 1) X(128, 1, 1) X(256, 1, 1) X(512, 1, 1) X(1024, 1, 1)
+
+template <bool TV, bool FIT>
+bool dispatch_a1(const FoldGeom& G, const double2* Yl, const double2* lam, const double2* xbh, double2* W,
+                 double2* out, const GammaTables& tabs, double cA, double shift, double inv_scale,
+                 double fwd_scale, double* fit, cudaStream_t st) {
+    const int A = G.dc * G.ds;
+#define VSR_X(LL, AA, DD)                                                                           \
+    if (G.m == LL && A == AA && G.dr == DD && G.nl % A1Shape<LL, AA, DD>::T == 0) {                  \
+        launch_a1<LL, AA, DD, TV, FIT>(G, Yl, lam, xbh, W, out, tabs, cA, shift, inv_scale, fwd_scale, \
+                                       fit, st);                                                    \
+        return true;                                                                                \
+    }
+    VSR_A1_TABLE(VSR_X)
+#undef VSR_X
+    return false;
+}
+
 // ---------------------------------------------------------------- dispatch
 struct Key {
     int L, A, DS;
@@ -210,6 +479,11 @@ void launch_tik_fold_ifft3(const FoldGeom& G, const double2* Yl, const double2* 
     GammaTables none{nullptr, nullptr, nullptr, 0.0};
     const double shift = 2.0 * reg * (double)G.d;  // solvers.cpp:43
     const double inv2l = 1.0 / (2.0 * reg);         // solvers.cpp:59
+    static const bool v2 = [] {
+        const char* e = std::getenv("VSR_TIK_V2");
+        return e && e[0] == '1';
+    }();
+    if (v2 && dispatch_tik_v2(G, Yl, lam, xbh, out, reg, st)) return;
     if (!dispatch<false, false>(G, Yl, lam, xbh, nullptr, out, none, 2.0 * reg, shift, inv2l, 1.0,
                                 nullptr, st))
         throw std::logic_error("launch_tik_fold_ifft3: unsupported geometry");
@@ -235,6 +509,43 @@ void launch_tv_sandwich(const FoldGeom& G, const double2* Yl, const double2* lam
                         : dispatch<true, false>(G, Yl, lam, nullptr, W, nullptr, tabs, mu, shift, inv_mu,
                                                 fwd_scale, nullptr, st);
     if (!ok) throw std::logic_error("launch_tv_sandwich: unsupported geometry");
+}
+
+bool fused_axis1_ok(const FoldGeom& G) {
+    const int A = G.dc * G.ds;
+#define VSR_X(LL, AA, DD) \
+    if (G.m == LL && A == AA && G.dr == DD && G.nl % A1Shape<LL, AA, DD>::T == 0) return true;
+    VSR_A1_TABLE(VSR_X)
+#undef VSR_X
+    return false;
+}
+
+void launch_tik_fold_ifft1(const FoldGeom& G, const double2* Yl, const double2* lam, const double2* xbh,
+                           double2* out, double reg, cudaStream_t st) {
+    GammaTables none{nullptr, nullptr, nullptr, 0.0};
+    if (!dispatch_a1<false, false>(G, Yl, lam, xbh, nullptr, out, none, 2.0 * reg, 2.0 * reg * (double)G.d,
+                                   1.0 / (2.0 * reg), 1.0, nullptr, st))
+        throw std::logic_error("launch_tik_fold_ifft1: unsupported geometry");
+}
+
+size_t tv_sandwich1_blocks(const FoldGeom& G) {
+    const int A = G.dc * G.ds;
+#define VSR_X(LL, AA, DD) \
+    if (G.m == LL && A == AA && G.dr == DD) return (size_t)((G.nl / A1Shape<LL, AA, DD>::T) * G.sl);
+    VSR_A1_TABLE(VSR_X)
+#undef VSR_X
+    return 0;
+}
+
+void launch_tv_sandwich1(const FoldGeom& G, const double2* Yl, const double2* lam, double2* W,
+                         const GammaTables& tabs, double mu, double fwd_scale, double* fit_partials,
+                         cudaStream_t st) {
+    const double shift = mu * (double)G.d, inv_mu = 1.0 / mu;
+    const bool ok = fit_partials ? dispatch_a1<true, true>(G, Yl, lam, nullptr, W, nullptr, tabs, mu, shift, inv_mu,
+                                                           fwd_scale, fit_partials, st)
+                                 : dispatch_a1<true, false>(G, Yl, lam, nullptr, W, nullptr, tabs, mu, shift,
+                                                            inv_mu, fwd_scale, nullptr, st);
+    if (!ok) throw std::logic_error("launch_tv_sandwich1: unsupported geometry");
 }
 
 }  // namespace vsr

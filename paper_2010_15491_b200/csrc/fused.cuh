@@ -31,4 +31,15 @@ void launch_tv_sandwich(const FoldGeom& G, const double2* Yl, const double2* lam
                         const GammaTables& tabs, double mu, double fwd_scale, double* fit_partials,
                         cudaStream_t st);
 
+// Same folds fused with the contiguous axis-1 pass instead (tile = the
+// dc*ds alias rows of T consecutive g2, full rows along axis 1):
+//   Tikhonov: out = IFFT_axis1(x̂); TV: W -> FFT_axis1 -> fold -> IFFT_axis1 -> W.
+bool fused_axis1_ok(const FoldGeom& G);
+void launch_tik_fold_ifft1(const FoldGeom& G, const double2* Yl, const double2* lam, const double2* xbh,
+                           double2* out, double reg, cudaStream_t st);
+size_t tv_sandwich1_blocks(const FoldGeom& G);
+void launch_tv_sandwich1(const FoldGeom& G, const double2* Yl, const double2* lam, double2* W,
+                         const GammaTables& tabs, double mu, double fwd_scale, double* fit_partials,
+                         cudaStream_t st);
+
 }  // namespace vsr
