@@ -253,10 +253,8 @@ __global__ void __launch_bounds__(STH)
                            double* __restrict__ theta, double thr, const double* __restrict__ xprev,
                            double* __restrict__ partials, int halo, long long dsi, long long dso) {
     extern __shared__ double sm[];
-    double* xs = sm;                 // [3][FXH][FXW]
-    double* ds = xs + 3 * FXS;       // [2][3][FDH][FDW]
-    double* rx = ds + 2 * FDS;       // [TY][TX+1]
-    double* ry = rx + TY * (TX + 1); // [TY+1][TX]
+    double* rx = sm + 3 * FXS + 2 * FDS;  // [TY][TX+1]
+    double* ry = rx + TY * (TX + 1);       // [TY+1][TX]
     __shared__ double red[32 * 4];
 
     const int tid = threadIdx.x;
@@ -265,7 +263,6 @@ __global__ void __launch_bounds__(STH)
     const int k0 = blockIdx.z * KC;
     const int k1 = min(k0 + KC, s);
     const long long plane = (long long)m * n;
-    const long long N = plane * s;
     const bool valid = (i0 + tx) < m && (j0 + ty) < n;
     const int col = valid ? (i0 + tx) + m * (j0 + ty) : 0;
 
@@ -293,58 +290,75 @@ __global__ void __launch_bounds__(STH)
         doff[q] = (long long)c * dsi + wrap(i0 - 2 + 2 * pc, m) + (long long)m * wrap(j0 - 1 + row, n);
         dsm[q] = c * FDH * FDW + row * FDW + 2 * pc;
     }
-    // z only leaves [0, s) by one plane at a chunk edge (z = -1 or z = s): periodic
-    // wrap on a whole volume, or explicit halo planes (x, dual_in pre-offset by
-    // one plane) on a slab of a distributed volume
-    auto zoff = [&](int z) {
+    // plane pointers advance by one plane per step; in periodic mode they wrap
+    // only where z leaves [0, s) (z = -1 at the chunk start, z = s at its end)
+    auto zp = [&](int z) -> long long {
         return plane * (long long)(halo ? z : (z < 0 ? z + s : (z >= s ? z - s : z)));
     };
+    // smem ring: x slots rotate through three buffers, dual through two
+    double* xsl[3] = {sm, sm + FXS, sm + 2 * FXS};
+    double* dsl[2] = {sm + 3 * FXS, sm + 3 * FXS + FDS};
 
     double2 rxv = make_double2(0.0, 0.0), rdv[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
-    auto load_x = [&](int z) {
-        if (xa) rxv = __ldg(reinterpret_cast<const double2*>(x + zoff(z) + xoff));
-    };
-    auto load_d = [&](int z) {
-        const long long zo = zoff(z);
-#pragma unroll
-        for (int q = 0; q < 2; ++q)
-            if (da[q]) rdv[q] = __ldg(reinterpret_cast<const double2*>(dual_in + zo + doff[q]));
-    };
-    auto store_x = [&](int z) {
-        if (xa) *reinterpret_cast<double2*>(xs + ((z - k0 + 1) % 3) * FXS + xsm) = rxv;
-    };
-    auto store_d = [&](int z) {
-#pragma unroll
-        for (int q = 0; q < 2; ++q)
-            if (da[q]) *reinterpret_cast<double2*>(ds + ((z - k0 + 1) & 1) * FDS + dsm[q]) = rdv[q];
-    };
-
     // prologue: x(k0-1), x(k0), dual(k0-1) resident; x(k0+1), dual(k0) in registers
-    load_x(k0 - 1);
-    if (!INIT) load_d(k0 - 1);
-    store_x(k0 - 1);
-    if (!INIT) store_d(k0 - 1);
-    load_x(k0);
-    store_x(k0);
-    if (k0 + 1 <= k1) load_x(k0 + 1);
-    if (!INIT && k0 < k1) load_d(k0);
+    if (xa) *reinterpret_cast<double2*>(xsl[0] + xsm) = __ldg(reinterpret_cast<const double2*>(x + zp(k0 - 1) + xoff));
+    if (!INIT) {
+        const long long zo = zp(k0 - 1);
+#pragma unroll
+        for (int q = 0; q < 2; ++q)
+            if (da[q]) *reinterpret_cast<double2*>(dsl[0] + dsm[q]) =
+                __ldg(reinterpret_cast<const double2*>(dual_in + zo + doff[q]));
+    }
+    if (xa) *reinterpret_cast<double2*>(xsl[1] + xsm) = __ldg(reinterpret_cast<const double2*>(x + zp(k0) + xoff));
+    const double* xnext = x + xoff;       // advanced below; holds plane k+3 at step k
+    const double* dnext = dual_in;        // plane k+2 at step k
+    long long zx = zp(k0 + 1), zd = zp(k0);
+    if (xa && k0 + 1 <= k1) rxv = __ldg(reinterpret_cast<const double2*>(xnext + zx));
+    if (!INIT && k0 < k1) {
+#pragma unroll
+        for (int q = 0; q < 2; ++q)
+            if (da[q]) rdv[q] = __ldg(reinterpret_cast<const double2*>(dnext + zd + doff[q]));
+    }
+    // halo work spread over all warps: lanes 0..4 of each warp take 5 of the 40 points
+    const int lane = tid & 31, warp = tid >> 5;
+    const int hslot = warp * 5 + lane;  // valid when lane < 5
+    const bool hwork = lane < 5 && hslot < TY + TX;
+    const int hii = hslot < TY ? -1 : hslot - TY;
+    const int hjj = hslot < TY ? hslot : -1;
+    const int hx = (hjj + 1) * FXW + hii + 2;
+    const int hd = (hjj + 1) * FDW + hii + 2;
+    const int xi = (ty + 1) * FXW + tx + 2;
+    const int di = (ty + 1) * FDW + tx + 2;
 
     double acc_res = 0.0, acc_tv = 0.0, acc_dx = 0.0, acc_xp = 0.0;
     double rz_prev = 0.0;
+    long long zo = zp(k0 - 1);
     for (int k = k0 - 1; k < k1; ++k) {
-        // registers -> smem for step k+1, then request the next planes
-        if (k + 2 <= k1) store_x(k + 2);
-        if (!INIT && k + 1 <= k1 - 1) store_d(k + 1);
-        if (k + 3 <= k1) load_x(k + 3);
-        if (!INIT && k + 2 <= k1 - 1) load_d(k + 2);
+        // registers -> smem for step k+1, then request x(k+3), dual(k+2)
+        if (k + 2 <= k1 && xa) *reinterpret_cast<double2*>(xsl[2] + xsm) = rxv;
+        if (!INIT && k + 1 <= k1 - 1) {
+#pragma unroll
+            for (int q = 0; q < 2; ++q)
+                if (da[q]) *reinterpret_cast<double2*>(dsl[1] + dsm[q]) = rdv[q];
+        }
+        if (k + 3 <= k1) {
+            zx += plane;
+            if (!halo && zx >= plane * s) zx -= plane * s;
+            if (xa) rxv = __ldg(reinterpret_cast<const double2*>(xnext + zx));
+        }
+        if (!INIT && k + 2 <= k1 - 1) {
+            zd += plane;
+            if (!halo && zd >= plane * s) zd -= plane * s;
+#pragma unroll
+            for (int q = 0; q < 2; ++q)
+                if (da[q]) rdv[q] = __ldg(reinterpret_cast<const double2*>(dnext + zd + doff[q]));
+        }
         __syncthreads();
         const bool warm = k < k0;
-        const double* X0 = xs + ((k - k0 + 1) % 3) * FXS;
-        const double* X1 = xs + ((k - k0 + 2) % 3) * FXS;
-        const double* D0 = ds + ((k - k0 + 1) & 1) * FDS;
-        const long long zo = zoff(k);
+        const double* X0 = xsl[0];
+        const double* X1 = xsl[1];
+        const double* D0 = dsl[0];
 
-        const int xi = (ty + 1) * FXW + tx + 2;
         const double xc = X0[xi];
         const double l0 = X0[xi + 1] - xc;
         const double l1 = X0[xi + FXW] - xc;
@@ -362,7 +376,6 @@ __global__ void __launch_bounds__(STH)
                 acc_tv += sqrt(l0 * l0 + l1 * l1 + l2 * l2);
             }
         } else {
-            const int di = (ty + 1) * FDW + tx + 2;
             const Shrunk o = shrink_point(l0, l1, l2, D0[di], D0[FDH * FDW + di], D0[2 * FDH * FDW + di], thr);
             r0 = o.r0;
             r1 = o.r1;
@@ -388,10 +401,7 @@ __global__ void __launch_bounds__(STH)
         if (!warm) {
             rx[ty * (TX + 1) + tx + 1] = r0;
             ry[(ty + 1) * TX + tx] = r1;
-            if (tid < TY + TX) {  // halo: rho_x at ii = -1, rho_y at jj = -1
-                const int ii = tid < TY ? -1 : tid - TY;
-                const int jj = tid < TY ? tid : -1;
-                const int hx = (jj + 1) * FXW + ii + 2;
+            if (hwork) {  // halo: rho_x at ii = -1, rho_y at jj = -1
                 const double hc = X0[hx];
                 const double h0 = X0[hx + 1] - hc;
                 const double h1 = X0[hx + FXW] - hc;
@@ -401,16 +411,15 @@ __global__ void __launch_bounds__(STH)
                     q0 = h0;
                     q1 = h1;
                 } else {
-                    const int hd = (jj + 1) * FDW + ii + 2;
                     const Shrunk o =
                         shrink_point(h0, h1, h2, D0[hd], D0[FDH * FDW + hd], D0[2 * FDH * FDW + hd], thr);
                     q0 = o.r0;
                     q1 = o.r1;
                 }
-                if (tid < TY)
-                    rx[jj * (TX + 1)] = q0;
+                if (hslot < TY)
+                    rx[hjj * (TX + 1)] = q0;
                 else
-                    ry[ii] = q1;
+                    ry[hii] = q1;
             }
         }
         __syncthreads();
@@ -422,6 +431,16 @@ __global__ void __launch_bounds__(STH)
             theta[col + zo] = (ax + ay) + az;
         }
         rz_prev = r2;
+        // rotate the rings: x slots (k, k+1, k+2) -> (k+1, k+2, k+3); dual (k, k+1) -> (k+1, k+2)
+        double* t0 = xsl[0];
+        xsl[0] = xsl[1];
+        xsl[1] = xsl[2];
+        xsl[2] = t0;
+        double* t1 = dsl[0];
+        dsl[0] = dsl[1];
+        dsl[1] = t1;
+        zo += plane;
+        if (!halo && zo >= plane * s) zo -= plane * s;
     }
 
     double v[4] = {acc_res, acc_tv, acc_dx, acc_xp};
