@@ -23,13 +23,24 @@ struct Shrunk {
     double u0, u1, u2, dn0, dn1, dn2, r0, r1, r2;
 };
 
-// solvers.cpp:286-301 (factor = mag > t ? 1 - t/mag : 0) and :387-390.
+// |v| via the fp64 reciprocal square root (MUFU seed + Newton, <= 1 ulp): no
+// IEEE sqrt/div slow paths in the hot loop.  |0| = 0.
+__device__ __forceinline__ double norm3(double a, double b, double c, double* inv) {
+    const double m2 = a * a + b * b + c * c;
+    const double r = m2 > 0.0 ? rsqrt(m2) : 0.0;
+    *inv = r;
+    return m2 * r;
+}
+
+// solvers.cpp:286-301 (factor = mag > t ? 1 - t/mag : 0) and :387-390;
+// t/mag evaluated as t * rsqrt(mag^2).
 __device__ __forceinline__ Shrunk shrink_point(double l0, double l1, double l2, double d0, double d1,
                                                double d2, double thr) {
     Shrunk o;
     const double n0 = l0 + d0, n1 = l1 + d1, n2 = l2 + d2;
-    const double mag = sqrt(n0 * n0 + n1 * n1 + n2 * n2);
-    const double f = mag > thr ? 1.0 - thr / mag : 0.0;
+    double inv;
+    const double mag = norm3(n0, n1, n2, &inv);
+    const double f = mag > thr ? 1.0 - thr * inv : 0.0;
     o.u0 = f * n0;
     o.u1 = f * n1;
     o.u2 = f * n2;
@@ -373,7 +384,10 @@ __global__ void __launch_bounds__(STH)
                 dual_out[idx] = 0.0;
                 dual_out[dso + idx] = 0.0;
                 dual_out[2 * dso + idx] = 0.0;
-                acc_tv += sqrt(l0 * l0 + l1 * l1 + l2 * l2);
+                {
+                    double inv_;
+                    acc_tv += norm3(l0, l1, l2, &inv_);
+                }
             }
         } else {
             const Shrunk o = shrink_point(l0, l1, l2, D0[di], D0[FDH * FDW + di], D0[2 * FDH * FDW + di], thr);
@@ -387,7 +401,10 @@ __global__ void __launch_bounds__(STH)
                 dual_out[2 * dso + idx] = o.dn2;
                 const double e0 = l0 - o.u0, e1 = l1 - o.u1, e2 = l2 - o.u2;
                 acc_res += e0 * e0 + e1 * e1 + e2 * e2;
-                acc_tv += sqrt(l0 * l0 + l1 * l1 + l2 * l2);
+                {
+                    double inv_;
+                    acc_tv += norm3(l0, l1, l2, &inv_);
+                }
             }
         }
         if constexpr (RELCHG) {
