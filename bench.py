@@ -216,6 +216,10 @@ STAGE_BYTES = {
 }
 
 
+# fused fold stages that read the 16N-byte HR Lambda unless it is separable
+SEP_STAGES = {"tik_fold_ifft_axis3", "tv_fft3_fold_ifft3", "tik_fold_ifft_axis1", "tv_fft1_fold_ifft1"}
+
+
 def run_b200(args, rank, world, local):
     import torch
     from paper_2010_15491_b200 import synth
@@ -311,11 +315,14 @@ def run_b200(args, rank, world, local):
     if not hbm:
         hbm, peak_src = 6650.0, "fallback (B200_PROFILING.md)"
     st_rows = {}
+    sep = op.separable()
     for name, (tot_ms, cnt) in stages.items():
         avg = tot_ms / max(cnt, 1)
         row = {"avg_us": avg * 1e3, "launches": cnt, "share": tot_ms / (ms * args.steps)}
         if name in STAGE_BYTES:
             a, b = STAGE_BYTES[name]
+            if sep and name in SEP_STAGES:
+                a -= 16  # Lambda rebuilt from 1-D tables, not streamed
             byts = a * N + b * Nl
             row["alg_bytes"] = byts
             row["gbs"] = byts / (avg * 1e-3) / 1e9
@@ -330,7 +337,10 @@ def run_b200(args, rank, world, local):
                 "alg_bytes_per_launch": d["alg_bytes"],
                 "path": {"alg_bytes_per_step": path_bytes, "achieved": path_bytes / (ms * 1e-3) / 1e9,
                          "frac": path_bytes / (ms * 1e-3) / 1e9 / hbm,
-                         "model": "(72 + 40/d) N bytes per Tikhonov solve (SURVEY 8(d))"}}
+                         "model": "(72 + 40/d) N bytes per Tikhonov solve (SURVEY 8(d))",
+                         "lambda_separable": sep,
+                         "note": ("Lambda rebuilt from 1-D tables: compulsory traffic is (56 + 40/d) N"
+                                  if sep else "general Lambda streamed")}}
     try:
         prof = json.loads((ROOT / "profiles" / "traffic.json").read_text())
         if dom in prof:
@@ -385,22 +395,26 @@ def bench_tv(args, ctx, V, synth, torch, stream, local, hbm):
     stages = V.profile_read(ctx)
     V.profile_enable(ctx, False)
     rep = tv.report()
+    tv_sep = tv.separable()
     tv.close()
     ms = e0.elapsed_time(e1) / k
     path = V.tv_algorithmic_bytes(cfg.hr, cfg.rates)
     rows = {}
+    sep = tv_sep
     for name, (tot, cnt) in stages.items():
         avg = tot / max(cnt, 1)
         r = {"avg_us": avg * 1e3, "launches": cnt, "share": tot / (ms * k)}
         if name in STAGE_BYTES:
             a, b = STAGE_BYTES[name]
+            if sep and name in SEP_STAGES:
+                a -= 16
             byts = a * N + b * (N // cfg.d)
             r["gbs"] = byts / (avg * 1e-3) / 1e9
             r["frac"] = r["gbs"] / hbm
         rows[name] = r
     return {"workload": "config2: ADMM-TV fp64 256^3 -> 64^3 (d=64), lambda 2e-3, mu 0.05, tau 1e-3*mu",
             "value": N / (ms * 1e-3), "unit": "HR voxels/s per ADMM-TV iteration", "ms_per_iter": ms,
-            "iters_timed": k, "path_frac": path / (ms * 1e-3) / 1e9 / hbm,
+            "iters_timed": k, "path_frac": path / (ms * 1e-3) / 1e9 / hbm, "lambda_separable": tv_sep,
             "path_model": "(160 + 16/d) N bytes per iteration", "objective_last": rep.objective[-1],
             "stages": rows}
 

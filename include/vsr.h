@@ -214,6 +214,12 @@ int vsr_slab_tv_stencil_d(vsr_ctx* ctx, const size_t hr_dims[3], const size_t ra
 int vsr_slab_fit_d(vsr_ctx* ctx, const size_t hr_dims[3], const size_t rates[3], int P,
                    const double* Yl_loc, const double* lam_loc, const double* xh_loc, double* fit_out);
 
+/* 1 when the operator's blur spectrum was detected separable, Lambda(f) =
+ * a[f1] b[f2] c[f3] (any Gaussian PSF): the fused folds then rebuild Lambda
+ * from three 1-D tables instead of streaming the 16N-byte HR spectrum. */
+int vsr_tikhonov_separable(vsr_tikhonov* t);
+int vsr_tv_separable(vsr_tv* h);
+
 /* ---- instrumentation (bench): kernels launched by this library so far, and
  *      per-stage CUDA-event durations on the context stream when enabled. */
 int vsr_launch_count(uint64_t* out);

@@ -359,6 +359,25 @@ int fuse_axis(const FoldGeom& G, int dflt) {
     return 0;
 }
 
+// Separable-spectrum tables (fold.cuh SepTables); VSR_NO_SEP=1 disables.
+struct SepState {
+    DevBuf<double2> tab;  // a[m], b[n], c[s]
+    SepTables t;
+    void detect(const Dims& hr, const double2* lam, cudaStream_t st) {
+        static const bool off = [] {
+            const char* e = std::getenv("VSR_NO_SEP");
+            return e && e[0] == '1';
+        }();
+        t = SepTables{};
+        if (off) return;
+        tab.alloc(hr.m + hr.n + hr.s);
+        if (detect_separable(hr, lam, tab.p, tab.p + hr.m, tab.p + hr.m + hr.n, 1e-13, st))
+            t = SepTables{tab.p, tab.p + hr.m, tab.p + hr.m + hr.n};
+        else
+            tab.release();
+    }
+};
+
 bool use_fused(const FoldGeom& G) {
     static const bool off = [] {
         const char* e = std::getenv("VSR_NO_FUSE");
@@ -781,6 +800,7 @@ struct vsr_tikhonov {
     DevBuf<double> partials, status;  // status: [violated, ratio, last ratio, pad]
     DevBuf<unsigned long long> bad;
     size_t res_blocks = 0;
+    SepState sep;                     // Lambda = a[f1] b[f2] c[f3] when the PSF is separable
     ChainPlan chain;                  // chained inverse axes 2 -> 1 (L2 ring)
     DevBuf<double2> ring;
     DevBuf<int> chain_ctr;
@@ -835,6 +855,7 @@ int vsr_tikhonov_create(vsr_ctx* ctx, const size_t hr_dims[3], const size_t rate
         try {
             h2d(ctx, t->lam.p, lambda_c, t->lam.bytes());
             h2d(ctx, t->x.p, xbar_r, t->x.bytes());
+            t->sep.detect(t->sp.hr, t->lam.p, ctx->stream);
             // xbar_hat_ = fft3(cfg.xbar)   (solvers.cpp:45)
             fft_engine().forward3(t->sp.hr, t->x.p, IN_REAL, t->xbh.p, inv_sqrt_count(t->sp.hr),
                                   ctx->stream);
@@ -858,6 +879,7 @@ int vsr_tikhonov_create_d(vsr_ctx* ctx, const size_t hr_dims[3], const size_t ra
         try {
             VSR_CUDA(cudaMemcpyAsync(t->lam.p, lambda_c_dev, t->lam.bytes(),
                                      cudaMemcpyDeviceToDevice, ctx->stream));
+            t->sep.detect(t->sp.hr, t->lam.p, ctx->stream);
             fft_engine().forward3(t->sp.hr, xbar_r_dev, IN_REAL, t->xbh.p,
                                   inv_sqrt_count(t->sp.hr), ctx->stream);
             ++g_fwd;
@@ -895,7 +917,7 @@ static void tik_enqueue(vsr_tikhonov* t, const double* y_dev, double* x_dev) {
         // fold + inverse axis 1 (contiguous rows), then axis 2, then axis 3 -> real x
         {
             ProfScope ps(prof, "tik_fold_ifft_axis1", st);
-            launch_tik_fold_ifft1(t->G, t->Yl.p, t->lam.p, t->xbh.p, t->xh.p, t->reg, st);
+            launch_tik_fold_ifft1(t->G, t->Yl.p, t->lam.p, t->xbh.p, t->xh.p, t->reg, st, t->sep.t);
         }
         {
             ProfScope ps(prof, "fft_inv_axis2", st);
@@ -909,7 +931,7 @@ static void tik_enqueue(vsr_tikhonov* t, const double* y_dev, double* x_dev) {
     } else if (use_fused(t->G)) {
         {
             ProfScope ps(prof, "tik_fold_ifft_axis3", st);
-            launch_tik_fold_ifft3(t->G, t->Yl.p, t->lam.p, t->xbh.p, t->xh.p, t->reg, st);
+            launch_tik_fold_ifft3(t->G, t->Yl.p, t->lam.p, t->xbh.p, t->xh.p, t->reg, st, t->sep.t);
         }
         if (t->chain.ok) {
             ProfScope ps(prof, "chain_inv_axis2_axis1_c2r", st);
@@ -1125,6 +1147,7 @@ struct vsr_tv {
     ChainPlan chain;
     DevBuf<double2> ring;
     DevBuf<int> chain_ctr;
+    SepState sep;
     size_t iters_done = 0;
     bool dual_in_a = true;
     bool stopped = false;
@@ -1202,6 +1225,7 @@ static vsr_tv* tv_build(vsr_ctx* ctx, const Spec& sp, const double* y_dev, const
         fft_engine().forward3(hr, psf_dev, IN_REAL, h->lam.p, 1.0, st);
         fft_engine().forward3(sp.lr, y_dev, IN_REAL, h->Yl.p, inv_sqrt_count(sp.lr), st);
         g_fwd += 2;
+        h->sep.detect(hr, h->lam.p, st);
         // init (solvers.cpp:346-354)
         if (cfg->init == VSR_INIT_ZERO) {
             VSR_CUDA(cudaMemsetAsync(h->x.p, 0, h->x.bytes(), st));
@@ -1250,7 +1274,7 @@ static void tv_step(vsr_tv* h) {
             fft_engine().axis_pass(hr, 1, false, h->W.p, IN_COMPLEX, h->W.p, OUT_COMPLEX, 1.0, nullptr, st);
         }
         ProfScope ps(prof, "tv_fft1_fold_ifft1", st);
-        launch_tv_sandwich1(h->G, h->Yl.p, h->lam.p, h->W.p, tabs, h->mu, s, h->fitp.p, st);
+        launch_tv_sandwich1(h->G, h->Yl.p, h->lam.p, h->W.p, tabs, h->mu, s, h->fitp.p, st, h->sep.t);
     } else if (fused) {
         if (h->chain.ok) {
             ProfScope ps(prof, "chain_fwd_axis1_r2c_axis2", st);
@@ -1259,7 +1283,7 @@ static void tv_step(vsr_tv* h) {
             fft_engine().forward12(hr, h->theta.p, IN_REAL, h->W.p, st, prof);
         }
         ProfScope ps(prof, "tv_fft3_fold_ifft3", st);
-        launch_tv_sandwich(h->G, h->Yl.p, h->lam.p, h->W.p, tabs, h->mu, s, h->fitp.p, st);
+        launch_tv_sandwich(h->G, h->Yl.p, h->lam.p, h->W.p, tabs, h->mu, s, h->fitp.p, st, h->sep.t);
     } else {
         fft_engine().forward3(hr, h->theta.p, IN_REAL, h->W.p, s, st, prof);
         ProfScope ps(prof, "tv_fold", st);
@@ -1409,6 +1433,9 @@ int vsr_tv_destroy(vsr_tv* h) {
         delete h;
     });
 }
+
+int vsr_tikhonov_separable(vsr_tikhonov* t) { return t && t->sep.t.a ? 1 : 0; }
+int vsr_tv_separable(vsr_tv* h) { return h && h->sep.t.a ? 1 : 0; }
 
 int vsr_launch_count(uint64_t* out) {
     if (out) *out = g_launches.load(std::memory_order_relaxed);

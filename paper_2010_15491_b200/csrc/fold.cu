@@ -4,6 +4,8 @@
 // For d <= 8 the per-alias operands stay in registers (one HBM read per
 // alias); for larger d a second sweep re-reads them (L2-resident: the CTA's
 // alias footprint is a few tens of KB).
+#include <cstring>
+
 #include "fold.cuh"
 
 namespace vsr {
@@ -511,6 +513,74 @@ void launch_finalize_sum(const double* partials, int stride, int nvals, size_t n
                          double* out, cudaStream_t st) {
     finalize_sum_kernel<<<1, 1024, 0, st>>>(partials, stride, nvals, (long long)nblocks, out);
     VSR_LAUNCH_CHECK();
+}
+
+namespace {
+__global__ void sep_dev_kernel(long long m, long long n, long long N, const double2* __restrict__ lam,
+                               unsigned long long* __restrict__ dev_bits, unsigned long long* __restrict__ mag_bits) {
+    const long long f = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    double dev = 0.0, mag = 0.0;
+    if (f < N) {
+        const long long f1 = f % m, f2 = (f / m) % n, f3 = f / (m * n);
+        const double2 L0 = lam[0];
+        const double2 l = lam[f];
+        const double2 lhs = cmul(l, cmul(L0, L0));
+        const double2 rhs = cmul(cmul(lam[f1], lam[m * f2]), lam[m * n * f3]);
+        const double2 d = csub(lhs, rhs);
+        dev = sqrt(cnorm(d));
+        mag = sqrt(cnorm(l));
+    }
+    // non-negative doubles order like their bit patterns
+    for (int o = 16; o > 0; o >>= 1) {
+        dev = fmax(dev, __shfl_down_sync(0xffffffffu, dev, o));
+        mag = fmax(mag, __shfl_down_sync(0xffffffffu, mag, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMax(dev_bits, (unsigned long long)__double_as_longlong(dev));
+        atomicMax(mag_bits, (unsigned long long)__double_as_longlong(mag));
+    }
+}
+
+__global__ void sep_tables_kernel(long long m, long long n, long long s, const double2* __restrict__ lam,
+                                  double2* a, double2* b, double2* c) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const double2 L0 = lam[0];
+    const double den = cnorm(L0);
+    // x / L0 = x conj(L0) / |L0|^2
+    auto divL0 = [&](double2 x) {
+        const double2 p = cmul(x, make_double2(L0.x, -L0.y));
+        return make_double2(p.x / den, p.y / den);
+    };
+    if (i < m) a[i] = divL0(lam[i]);
+    if (i < n) b[i] = divL0(lam[m * i]);
+    if (i < s) c[i] = lam[m * n * i];
+}
+}  // namespace
+
+bool detect_separable(const Dims& hr, const double2* lam, double2* a, double2* b, double2* c, double tol,
+                      cudaStream_t st) {
+    const long long N = (long long)hr.count();
+    unsigned long long* bits = nullptr;
+    VSR_CUDA(cudaMallocAsync(&bits, 2 * sizeof(unsigned long long), st));
+    VSR_CUDA(cudaMemsetAsync(bits, 0, 2 * sizeof(unsigned long long), st));
+    sep_dev_kernel<<<(unsigned)((N + 255) / 256), 256, 0, st>>>((long long)hr.m, (long long)hr.n, N, lam, bits,
+                                                              bits + 1);
+    VSR_LAUNCH_CHECK();
+    unsigned long long h[2];
+    VSR_CUDA(cudaMemcpyAsync(h, bits, sizeof(h), cudaMemcpyDeviceToHost, st));
+    VSR_CUDA(cudaStreamSynchronize(st));
+    cudaFreeAsync(bits, st);
+    double dev, mag, l0[2];
+    std::memcpy(&dev, &h[0], 8);
+    std::memcpy(&mag, &h[1], 8);
+    VSR_CUDA(cudaMemcpy(l0, lam, sizeof(l0), cudaMemcpyDeviceToHost));
+    const double l0m2 = l0[0] * l0[0] + l0[1] * l0[1];
+    if (!(l0m2 > 0.0) || !(mag > 0.0) || !(dev <= tol * mag * l0m2)) return false;
+    const long long mx = std::max<long long>(hr.m, std::max<long long>(hr.n, hr.s));
+    sep_tables_kernel<<<(unsigned)((mx + 255) / 256), 256, 0, st>>>((long long)hr.m, (long long)hr.n,
+                                                                  (long long)hr.s, lam, a, b, c);
+    VSR_LAUNCH_CHECK();
+    return true;
 }
 
 }  // namespace vsr

@@ -18,6 +18,22 @@ struct FoldGeom {
 
 FoldGeom make_geom(const Dims& hr, const int rates[3]);
 
+// Separable blur spectrum Lambda(f) = a[f1] * b[f2] * c[f3] (a Gaussian PSF
+// is separable, so its DFT is the product of three 1-D DFTs).  When set, the
+// fused fold kernels rebuild Lambda from these O(m+n+s) tables instead of
+// streaming the 16N-byte HR spectrum.  a == nullptr: not separable.
+struct SepTables {
+    const double2* a = nullptr;
+    const double2* b = nullptr;
+    const double2* c = nullptr;
+};
+
+// Detects separability of an HR spectrum on the device (relative deviation
+// <= tol) and, if so, fills a/b/c (device arrays of m, n, s) so that
+// lam ~= a[f1] b[f2] c[f3].  Synchronizes the stream.
+bool detect_separable(const Dims& hr, const double2* lam, double2* a, double2* b, double2* c, double tol,
+                      cudaStream_t st);
+
 // Per-axis |e^{2 pi i f/len} - 1|^2 tables on the device for make_gamma
 // (reference src/operators.cpp:225-243, src/solvers.cpp:191-205).
 struct GammaTables {

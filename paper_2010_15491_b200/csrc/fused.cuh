@@ -20,7 +20,8 @@ bool fused_axis3_ok(const FoldGeom& G);
 // out = IFFT_axis3(x̂) (unscaled) with x̂ from TikhonovOperator::solve's fold
 // (solvers.cpp:53-62).  out must not alias lam / xbh.
 void launch_tik_fold_ifft3(const FoldGeom& G, const double2* Yl, const double2* lam,
-                           const double2* xbh, double2* out, double reg, cudaStream_t st);
+                           const double2* xbh, double2* out, double reg, cudaStream_t st,
+                           const SepTables& sep = SepTables{});
 
 // In place on W (spectrum after forward axes 1,2): forward axis-3 FFT scaled
 // by fwd_scale, TV x-update fold (solvers.cpp:219-233 with k̂ = data_hat +
@@ -29,17 +30,17 @@ void launch_tik_fold_ifft3(const FoldGeom& G, const double2* Yl, const double2* 
 size_t tv_sandwich_blocks(const FoldGeom& G);
 void launch_tv_sandwich(const FoldGeom& G, const double2* Yl, const double2* lam, double2* W,
                         const GammaTables& tabs, double mu, double fwd_scale, double* fit_partials,
-                        cudaStream_t st);
+                        cudaStream_t st, const SepTables& sep = SepTables{});
 
 // Same folds fused with the contiguous axis-1 pass instead (tile = the
 // dc*ds alias rows of T consecutive g2, full rows along axis 1):
 //   Tikhonov: out = IFFT_axis1(x̂); TV: W -> FFT_axis1 -> fold -> IFFT_axis1 -> W.
 bool fused_axis1_ok(const FoldGeom& G);
 void launch_tik_fold_ifft1(const FoldGeom& G, const double2* Yl, const double2* lam, const double2* xbh,
-                           double2* out, double reg, cudaStream_t st);
+                           double2* out, double reg, cudaStream_t st, const SepTables& sep = SepTables{});
 size_t tv_sandwich1_blocks(const FoldGeom& G);
 void launch_tv_sandwich1(const FoldGeom& G, const double2* Yl, const double2* lam, double2* W,
                          const GammaTables& tabs, double mu, double fwd_scale, double* fit_partials,
-                         cudaStream_t st);
+                         cudaStream_t st, const SepTables& sep = SepTables{});
 
 }  // namespace vsr

@@ -665,6 +665,8 @@ _sig("vsr_slab_fit_d", [_vp, _szp, _szp, C.c_int, _vp, _vp, _vp, _vp])
 
 # ---------------------------------------------------------------- instrumentation
 _sig("vsr_launch_count", [C.POINTER(C.c_uint64)])
+_sig("vsr_tikhonov_separable", [_vp])
+_sig("vsr_tv_separable", [_vp])
 _sig("vsr_profile_enable", [_vp, C.c_int])
 _sig("vsr_profile_read", [_vp, C.c_int, C.c_char_p, C.c_size_t, _dp, C.POINTER(C.c_uint64),
                           C.POINTER(C.c_int)])
@@ -766,6 +768,9 @@ class TikhonovDevice:
     def check(self):
         check(_lib.vsr_tikhonov_check(self.handle))
 
+    def separable(self) -> bool:
+        return bool(_lib.vsr_tikhonov_separable(self.handle))
+
     def close(self):
         if self.handle:
             _lib.vsr_tikhonov_destroy(self.handle)
@@ -798,6 +803,9 @@ class TvDevice:
         it = int(rep.iterations)
         return SolveReport(it, float(rep.initial_objective), obj[:it].tolist(), res[:it].tolist(),
                            float(rep.seconds))
+
+    def separable(self) -> bool:
+        return bool(_lib.vsr_tv_separable(self.handle))
 
     def x_ptr(self) -> int:
         p = _vp()
