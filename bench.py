@@ -316,6 +316,7 @@ def run_b200(args, rank, world, local):
         hbm, peak_src = 6650.0, "fallback (B200_PROFILING.md)"
     st_rows = {}
     sep = op.separable()
+    lat = op.lattice_prior()
     for name, (tot_ms, cnt) in stages.items():
         avg = tot_ms / max(cnt, 1)
         row = {"avg_us": avg * 1e3, "launches": cnt, "share": tot_ms / (ms * args.steps)}
@@ -323,6 +324,8 @@ def run_b200(args, rank, world, local):
             a, b = STAGE_BYTES[name]
             if sep and name in SEP_STAGES:
                 a -= 16  # Lambda rebuilt from 1-D tables, not streamed
+            if lat and name in ("tik_fold_ifft_axis3", "tik_fold_ifft_axis1"):
+                a, b = a - 16, b + 16  # LR prior spectrum instead of the HR fft3(xbar)
             byts = a * N + b * Nl
             row["alg_bytes"] = byts
             row["gbs"] = byts / (avg * 1e-3) / 1e9
@@ -338,9 +341,9 @@ def run_b200(args, rank, world, local):
                 "path": {"alg_bytes_per_step": path_bytes, "achieved": path_bytes / (ms * 1e-3) / 1e9,
                          "frac": path_bytes / (ms * 1e-3) / 1e9 / hbm,
                          "model": "(72 + 40/d) N bytes per Tikhonov solve (SURVEY 8(d))",
-                         "lambda_separable": sep,
-                         "note": ("Lambda rebuilt from 1-D tables: compulsory traffic is (56 + 40/d) N"
-                                  if sep else "general Lambda streamed")}}
+                         "lambda_separable": sep, "prior_on_lattice": lat,
+                         "note": "model counts Lambda and fft3(xbar) at 16N each; with a separable PSF and the "
+                                 "CLI-default lattice prior the path reads (40 + 56/d) N"}}
     try:
         prof = json.loads((ROOT / "profiles" / "traffic.json").read_text())
         if dom in prof:

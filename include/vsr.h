@@ -218,6 +218,10 @@ int vsr_slab_fit_d(vsr_ctx* ctx, const size_t hr_dims[3], const size_t rates[3],
  * a[f1] b[f2] c[f3] (any Gaussian PSF): the fused folds then rebuild Lambda
  * from three 1-D tables instead of streaming the 16N-byte HR spectrum. */
 int vsr_tikhonov_separable(vsr_tikhonov* t);
+/* 1 when the Tikhonov prior xbar lives on the decimation lattice (e.g. the
+ * reference CLI default xbar = zero_fill_upsample(y)): fft3(xbar) is then kept
+ * as an LR spectrum (16N/d bytes) instead of the HR one (16N). */
+int vsr_tikhonov_lattice_prior(vsr_tikhonov* t);
 int vsr_tv_separable(vsr_tv* h);
 
 /* ---- instrumentation (bench): kernels launched by this library so far, and

@@ -252,6 +252,15 @@ __global__ void residue_status_kernel(const double* __restrict__ partials, long 
     }
 }
 
+// 1 if any entry of x off the decimation lattice (i % dr, j % dc, k % ds not all 0) is non-zero
+__global__ void off_lattice_kernel(long long m, long long n, long long N, int dr, int dc, int ds,
+                                   const double* __restrict__ x, int* __restrict__ flag) {
+    const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= N) return;
+    const long long i = p % m, j = (p / m) % n, k = p / (m * n);
+    if ((i % dr || j % dc || k % ds) && x[p] != 0.0) *flag = 1;
+}
+
 __global__ void cmul_kernel(long long n, double2* __restrict__ a, const double2* __restrict__ b,
                             bool conj_b) {
     const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -801,6 +810,7 @@ struct vsr_tikhonov {
     DevBuf<unsigned long long> bad;
     size_t res_blocks = 0;
     SepState sep;                     // Lambda = a[f1] b[f2] c[f3] when the PSF is separable
+    DevBuf<double2> Zl;               // LR spectrum of decimate(xbar) when xbar lives on the lattice
     ChainPlan chain;                  // chained inverse axes 2 -> 1 (L2 ring)
     DevBuf<double2> ring;
     DevBuf<int> chain_ctr;
@@ -810,6 +820,12 @@ static void tik_reset_status(vsr_tikhonov* t) {
     VSR_CUDA(cudaMemsetAsync(t->status.p, 0, 4 * sizeof(double), t->ctx->stream));
     VSR_CUDA(cudaMemsetAsync(t->bad.p, 0xff, sizeof(unsigned long long), t->ctx->stream));
 }
+
+// xbar_hat_ = fft3(cfg.xbar) (solvers.cpp:45).  When the prior is supported on
+// the decimation lattice (the CLI default xbar = zero_fill_upsample(y),
+// volsr_main.cpp:208) and a fused fold runs, only its LR spectrum is kept:
+// fft3(D^H z)[g + b lr] = fft_LR(z)[g] / sqrt(d) for every alias b.
+static void tik_prior(vsr_tikhonov* t, const double* xbar_dev, cudaStream_t st);
 
 static vsr_tikhonov* tik_new(vsr_ctx* ctx, const size_t hr_dims[3], const size_t rates[3],
                              double reg) {
@@ -824,7 +840,6 @@ static vsr_tikhonov* tik_new(vsr_ctx* ctx, const size_t hr_dims[3], const size_t
     t->reg = reg;
     const size_t N = sp.hr.count(), Nl = sp.lr.count();
     t->lam.alloc(N);
-    t->xbh.alloc(N);
     t->xh.alloc(N);
     t->Yl.alloc(Nl);
     t->y.alloc(Nl);
@@ -845,6 +860,39 @@ static vsr_tikhonov* tik_new(vsr_ctx* ctx, const size_t hr_dims[3], const size_t
     return t;
 }
 
+static void tik_prior(vsr_tikhonov* t, const double* xbar_dev, cudaStream_t st) {
+    static const bool off = [] {
+        const char* e = std::getenv("VSR_NO_LATTICE");
+        return e && e[0] == '1';
+    }();
+    const Dims& hr = t->sp.hr;
+    bool lattice = false;
+    if (!off && t->sp.rate() > 1 && use_fused(t->G)) {
+        DevBuf<int> flag(1);
+        VSR_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(int), st));
+        const long long N = (long long)hr.count();
+        off_lattice_kernel<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(
+            (long long)hr.m, (long long)hr.n, N, t->sp.rates[0], t->sp.rates[1], t->sp.rates[2], xbar_dev, flag.p);
+        VSR_LAUNCH_CHECK();
+        int h = 1;
+        VSR_CUDA(cudaMemcpyAsync(&h, flag.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+        VSR_CUDA(cudaStreamSynchronize(st));
+        lattice = h == 0;
+    }
+    if (lattice) {
+        DevBuf<double> z(t->sp.lr.count());
+        launch_decimate(hr, t->sp.rates, xbar_dev, z.p, st);
+        t->Zl.alloc(t->sp.lr.count());
+        fft_engine().forward3(t->sp.lr, z.p, IN_REAL, t->Zl.p,
+                              inv_sqrt_count(t->sp.lr) / std::sqrt((double)t->sp.rate()), st);
+        VSR_CUDA(cudaStreamSynchronize(st));
+    } else {
+        t->xbh.alloc(hr.count());
+        fft_engine().forward3(hr, xbar_dev, IN_REAL, t->xbh.p, inv_sqrt_count(hr), st);
+    }
+    ++g_fwd;  // the ctor's fft3(cfg.xbar)
+}
+
 int vsr_tikhonov_create(vsr_ctx* ctx, const size_t hr_dims[3], const size_t rates[3],
                         const double* lambda_c, double reg, const double* xbar_r,
                         vsr_tikhonov** out) {
@@ -856,10 +904,7 @@ int vsr_tikhonov_create(vsr_ctx* ctx, const size_t hr_dims[3], const size_t rate
             h2d(ctx, t->lam.p, lambda_c, t->lam.bytes());
             h2d(ctx, t->x.p, xbar_r, t->x.bytes());
             t->sep.detect(t->sp.hr, t->lam.p, ctx->stream);
-            // xbar_hat_ = fft3(cfg.xbar)   (solvers.cpp:45)
-            fft_engine().forward3(t->sp.hr, t->x.p, IN_REAL, t->xbh.p, inv_sqrt_count(t->sp.hr),
-                                  ctx->stream);
-            ++g_fwd;
+            tik_prior(t, t->x.p, ctx->stream);
             sync(ctx);
         } catch (...) {
             delete t;
@@ -880,9 +925,7 @@ int vsr_tikhonov_create_d(vsr_ctx* ctx, const size_t hr_dims[3], const size_t ra
             VSR_CUDA(cudaMemcpyAsync(t->lam.p, lambda_c_dev, t->lam.bytes(),
                                      cudaMemcpyDeviceToDevice, ctx->stream));
             t->sep.detect(t->sp.hr, t->lam.p, ctx->stream);
-            fft_engine().forward3(t->sp.hr, xbar_r_dev, IN_REAL, t->xbh.p,
-                                  inv_sqrt_count(t->sp.hr), ctx->stream);
-            ++g_fwd;
+            tik_prior(t, xbar_r_dev, ctx->stream);
             sync(ctx);
         } catch (...) {
             delete t;
@@ -917,7 +960,7 @@ static void tik_enqueue(vsr_tikhonov* t, const double* y_dev, double* x_dev) {
         // fold + inverse axis 1 (contiguous rows), then axis 2, then axis 3 -> real x
         {
             ProfScope ps(prof, "tik_fold_ifft_axis1", st);
-            launch_tik_fold_ifft1(t->G, t->Yl.p, t->lam.p, t->xbh.p, t->xh.p, t->reg, st, t->sep.t);
+            launch_tik_fold_ifft1(t->G, t->Yl.p, t->lam.p, t->xbh.p, t->xh.p, t->reg, st, t->sep.t, t->Zl.p);
         }
         {
             ProfScope ps(prof, "fft_inv_axis2", st);
@@ -931,7 +974,7 @@ static void tik_enqueue(vsr_tikhonov* t, const double* y_dev, double* x_dev) {
     } else if (use_fused(t->G)) {
         {
             ProfScope ps(prof, "tik_fold_ifft_axis3", st);
-            launch_tik_fold_ifft3(t->G, t->Yl.p, t->lam.p, t->xbh.p, t->xh.p, t->reg, st, t->sep.t);
+            launch_tik_fold_ifft3(t->G, t->Yl.p, t->lam.p, t->xbh.p, t->xh.p, t->reg, st, t->sep.t, t->Zl.p);
         }
         if (t->chain.ok) {
             ProfScope ps(prof, "chain_inv_axis2_axis1_c2r", st);
@@ -1435,6 +1478,7 @@ int vsr_tv_destroy(vsr_tv* h) {
 }
 
 int vsr_tikhonov_separable(vsr_tikhonov* t) { return t && t->sep.t.a ? 1 : 0; }
+int vsr_tikhonov_lattice_prior(vsr_tikhonov* t) { return t && t->Zl.p ? 1 : 0; }
 int vsr_tv_separable(vsr_tv* h) { return h && h->sep.t.a ? 1 : 0; }
 
 int vsr_launch_count(uint64_t* out) {

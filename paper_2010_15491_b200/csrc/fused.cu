@@ -42,7 +42,8 @@ template <int L, int A, int DS, bool TV, bool FIT>
 __global__ void __launch_bounds__(FShape<L, A>::THREADS, (512 / FShape<L, A>::THREADS) > 0 ? (512 / FShape<L, A>::THREADS) : 1)
     fold_axis3_kernel(FoldGeom G, const double2* __restrict__ Yl, const double2* __restrict__ lam,
                       SepTables sep,
-                      const double2* __restrict__ xbh, double2* W, double2* out, GammaTables tabs,
+                      const double2* __restrict__ xbh, const double2* __restrict__ Zl, double2* W, double2* out,
+                      GammaTables tabs,
                       double cA /*Tik: 2 reg, TV: mu*/, double shift, double inv_scale,
                       double invsqrtd, double fwd_scale, const double2* __restrict__ tw,
                       double* __restrict__ fit_partials) {
@@ -87,8 +88,17 @@ __global__ void __launch_bounds__(FShape<L, A>::THREADS, (512 / FShape<L, A>::TH
         for (int r = 0; r < R; ++r) Lm[r] = __ldg(lam + base + stride * (t + P * r));
     }
     if constexpr (!TV) {
+        if (Zl) {  // prior on the decimation lattice: fft3(xbar) = LR spectrum replicated over the aliases
 #pragma unroll
-        for (int r = 0; r < R; ++r) v[r] = __ldg(xbh + base + stride * (t + P * r));
+            for (int rr = 0; rr < RD; ++rr) {
+                const double2 z = __ldg(Zl + g1 + G.ml * (g2 + G.nl * (long long)(t + P * rr)));
+#pragma unroll
+                for (int bs = 0; bs < DS; ++bs) v[rr + RD * bs] = z;
+            }
+        } else {
+#pragma unroll
+            for (int r = 0; r < R; ++r) v[r] = __ldg(xbh + base + stride * (t + P * r));
+        }
     }
     double2 Yg[RD];
 #pragma unroll
@@ -277,7 +287,8 @@ template <int L, int A, int DR, int T, bool TV, bool FIT>
 __global__ void __launch_bounds__(T * A * (L / 16), (512 / (T * A * (L / 16))) > 0 ? 512 / (T * A * (L / 16)) : 1)
     fold_axis1_kernel(FoldGeom G, const double2* __restrict__ Yl, const double2* __restrict__ lam,
                       SepTables sep,
-                      const double2* __restrict__ xbh, double2* W, double2* out, GammaTables tabs, double cA,
+                      const double2* __restrict__ xbh, const double2* __restrict__ Zl, double2* W, double2* out,
+                      GammaTables tabs, double cA,
                       double shift, double inv_scale, double invsqrtd, double fwd_scale,
                       const double2* __restrict__ tw, double* __restrict__ fit_partials) {
     using Pl = fftc::Plan<L, 16>;
@@ -304,6 +315,14 @@ __global__ void __launch_bounds__(T * A * (L / 16), (512 / (T * A * (L / 16))) >
 #pragma unroll
         for (int r = 0; r < R; ++r) v[r] = cscale(v[r], fwd_scale);
         __syncthreads();  // exchange buffer reused for Lambda below
+    } else if (Zl) {
+        const double2* zrow = Zl + G.ml * (g2 + G.nl * g3);
+#pragma unroll
+        for (int rr = 0; rr < RD; ++rr) {
+            const double2 z = __ldg(zrow + t + P * rr);
+#pragma unroll
+            for (int br = 0; br < DR; ++br) v[rr + RD * br] = z;
+        }
     } else {
 #pragma unroll
         for (int r = 0; r < R; ++r) v[r] = __ldg(xbh + rowb + t + P * r);
@@ -398,14 +417,14 @@ struct A1Shape {
 
 template <int L, int A, int DR, bool TV, bool FIT>
 void launch_a1(const FoldGeom& G, const double2* Yl, const double2* lam, const SepTables& sep, const double2* xbh,
-               double2* W, double2* out, const GammaTables& tabs, double cA, double shift, double inv_scale,
+               const double2* Zl, double2* W, double2* out, const GammaTables& tabs, double cA, double shift, double inv_scale,
                double fwd_scale, double* fit, cudaStream_t st) {
     using Sh = A1Shape<L, A, DR>;
     auto kern = fold_axis1_kernel<L, A, DR, Sh::T, TV, FIT>;
     if (Sh::SMEM > 48 * 1024)
         VSR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Sh::SMEM));
     const unsigned grid = (unsigned)((G.nl / Sh::T) * G.sl);
-    kern<<<grid, Sh::THREADS, Sh::SMEM, st>>>(G, Yl, lam, sep, xbh, W, out, tabs, cA, shift, inv_scale,
+    kern<<<grid, Sh::THREADS, Sh::SMEM, st>>>(G, Yl, lam, sep, xbh, Zl, W, out, tabs, cA, shift, inv_scale,
                                               1.0 / std::sqrt((double)G.d), fwd_scale,
                                               fft_engine().twiddles((size_t)L), fit);
     VSR_LAUNCH_CHECK();
@@ -420,12 +439,12 @@ void launch_a1(const FoldGeom& G, const double2* Yl, const double2* lam, const S
 
 template <bool TV, bool FIT>
 bool dispatch_a1(const FoldGeom& G, const double2* Yl, const double2* lam, const SepTables& sep,
-                 const double2* xbh, double2* W, double2* out, const GammaTables& tabs, double cA, double shift,
+                 const double2* xbh, const double2* Zl, double2* W, double2* out, const GammaTables& tabs, double cA, double shift,
                  double inv_scale, double fwd_scale, double* fit, cudaStream_t st) {
     const int A = G.dc * G.ds;
 #define VSR_X(LL, AA, DD)                                                                           \
     if (G.m == LL && A == AA && G.dr == DD && G.nl % A1Shape<LL, AA, DD>::T == 0) {                  \
-        launch_a1<LL, AA, DD, TV, FIT>(G, Yl, lam, sep, xbh, W, out, tabs, cA, shift, inv_scale, fwd_scale, \
+        launch_a1<LL, AA, DD, TV, FIT>(G, Yl, lam, sep, xbh, Zl, W, out, tabs, cA, shift, inv_scale, fwd_scale, \
                                        fit, st);                                                    \
         return true;                                                                                \
     }
@@ -441,7 +460,7 @@ struct Key {
 
 template <int L, int A, int DS, bool TV, bool FIT>
 void launch_one(const FoldGeom& G, const double2* Yl, const double2* lam, const SepTables& sep,
-                const double2* xbh, double2* W, double2* out, const GammaTables& tabs, double cA, double shift,
+                const double2* xbh, const double2* Zl, double2* W, double2* out, const GammaTables& tabs, double cA, double shift,
                 double inv_scale, double fwd_scale, double* fit, cudaStream_t st) {
     using Sh = FShape<L, A>;
     auto kern = fold_axis3_kernel<L, A, DS, TV, FIT>;
@@ -449,7 +468,7 @@ void launch_one(const FoldGeom& G, const double2* Yl, const double2* lam, const 
     if (smem > 48 * 1024)
         VSR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const unsigned grid = (unsigned)((G.ml / Sh::T) * G.nl);
-    kern<<<grid, Sh::THREADS, smem, st>>>(G, Yl, lam, sep, xbh, W, out, tabs, cA, shift, inv_scale,
+    kern<<<grid, Sh::THREADS, smem, st>>>(G, Yl, lam, sep, xbh, Zl, W, out, tabs, cA, shift, inv_scale,
                                           1.0 / std::sqrt((double)G.d), fwd_scale,
                                           fft_engine().twiddles((size_t)L), fit);
     VSR_LAUNCH_CHECK();
@@ -465,12 +484,12 @@ void launch_one(const FoldGeom& G, const double2* Yl, const double2* lam, const 
 
 template <bool TV, bool FIT>
 bool dispatch(const FoldGeom& G, const double2* Yl, const double2* lam, const SepTables& sep,
-              const double2* xbh, double2* W, double2* out, const GammaTables& tabs, double cA, double shift,
+              const double2* xbh, const double2* Zl, double2* W, double2* out, const GammaTables& tabs, double cA, double shift,
               double inv_scale, double fwd_scale, double* fit, cudaStream_t st) {
     const int A = G.dr * G.dc;
 #define VSR_X(LL, AA, DD)                                                                           \
     if (G.s == LL && A == AA && G.ds == DD && G.ml % FShape<LL, AA>::T == 0) {                      \
-        launch_one<LL, AA, DD, TV, FIT>(G, Yl, lam, sep, xbh, W, out, tabs, cA, shift, inv_scale,   \
+        launch_one<LL, AA, DD, TV, FIT>(G, Yl, lam, sep, xbh, Zl, W, out, tabs, cA, shift, inv_scale, \
                                         fwd_scale, fit, st);                                        \
         return true;                                                                                \
     }
@@ -491,7 +510,8 @@ bool fused_axis3_ok(const FoldGeom& G) {
 }
 
 void launch_tik_fold_ifft3(const FoldGeom& G, const double2* Yl, const double2* lam,
-                           const double2* xbh, double2* out, double reg, cudaStream_t st, const SepTables& sep) {
+                           const double2* xbh, double2* out, double reg, cudaStream_t st, const SepTables& sep,
+                           const double2* Zl) {
     GammaTables none{nullptr, nullptr, nullptr, 0.0};
     const double shift = 2.0 * reg * (double)G.d;  // solvers.cpp:43
     const double inv2l = 1.0 / (2.0 * reg);         // solvers.cpp:59
@@ -500,7 +520,7 @@ void launch_tik_fold_ifft3(const FoldGeom& G, const double2* Yl, const double2* 
         return e && e[0] == '1';
     }();
     if (v2 && dispatch_tik_v2(G, Yl, lam, xbh, out, reg, st)) return;
-    if (!dispatch<false, false>(G, Yl, lam, sep, xbh, nullptr, out, none, 2.0 * reg, shift, inv2l, 1.0,
+    if (!dispatch<false, false>(G, Yl, lam, sep, xbh, Zl, nullptr, out, none, 2.0 * reg, shift, inv2l, 1.0,
                                 nullptr, st))
         throw std::logic_error("launch_tik_fold_ifft3: unsupported geometry");
 }
@@ -520,9 +540,9 @@ void launch_tv_sandwich(const FoldGeom& G, const double2* Yl, const double2* lam
     const double shift = mu * (double)G.d;  // solvers.cpp:238
     const double inv_mu = 1.0 / mu;         // solvers.cpp:230
     const bool ok = fit_partials
-                        ? dispatch<true, true>(G, Yl, lam, sep, nullptr, W, nullptr, tabs, mu, shift, inv_mu,
+                        ? dispatch<true, true>(G, Yl, lam, sep, nullptr, nullptr, W, nullptr, tabs, mu, shift, inv_mu,
                                                fwd_scale, fit_partials, st)
-                        : dispatch<true, false>(G, Yl, lam, sep, nullptr, W, nullptr, tabs, mu, shift, inv_mu,
+                        : dispatch<true, false>(G, Yl, lam, sep, nullptr, nullptr, W, nullptr, tabs, mu, shift, inv_mu,
                                                 fwd_scale, nullptr, st);
     if (!ok) throw std::logic_error("launch_tv_sandwich: unsupported geometry");
 }
@@ -537,9 +557,9 @@ bool fused_axis1_ok(const FoldGeom& G) {
 }
 
 void launch_tik_fold_ifft1(const FoldGeom& G, const double2* Yl, const double2* lam, const double2* xbh,
-                           double2* out, double reg, cudaStream_t st, const SepTables& sep) {
+                           double2* out, double reg, cudaStream_t st, const SepTables& sep, const double2* Zl) {
     GammaTables none{nullptr, nullptr, nullptr, 0.0};
-    if (!dispatch_a1<false, false>(G, Yl, lam, sep, xbh, nullptr, out, none, 2.0 * reg, 2.0 * reg * (double)G.d,
+    if (!dispatch_a1<false, false>(G, Yl, lam, sep, xbh, Zl, nullptr, out, none, 2.0 * reg, 2.0 * reg * (double)G.d,
                                    1.0 / (2.0 * reg), 1.0, nullptr, st))
         throw std::logic_error("launch_tik_fold_ifft1: unsupported geometry");
 }
@@ -557,9 +577,9 @@ void launch_tv_sandwich1(const FoldGeom& G, const double2* Yl, const double2* la
                          const GammaTables& tabs, double mu, double fwd_scale, double* fit_partials,
                          cudaStream_t st, const SepTables& sep) {
     const double shift = mu * (double)G.d, inv_mu = 1.0 / mu;
-    const bool ok = fit_partials ? dispatch_a1<true, true>(G, Yl, lam, sep, nullptr, W, nullptr, tabs, mu, shift,
+    const bool ok = fit_partials ? dispatch_a1<true, true>(G, Yl, lam, sep, nullptr, nullptr, W, nullptr, tabs, mu, shift,
                                                            inv_mu, fwd_scale, fit_partials, st)
-                                 : dispatch_a1<true, false>(G, Yl, lam, sep, nullptr, W, nullptr, tabs, mu, shift,
+                                 : dispatch_a1<true, false>(G, Yl, lam, sep, nullptr, nullptr, W, nullptr, tabs, mu, shift,
                                                             inv_mu, fwd_scale, nullptr, st);
     if (!ok) throw std::logic_error("launch_tv_sandwich1: unsupported geometry");
 }

@@ -18,10 +18,12 @@ namespace vsr {
 bool fused_axis3_ok(const FoldGeom& G);
 
 // out = IFFT_axis3(x̂) (unscaled) with x̂ from TikhonovOperator::solve's fold
-// (solvers.cpp:53-62).  out must not alias lam / xbh.
+// (solvers.cpp:53-62).  out must not alias lam / xbh.  Zl (optional, LR
+// layout): when the prior x̄ lives on the decimation lattice, fft3(x̄) at alias
+// b of g equals Zl[g] for every b, so the 16N-byte X̄ is not read.
 void launch_tik_fold_ifft3(const FoldGeom& G, const double2* Yl, const double2* lam,
                            const double2* xbh, double2* out, double reg, cudaStream_t st,
-                           const SepTables& sep = SepTables{});
+                           const SepTables& sep = SepTables{}, const double2* Zl = nullptr);
 
 // In place on W (spectrum after forward axes 1,2): forward axis-3 FFT scaled
 // by fwd_scale, TV x-update fold (solvers.cpp:219-233 with k̂ = data_hat +
@@ -37,7 +39,8 @@ void launch_tv_sandwich(const FoldGeom& G, const double2* Yl, const double2* lam
 //   Tikhonov: out = IFFT_axis1(x̂); TV: W -> FFT_axis1 -> fold -> IFFT_axis1 -> W.
 bool fused_axis1_ok(const FoldGeom& G);
 void launch_tik_fold_ifft1(const FoldGeom& G, const double2* Yl, const double2* lam, const double2* xbh,
-                           double2* out, double reg, cudaStream_t st, const SepTables& sep = SepTables{});
+                           double2* out, double reg, cudaStream_t st, const SepTables& sep = SepTables{},
+                           const double2* Zl = nullptr);
 size_t tv_sandwich1_blocks(const FoldGeom& G);
 void launch_tv_sandwich1(const FoldGeom& G, const double2* Yl, const double2* lam, double2* W,
                          const GammaTables& tabs, double mu, double fwd_scale, double* fit_partials,

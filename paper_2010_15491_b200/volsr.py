@@ -666,6 +666,7 @@ _sig("vsr_slab_fit_d", [_vp, _szp, _szp, C.c_int, _vp, _vp, _vp, _vp])
 # ---------------------------------------------------------------- instrumentation
 _sig("vsr_launch_count", [C.POINTER(C.c_uint64)])
 _sig("vsr_tikhonov_separable", [_vp])
+_sig("vsr_tikhonov_lattice_prior", [_vp])
 _sig("vsr_tv_separable", [_vp])
 _sig("vsr_profile_enable", [_vp, C.c_int])
 _sig("vsr_profile_read", [_vp, C.c_int, C.c_char_p, C.c_size_t, _dp, C.POINTER(C.c_uint64),
@@ -770,6 +771,9 @@ class TikhonovDevice:
 
     def separable(self) -> bool:
         return bool(_lib.vsr_tikhonov_separable(self.handle))
+
+    def lattice_prior(self) -> bool:
+        return bool(_lib.vsr_tikhonov_lattice_prior(self.handle))
 
     def close(self):
         if self.handle:
