@@ -222,6 +222,11 @@ int vsr_tikhonov_separable(vsr_tikhonov* t);
  * reference CLI default xbar = zero_fill_upsample(y)): fft3(xbar) is then kept
  * as an LR spectrum (16N/d bytes) instead of the HR one (16N). */
 int vsr_tikhonov_lattice_prior(vsr_tikhonov* t);
+/* 1 when the solve runs as the spatial expansion: separable Lambda with a
+ * compact real 1-D PSF factor per axis and a lattice prior.  The alias fold
+ * then factors per axis and x = xbar + sqrt(d) H^T D^H F_l^-1(U) is formed in
+ * one HBM pass (two LR transforms, no HR transform).  VSR_NO_SPATIAL=1 off. */
+int vsr_tikhonov_spatial(vsr_tikhonov* t);
 int vsr_tv_separable(vsr_tv* h);
 
 /* ---- instrumentation (bench): kernels launched by this library so far, and

@@ -18,6 +18,7 @@
 #include "fft.cuh"
 #include "fold.cuh"
 #include "fused.cuh"
+#include "spatial.cuh"
 #include "chain.cuh"
 #include "tv.cuh"
 
@@ -811,6 +812,11 @@ struct vsr_tikhonov {
     size_t res_blocks = 0;
     SepState sep;                     // Lambda = a[f1] b[f2] c[f3] when the PSF is separable
     DevBuf<double2> Zl;               // LR spectrum of decimate(xbar) when xbar lives on the lattice
+    DevBuf<double> zlat;              // decimate(xbar) (lattice prior)
+    SpatialPlan spl;                  // spatial expansion (separable compact PSF + lattice prior)
+    DevBuf<double> sp_taps, sp_s2, u;
+    DevBuf<double2> sp_s1, U;
+    DevBuf<unsigned long long> lrbad;
     ChainPlan chain;                  // chained inverse axes 2 -> 1 (L2 ring)
     DevBuf<double2> ring;
     DevBuf<int> chain_ctr;
@@ -826,6 +832,7 @@ static void tik_reset_status(vsr_tikhonov* t) {
 // volsr_main.cpp:208) and a fused fold runs, only its LR spectrum is kept:
 // fft3(D^H z)[g + b lr] = fft_LR(z)[g] / sqrt(d) for every alias b.
 static void tik_prior(vsr_tikhonov* t, const double* xbar_dev, cudaStream_t st);
+static void tik_spatial(vsr_tikhonov* t, cudaStream_t st);
 
 static vsr_tikhonov* tik_new(vsr_ctx* ctx, const size_t hr_dims[3], const size_t rates[3],
                              double reg) {
@@ -867,7 +874,7 @@ static void tik_prior(vsr_tikhonov* t, const double* xbar_dev, cudaStream_t st) 
     }();
     const Dims& hr = t->sp.hr;
     bool lattice = false;
-    if (!off && t->sp.rate() > 1 && use_fused(t->G)) {
+    if (!off && t->sp.rate() > 1) {
         DevBuf<int> flag(1);
         VSR_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(int), st));
         const long long N = (long long)hr.count();
@@ -880,17 +887,78 @@ static void tik_prior(vsr_tikhonov* t, const double* xbar_dev, cudaStream_t st) 
         lattice = h == 0;
     }
     if (lattice) {
-        DevBuf<double> z(t->sp.lr.count());
+        DevBuf<double>& z = t->zlat;
+        z.alloc(t->sp.lr.count());
         launch_decimate(hr, t->sp.rates, xbar_dev, z.p, st);
         t->Zl.alloc(t->sp.lr.count());
         fft_engine().forward3(t->sp.lr, z.p, IN_REAL, t->Zl.p,
                               inv_sqrt_count(t->sp.lr) / std::sqrt((double)t->sp.rate()), st);
         VSR_CUDA(cudaStreamSynchronize(st));
-    } else {
+        tik_spatial(t, st);
+        if (!t->spl.ok && !use_fused(t->G)) {  // the unfused fold reads the HR fft3(xbar)
+            t->Zl.release();
+            t->zlat.release();
+            lattice = false;
+        }
+    }
+    if (!lattice) {
         t->xbh.alloc(hr.count());
         fft_engine().forward3(hr, xbar_dev, IN_REAL, t->xbh.p, inv_sqrt_count(hr), st);
     }
     ++g_fwd;  // the ctor's fft3(cfg.xbar)
+}
+
+// Spatial expansion (spatial.cuh) when Lambda is separable with a compact
+// real 1-D factor per axis and xbar lives on the decimation lattice.
+// VSR_NO_SPATIAL=1 keeps the FFT path.
+static void tik_spatial(vsr_tikhonov* t, cudaStream_t st) {
+    const char* env = std::getenv("VSR_NO_SPATIAL");  // read per operator (bench compares both paths)
+    const bool off = env && env[0] == '1';
+    if (off || !t->sep.t.a || !t->Zl.p || t->sp.rate() < 2) return;
+    const Dims& hr = t->sp.hr;
+    std::vector<double2> tabs(hr.m + hr.n + hr.s);
+    VSR_CUDA(cudaMemcpyAsync(tabs.data(), t->sep.tab.p, tabs.size() * sizeof(double2), cudaMemcpyDeviceToHost, st));
+    VSR_CUDA(cudaStreamSynchronize(st));
+    std::vector<double> taps, s2;
+    std::vector<double2> s1;
+    SpatialPlan p;
+    if (!spatial_plan_host(hr, t->sp.rates, tabs, taps, p.h, s1, s2)) return;
+    for (int a = 0; a < 3; ++a) {
+        const int r = t->sp.rates[a], h = p.h[a];
+        p.dmin[a] = -(h / r);
+        p.ndelta[a] = (r - 1 + h) / r - p.dmin[a] + 1;
+    }
+    p.dm = spatial_tile(p, t->sp.rates);
+    if (!p.dm) return;
+    std::vector<double> kp;
+    spatial_phase_taps(t->sp.rates, p.h, p.dmin, taps, p.dm, kp);
+    taps.swap(kp);
+    t->sp_taps.alloc(taps.size());
+    t->sp_s1.alloc(s1.size());
+    t->sp_s2.alloc(s2.size());
+    VSR_CUDA(cudaMemcpyAsync(t->sp_taps.p, taps.data(), taps.size() * sizeof(double), cudaMemcpyHostToDevice, st));
+    VSR_CUDA(cudaMemcpyAsync(t->sp_s1.p, s1.data(), s1.size() * sizeof(double2), cudaMemcpyHostToDevice, st));
+    VSR_CUDA(cudaMemcpyAsync(t->sp_s2.p, s2.data(), s2.size() * sizeof(double), cudaMemcpyHostToDevice, st));
+    const size_t L[3] = {t->sp.lr.m, t->sp.lr.n, t->sp.lr.s};
+    size_t so = 0;
+    p.kp = t->sp_taps.p;
+    for (int a = 0; a < 3; ++a) {
+        p.s1[a] = t->sp_s1.p + so;
+        p.s2[a] = t->sp_s2.p + so;
+        so += L[a];
+    }
+    p.ok = true;
+    t->U.alloc(t->sp.lr.count());
+    t->u.alloc(t->sp.lr.count());
+    t->lrbad.alloc(1);
+    t->xh.release();  // the HR spectrum is never formed on this path
+    const size_t nres = fft_engine().inverse_final_blocks(t->sp.lr);
+    if (nres > t->res_blocks) {
+        t->res_blocks = nres;
+        t->partials.alloc(2 * nres);
+    }
+    VSR_CUDA(cudaStreamSynchronize(st));
+    t->spl = p;
 }
 
 int vsr_tikhonov_create(vsr_ctx* ctx, const size_t hr_dims[3], const size_t rates[3],
@@ -956,7 +1024,23 @@ static void tik_enqueue(vsr_tikhonov* t, const double* y_dev, double* x_dev) {
     }
     ++g_fwd;  // the one forward transform of solve() (solvers.cpp:52)
     PassReduce red{t->partials.p, t->bad.p};
-    if (fuse_axis(t->G, 3) == 1) {
+    if (t->spl.ok) {
+        // U on the LR grid -> u = sqrt(d) F_l^-1(U) -> x = D^H z + H^T D^H u
+        {
+            ProfScope ps(prof, "spatial_u", st);
+            launch_spatial_v(t->sp.lr, t->sp.rate(), t->spl, t->Yl.p, t->Zl.p, t->reg, t->U.p, st);
+        }
+        PassReduce lred{t->partials.p, t->lrbad.p};
+        {
+            ProfScope ps(prof, "lr_ifft3", st);
+            fft_engine().inverse3(t->sp.lr, t->U.p, t->u.p, OUT_REAL,
+                                  inv_sqrt_count(t->sp.lr) * std::sqrt((double)t->sp.rate()), &lred, st);
+        }
+        {
+            ProfScope ps(prof, "spatial_expand", st);
+            launch_spatial_expand(t->sp.hr, t->sp.rates, t->spl, t->u.p, t->zlat.p, 1.0, x_dev, t->bad.p, st);
+        }
+    } else if (fuse_axis(t->G, 3) == 1) {
         // fold + inverse axis 1 (contiguous rows), then axis 2, then axis 3 -> real x
         {
             ProfScope ps(prof, "tik_fold_ifft_axis1", st);
@@ -995,7 +1079,8 @@ static void tik_enqueue(vsr_tikhonov* t, const double* y_dev, double* x_dev) {
     ++g_inv;  // the one inverse transform (solvers.cpp:64)
     {
         ProfScope ps(prof, "residue_status", st);
-        const size_t nres = fuse_axis(t->G, 3) == 1 ? fft_engine().pass_blocks(t->sp.hr, 2)
+        const size_t nres = t->spl.ok ? fft_engine().inverse_final_blocks(t->sp.lr)
+                            : fuse_axis(t->G, 3) == 1 ? fft_engine().pass_blocks(t->sp.hr, 2)
                             : (use_fused(t->G) && t->chain.ok) ? t->chain.b_total()
                                                                : fft_engine().inverse_final_blocks(t->sp.hr);
         residue_status_kernel<<<1, 1024, 0, st>>>(t->partials.p, (long long)nres, 1e-8, t->status.p);
@@ -1479,6 +1564,7 @@ int vsr_tv_destroy(vsr_tv* h) {
 
 int vsr_tikhonov_separable(vsr_tikhonov* t) { return t && t->sep.t.a ? 1 : 0; }
 int vsr_tikhonov_lattice_prior(vsr_tikhonov* t) { return t && t->Zl.p ? 1 : 0; }
+int vsr_tikhonov_spatial(vsr_tikhonov* t) { return t && t->spl.ok ? 1 : 0; }
 int vsr_tv_separable(vsr_tv* h) { return h && h->sep.t.a ? 1 : 0; }
 
 int vsr_launch_count(uint64_t* out) {

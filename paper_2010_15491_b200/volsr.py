@@ -508,6 +508,13 @@ class TikhonovOperator:
         check(_lib.vsr_tikhonov_solve(self.handle, _p(a), _p(out)))
         return out
 
+    def path(self) -> dict:
+        """Which specialisations the device solve uses (vsr_tikhonov_separable /
+        _lattice_prior / _spatial)."""
+        return {"separable": bool(_lib.vsr_tikhonov_separable(self.handle)),
+                "lattice_prior": bool(_lib.vsr_tikhonov_lattice_prior(self.handle)),
+                "spatial": bool(_lib.vsr_tikhonov_spatial(self.handle))}
+
     def close(self):
         if getattr(self, "handle", None):
             _lib.vsr_tikhonov_destroy(self.handle)
@@ -667,6 +674,7 @@ _sig("vsr_slab_fit_d", [_vp, _szp, _szp, C.c_int, _vp, _vp, _vp, _vp])
 _sig("vsr_launch_count", [C.POINTER(C.c_uint64)])
 _sig("vsr_tikhonov_separable", [_vp])
 _sig("vsr_tikhonov_lattice_prior", [_vp])
+_sig("vsr_tikhonov_spatial", [_vp])
 _sig("vsr_tv_separable", [_vp])
 _sig("vsr_profile_enable", [_vp, C.c_int])
 _sig("vsr_profile_read", [_vp, C.c_int, C.c_char_p, C.c_size_t, _dp, C.POINTER(C.c_uint64),
@@ -774,6 +782,9 @@ class TikhonovDevice:
 
     def lattice_prior(self) -> bool:
         return bool(_lib.vsr_tikhonov_lattice_prior(self.handle))
+
+    def spatial(self) -> bool:
+        return bool(_lib.vsr_tikhonov_spatial(self.handle))
 
     def close(self):
         if self.handle:

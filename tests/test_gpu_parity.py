@@ -149,6 +149,70 @@ def test_tikhonov_vs_oracle(V, O, dims, rates):
     assert rel_err(got, want) < TOL
 
 
+# Gaussian (separable, compact) PSF + lattice prior xbar = zero_fill_upsample(y):
+# the spatial-expansion solve (vsr_tikhonov_spatial).  Tiles wider than the
+# volume, non-multiple-of-32 rows, rate 1 axes and anisotropic supports.
+SPATIAL_CASES = [((64, 64, 64), (2, 2, 2), (9, 9, 9), (1.0, 1.0, 1.0)),
+                 ((32, 48, 64), (2, 2, 4), (5, 7, 9), (1.0, 1.2, 2.0)),
+                 ((64, 64, 64), (4, 4, 4), (13, 13, 13), (1.5, 1.5, 1.5)),
+                 ((20, 12, 6), (5, 3, 2), (5, 5, 3), (1.0, 0.8, 0.7)),
+                 ((8, 8, 8), (2, 2, 2), (3, 3, 3), (1.0, 1.0, 1.0)),
+                 ((40, 24, 16), (2, 2, 2), (7, 5, 5), (1.3, 1.1, 0.9)),
+                 ((6, 4, 4), (3, 2, 1), (3, 3, 3), (1.0, 1.0, 1.0)),
+                 ((128, 32, 64), (2, 1, 2), (15, 15, 9), (1.2, 1.2, 2.0)),
+                 ((96, 16, 8), (3, 2, 2), (9, 7, 7), (1.4, 1.0, 1.0))]
+
+
+@pytest.mark.parametrize("dims,rates,ksz,sigma", SPATIAL_CASES)
+def test_tikhonov_spatial_vs_oracle(V, O, dims, rates, ksz, sigma):
+    rng = np.random.default_rng(11)
+    spec, ospec = V.DecimationSpec(dims, rates), O.DecimationSpec(dims, rates)
+    lam = O.psf_to_spectrum(O.make_gaussian_psf(ksz, sigma, dims))
+    y = random_volume(spec.lr, rng)
+    xbar = O.zero_fill_upsample(y, ospec)
+    for reg in (1e-3, 0.3):
+        op = V.TikhonovOperator(lam, spec, V.TikhonovConfig(reg, xbar))
+        assert op.path()["spatial"]
+        got = op.solve(y)
+        want = O.tikhonov_fast(y, lam, ospec, reg, xbar)
+        assert rel_err(got, want) < TOL, (reg, rel_err(got, want))
+
+
+def test_tikhonov_spatial_only_when_structured(V, O):
+    rng = np.random.default_rng(12)
+    dims, rates = (16, 16, 16), (2, 2, 2)
+    spec, ospec = V.DecimationSpec(dims, rates), O.DecimationSpec(dims, rates)
+    y = random_volume(spec.lr, rng)
+    gauss = O.psf_to_spectrum(O.make_gaussian_psf((5, 5, 5), (1.0, 1.0, 1.0), dims))
+    dense = O.psf_to_spectrum(random_psf(dims, 3, rng))
+    lat, full = O.zero_fill_upsample(y, ospec), random_volume(dims, rng)
+    cases = {(0, 0): (gauss, lat, True), (0, 1): (gauss, full, False), (1, 0): (dense, lat, False)}
+    for (i, j), (lam, xbar, spatial) in cases.items():
+        op = V.TikhonovOperator(lam, spec, V.TikhonovConfig(0.05, xbar))
+        assert op.path()["spatial"] == spatial, (i, j)
+        assert rel_err(op.solve(y), O.tikhonov_fast(y, lam, ospec, 0.05, xbar)) < TOL
+
+
+def test_tikhonov_spatial_budget_and_determinism(V, O):
+    """test_solvers.cpp:141-157 and test_cli.cpp:237-268 on the spatial path."""
+    rng = np.random.default_rng(13)
+    dims = (64, 64, 64)
+    spec, ospec = V.DecimationSpec(dims, (2, 2, 2)), O.DecimationSpec(dims, (2, 2, 2))
+    y = random_volume(spec.lr, rng)
+    lam = O.psf_to_spectrum(O.make_gaussian_psf((9, 9, 9), (1.0, 1.0, 1.0), dims))
+    op = V.TikhonovOperator(lam, spec, V.TikhonovConfig(1e-3, O.zero_fill_upsample(y, ospec)))
+    assert op.path()["spatial"]
+    V.reset_fft_counters()
+    a = op.solve(y)
+    assert V.fft_counters() == {"forward": 1, "inverse": 1}
+    assert a.tobytes() == op.solve(y).tobytes()
+    y2 = y.copy()
+    y2[1, 2, 3] = np.inf
+    with pytest.raises(V.NumericError, match="non-finite"):
+        op.solve(y2)
+    assert a.tobytes() == op.solve(y).tobytes()
+
+
 def test_tikhonov_identity_formula(V):
     """test_solvers.cpp:55-69."""
     rng = np.random.default_rng(1)
