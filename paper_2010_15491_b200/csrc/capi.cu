@@ -948,7 +948,8 @@ static void tik_spatial(vsr_tikhonov* t, cudaStream_t st) {
         so += L[a];
     }
     p.ok = true;
-    t->U.alloc(t->sp.lr.count());
+    if (!spatial_sandwich_ok(t->sp.lr))
+        t->U.alloc(t->sp.lr.count());  // unfused LR stage: U kernel + inverse3
     t->u.alloc(t->sp.lr.count());
     t->lrbad.alloc(1);
     t->xh.release();  // the HR spectrum is never formed on this path
@@ -1018,7 +1019,10 @@ int vsr_tikhonov_destroy(vsr_tikhonov* t) {
 static void tik_enqueue(vsr_tikhonov* t, const double* y_dev, double* x_dev) {
     cudaStream_t st = t->ctx->stream;
     Profiler* prof = t->ctx->prof();
-    {
+    if (t->spl.ok && t->U.p == nullptr) {
+        ProfScope ps(prof, "lr_fft12", st);
+        fft_engine().forward12(t->sp.lr, y_dev, IN_REAL, t->Yl.p, st);
+    } else {
         ProfScope ps(prof, "lr_fft3", st);
         fft_engine().forward3(t->sp.lr, y_dev, IN_REAL, t->Yl.p, inv_sqrt_count(t->sp.lr), st);
     }
@@ -1026,15 +1030,30 @@ static void tik_enqueue(vsr_tikhonov* t, const double* y_dev, double* x_dev) {
     PassReduce red{t->partials.p, t->bad.p};
     if (t->spl.ok) {
         // U on the LR grid -> u = sqrt(d) F_l^-1(U) -> x = D^H z + H^T D^H u
-        {
-            ProfScope ps(prof, "spatial_u", st);
-            launch_spatial_v(t->sp.lr, t->sp.rate(), t->spl, t->Yl.p, t->Zl.p, t->reg, t->U.p, st);
-        }
         PassReduce lred{t->partials.p, t->lrbad.p};
-        {
+        const double usc = inv_sqrt_count(t->sp.lr) * std::sqrt((double)t->sp.rate());
+        if (t->U.p == nullptr) {
+            // fused: lr_fft3 ran the forward axis-1/2 passes only (unscaled)
+            {
+                ProfScope ps(prof, "lr_sandwich_axis3", st);
+                launch_spatial_sandwich(t->sp.lr, t->sp.rate(), t->spl, t->Yl.p, t->Zl.p, t->reg,
+                                        inv_sqrt_count(t->sp.lr), usc, st);
+            }
+            {
+                ProfScope ps(prof, "lr_ifft_axis2", st);
+                fft_engine().axis_pass(t->sp.lr, 1, true, t->Yl.p, IN_COMPLEX, t->Yl.p, OUT_COMPLEX, 1.0, nullptr, st);
+            }
+            {
+                ProfScope ps(prof, "lr_ifft_axis1_c2r", st);
+                fft_engine().axis_pass(t->sp.lr, 0, true, t->Yl.p, IN_COMPLEX, t->u.p, OUT_REAL, 1.0, &lred, st);
+            }
+        } else {
+            {
+                ProfScope ps(prof, "spatial_u", st);
+                launch_spatial_v(t->sp.lr, t->sp.rate(), t->spl, t->Yl.p, t->Zl.p, t->reg, t->U.p, st);
+            }
             ProfScope ps(prof, "lr_ifft3", st);
-            fft_engine().inverse3(t->sp.lr, t->U.p, t->u.p, OUT_REAL,
-                                  inv_sqrt_count(t->sp.lr) * std::sqrt((double)t->sp.rate()), &lred, st);
+            fft_engine().inverse3(t->sp.lr, t->U.p, t->u.p, OUT_REAL, usc, &lred, st);
         }
         {
             ProfScope ps(prof, "spatial_expand", st);
@@ -1079,7 +1098,7 @@ static void tik_enqueue(vsr_tikhonov* t, const double* y_dev, double* x_dev) {
     ++g_inv;  // the one inverse transform (solvers.cpp:64)
     {
         ProfScope ps(prof, "residue_status", st);
-        const size_t nres = t->spl.ok ? fft_engine().inverse_final_blocks(t->sp.lr)
+        const size_t nres = t->spl.ok ? fft_engine().pass_blocks(t->sp.lr, 0)
                             : fuse_axis(t->G, 3) == 1 ? fft_engine().pass_blocks(t->sp.hr, 2)
                             : (use_fused(t->G) && t->chain.ok) ? t->chain.b_total()
                                                                : fft_engine().inverse_final_blocks(t->sp.hr);

@@ -6,6 +6,8 @@
 #include <complex>
 #include <vector>
 
+#include "fft.cuh"
+#include "fft_core.cuh"
 #include "spatial.cuh"
 
 namespace vsr {
@@ -41,6 +43,106 @@ void launch_spatial_v(const Dims& lr, int d, const SpatialPlan& p, const double2
     VSR_LAUNCH_CHECK();
 }
 
+// --------------------------------------------------- LR axis-3 sandwich
+// In place on Y (LR spectrum after the forward axis-1/2 passes, unscaled):
+// forward axis-3 FFT, scale fs, U(g) as in spatial_u_kernel, inverse axis-3
+// FFT scaled by out_scale.  A CTA owns TG tiles of T consecutive inner
+// positions p = g1 + ml g2, each line held by P threads x R registers.
+template <int L>
+struct SwShape {
+    using Pl = fftc::Plan<L>;
+    static constexpr int R = Pl::R, P = Pl::P, T = 8;
+    static constexpr int TG = (T * P) >= 128 ? 1 : 128 / (T * P);
+    static constexpr int THREADS = TG * T * P;
+    static constexpr int SMEM = Pl::NEEDS_SMEM ? TG * T * L : 0;  // double2 elements
+};
+
+template <int L>
+__global__ void __launch_bounds__(SwShape<L>::THREADS, 512 / SwShape<L>::THREADS)
+    lr_sandwich_kernel(double2* Y, const double2* __restrict__ Zl, long long S, int ml, int nl,
+                       const double2* __restrict__ a1, const double2* __restrict__ b1,
+                       const double2* __restrict__ c1, const double* __restrict__ a2,
+                       const double* __restrict__ b2, const double* __restrict__ c2, double cy,
+                       double shift, double out_scale, const double2* __restrict__ tw) {
+    using Sh = SwShape<L>;
+    using Pl = typename Sh::Pl;
+    constexpr int R = Sh::R, P = Sh::P, T = Sh::T;
+    extern __shared__ double2 smw[];
+    const int tid = threadIdx.x;
+    const int g = tid / (T * P), rem = tid % (T * P), lt = rem % T, t = rem / T;
+    const int ls = g * T + lt;
+    const long long tile = (long long)blockIdx.x * Sh::TG + g;
+    const bool active = tile * T < S;
+    const long long p = active ? tile * T + lt : 0;
+    auto sidx = [&](int q) { return (ls / T) * (L * T) + q * T + (ls % T); };
+
+    double2 v[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[r] = active ? Y[p + S * (t + P * r)] : make_double2(0.0, 0.0);
+    if (Zl && active) {  // pull the prior's spectrum toward L2 while the forward transform runs
+#pragma unroll
+        for (int r = 0; r < R; ++r) asm volatile("prefetch.global.L2 [%0];" ::"l"(Zl + p + S * (t + P * r)));
+    }
+    fftc::stockham<L, false>(v, t, smw, sidx, tw);
+    fftc::to_natural<L>(v);
+    // v[r] = F_l(y) at g3 = t + P r (times 1/fs)
+    const int g1 = (int)(p % ml), g2 = (int)(p / ml);
+    const double2 ab1 = cmul(__ldg(a1 + g1), __ldg(b1 + g2));
+    const double ab2 = __ldg(a2 + g1) * __ldg(b2 + g2);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int g3 = t + P * r;
+        const double2 y = cscale(v[r], cy);
+        const double2 num = Zl ? csub(y, cmul(__ldg(Zl + p + S * g3), cmul(ab1, __ldg(c1 + g3)))) : y;
+        v[r] = cscale(num, 1.0 / (ab2 * __ldg(c2 + g3) + shift));
+    }
+    __syncthreads();  // the exchange buffer is reused by the inverse transform
+    fftc::stockham<L, true>(v, t, smw, sidx, tw);
+    if (active) {
+#pragma unroll
+        for (int j = 0; j < R; ++j) Y[p + S * Pl::out_q(t, j)] = cscale(v[j], out_scale);
+    }
+}
+
+template <int L>
+static void launch_sandwich_L(const Dims& lr, const SpatialPlan& p, double2* Y, const double2* Zl, double cy,
+                              double shift, double out_scale, cudaStream_t st) {
+    using Sh = SwShape<L>;
+    const long long S = (long long)(lr.m * lr.n);
+    const long long tiles = S / Sh::T;
+    const unsigned blocks = (unsigned)((tiles + Sh::TG - 1) / Sh::TG);
+    const size_t smem = (size_t)Sh::SMEM * sizeof(double2);
+    auto kern = lr_sandwich_kernel<L>;
+    if (smem > 48 * 1024)
+        VSR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<blocks, Sh::THREADS, smem, st>>>(Y, Zl, S, (int)lr.m, (int)lr.n, p.s1[0], p.s1[1], p.s1[2], p.s2[0],
+                                            p.s2[1], p.s2[2], cy, shift, out_scale,
+                                            fft_engine().twiddles(L));
+    VSR_LAUNCH_CHECK();
+}
+
+bool spatial_sandwich_ok(const Dims& lr) {
+    const size_t L = lr.s;
+    return L >= 8 && L <= 1024 && is_pow2(L) && (lr.m * lr.n) % 8 == 0 && lr.m * lr.n * L < (1ull << 31);
+}
+
+void launch_spatial_sandwich(const Dims& lr, int d, const SpatialPlan& p, double2* Y, const double2* Zl,
+                             double reg, double fwd_scale, double out_scale, cudaStream_t st) {
+    const double cy = fwd_scale * (double)d / std::sqrt((double)d);
+    const double shift = 2.0 * reg * d;
+    switch (lr.s) {
+        case 8: launch_sandwich_L<8>(lr, p, Y, Zl, cy, shift, out_scale, st); break;
+        case 16: launch_sandwich_L<16>(lr, p, Y, Zl, cy, shift, out_scale, st); break;
+        case 32: launch_sandwich_L<32>(lr, p, Y, Zl, cy, shift, out_scale, st); break;
+        case 64: launch_sandwich_L<64>(lr, p, Y, Zl, cy, shift, out_scale, st); break;
+        case 128: launch_sandwich_L<128>(lr, p, Y, Zl, cy, shift, out_scale, st); break;
+        case 256: launch_sandwich_L<256>(lr, p, Y, Zl, cy, shift, out_scale, st); break;
+        case 512: launch_sandwich_L<512>(lr, p, Y, Zl, cy, shift, out_scale, st); break;
+        case 1024: launch_sandwich_L<1024>(lr, p, Y, Zl, cy, shift, out_scale, st); break;
+        default: throw std::logic_error("spatial_sandwich: unsupported axis-3 length");
+    }
+}
+
 // ------------------------------------------------------------ expand kernel
 // Polyphase form: a tile is CX x CY x CZ LR cells (origin on the lattice), i.e.
 // r1 CX x r2 CY x r3 CZ outputs.  Output n = r (c0 + c) + phi reads LR cells
@@ -51,7 +153,7 @@ void launch_spatial_v(const Dims& lr, int d, const SpatialPlan& p, const double2
 //   stage B (axis 2): T2[tz][ty][qx], one (tz, qx) column per thread
 //   stage C (axis 1): x rows; a thread owns XB consecutive LR columns of a row
 //                     and all r1 phases (R1 > 0: compile-time, vector stores)
-constexpr int SP_THREADS = 256;
+constexpr int SP_THREADS = 128;
 constexpr int SP_CX = 16, SP_CY = 4, SP_CZ = 4, SP_XB = 2;
 constexpr int SP_MAX_ROWS = 1024;  // TZ * TY bound (rates r2 * r3 <= 64)
 
@@ -76,7 +178,7 @@ __device__ __forceinline__ int wrap_idx(int j, int L) {
 }
 
 template <int DM, int R1>
-__global__ void __launch_bounds__(SP_THREADS, (DM <= 8 ? 4 : 3)) spatial_expand_kernel(ExpandArgs A) {
+__global__ void __launch_bounds__(SP_THREADS, (DM <= 8 ? 8 : 6)) spatial_expand_kernel(ExpandArgs A) {
     extern __shared__ double sm[];
     constexpr int LX = SP_CX + DM - 1, LY = SP_CY + DM - 1, LZ = SP_CZ + DM - 1;
     const int r1 = R1 > 0 ? R1 : A.ax[0].r, r2 = A.ax[1].r, r3 = A.ax[2].r;
@@ -87,10 +189,12 @@ __global__ void __launch_bounds__(SP_THREADS, (DM <= 8 ? 4 : 3)) spatial_expand_
     double* kp3 = kp2 + r2 * DM;
     double* t1 = sm + nkp;                 // TZ * LY * LX
     double* t2 = t1 + TZ * LY * LX;        // TZ * TY * LX
+    // stage-C row tables: tz | ty << 8, and the LR index of the row's prior
+    // samples (-1 off the lattice)
+    int* rowinfo = reinterpret_cast<int*>(t2 + TZ * TY * LX);
+    int* zrow = rowinfo + TZ * TY;
     __shared__ long long zoff[LZ];
     __shared__ int yoff[LY], xoff[LX];
-    // stage-C row table: tz | ty << 8 | lattice << 16 (rows <= 256 * 256)
-    __shared__ int rowinfo[SP_MAX_ROWS];
 
     const int tid = threadIdx.x;
     const int cx0 = blockIdx.x * SP_CX, cy0 = blockIdx.y * SP_CY, cz0 = blockIdx.z * SP_CZ;
@@ -102,7 +206,9 @@ __global__ void __launch_bounds__(SP_THREADS, (DM <= 8 ? 4 : 3)) spatial_expand_
     else if (tid >= 64 && tid < 64 + LX) xoff[tid - 64] = wrap_idx(cx0 + A.ax[0].dmin + tid - 64, A.ml);
     for (int row = tid; row < rows; row += SP_THREADS) {
         const int tz = row / TY, ty = row - tz * TY;
-        rowinfo[row] = tz | (ty << 8) | (((ty % r2) == 0 && (tz % r3) == 0) ? 1 << 16 : 0);
+        const bool lat = A.z != nullptr && (ty % r2) == 0 && (tz % r3) == 0;
+        rowinfo[row] = tz | (ty << 8);
+        zrow[row] = lat ? ((cz0 + tz / r3) * A.nl + cy0 + ty / r2) * A.ml + cx0 : -1;
     }
     __syncthreads();
     // stage A: axis 3
@@ -149,19 +255,22 @@ __global__ void __launch_bounds__(SP_THREADS, (DM <= 8 ? 4 : 3)) spatial_expand_
     // stage C: axis 1 + lattice prior
     constexpr int NXB = SP_CX / SP_XB;
     const int X0 = cx0 * r1, Y0 = cy0 * r2, Z0 = cz0 * r3;
-    const size_t zplane = (size_t)A.nl * A.ml;
     const int xb = tid % NXB, c0 = xb * SP_XB, n1 = X0 + r1 * c0;
+    constexpr bool HOIST = R1 > 0 && R1 * DM <= 16;  // all phases' taps in registers
+    double kh[HOIST ? R1 * DM : 1];
+    if constexpr (HOIST) {
+#pragma unroll
+        for (int i = 0; i < R1 * DM; ++i) kh[i] = kp1[i];
+    }
     for (int row = tid / NXB; row < rows; row += SP_THREADS / NXB) {
-        const int info = rowinfo[row];
-        const int tz = info & 0xff, ty = (info >> 8) & 0xff;
+        const int info = rowinfo[row], zr = zrow[row];
+        const int tz = info & 0xff, ty = info >> 8;
         const int n2 = Y0 + ty, n3 = Z0 + tz;
         if (n2 >= A.n || n3 >= A.s || n1 >= A.m) continue;
-        const bool lat = A.z != nullptr && (info >> 16);
+        const bool lat = zr >= 0;
         double zv[SP_XB];
-        const double* zp = lat ? A.z + (size_t)(cz0 + tz / r3) * zplane + (size_t)(cy0 + ty / r2) * A.ml + cx0 + c0
-                               : nullptr;
 #pragma unroll
-        for (int j = 0; j < SP_XB; ++j) zv[j] = lat ? __ldg(zp + j) : 0.0;
+        for (int j = 0; j < SP_XB; ++j) zv[j] = lat ? __ldg(A.z + zr + c0 + j) : 0.0;
         double in[DM + SP_XB - 1];
         const double* src = t2 + row * LX + c0;
 #pragma unroll
@@ -174,7 +283,7 @@ __global__ void __launch_bounds__(SP_THREADS, (DM <= 8 ? 4 : 3)) spatial_expand_
             for (int ph = 0; ph < R1; ++ph) {
                 double k[DM];
 #pragma unroll
-                for (int d = 0; d < DM; ++d) k[d] = kp1[ph * DM + d];
+                for (int d = 0; d < DM; ++d) k[d] = HOIST ? kh[(HOIST ? ph * DM + d : 0)] : kp1[ph * DM + d];
 #pragma unroll
                 for (int j = 0; j < SP_XB; ++j) {
                     double acc = 0.0;
@@ -233,7 +342,7 @@ static size_t expand_smem(const int rates[3], int dm) {
     const size_t LX = SP_CX + dm - 1, LY = SP_CY + dm - 1;
     const size_t TY = (size_t)rates[1] * SP_CY, TZ = (size_t)rates[2] * SP_CZ;
     const size_t kp = (size_t)(rates[0] + rates[1] + rates[2]) * dm;
-    return (kp + TZ * LY * LX + TZ * TY * LX) * sizeof(double);
+    return (kp + TZ * LY * LX + TZ * TY * LX) * sizeof(double) + 2 * TZ * TY * sizeof(int);
 }
 
 int spatial_tile(const SpatialPlan& p, const int rates[3]) {
@@ -278,6 +387,8 @@ void launch_spatial_expand(const Dims& hr, const int rates[3], const SpatialPlan
         throw std::logic_error("spatial_expand: tile grid out of range");
     A.kp = p.kp;
     A.u = u, A.z = z, A.x = x, A.bad = bad;
+    if ((size_t)A.ml * A.nl * A.sl >= (1ull << 31) || hr.count() >= (1ull << 40))
+        throw std::logic_error("spatial_expand: LR volume exceeds 32-bit indexing");
     const size_t smem = expand_smem(rates, dm);
     const dim3 blocks((unsigned)A.tiles1, (unsigned)A.tiles2, (unsigned)tiles3);
     switch (dm) {

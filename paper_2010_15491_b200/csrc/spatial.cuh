@@ -53,6 +53,13 @@ void spatial_phase_taps(const int rates[3], const int h[3], const int dmin[3], c
 void launch_spatial_v(const Dims& lr, int d, const SpatialPlan& p, const double2* Yl, const double2* Zl,
                       double reg, double2* V, cudaStream_t st);
 
+// Fused LR stage, in place on Y holding the forward axis-1/2 passes of y
+// (unscaled): forward axis-3 FFT (x fwd_scale), U, inverse axis-3 FFT
+// (x out_scale).  The axis-2/1 inverse passes then give u.
+bool spatial_sandwich_ok(const Dims& lr);
+void launch_spatial_sandwich(const Dims& lr, int d, const SpatialPlan& p, double2* Y, const double2* Zl,
+                             double reg, double fwd_scale, double out_scale, cudaStream_t st);
+
 // x = D^H z + c0 * H^T D^H v   (hr grid, rates); non-finite index -> bad (atomicMin)
 void launch_spatial_expand(const Dims& hr, const int rates[3], const SpatialPlan& p, const double* v,
                            const double* z, double c0, double* x, unsigned long long* bad, cudaStream_t st);
