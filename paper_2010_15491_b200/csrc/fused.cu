@@ -283,18 +283,18 @@ bool dispatch_tik_v2(const FoldGeom& G, const double2* Yl, const double2* lam, c
 //   TV = true : W -> forward axis-1 FFT (scaled) -> TV fold (:219-233) -> inverse
 //               axis-1 FFT -> W (in place), + LR-Parseval data-fit partials
 // Lambda waits in the thread's own slots of the exchange buffer during the fold.
-template <int L, int A, int DR, int T, bool TV, bool FIT>
-__global__ void __launch_bounds__(T * A * (L / 16), (512 / (T * A * (L / 16))) > 0 ? 512 / (T * A * (L / 16)) : 1)
+template <int L, int A, int DR, int T, bool TV, bool FIT, int RM>
+__global__ void __launch_bounds__(T * A * (L / RM), ((RM == 8 ? 1024 : 512) / (T * A * (L / RM))) > 0 ? (RM == 8 ? 1024 : 512) / (T * A * (L / RM)) : 1)
     fold_axis1_kernel(FoldGeom G, const double2* __restrict__ Yl, const double2* __restrict__ lam,
                       SepTables sep,
                       const double2* __restrict__ xbh, const double2* __restrict__ Zl, double2* W, double2* out,
                       GammaTables tabs, double cA,
                       double shift, double inv_scale, double invsqrtd, double fwd_scale,
                       const double2* __restrict__ tw, double* __restrict__ fit_partials) {
-    using Pl = fftc::Plan<L, 16>;
+    using Pl = fftc::Plan<L, RM>;
     constexpr int R = Pl::R, P = Pl::P, NLN = T * A;
     constexpr int RD = R / DR;  // r = rr + RD * br: alias br of g1 = t + P rr
-    static_assert(R % DR == 0, "dr must divide 16");
+    static_assert(R % DR == 0, "dr must divide the radix");
     extern __shared__ double2 sm[];
     const int tid = threadIdx.x;
     const int ln = tid % NLN, t = tid / NLN;
@@ -307,11 +307,17 @@ __global__ void __launch_bounds__(T * A * (L / 16), (512 / (T * A * (L / 16))) >
     // line-interleaved: a quarter-warp (8 lines at one position) is one 128-B row
     auto sidx = [&](int q) { return q * NLN + ln; };
     double2 v[R];
+    // LR spectrum of y for this row: issued first so its latency overlaps the
+    // forward transform
+    const double2* Yrow = Yl + G.ml * (g2 + G.nl * g3);
+    double2 yr[RD];
+#pragma unroll
+    for (int rr = 0; rr < RD; ++rr) yr[rr] = __ldg(Yrow + t + P * rr);
     if constexpr (TV) {
 #pragma unroll
         for (int r = 0; r < R; ++r) v[r] = W[rowb + t + P * r];
-        fftc::stockham<L, false, decltype(sidx), 16>(v, t, sm, sidx, tw);
-        fftc::to_natural<L, 16>(v);
+        fftc::stockham<L, false, decltype(sidx), RM>(v, t, sm, sidx, tw);
+        fftc::to_natural<L, RM>(v);
 #pragma unroll
         for (int r = 0; r < R; ++r) v[r] = cscale(v[r], fwd_scale);
         __syncthreads();  // exchange buffer reused for Lambda below
@@ -338,11 +344,10 @@ __global__ void __launch_bounds__(T * A * (L / 16), (512 / (T * A * (L / 16))) >
     }
     double base_g = 0.0;
     if constexpr (TV) base_g = __ldg(tabs.nc + f2) + __ldg(tabs.ns + f3);
-    const double2* Yrow = Yl + G.ml * (g2 + G.nl * g3);
     double fit = 0.0;
 #pragma unroll
     for (int rr = 0; rr < RD; ++rr) {
-        const double2 yraw = __ldg(Yrow + t + P * rr);
+        const double2 yraw = yr[rr];
         const double2 yv = cscale(yraw, invsqrtd);
         double Gg[DR];
         double Sx = 0.0, Sy = 0.0, gram = 0.0;
@@ -394,7 +399,7 @@ __global__ void __launch_bounds__(T * A * (L / 16), (512 / (T * A * (L / 16))) >
         }
     }
     __syncthreads();
-    fftc::stockham<L, true, decltype(sidx), 16>(v, t, sm, sidx, tw);
+    fftc::stockham<L, true, decltype(sidx), RM>(v, t, sm, sidx, tw);
     double2* dst = TV ? W : out;
 #pragma unroll
     for (int j = 0; j < R; ++j) dst[rowb + Pl::out_q(t, j)] = v[j];
@@ -406,21 +411,22 @@ __global__ void __launch_bounds__(T * A * (L / 16), (512 / (T * A * (L / 16))) >
     }
 }
 
-template <int L, int A, int DR>
+template <int L, int A, int DR, int RM = 16>
 struct A1Shape {
+    static constexpr int PP = L / (L < RM ? L : RM);              // threads per line
     static constexpr int T0 = 32 / A > 0 ? 32 / A : 1;          // NLN <= 32 (alias lanes in a warp)
-    static constexpr int TT = (T0 * A * (L / 16)) > 256 ? (256 / (A * (L / 16)) > 0 ? 256 / (A * (L / 16)) : 1) : T0;
+    static constexpr int TT = (T0 * A * PP) > 256 ? (256 / (A * PP) > 0 ? 256 / (A * PP) : 1) : T0;
     static constexpr int T = TT > 2 ? 2 : TT;                    // 2 consecutive g2 per tile
-    static constexpr int THREADS = T * A * (L / 16);
+    static constexpr int THREADS = T * A * PP;
     static constexpr size_t SMEM = (size_t)T * A * L * sizeof(double2);
 };
 
-template <int L, int A, int DR, bool TV, bool FIT>
+template <int L, int A, int DR, bool TV, bool FIT, int RM = 16>
 void launch_a1(const FoldGeom& G, const double2* Yl, const double2* lam, const SepTables& sep, const double2* xbh,
                const double2* Zl, double2* W, double2* out, const GammaTables& tabs, double cA, double shift, double inv_scale,
                double fwd_scale, double* fit, cudaStream_t st) {
-    using Sh = A1Shape<L, A, DR>;
-    auto kern = fold_axis1_kernel<L, A, DR, Sh::T, TV, FIT>;
+    using Sh = A1Shape<L, A, DR, RM>;
+    auto kern = fold_axis1_kernel<L, A, DR, Sh::T, TV, FIT, RM>;
     if (Sh::SMEM > 48 * 1024)
         VSR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Sh::SMEM));
     const unsigned grid = (unsigned)((G.nl / Sh::T) * G.sl);
@@ -442,10 +448,18 @@ bool dispatch_a1(const FoldGeom& G, const double2* Yl, const double2* lam, const
                  const double2* xbh, const double2* Zl, double2* W, double2* out, const GammaTables& tabs, double cA, double shift,
                  double inv_scale, double fwd_scale, double* fit, cudaStream_t st) {
     const int A = G.dc * G.ds;
+    static const int rm = [] {
+        const char* e = std::getenv("VSR_A1_RM");
+        return e ? std::atoi(e) : 16;
+    }();
 #define VSR_X(LL, AA, DD)                                                                           \
     if (G.m == LL && A == AA && G.dr == DD && G.nl % A1Shape<LL, AA, DD>::T == 0) {                  \
-        launch_a1<LL, AA, DD, TV, FIT>(G, Yl, lam, sep, xbh, Zl, W, out, tabs, cA, shift, inv_scale, fwd_scale, \
-                                       fit, st);                                                    \
+        if (rm == 8 && DD <= 8 && A1Shape<LL, AA, DD, 8>::T == A1Shape<LL, AA, DD>::T)               \
+            launch_a1<LL, AA, DD, TV, FIT, 8>(G, Yl, lam, sep, xbh, Zl, W, out, tabs, cA, shift, inv_scale, \
+                                              fwd_scale, fit, st);                                  \
+        else                                                                                        \
+            launch_a1<LL, AA, DD, TV, FIT>(G, Yl, lam, sep, xbh, Zl, W, out, tabs, cA, shift, inv_scale, \
+                                           fwd_scale, fit, st);                                     \
         return true;                                                                                \
     }
     VSR_A1_TABLE(VSR_X)
