@@ -1295,6 +1295,7 @@ struct vsr_tv {
     DevBuf<double2> ring;
     DevBuf<int> chain_ctr;
     SepState sep;
+    DevBuf<double> gw;  // LR table sum_b Gamma_b |Lambda_b|^2 (axis-1 sandwich)
     size_t iters_done = 0;
     bool dual_in_a = true;
     bool stopped = false;
@@ -1373,6 +1374,11 @@ static vsr_tv* tv_build(vsr_ctx* ctx, const Spec& sp, const double* y_dev, const
         fft_engine().forward3(sp.lr, y_dev, IN_REAL, h->Yl.p, inv_sqrt_count(sp.lr), st);
         g_fwd += 2;
         h->sep.detect(hr, h->lam.p, st);
+        if (fuse_axis(h->G, 1) == 1) {
+            h->gw.alloc(Nl);
+            GammaTables tabs{h->tnr.p, h->tnc.p, h->tns.p, h->tau};
+            launch_tv_gram(h->G, h->lam.p, h->sep.t, tabs, h->gw.p, st);
+        }
         // init (solvers.cpp:346-354)
         if (cfg->init == VSR_INIT_ZERO) {
             VSR_CUDA(cudaMemsetAsync(h->x.p, 0, h->x.bytes(), st));
@@ -1407,7 +1413,7 @@ static void tv_step(vsr_tv* h) {
     const double s = inv_sqrt_count(hr);
     // theta_hat = fft3(theta); k_hat = data_hat + mu theta_hat (:374-375), folded x-update (:376)
     Profiler* prof = h->ctx->prof();
-    GammaTables tabs{h->tnr.p, h->tnc.p, h->tns.p, h->tau};
+    GammaTables tabs{h->tnr.p, h->tnc.p, h->tns.p, h->tau, h->gw.p};
     const bool fused = use_fused(h->G);
     ChainWork cw{h->ring.p, h->chain_ctr.p};
     const bool a1 = fuse_axis(h->G, 1) == 1;

@@ -6,6 +6,8 @@
 // alias footprint is a few tens of KB).
 #include <cstring>
 
+#include <algorithm>
+
 #include "fold.cuh"
 
 namespace vsr {
@@ -581,6 +583,36 @@ bool detect_separable(const Dims& hr, const double2* lam, double2* a, double2* b
                                                                   (long long)hr.s, lam, a, b, c);
     VSR_LAUNCH_CHECK();
     return true;
+}
+
+// ------------------------------------------------------------ TV gram table
+__global__ void __launch_bounds__(256) tv_gram_kernel(FoldGeom G, const double2* __restrict__ lam, SepTables sep,
+                                                      GammaTables tabs, double* __restrict__ gw) {
+    const long long Nl = G.ml * G.nl * G.sl;
+    for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < Nl;
+         g += (long long)gridDim.x * blockDim.x) {
+        const long long g1 = g % G.ml, r = g / G.ml, g2 = r % G.nl, g3 = r / G.nl;
+        double acc = 0.0;
+        for (int bs = 0; bs < G.ds; ++bs)
+            for (int bc = 0; bc < G.dc; ++bc)
+                for (int br = 0; br < G.dr; ++br) {
+                    const long long f1 = g1 + br * G.ml, f2 = g2 + bc * G.nl, f3 = g3 + bs * G.sl;
+                    const double2 L = sep.a ? cmul(__ldg(sep.a + f1), cmul(__ldg(sep.b + f2), __ldg(sep.c + f3)))
+                                            : __ldg(lam + f1 + G.m * (f2 + G.n * f3));
+                    const double gam =
+                        1.0 / ((__ldg(tabs.nr + f1) + (__ldg(tabs.nc + f2) + __ldg(tabs.ns + f3))) + tabs.tau);
+                    acc += gam * cnorm(L);
+                }
+        gw[g] = acc;
+    }
+}
+
+void launch_tv_gram(const FoldGeom& G, const double2* lam, const SepTables& sep, const GammaTables& tabs,
+                    double* gw, cudaStream_t st) {
+    const long long Nl = G.ml * G.nl * G.sl;
+    const unsigned blocks = (unsigned)std::min<long long>((Nl + 255) / 256, 148LL * 16);
+    tv_gram_kernel<<<blocks, 256, 0, st>>>(G, lam, sep, tabs, gw);
+    VSR_LAUNCH_CHECK();
 }
 
 }  // namespace vsr

@@ -41,7 +41,16 @@ struct GammaTables {
     const double* nc;
     const double* ns;
     double tau;
+    // optional LR table Gw(g) = sum_b Gamma_b |Lambda_b|^2 (constant across
+    // ADMM iterations, spectral.cpp:133-142): the TV fold then needs only one
+    // cross-alias sum per LR frequency
+    const double* gw = nullptr;
 };
+
+// Gw(g) = sum_b Gamma_b |Lambda_b|^2 over the d aliases of every LR frequency
+// (b_lin ascending, gram_diag_weighted spectral.cpp:133-142).
+void launch_tv_gram(const FoldGeom& G, const double2* lam, const SepTables& sep, const GammaTables& tabs,
+                    double* gw, cudaStream_t st);
 
 // ---- fused Tikhonov fold (TikhonovOperator::solve, solvers.cpp:53-62)
 // x_hat[f] for every HR f from the LR spectrum Yl of y, Lambda and X̄ = fft3(xbar).

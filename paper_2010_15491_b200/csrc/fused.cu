@@ -300,12 +300,23 @@ __global__ void __launch_bounds__(T * A * (L / RM), ((RM == 8 ? 1024 : 512) / (T
     const int ln = tid % NLN, t = tid / NLN;
     const int a = ln % A, ti = ln / A;
     const int bc = a % G.dc, bs = a / G.dc;
-    const long long ng2 = G.nl / T;
-    const long long g2 = (blockIdx.x % ng2) * T + ti, g3 = blockIdx.x / ng2;
+    const int ng2 = (int)(G.nl / T);
+    const int bx2 = (int)blockIdx.x % ng2, bx3 = (int)blockIdx.x / ng2;
+    const long long g2 = (long long)bx2 * T + ti, g3 = bx3;
     const long long f2 = g2 + bc * G.nl, f3 = g3 + bs * G.sl;
     const long long rowb = G.m * (f2 + G.n * f3);
     // line-interleaved: a quarter-warp (8 lines at one position) is one 128-B row
     auto sidx = [&](int q) { return q * NLN + ln; };
+    // Staged HBM I/O: whole rows move through shared memory (pitch L + 1, bank-
+    // conflict free both ways) so every warp access is a contiguous row segment
+    // instead of NLN rows x 32 B.
+    constexpr int THREADS = NLN * P;
+    constexpr bool STAGED = NLN >= 8 && L >= 32 && THREADS % L == 0;
+    constexpr int PITCH = L + 1;
+    __shared__ long long rowbase_s[NLN];  // HBM offset of each line of the tile
+    if (tid < NLN) rowbase_s[tid] = rowb;  // thread tid owns line ln = tid
+    __syncthreads();
+    auto row_base = [&](int j) { return rowbase_s[j]; };
     double2 v[R];
     // LR spectrum of y for this row: issued first so its latency overlaps the
     // forward transform
@@ -314,8 +325,25 @@ __global__ void __launch_bounds__(T * A * (L / RM), ((RM == 8 ? 1024 : 512) / (T
 #pragma unroll
     for (int rr = 0; rr < RD; ++rr) yr[rr] = __ldg(Yrow + t + P * rr);
     if constexpr (TV) {
+        if constexpr (STAGED) {
 #pragma unroll
-        for (int r = 0; r < R; ++r) v[r] = W[rowb + t + P * r];
+            for (int k = 0; k < R; ++k) {
+                const int e = tid + THREADS * k, j = e / L, q = e % L;
+                v[k] = W[row_base(j) + q];
+            }
+#pragma unroll
+            for (int k = 0; k < R; ++k) {
+                const int e = tid + THREADS * k, j = e / L, q = e % L;
+                sm[j * PITCH + q] = v[k];
+            }
+            __syncthreads();
+#pragma unroll
+            for (int r = 0; r < R; ++r) v[r] = sm[ln * PITCH + t + P * r];
+            __syncthreads();
+        } else {
+#pragma unroll
+            for (int r = 0; r < R; ++r) v[r] = W[rowb + t + P * r];
+        }
         fftc::stockham<L, false, decltype(sidx), RM>(v, t, sm, sidx, tw);
         fftc::to_natural<L, RM>(v);
 #pragma unroll
@@ -345,6 +373,52 @@ __global__ void __launch_bounds__(T * A * (L / RM), ((RM == 8 ? 1024 : 512) / (T
     double base_g = 0.0;
     if constexpr (TV) base_g = __ldg(tabs.nc + f2) + __ldg(tabs.ns + f3);
     double fit = 0.0;
+    if constexpr (TV) {
+        if (tabs.gw) {
+            // one cross-alias sum: S = sum_b Lambda_b g_b with g_b = Gamma_b k_b; the
+            // denominator Gw + mu d is tabled and the data fit follows from S and w:
+            // sum_b Lambda_b x̂_b = (S - Gw w) / mu
+            double gwv[RD];
+#pragma unroll
+            for (int rr = 0; rr < RD; ++rr) gwv[rr] = __ldg(tabs.gw + (Yrow - Yl) + t + P * rr);
+#pragma unroll
+            for (int rr = 0; rr < RD; ++rr) {
+                const double2 yraw = yr[rr];
+                const double2 yv = cscale(yraw, invsqrtd);
+                double Gg[DR];
+                double Sx = 0.0, Sy = 0.0;
+#pragma unroll
+                for (int br = 0; br < DR; ++br) {
+                    const int r = rr + RD * br;
+                    const double2 Lr = sm[sidx(t + P * r)];
+                    Gg[br] = 1.0 / ((__ldg(tabs.nr + (t + P * r)) + base_g) + tabs.tau);
+                    v[r] = cscale(cadd(cmulc(Lr, yv), cscale(v[r], cA)), Gg[br]);
+                    const double2 pr = cmul(Lr, v[r]);
+                    Sx += pr.x;
+                    Sy += pr.y;
+                }
+                Sx = lanes_sum<1, A>(Sx);
+                Sy = lanes_sum<1, A>(Sy);
+                const double den = gwv[rr] + shift;
+                const double2 w = make_double2(Sx / den, Sy / den);
+#pragma unroll
+                for (int br = 0; br < DR; ++br) {
+                    const int r = rr + RD * br;
+                    const double2 Lr = sm[sidx(t + P * r)];
+                    const double2 c = cmul(make_double2(Gg[br] * Lr.x, -(Gg[br] * Lr.y)), w);
+                    v[r] = cscale(csub(v[r], c), inv_scale);
+                }
+                if constexpr (FIT) {
+                    if (a == 0) {
+                        const double ax = (Sx - gwv[rr] * w.x) * inv_scale, ay = (Sy - gwv[rr] * w.y) * inv_scale;
+                        const double rx = yraw.x - invsqrtd * ax, ry = yraw.y - invsqrtd * ay;
+                        fit += rx * rx + ry * ry;
+                    }
+                }
+            }
+            goto folded;
+        }
+    }
 #pragma unroll
     for (int rr = 0; rr < RD; ++rr) {
         const double2 yraw = yr[rr];
@@ -398,11 +472,23 @@ __global__ void __launch_bounds__(T * A * (L / RM), ((RM == 8 ? 1024 : 512) / (T
             }
         }
     }
+folded:
     __syncthreads();
     fftc::stockham<L, true, decltype(sidx), RM>(v, t, sm, sidx, tw);
     double2* dst = TV ? W : out;
+    if constexpr (STAGED) {
 #pragma unroll
-    for (int j = 0; j < R; ++j) dst[rowb + Pl::out_q(t, j)] = v[j];
+        for (int j = 0; j < R; ++j) sm[ln * PITCH + Pl::out_q(t, j)] = v[j];
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+            const int e = tid + THREADS * k, j = e / L, q = e % L;
+            dst[row_base(j) + q] = sm[j * PITCH + q];
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < R; ++j) dst[rowb + Pl::out_q(t, j)] = v[j];
+    }
     if constexpr (FIT) {
         __shared__ double red[32];
         double vv[1] = {fit};
@@ -418,7 +504,8 @@ struct A1Shape {
     static constexpr int TT = (T0 * A * PP) > 256 ? (256 / (A * PP) > 0 ? 256 / (A * PP) : 1) : T0;
     static constexpr int T = TT > 2 ? 2 : TT;                    // 2 consecutive g2 per tile
     static constexpr int THREADS = T * A * PP;
-    static constexpr size_t SMEM = (size_t)T * A * L * sizeof(double2);
+    static constexpr bool STAGED = T * A >= 8 && L >= 32 && THREADS % L == 0;  // fold_axis1_kernel
+    static constexpr size_t SMEM = (size_t)T * A * (STAGED ? L + 1 : L) * sizeof(double2);
 };
 
 template <int L, int A, int DR, bool TV, bool FIT, int RM = 16>
