@@ -284,8 +284,7 @@ bool dispatch_tik_v2(const FoldGeom& G, const double2* Yl, const double2* lam, c
 //               axis-1 FFT -> W (in place), + LR-Parseval data-fit partials
 // Lambda waits in the thread's own slots of the exchange buffer during the fold.
 template <int L, int A, int DR, int T, bool TV, bool FIT, int RM>
-__global__ void __launch_bounds__(T * A * (L / RM), ((RM == 8 ? 1024 : 512) / (T * A * (L / RM))) > 0 ? (RM == 8 ? 1024 : 512) / (T * A * (L / RM)) : 1)
-    fold_axis1_kernel(FoldGeom G, const double2* __restrict__ Yl, const double2* __restrict__ lam,
+__device__ __forceinline__ void fold_axis1_tile(int tile, FoldGeom G, const double2* __restrict__ Yl, const double2* __restrict__ lam,
                       SepTables sep,
                       const double2* __restrict__ xbh, const double2* __restrict__ Zl, double2* W, double2* out,
                       GammaTables tabs, double cA,
@@ -301,7 +300,7 @@ __global__ void __launch_bounds__(T * A * (L / RM), ((RM == 8 ? 1024 : 512) / (T
     const int a = ln % A, ti = ln / A;
     const int bc = a % G.dc, bs = a / G.dc;
     const int ng2 = (int)(G.nl / T);
-    const int bx2 = (int)blockIdx.x % ng2, bx3 = (int)blockIdx.x / ng2;
+    const int bx2 = tile % ng2, bx3 = tile / ng2;
     const long long g2 = (long long)bx2 * T + ti, g3 = bx3;
     const long long f2 = g2 + bc * G.nl, f3 = g3 + bs * G.sl;
     const long long rowb = G.m * (f2 + G.n * f3);
@@ -493,7 +492,35 @@ folded:
         __shared__ double red[32];
         double vv[1] = {fit};
         block_reduce_sum<1>(vv, red);
-        if (tid == 0) fit_partials[blockIdx.x] = vv[0];
+        if (tid == 0) fit_partials[tile] = vv[0];
+    }
+}
+
+
+// Persistent wrapper: a CTA walks tiles tile0, tile0 + grid, ... and, for the
+// TV sandwich, asks the TMA unit to pull the next tile's rows into L2
+// (cp.async.bulk.prefetch) while the current tile computes.
+template <int L, int A, int DR, int T, bool TV, bool FIT, int RM>
+__global__ void __launch_bounds__(T * A * (L / RM), ((RM == 8 ? 1024 : 512) / (T * A * (L / RM))) > 0 ? (RM == 8 ? 1024 : 512) / (T * A * (L / RM)) : 1)
+    fold_axis1_kernel(int ntiles, FoldGeom G, const double2* __restrict__ Yl, const double2* __restrict__ lam,
+                      SepTables sep, const double2* __restrict__ xbh, const double2* __restrict__ Zl, double2* W,
+                      double2* out, GammaTables tabs, double cA, double shift, double inv_scale, double invsqrtd,
+                      double fwd_scale, const double2* __restrict__ tw, double* __restrict__ fit_partials) {
+    constexpr int NLN = T * A;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int next = tile + gridDim.x;
+        if (TV && next < ntiles && threadIdx.x < NLN) {
+            const int ln = threadIdx.x, a = ln % A, ti = ln / A;
+            const int ng2 = (int)(G.nl / T);
+            const long long f2 = (long long)(next % ng2) * T + ti + (a % G.dc) * G.nl;
+            const long long f3 = (long long)(next / ng2) + (a / G.dc) * G.sl;
+            const double2* row = W + G.m * (f2 + G.n * f3);
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(row), "r"((unsigned)(L * sizeof(double2)))
+                         : "memory");
+        }
+        fold_axis1_tile<L, A, DR, T, TV, FIT, RM>(tile, G, Yl, lam, sep, xbh, Zl, W, out, tabs, cA, shift, inv_scale,
+                                                   invsqrtd, fwd_scale, tw, fit_partials);
+        __syncthreads();  // shared buffers are reused by the next tile
     }
 }
 
@@ -516,8 +543,20 @@ void launch_a1(const FoldGeom& G, const double2* Yl, const double2* lam, const S
     auto kern = fold_axis1_kernel<L, A, DR, Sh::T, TV, FIT, RM>;
     if (Sh::SMEM > 48 * 1024)
         VSR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Sh::SMEM));
-    const unsigned grid = (unsigned)((G.nl / Sh::T) * G.sl);
-    kern<<<grid, Sh::THREADS, Sh::SMEM, st>>>(G, Yl, lam, sep, xbh, Zl, W, out, tabs, cA, shift, inv_scale,
+    const int ntiles = (int)((G.nl / Sh::T) * G.sl);
+    static const bool persist = [] {
+        const char* e = std::getenv("VSR_A1_PERSIST");  // opt-in: measured slower (254 vs 241 us)
+        return e && e[0] == '1';
+    }();
+    unsigned grid = (unsigned)ntiles;
+    if (persist) {
+        int per_sm = 0, dev = 0, sms = 0;
+        VSR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, Sh::THREADS, Sh::SMEM));
+        VSR_CUDA(cudaGetDevice(&dev));
+        VSR_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        grid = (unsigned)std::min<long long>(ntiles, (long long)std::max(per_sm, 1) * sms);
+    }
+    kern<<<grid, Sh::THREADS, Sh::SMEM, st>>>(ntiles, G, Yl, lam, sep, xbh, Zl, W, out, tabs, cA, shift, inv_scale,
                                               1.0 / std::sqrt((double)G.d), fwd_scale,
                                               fft_engine().twiddles((size_t)L), fit);
     VSR_LAUNCH_CHECK();
