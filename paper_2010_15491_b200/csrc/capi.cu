@@ -19,6 +19,7 @@
 #include "fold.cuh"
 #include "fused.cuh"
 #include "spatial.cuh"
+#include "rfft.cuh"
 #include "chain.cuh"
 #include "tv.cuh"
 
@@ -815,6 +816,8 @@ struct vsr_tikhonov {
     DevBuf<double> zlat;              // decimate(xbar) (lattice prior)
     SpatialPlan spl;                  // spatial expansion (separable compact PSF + lattice prior)
     DevBuf<double> sp_taps, sp_s2, u;
+    DevBuf<double> q;                 // constant LR prior term sqrt(d) F_l^-1(Z G1 / (G2 + 2 reg d))
+    bool half = false;                // LR stage on the Hermitian half spectrum
     DevBuf<double2> sp_s1, U;
     DevBuf<unsigned long long> lrbad;
     ChainPlan chain;                  // chained inverse axes 2 -> 1 (L2 ring)
@@ -948,8 +951,29 @@ static void tik_spatial(vsr_tikhonov* t, cudaStream_t st) {
         so += L[a];
     }
     p.ok = true;
-    if (!spatial_sandwich_ok(t->sp.lr))
-        t->U.alloc(t->sp.lr.count());  // unfused LR stage: U kernel + inverse3
+    const Dims& lr = t->sp.lr;
+    const Dims lrh{(size_t)half_pitch(lr.m), lr.n, lr.s};
+    const char* henv = std::getenv("VSR_NO_HALF");
+    if (!(henv && henv[0] == '1') && rfft_rows_ok(lr.m) && spatial_sandwich_ok(lrh)) {
+        // U = (d yv - Z G1) / (G2 + s) splits into a real even filter of y and a
+        // constant: u = (d / N_l) F^-1(F(y) / (G2 + s)) - q with
+        // q = sqrt(d) F_l^-1(Z G1 / (G2 + s)), formed here once.
+        const size_t Nl = lr.count();
+        DevBuf<double2> yz(Nl), uq(Nl);
+        VSR_CUDA(cudaMemsetAsync(yz.p, 0, yz.bytes(), st));
+        launch_spatial_v(lr, t->sp.rate(), p, yz.p, t->Zl.p, t->reg, uq.p, st);  // -Z G1 / (G2 + s)
+        t->q.alloc(Nl);
+        const size_t qb = fft_engine().inverse_final_blocks(lr);
+        DevBuf<double> qpart(2 * std::max<size_t>(qb, 1));
+        DevBuf<unsigned long long> qbad(1);
+        PassReduce qr{qpart.p, qbad.p};
+        fft_engine().inverse3(lr, uq.p, t->q.p, OUT_REAL,
+                              -inv_sqrt_count(lr) * std::sqrt((double)t->sp.rate()), &qr, st);
+        VSR_CUDA(cudaStreamSynchronize(st));
+        t->half = true;
+    } else if (!spatial_sandwich_ok(lr)) {
+        t->U.alloc(lr.count());  // unfused LR stage: U kernel + inverse3
+    }
     t->u.alloc(t->sp.lr.count());
     t->lrbad.alloc(1);
     t->xh.release();  // the HR spectrum is never formed on this path
@@ -1019,6 +1043,41 @@ int vsr_tikhonov_destroy(vsr_tikhonov* t) {
 static void tik_enqueue(vsr_tikhonov* t, const double* y_dev, double* x_dev) {
     cudaStream_t st = t->ctx->stream;
     Profiler* prof = t->ctx->prof();
+    if (t->spl.ok && t->half) {
+        // half-spectrum LR stage: r2c rows, axis 2, filter sandwich on axis 3,
+        // inverse axis 2, c2r rows minus the constant prior term -> u
+        const Dims& lr = t->sp.lr;
+        const Dims lrh{(size_t)half_pitch(lr.m), lr.n, lr.s};
+        const long long rows = (long long)(lr.n * lr.s);
+        {
+            ProfScope ps(prof, "lr_r2c_axis1", st);
+            rfft_rows_forward(lr.m, y_dev, t->Yl.p, rows, st);
+        }
+        {
+            ProfScope ps(prof, "lr_fft_axis2_half", st);
+            fft_engine().axis_pass(lrh, 1, false, t->Yl.p, IN_COMPLEX, t->Yl.p, OUT_COMPLEX, 1.0, nullptr, st);
+        }
+        ++g_fwd;
+        {
+            ProfScope ps(prof, "lr_filter_axis3_half", st);
+            launch_spatial_sandwich(lrh, t->sp.rate(), t->spl, t->Yl.p, nullptr, t->reg, inv_sqrt_count(lr),
+                                    inv_sqrt_count(lr) * std::sqrt((double)t->sp.rate()), st);
+        }
+        {
+            ProfScope ps(prof, "lr_ifft_axis2_half", st);
+            fft_engine().axis_pass(lrh, 1, true, t->Yl.p, IN_COMPLEX, t->Yl.p, OUT_COMPLEX, 1.0, nullptr, st);
+        }
+        {
+            ProfScope ps(prof, "lr_c2r_axis1", st);
+            rfft_rows_inverse(lr.m, t->Yl.p, t->u.p, rows, 1.0, t->q.p, st);
+        }
+        ++g_inv;
+        {
+            ProfScope ps(prof, "spatial_expand", st);
+            launch_spatial_expand(t->sp.hr, t->sp.rates, t->spl, t->u.p, t->zlat.p, 1.0, x_dev, t->bad.p, st);
+        }
+        return;  // real by construction: no imaginary residue to reduce
+    }
     if (t->spl.ok && t->U.p == nullptr) {
         ProfScope ps(prof, "lr_fft12", st);
         fft_engine().forward12(t->sp.lr, y_dev, IN_REAL, t->Yl.p, st);

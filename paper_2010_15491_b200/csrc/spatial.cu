@@ -59,7 +59,7 @@ struct SwShape {
 
 template <int L>
 __global__ void __launch_bounds__(SwShape<L>::THREADS, 512 / SwShape<L>::THREADS)
-    lr_sandwich_kernel(double2* Y, const double2* __restrict__ Zl, long long S, int ml, int nl,
+    lr_sandwich_kernel(double2* Y, const double2* __restrict__ Zl, long long S, int pitch, int nl,
                        const double2* __restrict__ a1, const double2* __restrict__ b1,
                        const double2* __restrict__ c1, const double* __restrict__ a2,
                        const double* __restrict__ b2, const double* __restrict__ c2, double cy,
@@ -86,8 +86,8 @@ __global__ void __launch_bounds__(SwShape<L>::THREADS, 512 / SwShape<L>::THREADS
     fftc::stockham<L, false>(v, t, smw, sidx, tw);
     fftc::to_natural<L>(v);
     // v[r] = F_l(y) at g3 = t + P r (times 1/fs)
-    const int g1 = (int)(p % ml), g2 = (int)(p / ml);
-    const double2 ab1 = cmul(__ldg(a1 + g1), __ldg(b1 + g2));
+    const int g1 = (int)(p % pitch), g2 = (int)(p / pitch);
+    const double2 ab1 = Zl ? cmul(__ldg(a1 + g1), __ldg(b1 + g2)) : make_double2(0.0, 0.0);
     const double ab2 = __ldg(a2 + g1) * __ldg(b2 + g2);
 #pragma unroll
     for (int r = 0; r < R; ++r) {
@@ -121,6 +121,8 @@ static void launch_sandwich_L(const Dims& lr, const SpatialPlan& p, double2* Y, 
     VSR_LAUNCH_CHECK();
 }
 
+// lr: the grid the sandwich runs on, lr.m = row pitch (ml, or the half-
+// spectrum pitch with Zl == nullptr).
 bool spatial_sandwich_ok(const Dims& lr) {
     const size_t L = lr.s;
     return L >= 8 && L <= 1024 && is_pow2(L) && (lr.m * lr.n) % 8 == 0 && lr.m * lr.n * L < (1ull << 31);
