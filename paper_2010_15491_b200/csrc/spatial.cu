@@ -193,8 +193,9 @@ __global__ void __launch_bounds__(SP_THREADS, (DM <= 8 ? 8 : 6)) spatial_expand_
     double* t2 = t1 + TZ * LY * LX;        // TZ * TY * LX
     // stage-C row tables: tz | ty << 8, and the LR index of the row's prior
     // samples (-1 off the lattice)
-    int* rowinfo = reinterpret_cast<int*>(t2 + TZ * TY * LX);
-    int* zrow = rowinfo + TZ * TY;
+    double* zt = t2 + TZ * TY * LX;                      // lattice prior tile, CZ x CY x CX
+    int* rowinfo = reinterpret_cast<int*>(zt + SP_CZ * SP_CY * SP_CX);
+    int* zrow = rowinfo + TZ * TY;                          // offset of the row's prior samples in zt, -1 off lattice
     __shared__ long long zoff[LZ];
     __shared__ int yoff[LY], xoff[LX];
 
@@ -203,6 +204,17 @@ __global__ void __launch_bounds__(SP_THREADS, (DM <= 8 ? 8 : 6)) spatial_expand_
     const int rows = TZ * TY;
 
     for (int i = tid; i < nkp; i += SP_THREADS) kp1[i] = A.kp[i];
+    // prior samples of the tile: loaded now into registers, parked in smem after
+    // stage A (their latency overlaps stage A), read in stage C
+    constexpr int NZT = SP_CZ * SP_CY * SP_CX, ZPER = (NZT + SP_THREADS - 1) / SP_THREADS;
+    double zreg[ZPER];
+#pragma unroll
+    for (int k = 0; k < ZPER; ++k) {
+        const int i = tid + k * SP_THREADS;
+        const int cx = i % SP_CX, r = i / SP_CX, cy = r % SP_CY, cz = r / SP_CY;
+        const bool in = A.z && i < NZT && cx0 + cx < A.ml && cy0 + cy < A.nl && cz0 + cz < A.sl;
+        zreg[k] = in ? __ldg(A.z + ((size_t)(cz0 + cz) * A.nl + cy0 + cy) * A.ml + cx0 + cx) : 0.0;
+    }
     if (tid < LZ) zoff[tid] = (long long)wrap_idx(cz0 + A.ax[2].dmin + tid, A.sl) * A.nl * A.ml;
     else if (tid >= 32 && tid < 32 + LY) yoff[tid - 32] = wrap_idx(cy0 + A.ax[1].dmin + tid - 32, A.nl) * A.ml;
     else if (tid >= 64 && tid < 64 + LX) xoff[tid - 64] = wrap_idx(cx0 + A.ax[0].dmin + tid - 64, A.ml);
@@ -210,7 +222,7 @@ __global__ void __launch_bounds__(SP_THREADS, (DM <= 8 ? 8 : 6)) spatial_expand_
         const int tz = row / TY, ty = row - tz * TY;
         const bool lat = A.z != nullptr && (ty % r2) == 0 && (tz % r3) == 0;
         rowinfo[row] = tz | (ty << 8);
-        zrow[row] = lat ? ((cz0 + tz / r3) * A.nl + cy0 + ty / r2) * A.ml + cx0 : -1;
+        zrow[row] = lat ? ((tz / r3) * SP_CY + ty / r2) * SP_CX : -1;
     }
     __syncthreads();
     // stage A: axis 3
@@ -233,6 +245,9 @@ __global__ void __launch_bounds__(SP_THREADS, (DM <= 8 ? 8 : 6)) spatial_expand_
             }
         }
     }
+#pragma unroll
+    for (int k = 0; k < ZPER; ++k)
+        if (tid + k * SP_THREADS < NZT) zt[tid + k * SP_THREADS] = zreg[k];
     __syncthreads();
     // stage B: axis 2
     for (int col = tid; col < TZ * LX; col += SP_THREADS) {
@@ -272,7 +287,7 @@ __global__ void __launch_bounds__(SP_THREADS, (DM <= 8 ? 8 : 6)) spatial_expand_
         const bool lat = zr >= 0;
         double zv[SP_XB];
 #pragma unroll
-        for (int j = 0; j < SP_XB; ++j) zv[j] = lat ? __ldg(A.z + zr + c0 + j) : 0.0;
+        for (int j = 0; j < SP_XB; ++j) zv[j] = lat ? zt[zr + c0 + j] : 0.0;
         double in[DM + SP_XB - 1];
         const double* src = t2 + row * LX + c0;
 #pragma unroll
@@ -344,7 +359,7 @@ static size_t expand_smem(const int rates[3], int dm) {
     const size_t LX = SP_CX + dm - 1, LY = SP_CY + dm - 1;
     const size_t TY = (size_t)rates[1] * SP_CY, TZ = (size_t)rates[2] * SP_CZ;
     const size_t kp = (size_t)(rates[0] + rates[1] + rates[2]) * dm;
-    return (kp + TZ * LY * LX + TZ * TY * LX) * sizeof(double) + 2 * TZ * TY * sizeof(int);
+    return (kp + TZ * LY * LX + TZ * TY * LX + SP_CZ * SP_CY * SP_CX) * sizeof(double) + 2 * TZ * TY * sizeof(int);
 }
 
 int spatial_tile(const SpatialPlan& p, const int rates[3]) {
