@@ -818,6 +818,15 @@ struct vsr_tikhonov {
     DevBuf<double> sp_taps, sp_s2, u;
     DevBuf<double> q;                 // constant LR prior term sqrt(d) F_l^-1(Z G1 / (G2 + 2 reg d))
     bool half = false;                // LR stage on the Hermitian half spectrum
+    // CUDA graph of one solve for a given (y, x) pair (replayed while they repeat)
+    cudaGraphExec_t gexec = nullptr;
+    const double* g_y = nullptr;
+    double* g_x = nullptr;
+    uint64_t g_kernels = 0;
+    uint64_t solves = 0;
+    ~vsr_tikhonov() {
+        if (gexec) cudaGraphExecDestroy(gexec);
+    }
     DevBuf<double2> sp_s1, U;
     DevBuf<unsigned long long> lrbad;
     ChainPlan chain;                  // chained inverse axes 2 -> 1 (L2 ring)
@@ -1166,6 +1175,54 @@ static void tik_enqueue(vsr_tikhonov* t, const double* y_dev, double* x_dev) {
     }
 }
 
+// One solve through a CUDA graph (launch gaps removed).  The first solve of an
+// operator runs eagerly (lazy twiddle tables, attribute setup); the next one is
+// captured for its (y, x) pair and replayed while the pair repeats.  The event
+// profiler and VSR_NO_GRAPH=1 keep the eager path.
+static void tik_run(vsr_tikhonov* t, const double* y_dev, double* x_dev) {
+    static const bool off = [] {
+        const char* e = std::getenv("VSR_NO_GRAPH");
+        return e && e[0] == '1';
+    }();
+    cudaStream_t st = t->ctx->stream;
+    const bool eager = off || t->ctx->prof() != nullptr || t->solves++ == 0;
+    if (eager) {
+        tik_enqueue(t, y_dev, x_dev);
+        return;
+    }
+    if (!(t->gexec && t->g_y == y_dev && t->g_x == x_dev)) {
+        if (t->gexec) {
+            cudaGraphExecDestroy(t->gexec);
+            t->gexec = nullptr;
+        }
+        const uint64_t l0 = g_launches.load();
+        const uint64_t f0 = g_fwd.load(), i0 = g_inv.load();
+        cudaGraph_t graph = nullptr;
+        VSR_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+        try {
+            tik_enqueue(t, y_dev, x_dev);
+        } catch (...) {
+            cudaStreamEndCapture(st, &graph);
+            if (graph) cudaGraphDestroy(graph);
+            throw;
+        }
+        VSR_CUDA(cudaStreamEndCapture(st, &graph));
+        const cudaError_t e = cudaGraphInstantiate(&t->gexec, graph, 0);
+        cudaGraphDestroy(graph);
+        VSR_CUDA(e);
+        t->g_kernels = g_launches.load() - l0;
+        g_launches.fetch_sub(t->g_kernels);  // counted when the graph runs
+        g_fwd.fetch_sub(g_fwd.load() - f0);
+        g_inv.fetch_sub(g_inv.load() - i0);
+        t->g_y = y_dev;
+        t->g_x = x_dev;
+    }
+    VSR_CUDA(cudaGraphLaunch(t->gexec, st));
+    g_launches.fetch_add(t->g_kernels);
+    ++g_fwd;  // the solve's transform budget (solvers.cpp:52,64)
+    ++g_inv;
+}
+
 static void tik_check(vsr_tikhonov* t) {
     double status[4];
     unsigned long long bad = 0;
@@ -1185,7 +1242,7 @@ int vsr_tikhonov_solve(vsr_tikhonov* t, const double* y_r, double* x_r) {
         if (!t) throw std::invalid_argument("vsr_tikhonov_solve: null operator");
         vsr_ctx::Guard g(t->ctx->device);
         h2d(t->ctx, t->y.p, y_r, t->y.bytes());
-        tik_enqueue(t, t->y.p, t->x.p);
+        tik_run(t, t->y.p, t->x.p);
         d2h(t->ctx, x_r, t->x.p, t->x.bytes());
         tik_check(t);
     });
@@ -1195,7 +1252,7 @@ int vsr_tikhonov_solve_d(vsr_tikhonov* t, const double* y_dev, double* x_dev) {
     return guarded([&] {
         if (!t) throw std::invalid_argument("vsr_tikhonov_solve_d: null operator");
         vsr_ctx::Guard g(t->ctx->device);
-        tik_enqueue(t, y_dev, x_dev);
+        tik_run(t, y_dev, x_dev);
     });
 }
 
