@@ -1058,11 +1058,21 @@ static void tik_enqueue(vsr_tikhonov* t, const double* y_dev, double* x_dev) {
         const Dims& lr = t->sp.lr;
         const Dims lrh{(size_t)half_pitch(lr.m), lr.n, lr.s};
         const long long rows = (long long)(lr.n * lr.s);
-        {
-            ProfScope ps(prof, "lr_r2c_axis1", st);
-            rfft_rows_forward(lr.m, y_dev, t->Yl.p, rows, st);
-        }
-        {
+        // whole-plane smem kernels: opt-in (VSR_LR_PLANE=1) - one CTA per plane
+        // leaves them latency-bound (29.6 us vs 28 us for the two row/column kernels)
+        static const bool use_plane = [] {
+            const char* e = std::getenv("VSR_LR_PLANE");
+            return e && e[0] == '1';
+        }();
+        const bool plane = use_plane && lr_plane_ok(lr.m, lr.n);
+        if (plane) {
+            ProfScope ps(prof, "lr_plane_r2c_axis12", st);
+            lr_plane_forward(lr.m, lr.n, y_dev, t->Yl.p, (long long)lr.s, st);
+        } else {
+            {
+                ProfScope ps(prof, "lr_r2c_axis1", st);
+                rfft_rows_forward(lr.m, y_dev, t->Yl.p, rows, st);
+            }
             ProfScope ps(prof, "lr_fft_axis2_half", st);
             fft_engine().axis_pass(lrh, 1, false, t->Yl.p, IN_COMPLEX, t->Yl.p, OUT_COMPLEX, 1.0, nullptr, st);
         }
@@ -1072,11 +1082,14 @@ static void tik_enqueue(vsr_tikhonov* t, const double* y_dev, double* x_dev) {
             launch_spatial_sandwich(lrh, t->sp.rate(), t->spl, t->Yl.p, nullptr, t->reg, inv_sqrt_count(lr),
                                     inv_sqrt_count(lr) * std::sqrt((double)t->sp.rate()), st);
         }
-        {
-            ProfScope ps(prof, "lr_ifft_axis2_half", st);
-            fft_engine().axis_pass(lrh, 1, true, t->Yl.p, IN_COMPLEX, t->Yl.p, OUT_COMPLEX, 1.0, nullptr, st);
-        }
-        {
+        if (plane) {
+            ProfScope ps(prof, "lr_plane_axis21_c2r", st);
+            lr_plane_inverse(lr.m, lr.n, t->Yl.p, t->u.p, (long long)lr.s, 1.0, t->q.p, st);
+        } else {
+            {
+                ProfScope ps(prof, "lr_ifft_axis2_half", st);
+                fft_engine().axis_pass(lrh, 1, true, t->Yl.p, IN_COMPLEX, t->Yl.p, OUT_COMPLEX, 1.0, nullptr, st);
+            }
             ProfScope ps(prof, "lr_c2r_axis1", st);
             rfft_rows_inverse(lr.m, t->Yl.p, t->u.p, rows, 1.0, t->q.p, st);
         }
