@@ -440,3 +440,57 @@ def test_admm_tv_deterministic(V):
     b, rb = V.admm_tv(y, psf, spec, cfg)
     assert a.tobytes() == b.tobytes()
     assert ra.objective == rb.objective and ra.primal_residual == rb.primal_residual
+
+
+# ------------------------------------------------------------------ opt-in variants
+# Every env-selected kernel variant (read once per process) runs in a fresh
+# interpreter against the oracle: Tikhonov spatial path with the whole-plane LR
+# kernels / full-spectrum LR stage / the general FFT path / no graphs, and the
+# TV sandwich with radix 8 / the persistent prefetching loop.
+_VARIANT_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, {root!r}); sys.path.insert(0, {root!r} + '/oracle'); sys.path.insert(0, {root!r} + '/tests')
+from paper_2010_15491_b200 import volsr as V
+import volsr_oracle as O
+from conftest import rel_err
+rng = np.random.default_rng(21)
+dims, rates = {dims}, {rates}
+spec, ospec = V.DecimationSpec(dims, rates), O.DecimationSpec(dims, rates)
+psf = O.make_gaussian_psf((5, 5, 5), (1.2, 1.2, 1.2), dims)
+lam = O.psf_to_spectrum(psf)
+y = rng.uniform(0, 1, V.shape_of(spec.lr))
+xbar = O.zero_fill_upsample(y, ospec)
+op = V.TikhonovOperator(lam, spec, V.TikhonovConfig(0.01, xbar))
+want = O.tikhonov_fast(y, lam, ospec, 0.01, xbar)
+for _ in range(3):  # eager, captured, replayed
+    e = rel_err(op.solve(y), want)
+    assert e < 1e-10, ("tikhonov", e)
+cfg = V.TvAdmmConfig(lambda_=2e-3, mu=0.05, max_iters=3, rel_tol=0.0, tau=5e-5)
+xt, _ = V.admm_tv(y, psf, spec, cfg)
+xo, _ = O.admm_tv(y, psf, ospec, lam_tv=2e-3, mu=0.05, max_iters=3, rel_tol=0.0, tau=5e-5)
+e2 = rel_err(xt, xo)
+assert e2 < 1e-10, ("admm_tv", e2)
+print("ok", op.path())
+"""
+
+
+@pytest.mark.parametrize("env,dims,rates", [
+    ({"VSR_LR_PLANE": "1"}, (64, 64, 32), (2, 2, 2)),
+    ({"VSR_LR_PLANE": "1"}, (128, 128, 32), (2, 2, 2)),
+    ({"VSR_LR_PLANE": "1"}, (256, 256, 16), (2, 2, 2)),
+    ({"VSR_NO_HALF": "1"}, (64, 64, 32), (2, 2, 2)),
+    ({"VSR_NO_SPATIAL": "1"}, (64, 64, 32), (2, 2, 2)),
+    ({"VSR_NO_GRAPH": "1"}, (64, 64, 32), (2, 2, 2)),
+    ({"VSR_A1_RM": "8"}, (64, 64, 64), (4, 4, 4)),
+    ({"VSR_A1_PERSIST": "1"}, (64, 64, 64), (4, 4, 4)),
+])
+def test_env_variants(env, dims, rates):
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = str(Path(__file__).resolve().parent.parent)
+    code = _VARIANT_SCRIPT.format(root=root, dims=dims, rates=rates)
+    r = subprocess.run([sys.executable, "-c", code], env={**os.environ, **env}, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
