@@ -211,6 +211,9 @@ STAGE_BYTES = {
     "tik_fold_ifft_axis3": (48, 16), "tv_fft3_fold_ifft3": (48, 16),
     "tik_fold_ifft_axis1": (48, 16), "tv_fft1_fold_ifft1": (48, 16),
     "fft_inv_axis3_c2r": (24, 0), "fft_fwd_axis3_r2c": (24, 0),
+    # TV on the Hermitian half spectrum along axis 3 (planes 0..s/2)
+    "fft_fwd_axis3_r2c_half": (16, 0), "fft_fwd_axis2_half": (16, 0), "tv_fft1_fold_ifft1_half": (32, 16),
+    "fft_inv_axis2_half": (16, 0), "fft_inv_axis3_c2r_half": (16, 0),
     # chained in-plane passes: one HBM read of the input, one write of the output
     "chain_inv_axis2_axis1_c2r": (24, 0), "chain_fwd_axis1_r2c_axis2": (24, 0),
     # spatial-expansion Tikhonov: LR transforms (r2c 24 + 2 x 32), LR pointwise
@@ -226,7 +229,8 @@ STAGE_BYTES = {
 
 
 # fused fold stages that read the 16N-byte HR Lambda unless it is separable
-SEP_STAGES = {"tik_fold_ifft_axis3", "tv_fft3_fold_ifft3", "tik_fold_ifft_axis1", "tv_fft1_fold_ifft1"}
+SEP_STAGES = {"tik_fold_ifft_axis3", "tv_fft3_fold_ifft3", "tik_fold_ifft_axis1", "tv_fft1_fold_ifft1",
+              "tv_fft1_fold_ifft1_half"}
 
 
 def run_b200(args, rank, world, local):

@@ -1425,6 +1425,7 @@ struct vsr_tv {
     DevBuf<int> chain_ctr;
     SepState sep;
     DevBuf<double> gw;  // LR table sum_b Gamma_b |Lambda_b|^2 (axis-1 sandwich)
+    DevBuf<double2> W2;  // sandwich output on the half-spectrum path (m x n x (s/2+1))
     size_t iters_done = 0;
     bool dual_in_a = true;
     bool stopped = false;
@@ -1436,6 +1437,15 @@ static void tv_validate(const vsr_tv_config* cfg) {
     require_positive(cfg->lambda, "lambda");  // solvers.cpp:323-326
     require_positive(cfg->mu, "mu");
     if (cfg->max_iters < 1) throw std::invalid_argument("admm_tv: max_iters must be >= 1");
+}
+
+// TV transforms on the Hermitian half spectrum along axis 3 (VSR_TV_FULL=1: full).
+static bool tv_half(const Dims& hr) {
+    static const bool off = [] {
+        const char* e = std::getenv("VSR_TV_FULL");
+        return e && e[0] == '1';
+    }();
+    return !off && fft_engine().half3_ok(hr);
 }
 
 static vsr_tv* tv_build(vsr_ctx* ctx, const Spec& sp, const double* y_dev, const double* psf_dev,
@@ -1504,6 +1514,7 @@ static vsr_tv* tv_build(vsr_ctx* ctx, const Spec& sp, const double* y_dev, const
         g_fwd += 2;
         h->sep.detect(hr, h->lam.p, st);
         if (fuse_axis(h->G, 1) == 1) {
+            if (tv_half(hr)) h->W2.alloc(hr.m * hr.n * (hr.s / 2 + 1));
             h->gw.alloc(Nl);
             GammaTables tabs{h->tnr.p, h->tnc.p, h->tns.p, h->tau};
             launch_tv_gram(h->G, h->lam.p, h->sep.t, tabs, h->gw.p, st);
@@ -1546,7 +1557,22 @@ static void tv_step(vsr_tv* h) {
     const bool fused = use_fused(h->G);
     ChainWork cw{h->ring.p, h->chain_ctr.p};
     const bool a1 = fuse_axis(h->G, 1) == 1;
-    if (a1) {
+    // Hermitian half spectrum along axis 3 (theta is real): planes 0..s/2 only
+    const bool half = a1 && tv_half(hr);
+    const Dims hrh{hr.m, hr.n, hr.s / 2 + 1};
+    if (half) {
+        tabs.half3 = 1;
+        {
+            ProfScope ps(prof, "fft_fwd_axis3_r2c_half", st);
+            fft_engine().r2c_axis3_half(hr, h->theta.p, h->W.p, st);
+        }
+        {
+            ProfScope ps(prof, "fft_fwd_axis2_half", st);
+            fft_engine().axis_pass(hrh, 1, false, h->W.p, IN_COMPLEX, h->W.p, OUT_COMPLEX, 1.0, nullptr, st);
+        }
+        ProfScope ps(prof, "tv_fft1_fold_ifft1_half", st);
+        launch_tv_sandwich1(h->G, h->Yl.p, h->lam.p, h->W.p, tabs, h->mu, s, h->fitp.p, st, h->sep.t, h->W2.p);
+    } else if (a1) {
         {
             ProfScope ps(prof, "fft_fwd_axis3_r2c", st);
             fft_engine().axis_pass(hr, 2, false, h->theta.p, IN_REAL, h->W.p, OUT_COMPLEX, 1.0, nullptr, st);
@@ -1573,7 +1599,14 @@ static void tv_step(vsr_tv* h) {
     }
     if (h->rel_tol > 0.0) std::swap(h->x, h->xprev);  // x_prev = x (:364)
     PassReduce red{h->resp.p, h->bad.p};
-    if (a1) {
+    if (half) {
+        {
+            ProfScope ps(prof, "fft_inv_axis2_half", st);
+            fft_engine().axis_pass(hrh, 1, true, h->W2.p, IN_COMPLEX, h->W2.p, OUT_COMPLEX, 1.0, nullptr, st);
+        }
+        ProfScope ps(prof, "fft_inv_axis3_c2r_half", st);
+        fft_engine().c2r_axis3_half(hr, h->W2.p, h->x.p, s, &red, st);
+    } else if (a1) {
         {
             ProfScope ps(prof, "fft_inv_axis2", st);
             fft_engine().axis_pass(hr, 1, true, h->W.p, IN_COMPLEX, h->W.p, OUT_COMPLEX, 1.0, nullptr, st);

@@ -87,6 +87,14 @@ __global__ void __launch_bounds__(PassShape<L, R, T, TG, CONTIG>::THREADS)
             const long long off = base + estride * (long long)(t + P * r);
             if constexpr (IK == IN_REAL) {
                 v[r] = make_double2(reinterpret_cast<const double*>(in_)[off], 0.0);
+            } else if constexpr (IK == IN_HALF) {
+                const int q = t + P * r;
+                if (q <= L / 2) {
+                    v[r] = reinterpret_cast<const double2*>(in_)[off];
+                } else {
+                    const double2 h = reinterpret_cast<const double2*>(in_)[base + estride * (long long)(L - q)];
+                    v[r] = make_double2(h.x, -h.y);
+                }
             } else {
                 v[r] = reinterpret_cast<const double2*>(in_)[off];
             }
@@ -111,6 +119,8 @@ __global__ void __launch_bounds__(PassShape<L, R, T, TG, CONTIG>::THREADS)
                 acc_tot += z.x * z.x + z.y * z.y;
                 reinterpret_cast<double*>(out_)[off] = z.x;
                 if (!isfinite(z.x)) atomicMin(bad_index, (unsigned long long)off);
+            } else if constexpr (OK == OUT_HALF) {
+                if (q <= L / 2) reinterpret_cast<double2*>(out_)[off] = z;
             } else {
                 reinterpret_cast<double2*>(out_)[off] = z;
             }
@@ -390,6 +400,29 @@ void FftEngine::axis_pass(const Dims& d, int axis, bool inverse, const void* in,
         VSR_CUDA(cudaMemcpyAsync(out, tmp, out_bytes, cudaMemcpyDeviceToDevice, st));
         VSR_CUDA(cudaFreeAsync(tmp, st));
     }
+}
+
+bool FftEngine::half3_ok(const Dims& d) const {
+    return d.s >= 4 && tiled_ok(d.s, 2, (long long)(d.m * d.n));
+}
+
+void FftEngine::r2c_axis3_half(const Dims& d, const double* in, double2* out, cudaStream_t st) {
+    long long S, L, total;
+    axis_geometry(d, 2, S, L, total);
+    if (!half3_ok(d)) throw std::logic_error("r2c_axis3_half: unsupported geometry");
+    const long long units = pass_units<false>(L, S, total);
+    if (!dispatch_L<false, false, IN_REAL, OUT_HALF>(L, S, units, in, out, twiddles((size_t)L), 1.0, nullptr, st))
+        throw std::logic_error("r2c_axis3_half: unsupported length");
+}
+
+void FftEngine::c2r_axis3_half(const Dims& d, const double2* in, double* out, double scale, const PassReduce* red,
+                               cudaStream_t st) {
+    long long S, L, total;
+    axis_geometry(d, 2, S, L, total);
+    if (!half3_ok(d)) throw std::logic_error("c2r_axis3_half: unsupported geometry");
+    const long long units = pass_units<false>(L, S, total);
+    if (!dispatch_L<false, true, IN_HALF, OUT_REAL>(L, S, units, in, out, twiddles((size_t)L), scale, red, st))
+        throw std::logic_error("c2r_axis3_half: unsupported length");
 }
 
 void FftEngine::forward3(const Dims& d, const void* in, InKind ik, double2* out, double scale,

@@ -18,8 +18,11 @@
 
 namespace vsr {
 
-enum InKind { IN_COMPLEX = 0, IN_REAL = 1 };
-enum OutKind { OUT_COMPLEX = 0, OUT_REAL = 1 };
+// IN_HALF / OUT_HALF (strided axes only): the line is Hermitian (the other two
+// axes are in the spatial domain of a real volume), so only positions
+// q <= L/2 are stored; the rest are conj(X[L - q]).
+enum InKind { IN_COMPLEX = 0, IN_REAL = 1, IN_HALF = 2 };
+enum OutKind { OUT_COMPLEX = 0, OUT_REAL = 1, OUT_HALF = 2 };
 
 // Deterministic reduction slots written by a pass with OUT_REAL: per-block
 // partial sums of (imag^2, |z|^2) and the minimum flat index of a non-finite
@@ -58,6 +61,14 @@ public:
     // Forward passes 1 then 2 only (axis 3 left to a fused kernel).
     void forward12(const Dims& d, const void* in, InKind ik, double2* out, cudaStream_t st,
                    Profiler* prof = nullptr);
+
+    // Real <-> Hermitian half spectrum along axis 3 (planes 0..s/2 of an
+    // (m, n, s/2+1) array): forward r2c of a real volume, and the inverse c2r
+    // (+ residue reduction) once axes 1 and 2 are back in the spatial domain.
+    bool half3_ok(const Dims& d) const;
+    void r2c_axis3_half(const Dims& d, const double* in, double2* out, cudaStream_t st);
+    void c2r_axis3_half(const Dims& d, const double2* in, double* out, double scale, const PassReduce* red,
+                        cudaStream_t st);
 
     // Blocks of the final (axis-1) pass of inverse3.
     size_t inverse_final_blocks(const Dims& d) const { return pass_blocks(d, 0); }

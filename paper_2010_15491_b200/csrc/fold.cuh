@@ -45,6 +45,9 @@ struct GammaTables {
     // ADMM iterations, spectral.cpp:133-142): the TV fold then needs only one
     // cross-alias sum per LR frequency
     const double* gw = nullptr;
+    // 1: W holds only planes f3 <= s/2 of a Hermitian spectrum (axis 3 r2c);
+    // alias rows with f3 > s/2 are read as conj(row(-f2, s - f3)) and not stored
+    int half3 = 0;
 };
 
 // Gw(g) = sum_b Gamma_b |Lambda_b|^2 over the d aliases of every LR frequency

@@ -304,6 +304,9 @@ __device__ __forceinline__ void fold_axis1_tile(int tile, FoldGeom G, const doub
     const long long g2 = (long long)bx2 * T + ti, g3 = bx3;
     const long long f2 = g2 + bc * G.nl, f3 = g3 + bs * G.sl;
     const long long rowb = G.m * (f2 + G.n * f3);
+    // half-spectrum W (tabs.half3): rows past the Nyquist plane are mirrors
+    const bool mir = TV && tabs.half3 && 2 * f3 > G.s;
+    const long long rowb_rd = mir ? G.m * ((G.n - f2) % G.n + G.n * (G.s - f3)) : rowb;
     // line-interleaved: a quarter-warp (8 lines at one position) is one 128-B row
     auto sidx = [&](int q) { return q * NLN + ln; };
     // Staged HBM I/O: whole rows move through shared memory (pitch L + 1, bank-
@@ -312,8 +315,12 @@ __device__ __forceinline__ void fold_axis1_tile(int tile, FoldGeom G, const doub
     constexpr int THREADS = NLN * P;
     constexpr bool STAGED = NLN >= 8 && L >= 32 && THREADS % L == 0;
     constexpr int PITCH = L + 1;
-    __shared__ long long rowbase_s[NLN];  // HBM offset of each line of the tile
-    if (tid < NLN) rowbase_s[tid] = rowb;  // thread tid owns line ln = tid
+    __shared__ long long rowbase_s[NLN];  // HBM offset each line of the tile is read from
+    __shared__ bool mir_s[NLN];           // line read as a conjugate mirror (not stored)
+    if (tid < NLN) {                      // thread tid owns line ln = tid
+        rowbase_s[tid] = rowb_rd;
+        mir_s[tid] = mir;
+    }
     __syncthreads();
     auto row_base = [&](int j) { return rowbase_s[j]; };
     double2 v[R];
@@ -329,6 +336,7 @@ __device__ __forceinline__ void fold_axis1_tile(int tile, FoldGeom G, const doub
             for (int k = 0; k < R; ++k) {
                 const int e = tid + THREADS * k, j = e / L, q = e % L;
                 v[k] = W[row_base(j) + q];
+                if (mir_s[j]) v[k].y = -v[k].y;
             }
 #pragma unroll
             for (int k = 0; k < R; ++k) {
@@ -341,7 +349,10 @@ __device__ __forceinline__ void fold_axis1_tile(int tile, FoldGeom G, const doub
             __syncthreads();
         } else {
 #pragma unroll
-            for (int r = 0; r < R; ++r) v[r] = W[rowb + t + P * r];
+            for (int r = 0; r < R; ++r) {
+                v[r] = W[rowb_rd + t + P * r];
+                if (mir) v[r].y = -v[r].y;
+            }
         }
         fftc::stockham<L, false, decltype(sidx), RM>(v, t, sm, sidx, tw);
         fftc::to_natural<L, RM>(v);
@@ -474,7 +485,7 @@ __device__ __forceinline__ void fold_axis1_tile(int tile, FoldGeom G, const doub
 folded:
     __syncthreads();
     fftc::stockham<L, true, decltype(sidx), RM>(v, t, sm, sidx, tw);
-    double2* dst = TV ? W : out;
+    double2* dst = (TV && out == nullptr) ? W : out;  // TV: in place unless a separate output is given
     if constexpr (STAGED) {
 #pragma unroll
         for (int j = 0; j < R; ++j) sm[ln * PITCH + Pl::out_q(t, j)] = v[j];
@@ -482,9 +493,9 @@ folded:
 #pragma unroll
         for (int k = 0; k < R; ++k) {
             const int e = tid + THREADS * k, j = e / L, q = e % L;
-            dst[row_base(j) + q] = sm[j * PITCH + q];
+            if (!mir_s[j]) dst[row_base(j) + q] = sm[j * PITCH + q];
         }
-    } else {
+    } else if (!mir) {
 #pragma unroll
         for (int j = 0; j < R; ++j) dst[rowb + Pl::out_q(t, j)] = v[j];
     }
@@ -715,11 +726,11 @@ size_t tv_sandwich1_blocks(const FoldGeom& G) {
 
 void launch_tv_sandwich1(const FoldGeom& G, const double2* Yl, const double2* lam, double2* W,
                          const GammaTables& tabs, double mu, double fwd_scale, double* fit_partials,
-                         cudaStream_t st, const SepTables& sep) {
+                         cudaStream_t st, const SepTables& sep, double2* Wout) {
     const double shift = mu * (double)G.d, inv_mu = 1.0 / mu;
-    const bool ok = fit_partials ? dispatch_a1<true, true>(G, Yl, lam, sep, nullptr, nullptr, W, nullptr, tabs, mu, shift,
+    const bool ok = fit_partials ? dispatch_a1<true, true>(G, Yl, lam, sep, nullptr, nullptr, W, Wout, tabs, mu, shift,
                                                            inv_mu, fwd_scale, fit_partials, st)
-                                 : dispatch_a1<true, false>(G, Yl, lam, sep, nullptr, nullptr, W, nullptr, tabs, mu, shift,
+                                 : dispatch_a1<true, false>(G, Yl, lam, sep, nullptr, nullptr, W, Wout, tabs, mu, shift,
                                                             inv_mu, fwd_scale, nullptr, st);
     if (!ok) throw std::logic_error("launch_tv_sandwich1: unsupported geometry");
 }

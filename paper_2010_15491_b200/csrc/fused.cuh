@@ -42,8 +42,10 @@ void launch_tik_fold_ifft1(const FoldGeom& G, const double2* Yl, const double2* 
                            double2* out, double reg, cudaStream_t st, const SepTables& sep = SepTables{},
                            const double2* Zl = nullptr);
 size_t tv_sandwich1_blocks(const FoldGeom& G);
+// Wout (optional): write x̂ there instead of in place (required with
+// tabs.half3, where lines read other tiles' rows as conjugate mirrors).
 void launch_tv_sandwich1(const FoldGeom& G, const double2* Yl, const double2* lam, double2* W,
                          const GammaTables& tabs, double mu, double fwd_scale, double* fit_partials,
-                         cudaStream_t st, const SepTables& sep = SepTables{});
+                         cudaStream_t st, const SepTables& sep = SepTables{}, double2* Wout = nullptr);
 
 }  // namespace vsr
