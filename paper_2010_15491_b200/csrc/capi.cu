@@ -1497,7 +1497,9 @@ static vsr_tv* tv_build(vsr_ctx* ctx, const Spec& sp, const double* y_dev, const
                      tv_sandwich1_blocks(h->G)),
             1));
         h->stp.alloc(kStencilVals * h->st_blocks);
-        h->resp.alloc(2 * std::max<size_t>(std::max(h->res_blocks, fft_engine().pass_blocks(hr, 2)), 1));
+        h->resp.alloc(2 * std::max<size_t>(std::max(std::max(h->res_blocks, fft_engine().pass_blocks(hr, 2)),
+                                                    fft_engine().half3_blocks(hr)),
+                                           1));
         h->bad.alloc(1);
         h->obj.alloc(h->max_iters);
         h->res.alloc(h->max_iters);
@@ -1637,7 +1639,9 @@ static void tv_step(vsr_tv* h) {
         launch_tv_finalize((int)h->iters_done, h->fitp.p,
                            a1 ? tv_sandwich1_blocks(h->G) : (fused ? tv_sandwich_blocks(h->G) : h->fit_blocks),
                            h->stp.p, h->st_blocks, h->resp.p,
-                           a1 ? fft_engine().pass_blocks(hr, 2) : h->res_blocks, h->lambda, 1e-8, sc, nullptr,
+                           half ? fft_engine().half3_blocks(hr)
+                                : (a1 ? fft_engine().pass_blocks(hr, 2) : h->res_blocks),
+                           h->lambda, 1e-8, sc, nullptr,
                            st);
     }
     ++h->iters_done;

@@ -137,6 +137,149 @@ __global__ void __launch_bounds__(PassShape<L, R, T, TG, CONTIG>::THREADS)
     }
 }
 
+// ------------------------------------------------- paired real lines (axis 3)
+// Two adjacent real columns (c, c + 1) of a strided axis form one complex line
+// z = x_c + i x_{c+1}: one complex FFT serves both (a double2 load is the pair).
+//   forward: X_c[k] = (Z[k] + conj Z[L-k]) / 2, X_{c+1}[k] = (Z[k] - conj Z[L-k]) / 2i,
+//            stored for k <= L/2 (Hermitian half spectrum along the axis)
+//   inverse: Z[k] = X_c[k] + i X_{c+1}[k] (k > L/2 from conj X[L-k]); the real and
+//            imaginary parts of IDFT(Z) are the two real columns.
+// A CTA owns one tile of T = 8 columns (4 pairs), full lines.
+template <int L>
+struct RPairShape {
+    using Pl = fftc::Plan<L>;
+    // 16 real columns per tile: 128-byte row segments in the real domain
+    static constexpr int R = Pl::R, P = Pl::P, T = L >= 1024 ? 8 : 16, TP = T / 2;
+    static constexpr int TG = (TP * P) >= 128 ? 1 : 128 / (TP * P);  // tiles per CTA
+    static constexpr int THREADS = TG * TP * P;
+    static constexpr int SMEM = TG * TP * L;
+};
+
+template <int L>
+__global__ void __launch_bounds__(RPairShape<L>::THREADS)
+    rpair_fwd_kernel(const double* __restrict__ in, double2* __restrict__ out, long long S, long long tiles,
+                     const double2* __restrict__ tw) {
+    using Sh = RPairShape<L>;
+    constexpr int R = Sh::R, P = Sh::P, T = Sh::T, TP = Sh::TP;
+    extern __shared__ double2 sm[];
+    const int tid = threadIdx.x, g = tid / (TP * P), rem = tid % (TP * P), lp = rem % TP, t = rem / TP;
+    const long long tile = (long long)blockIdx.x * Sh::TG + g;
+    const bool active = tile < tiles;
+    const long long tpo = S / T, o = active ? tile / tpo : 0, c = active ? (tile % tpo) * T + 2 * lp : 0;
+    auto sidx = [&](int q) { return g * (L * TP) + q * TP + lp; };
+    const double2* src = reinterpret_cast<const double2*>(in + c + S * (long long)L * o);
+    const long long S2 = S / 2;
+    double2 v[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[r] = active ? __ldg(src + S2 * (t + P * r)) : make_double2(0.0, 0.0);
+    fftc::stockham<L, false>(v, t, sm, sidx, tw);
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < R; ++j) sm[sidx(fftc::Plan<L>::out_q(t, j))] = v[j];
+    __syncthreads();
+    double2* dst = out + c + S * (long long)(L / 2 + 1) * o;
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+        const int k = t + P * j;
+        if (k > L / 2 || !active) continue;
+        const double2 a = sm[sidx(k)], b = sm[sidx((L - k) & (L - 1))];
+        const double2 xa = make_double2(0.5 * (a.x + b.x), 0.5 * (a.y - b.y));
+        const double2 xb = make_double2(0.5 * (a.y + b.y), -0.5 * (a.x - b.x));
+        double2* d = dst + S * k;
+        d[0] = xa;
+        d[1] = xb;
+    }
+}
+
+template <int L>
+__global__ void __launch_bounds__(RPairShape<L>::THREADS)
+    rpair_inv_kernel(const double2* __restrict__ in, double* __restrict__ out, long long S, long long tiles,
+                     const double2* __restrict__ tw, double scale, double* __restrict__ partials,
+                     unsigned long long* __restrict__ bad_index) {
+    using Sh = RPairShape<L>;
+    constexpr int R = Sh::R, P = Sh::P, T = Sh::T, TP = Sh::TP;
+    extern __shared__ double2 sm[];
+    const int tid = threadIdx.x, g = tid / (TP * P), rem = tid % (TP * P), lp = rem % TP, t = rem / TP;
+    const long long tile = (long long)blockIdx.x * Sh::TG + g;
+    const bool active = tile < tiles;
+    const long long tpo = S / T, o = active ? tile / tpo : 0, c = active ? (tile % tpo) * T + 2 * lp : 0;
+    auto sidx = [&](int q) { return g * (L * TP) + q * TP + lp; };
+    const double2* src = in + c + S * (long long)(L / 2 + 1) * o;
+    double2 v[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int q = t + P * r;
+        const bool lo = q <= L / 2;
+        const double2* p = src + S * (lo ? q : L - q);
+        double2 A = active ? __ldg(p) : make_double2(0.0, 0.0), B = active ? __ldg(p + 1) : make_double2(0.0, 0.0);
+        if (!lo) A.y = -A.y, B.y = -B.y;
+        v[r] = make_double2(A.x - B.y, A.y + B.x);  // A + i B
+    }
+    fftc::stockham<L, true>(v, t, sm, sidx, tw);
+    double2* dst = reinterpret_cast<double2*>(out + c + S * (long long)L * o);
+    const long long S2 = S / 2;
+    double acc = 0.0;
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+        const int q = fftc::Plan<L>::out_q(t, j);
+        const double2 z = cscale(v[j], scale);
+        if (!active) continue;
+        acc += z.x * z.x + z.y * z.y;
+        dst[S2 * q] = z;
+        if (!isfinite(z.x) || !isfinite(z.y)) {
+            const unsigned long long e = (unsigned long long)(c + S * (long long)L * o + S * (long long)q);
+            atomicMin(bad_index, isfinite(z.x) ? e + 1 : e);
+        }
+    }
+    if (partials) {
+        __shared__ double red[64];
+        double vals[2] = {0.0, acc};  // the pair is real by construction: no imaginary residue
+        block_reduce_sum<2>(vals, red);
+        if (tid == 0) {
+            partials[2 * blockIdx.x] = vals[0];
+            partials[2 * blockIdx.x + 1] = vals[1];
+        }
+    }
+}
+
+template <int L>
+bool launch_rpair(bool fwd, const void* in, void* out, long long S, long long total, const double2* tw,
+                  double scale, const PassReduce* red, cudaStream_t st) {
+    using Sh = RPairShape<L>;
+    const long long tiles = total / ((long long)Sh::T * L);
+    const unsigned blocks = (unsigned)((tiles + Sh::TG - 1) / Sh::TG);
+    const size_t smem = (size_t)Sh::SMEM * sizeof(double2);
+    if (fwd) {
+        auto kern = rpair_fwd_kernel<L>;
+        if (smem > 48 * 1024) VSR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        kern<<<blocks, Sh::THREADS, smem, st>>>(static_cast<const double*>(in), static_cast<double2*>(out), S,
+                                                       tiles, tw);
+    } else {
+        auto kern = rpair_inv_kernel<L>;
+        if (smem > 48 * 1024) VSR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        kern<<<blocks, Sh::THREADS, smem, st>>>(static_cast<const double2*>(in), static_cast<double*>(out), S,
+                                                       tiles, tw, scale, red ? red->partials : nullptr,
+                                                       red ? red->bad_index : nullptr);
+    }
+    VSR_LAUNCH_CHECK();
+    return true;
+}
+
+bool dispatch_rpair(bool fwd, size_t L, const void* in, void* out, long long S, long long total, const double2* tw,
+                    double scale, const PassReduce* red, cudaStream_t st) {
+    switch (L) {
+        case 8: return launch_rpair<8>(fwd, in, out, S, total, tw, scale, red, st);
+        case 16: return launch_rpair<16>(fwd, in, out, S, total, tw, scale, red, st);
+        case 32: return launch_rpair<32>(fwd, in, out, S, total, tw, scale, red, st);
+        case 64: return launch_rpair<64>(fwd, in, out, S, total, tw, scale, red, st);
+        case 128: return launch_rpair<128>(fwd, in, out, S, total, tw, scale, red, st);
+        case 256: return launch_rpair<256>(fwd, in, out, S, total, tw, scale, red, st);
+        case 512: return launch_rpair<512>(fwd, in, out, S, total, tw, scale, red, st);
+        case 1024: return launch_rpair<1024>(fwd, in, out, S, total, tw, scale, red, st);
+        default: return false;
+    }
+}
+
 // ------------------------------------------------------------ generic DFT
 // Direct O(L) per output DFT along one axis for any L (non powers of two,
 // L = 1, and strided shapes the tiled kernel cannot cover).  One thread per
@@ -403,15 +546,21 @@ void FftEngine::axis_pass(const Dims& d, int axis, bool inverse, const void* in,
 }
 
 bool FftEngine::half3_ok(const Dims& d) const {
-    return d.s >= 4 && tiled_ok(d.s, 2, (long long)(d.m * d.n));
+    return d.s >= 8 && d.s <= 1024 && is_pow2(d.s) && (d.m * d.n) % 16 == 0;
+}
+
+size_t FftEngine::half3_blocks(const Dims& d) const {
+    const size_t T = d.s >= 1024 ? 8 : 16;
+    const size_t P = d.s < 16 ? 1 : d.s / 16, tp = (T / 2) * P;
+    const size_t tg = tp >= 128 ? 1 : 128 / tp;
+    return (d.count() / (T * d.s) + tg - 1) / tg;
 }
 
 void FftEngine::r2c_axis3_half(const Dims& d, const double* in, double2* out, cudaStream_t st) {
     long long S, L, total;
     axis_geometry(d, 2, S, L, total);
     if (!half3_ok(d)) throw std::logic_error("r2c_axis3_half: unsupported geometry");
-    const long long units = pass_units<false>(L, S, total);
-    if (!dispatch_L<false, false, IN_REAL, OUT_HALF>(L, S, units, in, out, twiddles((size_t)L), 1.0, nullptr, st))
+    if (!dispatch_rpair(true, (size_t)L, in, out, S, total, twiddles((size_t)L), 1.0, nullptr, st))
         throw std::logic_error("r2c_axis3_half: unsupported length");
 }
 
@@ -420,8 +569,7 @@ void FftEngine::c2r_axis3_half(const Dims& d, const double2* in, double* out, do
     long long S, L, total;
     axis_geometry(d, 2, S, L, total);
     if (!half3_ok(d)) throw std::logic_error("c2r_axis3_half: unsupported geometry");
-    const long long units = pass_units<false>(L, S, total);
-    if (!dispatch_L<false, true, IN_HALF, OUT_REAL>(L, S, units, in, out, twiddles((size_t)L), scale, red, st))
+    if (!dispatch_rpair(false, (size_t)L, in, out, S, total, twiddles((size_t)L), scale, red, st))
         throw std::logic_error("c2r_axis3_half: unsupported length");
 }
 

@@ -66,6 +66,7 @@ public:
     // (m, n, s/2+1) array): forward r2c of a real volume, and the inverse c2r
     // (+ residue reduction) once axes 1 and 2 are back in the spatial domain.
     bool half3_ok(const Dims& d) const;
+    size_t half3_blocks(const Dims& d) const;  // blocks (residue partials) of c2r_axis3_half
     void r2c_axis3_half(const Dims& d, const double* in, double2* out, cudaStream_t st);
     void c2r_axis3_half(const Dims& d, const double2* in, double* out, double scale, const PassReduce* red,
                         cudaStream_t st);
