@@ -518,28 +518,36 @@ void launch_finalize_sum(const double* partials, int stride, int nvals, size_t n
 }
 
 namespace {
-__global__ void sep_dev_kernel(long long m, long long n, long long N, const double2* __restrict__ lam,
-                               unsigned long long* __restrict__ dev_bits, unsigned long long* __restrict__ mag_bits) {
-    const long long f = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+__global__ void __launch_bounds__(256) sep_dev_kernel(long long m, long long n, long long N,
+                                                      const double2* __restrict__ lam,
+                                                      unsigned long long* __restrict__ dev_bits,
+                                                      unsigned long long* __restrict__ mag_bits) {
+    // grid-stride max of |lam L0^2 - a b c| and |lam|; one atomic per block
+    // (non-negative doubles order like their bit patterns)
+    const double2 L0 = lam[0];
+    const double2 L02 = cmul(L0, L0);
     double dev = 0.0, mag = 0.0;
-    if (f < N) {
-        const long long f1 = f % m, f2 = (f / m) % n, f3 = f / (m * n);
-        const double2 L0 = lam[0];
-        const double2 l = lam[f];
-        const double2 lhs = cmul(l, cmul(L0, L0));
-        const double2 rhs = cmul(cmul(lam[f1], lam[m * f2]), lam[m * n * f3]);
-        const double2 d = csub(lhs, rhs);
-        dev = sqrt(cnorm(d));
-        mag = sqrt(cnorm(l));
+    const long long mn = m * n;
+    for (long long f = (long long)blockIdx.x * blockDim.x + threadIdx.x; f < N;
+         f += (long long)gridDim.x * blockDim.x) {
+        const long long f3 = f / mn, r = f - f3 * mn, f2 = r / m, f1 = r - f2 * m;
+        const double2 l = __ldg(lam + f);
+        const double2 rhs = cmul(cmul(__ldg(lam + f1), __ldg(lam + m * f2)), __ldg(lam + mn * f3));
+        dev = fmax(dev, cnorm(csub(cmul(l, L02), rhs)));
+        mag = fmax(mag, cnorm(l));
     }
-    // non-negative doubles order like their bit patterns
     for (int o = 16; o > 0; o >>= 1) {
         dev = fmax(dev, __shfl_down_sync(0xffffffffu, dev, o));
         mag = fmax(mag, __shfl_down_sync(0xffffffffu, mag, o));
     }
-    if ((threadIdx.x & 31) == 0) {
-        atomicMax(dev_bits, (unsigned long long)__double_as_longlong(dev));
-        atomicMax(mag_bits, (unsigned long long)__double_as_longlong(mag));
+    __shared__ double sd[8], smg[8];
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) sd[w] = dev, smg[w] = mag;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int i = 1; i < (int)(blockDim.x >> 5); ++i) dev = fmax(dev, sd[i]), mag = fmax(mag, smg[i]);
+        atomicMax(dev_bits, (unsigned long long)__double_as_longlong(sqrt(dev)));
+        atomicMax(mag_bits, (unsigned long long)__double_as_longlong(sqrt(mag)));
     }
 }
 
@@ -565,8 +573,8 @@ bool detect_separable(const Dims& hr, const double2* lam, double2* a, double2* b
     unsigned long long* bits = nullptr;
     VSR_CUDA(cudaMallocAsync(&bits, 2 * sizeof(unsigned long long), st));
     VSR_CUDA(cudaMemsetAsync(bits, 0, 2 * sizeof(unsigned long long), st));
-    sep_dev_kernel<<<(unsigned)((N + 255) / 256), 256, 0, st>>>((long long)hr.m, (long long)hr.n, N, lam, bits,
-                                                              bits + 1);
+    sep_dev_kernel<<<(unsigned)std::min<long long>((N + 255) / 256, 148LL * 8), 256, 0, st>>>(
+        (long long)hr.m, (long long)hr.n, N, lam, bits, bits + 1);
     VSR_LAUNCH_CHECK();
     unsigned long long h[2];
     VSR_CUDA(cudaMemcpyAsync(h, bits, sizeof(h), cudaMemcpyDeviceToHost, st));
