@@ -307,6 +307,27 @@ __device__ __forceinline__ void fold_axis1_tile(int tile, FoldGeom G, const doub
     // half-spectrum W (tabs.half3): rows past the Nyquist plane are mirrors
     const bool mir = TV && tabs.half3 && 2 * f3 > G.s;
     const long long rowb_rd = mir ? G.m * ((G.n - f2) % G.n + G.n * (G.s - f3)) : rowb;
+    // Mirror pairing (half3, one LR column per tile): the alias set of LR
+    // (g2, g3) and that of (-g2, -g3) give conjugate rows, so only one of the
+    // pair runs (role 1) and also stores the other's rows, conjugated; a
+    // self-mirror set (role 0) stores its direct rows; role 2 returns at once.
+    int role = 0;
+    if (TV && tabs.half3 && T == 1) {
+        const long long mg2 = (G.nl - bx2) % G.nl, mg3 = (G.sl - bx3) % G.sl;
+        if (mg2 == bx2 && mg3 == bx3)
+            role = 0;
+        else if (bx3 < mg3 || (bx3 == mg3 && bx2 < mg2))
+            role = 1;
+        else
+            role = 2;
+    }
+    if (role == 2) {
+        if (FIT && tid == 0) fit_partials[tile] = 0.0;
+        return;
+    }
+    // second copy of a row on the Nyquist/zero planes (its mirror is also <= s/2)
+    const long long mrow = G.m * ((G.n - f2) % G.n + G.n * f3);
+    const long long sec = (role == 1 && !mir && (f3 == 0 || 2 * f3 == G.s) && mrow != rowb) ? mrow : -1;
     // line-interleaved: a quarter-warp (8 lines at one position) is one 128-B row
     auto sidx = [&](int q) { return q * NLN + ln; };
     // Staged HBM I/O: whole rows move through shared memory (pitch L + 1, bank-
@@ -316,10 +337,12 @@ __device__ __forceinline__ void fold_axis1_tile(int tile, FoldGeom G, const doub
     constexpr bool STAGED = NLN >= 8 && L >= 32 && THREADS % L == 0;
     constexpr int PITCH = L + 1;
     __shared__ long long rowbase_s[NLN];  // HBM offset each line of the tile is read from
-    __shared__ bool mir_s[NLN];           // line read as a conjugate mirror (not stored)
+    __shared__ bool mir_s[NLN];           // line read as a conjugate mirror
+    __shared__ long long sec_s[NLN];      // extra conjugate copy location, -1 if none
     if (tid < NLN) {                      // thread tid owns line ln = tid
         rowbase_s[tid] = rowb_rd;
         mir_s[tid] = mir;
+        sec_s[tid] = sec;
     }
     __syncthreads();
     auto row_base = [&](int j) { return rowbase_s[j]; };
@@ -493,12 +516,25 @@ folded:
 #pragma unroll
         for (int k = 0; k < R; ++k) {
             const int e = tid + THREADS * k, j = e / L, q = e % L;
-            if (!mir_s[j]) dst[row_base(j) + q] = sm[j * PITCH + q];
+            const double2 val = sm[j * PITCH + q];
+            if (!mir_s[j])
+                dst[row_base(j) + q] = val;
+            else if (role == 1)
+                dst[row_base(j) + q] = make_double2(val.x, -val.y);
+            if (sec_s[j] >= 0) dst[sec_s[j] + q] = make_double2(val.x, -val.y);
         }
-    } else if (!mir) {
+    } else {
 #pragma unroll
-        for (int j = 0; j < R; ++j) dst[rowb + Pl::out_q(t, j)] = v[j];
+        for (int j = 0; j < R; ++j) {
+            const double2 val = v[j];
+            if (!mir)
+                dst[rowb + Pl::out_q(t, j)] = val;
+            else if (role == 1)
+                dst[rowb_rd + Pl::out_q(t, j)] = make_double2(val.x, -val.y);
+            if (sec >= 0) dst[sec + Pl::out_q(t, j)] = make_double2(val.x, -val.y);
+        }
     }
+    if (role == 1) fit *= 2.0;  // the skipped mirror set has the same |residual|^2
     if constexpr (FIT) {
         __shared__ double red[32];
         double vv[1] = {fit};
