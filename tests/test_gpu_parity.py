@@ -360,7 +360,9 @@ def test_objective_tv(V, O):
 # ------------------------------------------------------------------ ADMM-TV
 TV_CASES = [((8, 8, 8), (2, 2, 2), 6), ((16, 16, 16), (4, 4, 4), 10), ((32, 32, 16), (2, 2, 4), 8),
             ((12, 10, 8), (2, 2, 2), 5), ((64, 64, 64), (4, 4, 4), 12), ((40, 24, 16), (2, 2, 2), 5),
-            ((32, 32, 64), (2, 2, 4), 6), ((64, 32, 128), (2, 2, 2), 4), ((32, 32, 32), (1, 1, 1), 4)]
+            ((32, 32, 64), (2, 2, 4), 6), ((64, 32, 128), (2, 2, 2), 4), ((32, 32, 32), (1, 1, 1), 4),
+            # half-spectrum mirror pairing: nl not a power of two, and sl = 4 (self-mirror planes 0, 2)
+            ((64, 48, 32), (4, 4, 4), 5), ((64, 64, 16), (4, 4, 4), 5), ((128, 64, 32), (4, 4, 2), 4)]
 
 
 @pytest.mark.parametrize("dims,rates,iters", TV_CASES)
