@@ -344,7 +344,7 @@ __global__ void __launch_bounds__(SP_THREADS, (DM <= 8 ? 8 : 6)) spatial_expand_
     }
 }
 
-static const int kDms[] = {4, 8, 12, 16};
+static const int kDms[] = {4, 5, 7, 8, 12, 16};  // 5, 7: the 9- and 13-tap PSFs at rate 2
 
 // DM (padded taps per phase) serving every axis, 0 if the support is too wide.
 static int pick_dm(const SpatialPlan& p) {
@@ -410,6 +410,8 @@ void launch_spatial_expand(const Dims& hr, const int rates[3], const SpatialPlan
     const dim3 blocks((unsigned)A.tiles1, (unsigned)A.tiles2, (unsigned)tiles3);
     switch (dm) {
         case 4: launch_expand_dm<4>(A, smem, blocks, st); break;
+        case 5: launch_expand_dm<5>(A, smem, blocks, st); break;
+        case 7: launch_expand_dm<7>(A, smem, blocks, st); break;
         case 8: launch_expand_dm<8>(A, smem, blocks, st); break;
         case 12: launch_expand_dm<12>(A, smem, blocks, st); break;
         default: launch_expand_dm<16>(A, smem, blocks, st); break;
