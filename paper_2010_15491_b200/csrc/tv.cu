@@ -346,10 +346,12 @@ __global__ void __launch_bounds__(STH)
         for (int q = 0; q < 2; ++q)
             if (da[q]) rdv[q] = __ldg(reinterpret_cast<const double2*>(dnext + zd + doff[q]));
     }
-    // halo work spread over all warps: lanes 0..4 of each warp take 5 of the 40 points
+    // halo points (rho_x at ii = -1 for TY rows, rho_y at jj = -1 for TX columns)
+    // packed into whole warps: warp 0 takes the TX row points, warp 1 the TY
+    // column points, so the other warps skip the halo shrink entirely
     const int lane = tid & 31, warp = tid >> 5;
-    const int hslot = warp * 5 + lane;  // valid when lane < 5
-    const bool hwork = lane < 5 && hslot < TY + TX;
+    const int hslot = warp == 0 ? TY + lane : (warp == 1 && lane < TY ? lane : -1);
+    const bool hwork = hslot >= 0 && hslot < TY + TX;
     const int hii = hslot < TY ? -1 : hslot - TY;
     const int hjj = hslot < TY ? hslot : -1;
     const int hx = (hjj + 1) * FXW + hii + 2;
