@@ -481,6 +481,9 @@ print("ok", op.path())
     ({"VSR_LR_PLANE": "1"}, (128, 128, 32), (2, 2, 2)),
     ({"VSR_LR_PLANE": "1"}, (256, 256, 16), (2, 2, 2)),
     ({"VSR_NO_HALF": "1"}, (64, 64, 32), (2, 2, 2)),
+    ({"VSR_LR_PERSIST": "1"}, (64, 128, 64), (2, 2, 2)),
+    ({"VSR_LR_PERSIST": "1"}, (128, 128, 128), (2, 2, 2)),
+    ({"VSR_TV_FULL": "1"}, (64, 64, 64), (4, 4, 4)),
     ({"VSR_NO_SPATIAL": "1"}, (64, 64, 32), (2, 2, 2)),
     ({"VSR_NO_GRAPH": "1"}, (64, 64, 32), (2, 2, 2)),
     ({"VSR_A1_RM": "8"}, (64, 64, 64), (4, 4, 4)),
