@@ -31,6 +31,16 @@ struct FShape {
 // xor-butterfly over the A alias lanes (lane stride T): every lane ends with
 // the bit-identical total (fp addition is commutative, so each level combines
 // identical operand pairs on both partners).
+// 1/x for finite x > 0 (Gamma denominators): MUFU.RCP64H seed and two Newton
+// steps (~1 ulp), branch-free unlike the IEEE division sequence.
+__device__ __forceinline__ double fast_rcp(double x) {
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    y = y * fma(-x, y, 2.0);
+    y = y * fma(-x, y, 2.0);
+    return y;
+}
+
 template <int T, int A>
 __device__ __forceinline__ double lanes_sum(double v) {
 #pragma unroll
@@ -306,14 +316,15 @@ __device__ __forceinline__ void fold_axis1_tile(int tile, FoldGeom G, const doub
     const long long rowb = G.m * (f2 + G.n * f3);
     // half-spectrum W (tabs.half3): rows past the Nyquist plane are mirrors
     const bool mir = TV && tabs.half3 && 2 * f3 > G.s;
-    const long long rowb_rd = mir ? G.m * ((G.n - f2) % G.n + G.n * (G.s - f3)) : rowb;
+    const long long nf2 = f2 == 0 ? 0 : G.n - f2;  // -f2 mod n (0 <= f2 < n)
+    const long long rowb_rd = mir ? G.m * (nf2 + G.n * (G.s - f3)) : rowb;
     // Mirror pairing (half3, one LR column per tile): the alias set of LR
     // (g2, g3) and that of (-g2, -g3) give conjugate rows, so only one of the
     // pair runs (role 1) and also stores the other's rows, conjugated; a
     // self-mirror set (role 0) stores its direct rows; role 2 returns at once.
     int role = 0;
     if (TV && tabs.half3 && T == 1) {
-        const long long mg2 = (G.nl - bx2) % G.nl, mg3 = (G.sl - bx3) % G.sl;
+        const int mg2 = bx2 == 0 ? 0 : (int)G.nl - bx2, mg3 = bx3 == 0 ? 0 : (int)G.sl - bx3;
         if (mg2 == bx2 && mg3 == bx3)
             role = 0;
         else if (bx3 < mg3 || (bx3 == mg3 && bx2 < mg2))
@@ -326,7 +337,7 @@ __device__ __forceinline__ void fold_axis1_tile(int tile, FoldGeom G, const doub
         return;
     }
     // second copy of a row on the Nyquist/zero planes (its mirror is also <= s/2)
-    const long long mrow = G.m * ((G.n - f2) % G.n + G.n * f3);
+    const long long mrow = G.m * (nf2 + G.n * f3);
     const long long sec = (role == 1 && !mir && (f3 == 0 || 2 * f3 == G.s) && mrow != rowb) ? mrow : -1;
     // line-interleaved: a quarter-warp (8 lines at one position) is one 128-B row
     auto sidx = [&](int q) { return q * NLN + ln; };
@@ -424,7 +435,7 @@ __device__ __forceinline__ void fold_axis1_tile(int tile, FoldGeom G, const doub
                 for (int br = 0; br < DR; ++br) {
                     const int r = rr + RD * br;
                     const double2 Lr = sm[sidx(t + P * r)];
-                    Gg[br] = 1.0 / ((__ldg(tabs.nr + (t + P * r)) + base_g) + tabs.tau);
+                    Gg[br] = fast_rcp((__ldg(tabs.nr + (t + P * r)) + base_g) + tabs.tau);
                     v[r] = cscale(cadd(cmulc(Lr, yv), cscale(v[r], cA)), Gg[br]);
                     const double2 pr = cmul(Lr, v[r]);
                     Sx += pr.x;
@@ -432,8 +443,8 @@ __device__ __forceinline__ void fold_axis1_tile(int tile, FoldGeom G, const doub
                 }
                 Sx = lanes_sum<1, A>(Sx);
                 Sy = lanes_sum<1, A>(Sy);
-                const double den = gwv[rr] + shift;
-                const double2 w = make_double2(Sx / den, Sy / den);
+                const double iden = fast_rcp(gwv[rr] + shift);
+                const double2 w = make_double2(Sx * iden, Sy * iden);
 #pragma unroll
                 for (int br = 0; br < DR; ++br) {
                     const int r = rr + RD * br;
