@@ -224,7 +224,6 @@ STAGE_BYTES = {
     # half-spectrum LR stage (pitch ~ ml/2 + 8 complex per row: ~9 bytes per LR point per complex pass)
     "lr_r2c_axis1": (0, 17), "lr_fft_axis2_half": (0, 18), "lr_filter_axis3_half": (0, 18),
     "lr_ifft_axis2_half": (0, 18), "lr_c2r_axis1": (0, 25),
-    "lr_plane_r2c_axis12": (0, 17), "lr_plane_axis21_c2r": (0, 25),
 }
 
 
@@ -374,7 +373,7 @@ def run_b200(args, rank, world, local):
                          "reference_algorithm_equiv_frac": path_bytes / (ms * 1e-3) / 1e9 / hbm,
                          "note": "alg_bytes_per_step sums the stages this path runs; with a separable compact "
                                  "PSF and the CLI-default lattice prior the solve is x = xbar + sqrt(d) H^T D^H "
-                                 "F_l^-1(U) with the LR stage on the Hermitian half spectrum: 8 N + 76 N_l bytes (planes in smem)"}}
+                                 "F_l^-1(U) with the LR stage on the Hermitian half spectrum: 8 N + 112 N_l bytes"}}
     if spatial and not args.no_fft_path:
         roofline["path"]["fft_path_ms"] = tik_fft_path_ms(args, ctx, V, spec, lam_d, cfg, xbar_d, y_d, x_d,
                                                            stream, torch, flush)

@@ -20,7 +20,6 @@
 #include "fused.cuh"
 #include "spatial.cuh"
 #include "rfft.cuh"
-#include "lrstage.cuh"
 #include "chain.cuh"
 #include "tv.cuh"
 
@@ -1059,39 +1058,7 @@ static void tik_enqueue(vsr_tikhonov* t, const double* y_dev, double* x_dev) {
         const Dims& lr = t->sp.lr;
         const Dims lrh{(size_t)half_pitch(lr.m), lr.n, lr.s};
         const long long rows = (long long)(lr.n * lr.s);
-        // whole-plane smem kernels: opt-in (VSR_LR_PLANE=1) - one CTA per plane
-        // leaves them latency-bound (29.6 us vs 28 us for the two row/column kernels)
-        static const bool use_plane = [] {
-            const char* e = std::getenv("VSR_LR_PLANE");
-            return e && e[0] == '1';
-        }();
-        const bool plane = use_plane && lr_plane_ok(lr.m, lr.n);
-        // one cooperative launch for the five LR steps: opt-in (VSR_LR_PERSIST=1);
-        // at 128^3 it measured 61.5 us vs ~55 us for the five graph-replayed kernels
-        static const bool persist = [] {
-            const char* e = std::getenv("VSR_LR_PERSIST");
-            return e && e[0] == '1';
-        }();
-        if (persist && lr_stage_ok(lr)) {
-            // the five LR steps in one cooperative launch
-            {
-                ProfScope ps(prof, "lr_stage_persistent", st);
-                const double dd = (double)t->sp.rate();
-                launch_lr_stage(lr, y_dev, t->Yl.p, t->u.p, t->q.p, t->spl.s2[0], t->spl.s2[1], t->spl.s2[2],
-                                dd / (double)lr.count(), 2.0 * t->reg * dd, st);
-            }
-            ++g_fwd;
-            ++g_inv;
-            {
-                ProfScope ps(prof, "spatial_expand", st);
-                launch_spatial_expand(t->sp.hr, t->sp.rates, t->spl, t->u.p, t->zlat.p, 1.0, x_dev, t->bad.p, st);
-            }
-            return;
-        }
-        if (plane) {
-            ProfScope ps(prof, "lr_plane_r2c_axis12", st);
-            lr_plane_forward(lr.m, lr.n, y_dev, t->Yl.p, (long long)lr.s, st);
-        } else {
+        {
             {
                 ProfScope ps(prof, "lr_r2c_axis1", st);
                 rfft_rows_forward(lr.m, y_dev, t->Yl.p, rows, st);
@@ -1105,10 +1072,7 @@ static void tik_enqueue(vsr_tikhonov* t, const double* y_dev, double* x_dev) {
             launch_spatial_sandwich(lrh, t->sp.rate(), t->spl, t->Yl.p, nullptr, t->reg, inv_sqrt_count(lr),
                                     inv_sqrt_count(lr) * std::sqrt((double)t->sp.rate()), st);
         }
-        if (plane) {
-            ProfScope ps(prof, "lr_plane_axis21_c2r", st);
-            lr_plane_inverse(lr.m, lr.n, t->Yl.p, t->u.p, (long long)lr.s, 1.0, t->q.p, st);
-        } else {
+        {
             {
                 ProfScope ps(prof, "lr_ifft_axis2_half", st);
                 fft_engine().axis_pass(lrh, 1, true, t->Yl.p, IN_COMPLEX, t->Yl.p, OUT_COMPLEX, 1.0, nullptr, st);

@@ -135,190 +135,6 @@ void launch_c2r(const double2* X, double* x, long long rows, int Mp, double scal
     VSR_LAUNCH_CHECK();
 }
 
-// ------------------------------------------------------------ plane kernels
-// One CTA per z-plane of an LR volume (NY rows of length L = 2M): the row
-// r2c transform and the axis-2 (column) transform of the half spectrum run
-// back to back in shared memory, so the intermediate never touches L2/HBM.
-// The plane lives in smem as NY rows x PITCH = M + 1 (odd: column accesses
-// are bank-conflict free); threads without a row/column of their own point
-// their exchange slots at a scratch row.
-template <int M, int NY>
-struct PlaneShape {
-    using P1l = fftc::Plan<M>;
-    using P2l = fftc::Plan<NY>;
-    static constexpr int R1 = P1l::R, P1 = P1l::P, R2 = P2l::R, P2 = P2l::P;
-    static constexpr int PITCH = M + 1;
-    static constexpr int T1 = NY * P1;                         // row phase threads
-    static constexpr int COLS = (M + 1 + 3) / 4 * 4;
-    static constexpr int T2 = COLS * P2;                       // column phase threads
-    static constexpr int THREADS = ((T1 > T2 ? T1 : T2) + 31) / 32 * 32;
-    static constexpr int SCRATCH = (NY > M ? NY : M) + 1;
-    static constexpr int SMEM = NY * PITCH + SCRATCH;           // double2 elements
-};
-
-template <int M, int NY>
-__global__ void __launch_bounds__(PlaneShape<M, NY>::THREADS, 1)
-    lr_plane_fwd_kernel(const double* __restrict__ y, double2* __restrict__ Yh, int Mp,
-                        const double2* __restrict__ twM, const double2* __restrict__ twL,
-                        const double2* __restrict__ twN) {
-    using Sh = PlaneShape<M, NY>;
-    constexpr int R1 = Sh::R1, P1 = Sh::P1, R2 = Sh::R2, P2 = Sh::P2, PITCH = Sh::PITCH;
-    extern __shared__ double2 pl[];
-    double2* scratch = pl + NY * PITCH;
-    const int tid = threadIdx.x;
-    const long long plane = blockIdx.x;
-    // ---- rows: z = x[2n] + i x[2n+1], M-point FFT, Hermitian split
-    {
-        const int row = tid / P1, t = tid % P1;
-        const bool act = row < NY;
-        const double2* zr = reinterpret_cast<const double2*>(y) + (plane * NY + row) * M;
-        double2 v[R1];
-#pragma unroll
-        for (int r = 0; r < R1; ++r) v[r] = act ? __ldg(zr + t + P1 * r) : make_double2(0.0, 0.0);
-        fftc::stockham<M, false>(v, t, pl, [&](int q) { return act ? row * PITCH + q : (int)(scratch - pl) + (q % Sh::SCRATCH); }, twM);
-        __syncthreads();
-        if (act) {
-#pragma unroll
-            for (int j = 0; j < R1; ++j) pl[row * PITCH + fftc::Plan<M>::out_q(t, j)] = v[j];
-        }
-        __syncthreads();
-        if (act) {
-            double2* rz = pl + row * PITCH;
-            for (int k = t; k <= M / 2; k += P1) {
-                const double2 a = rz[k], b = rz[(M - k) & (M - 1)];
-                const double2 e = make_double2(0.5 * (a.x + b.x), 0.5 * (a.y - b.y));
-                const double2 o = make_double2(0.5 * (a.y + b.y), -0.5 * (a.x - b.x));
-                const double2 xk = cadd(e, cmul(__ldg(twL + k), o));
-                if (k == 0) {
-                    rz[0] = make_double2(a.x + a.y, 0.0);
-                    rz[M] = make_double2(a.x - a.y, 0.0);
-                } else if (2 * k == M) {
-                    rz[k] = xk;
-                } else {
-                    // X[M-k] = conj(E_k) + e^{-2 pi i (M-k)/L} conj(O_k)
-                    const double2 xm = cadd(make_double2(e.x, -e.y),
-                                            cmul(__ldg(twL + (M - k)), make_double2(o.x, -o.y)));
-                    rz[k] = xk;
-                    rz[M - k] = xm;
-                }
-            }
-        }
-        __syncthreads();
-    }
-    // ---- columns: NY-point FFT of each of the M + 1 columns, in place
-    {
-        const int col = tid / P2, t = tid % P2;
-        const bool act = col <= M;
-        double2 v[R2];
-#pragma unroll
-        for (int r = 0; r < R2; ++r) v[r] = act ? pl[(t + P2 * r) * PITCH + col] : make_double2(0.0, 0.0);
-        __syncthreads();
-        fftc::stockham<NY, false>(v, t, pl, [&](int q) { return act ? q * PITCH + col : (int)(scratch - pl) + (q % Sh::SCRATCH); }, twN);
-        __syncthreads();
-        if (act) {
-#pragma unroll
-            for (int j = 0; j < R2; ++j) pl[fftc::Plan<NY>::out_q(t, j) * PITCH + col] = v[j];
-        }
-        __syncthreads();
-    }
-    // ---- coalesced store of the half-spectrum plane (pad columns zero)
-    double2* out = Yh + plane * NY * Mp;
-    for (int e = tid; e < NY * Mp; e += Sh::THREADS) {
-        const int row = e / Mp, k = e - row * Mp;
-        out[e] = k <= M ? pl[row * PITCH + k] : make_double2(0.0, 0.0);
-    }
-}
-
-template <int M, int NY>
-__global__ void __launch_bounds__(PlaneShape<M, NY>::THREADS, 1)
-    lr_plane_inv_kernel(const double2* __restrict__ Yh, double* __restrict__ u, int Mp, double scale,
-                        const double* __restrict__ sub, const double2* __restrict__ twM,
-                        const double2* __restrict__ twL, const double2* __restrict__ twN) {
-    using Sh = PlaneShape<M, NY>;
-    constexpr int R1 = Sh::R1, P1 = Sh::P1, R2 = Sh::R2, P2 = Sh::P2, PITCH = Sh::PITCH;
-    extern __shared__ double2 pl[];
-    double2* scratch = pl + NY * PITCH;
-    const int tid = threadIdx.x;
-    const long long plane = blockIdx.x;
-    const double2* in = Yh + plane * NY * Mp;
-    for (int e = tid; e < NY * Mp; e += Sh::THREADS) {
-        const int row = e / Mp, k = e - row * Mp;
-        if (k <= M) pl[row * PITCH + k] = __ldg(in + e);
-    }
-    __syncthreads();
-    // ---- columns: inverse NY-point FFT in place
-    {
-        const int col = tid / P2, t = tid % P2;
-        const bool act = col <= M;
-        double2 v[R2];
-#pragma unroll
-        for (int r = 0; r < R2; ++r) v[r] = act ? pl[(t + P2 * r) * PITCH + col] : make_double2(0.0, 0.0);
-        __syncthreads();
-        fftc::stockham<NY, true>(v, t, pl, [&](int q) { return act ? q * PITCH + col : (int)(scratch - pl) + (q % Sh::SCRATCH); }, twN);
-        __syncthreads();
-        if (act) {
-#pragma unroll
-            for (int j = 0; j < R2; ++j) pl[fftc::Plan<NY>::out_q(t, j) * PITCH + col] = v[j];
-        }
-        __syncthreads();
-    }
-    // ---- rows: Hermitian merge, inverse M-point FFT, x[2n] + i x[2n+1]
-    {
-        const int row = tid / P1, t = tid % P1;
-        const bool act = row < NY;
-        double2 v[R1];
-        if (act) {
-            const double2* rz = pl + row * PITCH;
-#pragma unroll
-            for (int r = 0; r < R1; ++r) {
-                const int k = t + P1 * r;
-                const double2 a = rz[k], b = rz[M - k];
-                const double2 sm_ = make_double2(a.x + b.x, a.y - b.y);
-                const double2 d = make_double2(a.x - b.x, a.y + b.y);
-                const double2 wd = cmulc(__ldg(twL + k), d);
-                v[r] = make_double2(sm_.x - wd.y, sm_.y + wd.x);
-            }
-        } else {
-#pragma unroll
-            for (int r = 0; r < R1; ++r) v[r] = make_double2(0.0, 0.0);
-        }
-        __syncthreads();
-        fftc::stockham<M, true>(v, t, pl, [&](int q) { return act ? row * PITCH + q : (int)(scratch - pl) + (q % Sh::SCRATCH); }, twM);
-        if (act) {
-            double2* oz = reinterpret_cast<double2*>(u) + (plane * NY + row) * M;
-            const double2* sz = reinterpret_cast<const double2*>(sub) + (plane * NY + row) * M;
-#pragma unroll
-            for (int j = 0; j < R1; ++j) {
-                const int n = fftc::Plan<M>::out_q(t, j);
-                double2 r = cscale(v[j], scale);
-                if (sub) r = csub(r, __ldg(sz + n));
-                oz[n] = r;
-            }
-        }
-    }
-}
-
-template <int M, int NY>
-void launch_plane(bool fwd, const double* y, double2* Yh, double* u, long long planes, int Mp, double scale,
-                  const double* sub, cudaStream_t st) {
-    using Sh = PlaneShape<M, NY>;
-    const size_t smem = (size_t)Sh::SMEM * sizeof(double2);
-    const double2 *twM = fft_engine().twiddles(M), *twL = fft_engine().twiddles(2 * M),
-                  *twN = fft_engine().twiddles(NY);
-    if (fwd) {
-        auto kern = lr_plane_fwd_kernel<M, NY>;
-        VSR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        kern<<<(unsigned)planes, Sh::THREADS, smem, st>>>(y, Yh, Mp, twM, twL, twN);
-    } else {
-        auto kern = lr_plane_inv_kernel<M, NY>;
-        VSR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        kern<<<(unsigned)planes, Sh::THREADS, smem, st>>>(Yh, u, Mp, scale, sub, twM, twL, twN);
-    }
-    VSR_LAUNCH_CHECK();
-}
-
-#define VSR_PLANE_TABLE(X) X(16, 32) X(32, 32) X(32, 64) X(64, 64) X(64, 128) X(128, 64)
-
 }  // namespace
 
 bool rfft_rows_ok(size_t L) { return L >= 16 && L <= 2048 && is_pow2(L); }
@@ -354,37 +170,6 @@ void rfft_rows_inverse(size_t L, const double2* X, double* x, long long rows, do
         case 1024: launch_c2r<1024>(X, x, rows, Mp, scale, sub, st); break;
         default: throw std::logic_error("rfft_rows_inverse: unsupported length");
     }
-}
-
-bool lr_plane_ok(size_t L, size_t ny) {
-#define VSR_X(MM, NN) \
-    if (L == 2 * MM && ny == NN) return true;
-    VSR_PLANE_TABLE(VSR_X)
-#undef VSR_X
-    return false;
-}
-
-void lr_plane_forward(size_t L, size_t ny, const double* y, double2* Yh, long long planes, cudaStream_t st) {
-#define VSR_X(MM, NN)                                                                       \
-    if (L == 2 * MM && ny == NN) {                                                          \
-        launch_plane<MM, NN>(true, y, Yh, nullptr, planes, half_pitch(L), 1.0, nullptr, st); \
-        return;                                                                             \
-    }
-    VSR_PLANE_TABLE(VSR_X)
-#undef VSR_X
-    throw std::logic_error("lr_plane_forward: unsupported plane");
-}
-
-void lr_plane_inverse(size_t L, size_t ny, const double2* Yh, double* u, long long planes, double scale,
-                      const double* sub, cudaStream_t st) {
-#define VSR_X(MM, NN)                                                                                        \
-    if (L == 2 * MM && ny == NN) {                                                                           \
-        launch_plane<MM, NN>(false, nullptr, const_cast<double2*>(Yh), u, planes, half_pitch(L), scale, sub, st); \
-        return;                                                                                              \
-    }
-    VSR_PLANE_TABLE(VSR_X)
-#undef VSR_X
-    throw std::logic_error("lr_plane_inverse: unsupported plane");
 }
 
 }  // namespace vsr

@@ -17,12 +17,4 @@ void rfft_rows_forward(size_t L, const double* x, double2* X, long long rows, cu
 void rfft_rows_inverse(size_t L, const double2* X, double* x, long long rows, double scale, const double* sub,
                        cudaStream_t st);
 
-// Whole-plane variants (one CTA per z-plane, the intermediate stays in shared
-// memory): r2c along axis 1 + forward axis-2 FFT, and the inverse pair with
-// the optional subtraction.  Rows L (= 2M) x ny columns per plane.
-bool lr_plane_ok(size_t L, size_t ny);
-void lr_plane_forward(size_t L, size_t ny, const double* y, double2* Yh, long long planes, cudaStream_t st);
-void lr_plane_inverse(size_t L, size_t ny, const double2* Yh, double* u, long long planes, double scale,
-                      const double* sub, cudaStream_t st);
-
 }  // namespace vsr

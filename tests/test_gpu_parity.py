@@ -446,9 +446,9 @@ def test_admm_tv_deterministic(V):
 
 # ------------------------------------------------------------------ opt-in variants
 # Every env-selected kernel variant (read once per process) runs in a fresh
-# interpreter against the oracle: Tikhonov spatial path with the whole-plane LR
-# kernels / full-spectrum LR stage / the general FFT path / no graphs, and the
-# TV sandwich with radix 8 / the persistent prefetching loop.
+# interpreter against the oracle: Tikhonov spatial path with the full-spectrum
+# LR stage / the general FFT path / no graphs, and the TV iteration on the full
+# spectrum / with the radix-8 sandwich / the persistent prefetching loop.
 _VARIANT_SCRIPT = r"""
 import sys, numpy as np
 sys.path.insert(0, {root!r}); sys.path.insert(0, {root!r} + '/oracle'); sys.path.insert(0, {root!r} + '/tests')
@@ -477,12 +477,7 @@ print("ok", op.path())
 
 
 @pytest.mark.parametrize("env,dims,rates", [
-    ({"VSR_LR_PLANE": "1"}, (64, 64, 32), (2, 2, 2)),
-    ({"VSR_LR_PLANE": "1"}, (128, 128, 32), (2, 2, 2)),
-    ({"VSR_LR_PLANE": "1"}, (256, 256, 16), (2, 2, 2)),
     ({"VSR_NO_HALF": "1"}, (64, 64, 32), (2, 2, 2)),
-    ({"VSR_LR_PERSIST": "1"}, (64, 128, 64), (2, 2, 2)),
-    ({"VSR_LR_PERSIST": "1"}, (128, 128, 128), (2, 2, 2)),
     ({"VSR_TV_FULL": "1"}, (64, 64, 64), (4, 4, 4)),
     ({"VSR_NO_SPATIAL": "1"}, (64, 64, 32), (2, 2, 2)),
     ({"VSR_NO_GRAPH": "1"}, (64, 64, 32), (2, 2, 2)),
