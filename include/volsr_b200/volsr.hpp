@@ -404,6 +404,50 @@ inline Volume3D tikhonov_fast(const Volume3D& y, const SpectrumDiag& lambda, con
     return TikhonovOperator(lambda, spec, cfg).solve(y);
 }
 
+// solvers.hpp:54-70: iterative l2-l2 comparator (split v = Hx)
+struct AdmmL2State {
+    Volume3D x, v, dual;  // all HR dims
+};
+
+struct AdmmL2Options {
+    double mu = 0.1;
+    double rel_tol = 1e-10;
+    std::optional<AdmmL2State> warm_start;
+};
+
+inline std::pair<Volume3D, SolveReport> admm_l2l2(const Volume3D& y, const SpectrumDiag& lambda,
+                                                  const DecimationSpec& spec, const TikhonovConfig& cfg,
+                                                  std::size_t max_iters, const AdmmL2Options& opts = {}) {
+    if (!(cfg.lambda > 0.0)) throw std::invalid_argument("lambda must be positive, got " + std::to_string(cfg.lambda));
+    if (!(opts.mu > 0.0)) throw std::invalid_argument("mu must be positive, got " + std::to_string(opts.mu));
+    require_same_dims(y.dims(), spec.lr(), "admm_l2l2");
+    require_same_dims(cfg.xbar.dims(), spec.hr(), "admm_l2l2: xbar");
+    if (max_iters < 1) throw std::invalid_argument("admm_l2l2: max_iters must be >= 1");
+    vsr_l2_config c{opts.mu, opts.rel_tol, nullptr, nullptr, nullptr};
+    if (opts.warm_start) {
+        require_same_dims(opts.warm_start->x.dims(), spec.hr(), "admm_l2l2: warm start");
+        require_same_dims(opts.warm_start->v.dims(), spec.hr(), "admm_l2l2: warm start");
+        require_same_dims(opts.warm_start->dual.dims(), spec.hr(), "admm_l2l2: warm start");
+        c.warm_x = opts.warm_start->x.data().data();
+        c.warm_v = opts.warm_start->v.data().data();
+        c.warm_dual = opts.warm_start->dual.data().data();
+    }
+    SolveReport rep;
+    rep.objective.resize(max_iters);
+    rep.primal_residual.resize(max_iters);
+    vsr_report vr{0, 0.0, 0.0, rep.objective.data(), rep.primal_residual.data()};
+    Volume3D x(spec.hr());
+    detail::check(vsr_admm_l2l2(detail::ctx(), detail::D3(spec.hr()).v, spec.rates_ptr(), y.data().data(),
+                                detail::cp(lambda.values), cfg.lambda, cfg.xbar.data().data(), max_iters, &c,
+                                x.data().data(), &vr));
+    rep.iterations = vr.iterations;
+    rep.initial_objective = vr.initial_objective;
+    rep.seconds = vr.seconds;
+    rep.objective.resize(vr.iterations);
+    rep.primal_residual.resize(vr.iterations);
+    return {std::move(x), std::move(rep)};
+}
+
 struct TvAdmmConfig {
     double lambda = 0.06;
     double mu = 0.1;

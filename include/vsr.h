@@ -172,6 +172,22 @@ typedef struct vsr_report {
 int vsr_admm_tv(vsr_ctx* ctx, const size_t hr_dims[3], const size_t rates[3], const double* y_r,
                 const double* psf_r, const vsr_tv_config* cfg, double* x_r, vsr_report* report);
 
+/* admm_l2l2 (solvers.hpp:54-70, solvers.cpp:95-189): the iterative l2-l2
+ * comparator with the split v = Hx.  Same arithmetic as the reference (one
+ * forward and two inverse transforms per iteration); warm start optional (all
+ * three of x, v, dual, or none). */
+typedef struct vsr_l2_config {
+    double mu;                /* default 0.1 */
+    double rel_tol;           /* default 1e-10; 0 = fixed iteration count */
+    const double* warm_x;     /* HR real, optional */
+    const double* warm_v;
+    const double* warm_dual;
+} vsr_l2_config;
+
+int vsr_admm_l2l2(vsr_ctx* ctx, const size_t hr_dims[3], const size_t rates[3], const double* y_r,
+                  const double* lambda_c, double reg, const double* xbar_r, size_t max_iters,
+                  const vsr_l2_config* cfg, double* x_r, vsr_report* report);
+
 /* Stepwise ADMM-TV solver over device-resident state (bench / streaming use).
  * create: precompute (psf -> Lambda, y -> LR spectrum, Gamma tables) and the
  * iteration-0 state; iterate(k): k iterations enqueued on the stream. */

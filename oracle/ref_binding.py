@@ -47,6 +47,8 @@ def _setup():
     L.ref_objective_tv.argtypes = [_sz, _sz, _dp, _dp, _dp, C.c_double, _dp]
     L.ref_admm_tv.argtypes = [_sz, _sz, _dp, _dp, C.c_double, C.c_double, C.c_size_t, C.c_double,
                               C.c_int, C.c_double, C.c_int, _dp, _dp, _dp, _dp, _sz, _dp, _dp]
+    L.ref_admm_l2l2.argtypes = [_sz, _sz, _dp, _dp, C.c_double, _dp, C.c_size_t, C.c_double, C.c_double,
+                                _dp, _dp, _dp, _sz, _dp]
 
 
 class RefError(RuntimeError):
@@ -178,3 +180,21 @@ def admm_tv(y, psf, hr, rates, lam_tv, mu, max_iters, rel_tol, tau=None, init=0,
     k = iters.value
     return x, {"iterations": k, "initial_objective": init_obj.value, "objective": obj[:k],
                "primal_residual": res[:k], "seconds": secs.value}
+
+
+def admm_l2l2(y, lam, hr, rates, reg, xbar, max_iters, mu=0.1, rel_tol=1e-10):
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    lam = np.ascontiguousarray(lam, dtype=np.complex128)
+    xbar = np.ascontiguousarray(xbar, dtype=np.float64)
+    m, n, s = hr
+    x = np.empty((s, n, m))
+    obj = np.zeros(max_iters)
+    res = np.zeros(max_iters)
+    iters = C.c_size_t()
+    init_obj = C.c_double()
+    _chk(_lib.ref_admm_l2l2(_d(hr), _d(rates), _p(y), _p(lam.view(np.float64)), float(reg), _p(xbar),
+                            C.c_size_t(max_iters), float(mu), float(rel_tol), _p(x), _p(obj), _p(res),
+                            C.byref(iters), C.byref(init_obj)))
+    k = iters.value
+    return x, {"iterations": k, "initial_objective": init_obj.value, "objective": obj[:k],
+               "primal_residual": res[:k]}

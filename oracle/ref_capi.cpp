@@ -172,4 +172,28 @@ int ref_admm_tv(const size_t hr[3], const size_t rates[3], const double* y, cons
     });
 }
 
+int ref_admm_l2l2(const size_t hr[3], const size_t rates[3], const double* y, const double* lambda_c, double reg,
+                  const double* xbar, size_t max_iters, double mu, double rel_tol, double* x_out, double* obj_out,
+                  double* res_out, size_t* iters, double* init_obj) {
+    return wrap([&] {
+        DecimationSpec spec(D(hr), {rates[0], rates[1], rates[2]});
+        TikhonovConfig cfg;
+        cfg.lambda = reg;
+        cfg.xbar = vol(hr, xbar);
+        AdmmL2Options opts;
+        opts.mu = mu;
+        opts.rel_tol = rel_tol;
+        const Dims3 lr = spec.lr();
+        const size_t dl[3] = {lr.m, lr.n, lr.s};
+        auto [x, rep] = admm_l2l2(vol(dl, y), SpectrumDiag{cvol(hr, lambda_c)}, spec, cfg, max_iters, opts);
+        put(x, x_out);
+        for (size_t i = 0; i < rep.iterations; ++i) {
+            obj_out[i] = rep.objective[i];
+            res_out[i] = rep.primal_residual[i];
+        }
+        *iters = rep.iterations;
+        *init_obj = rep.initial_objective;
+    });
+}
+
 }  // extern "C"

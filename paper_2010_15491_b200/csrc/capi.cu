@@ -19,6 +19,7 @@
 #include "fold.cuh"
 #include "fused.cuh"
 #include "spatial.cuh"
+#include "l2l2.cuh"
 #include "rfft.cuh"
 #include "chain.cuh"
 #include "tv.cuh"
@@ -1666,6 +1667,109 @@ static void tv_fill_report(vsr_tv* h, vsr_report* rep, const char* where) {
         sync(h->ctx);
         rep->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - h->t0).count();
     }
+}
+
+// ============================================================ admm_l2l2
+// solvers.cpp:95-189, device loop: per iteration t = v - dual, fft3(t),
+// x_hat / L x_hat pointwise, two inverse transforms (x, Hx) with the residue
+// reductions, the v / dual update with the objective, residual and
+// rel-change partials, then a fixed-order finalize.  With rel_tol > 0 the host
+// reads rel_change after each iteration (the reference's stop rule, :182).
+int vsr_admm_l2l2(vsr_ctx* ctx, const size_t hr_dims[3], const size_t rates[3], const double* y_r,
+                  const double* lambda_c, double reg, const double* xbar_r, size_t max_iters,
+                  const vsr_l2_config* cfg, double* x_r, vsr_report* report) {
+    return guarded([&] {
+        require_ctx(ctx);
+        const vsr_l2_config def{0.1, 1e-10, nullptr, nullptr, nullptr};
+        const vsr_l2_config& c = cfg ? *cfg : def;
+        const Spec sp = make_spec(hr_dims, rates);
+        require_positive(reg, "lambda");  // solvers.cpp:98-99
+        require_positive(c.mu, "mu");
+        if (max_iters < 1) throw std::invalid_argument("admm_l2l2: max_iters must be >= 1");
+        const bool warm = c.warm_x || c.warm_v || c.warm_dual;
+        if (warm && !(c.warm_x && c.warm_v && c.warm_dual))
+            throw shape_error("admm_l2l2: warm start: dims mismatch");
+        vsr_ctx::Guard g(ctx->device);
+        const auto t0 = std::chrono::steady_clock::now();
+        cudaStream_t st = ctx->stream;
+        const Dims& hr = sp.hr;
+        const size_t N = hr.count(), Nl = sp.lr.count();
+        DevBuf<double2> lam(N), xbh(N), W(N), W2(N);
+        DevBuf<double> y(Nl), xbar(N), x(N), v(N), dual(N), t(N), hx(N), xprev;
+        if (c.rel_tol > 0.0) xprev.alloc(N);
+        h2d(ctx, lam.p, lambda_c, lam.bytes());
+        h2d(ctx, y.p, y_r, y.bytes());
+        h2d(ctx, xbar.p, xbar_r, xbar.bytes());
+        if (warm) {
+            h2d(ctx, x.p, c.warm_x, x.bytes());
+            h2d(ctx, v.p, c.warm_v, v.bytes());
+            h2d(ctx, dual.p, c.warm_dual, dual.bytes());
+        } else {
+            VSR_CUDA(cudaMemsetAsync(x.p, 0, x.bytes(), st));
+            VSR_CUDA(cudaMemsetAsync(v.p, 0, v.bytes(), st));
+            VSR_CUDA(cudaMemsetAsync(dual.p, 0, dual.bytes(), st));
+        }
+        const double s = inv_sqrt_count(hr);
+        fft_engine().forward3(hr, xbar.p, IN_REAL, xbh.p, s, st);  // xbar_hat (:105)
+        ++g_fwd;
+        const size_t nres = fft_engine().inverse_final_blocks(hr);
+        DevBuf<double> up(5 * l2_partial_blocks()), px(2 * nres), ph(2 * nres);
+        DevBuf<unsigned long long> bad(1), badh(1);
+        DevBuf<double> obj(max_iters), res(max_iters), rel(max_iters), status(2), init_obj(1);
+        VSR_CUDA(cudaMemsetAsync(bad.p, 0xff, sizeof(unsigned long long), st));
+        VSR_CUDA(cudaMemsetAsync(badh.p, 0xff, sizeof(unsigned long long), st));
+        VSR_CUDA(cudaMemsetAsync(status.p, 0, 2 * sizeof(double), st));
+        const L2Dims D{(long long)hr.m, (long long)hr.n, (long long)hr.s, (long long)N, (long long)sp.lr.m,
+                       (long long)sp.lr.n, sp.rates[0], sp.rates[1], sp.rates[2]};
+        const L2Scalars sc{obj.p, res.p, rel.p, status.p, init_obj.p};
+        PassReduce rx{px.p, bad.p}, rh{ph.p, badh.p};
+        // initial objective (:117-129): Hx via fft3 / L / ifft3_real
+        fft_engine().forward3(hr, x.p, IN_REAL, W.p, s, st);
+        launch_l2_mul(W.p, lam.p, (long long)N, st);
+        fft_engine().inverse3(hr, W.p, hx.p, OUT_REAL, s, &rh, st);
+        ++g_fwd;
+        ++g_inv;
+        launch_l2_update(D, false, hx.p, x.p, xbar.p, y.p, v.p, dual.p, nullptr, c.mu, up.p, st);
+        launch_l2_finalize(-1, up.p, nullptr, ph.p, (long long)nres, reg, 1e-8, sc, st);
+        size_t iters = 0;
+        for (size_t it = 0; it < max_iters; ++it) {
+            if (xprev.p) VSR_CUDA(cudaMemcpyAsync(xprev.p, x.p, x.bytes(), cudaMemcpyDeviceToDevice, st));
+            launch_l2_sub(v.p, dual.p, t.p, (long long)N, st);                 // :139
+            fft_engine().forward3(hr, t.p, IN_REAL, W.p, s, st);               // :140
+            launch_l2_xhat(W.p, W2.p, lam.p, xbh.p, c.mu, reg, (long long)N, st);  // :141-150
+            fft_engine().inverse3(hr, W.p, x.p, OUT_REAL, s, &rx, st);         // :146
+            fft_engine().inverse3(hr, W2.p, hx.p, OUT_REAL, s, &rh, st);       // :151
+            g_fwd += 1;
+            g_inv += 2;
+            launch_l2_update(D, true, hx.p, x.p, xbar.p, y.p, v.p, dual.p, xprev.p, c.mu, up.p, st);
+            launch_l2_finalize((int)it, up.p, px.p, ph.p, (long long)nres, reg, 1e-8, sc, st);
+            iters = it + 1;
+            if (c.rel_tol > 0.0) {  // :182
+                double rc = 0.0;
+                d2h(ctx, &rc, rel.p + it, sizeof(double));
+                sync(ctx);
+                if (rc < c.rel_tol) break;
+            }
+        }
+        double stv[2];
+        unsigned long long b0 = 0, b1 = 0;
+        d2h(ctx, stv, status.p, sizeof(stv));
+        d2h(ctx, &b0, bad.p, sizeof(b0));
+        d2h(ctx, &b1, badh.p, sizeof(b1));
+        sync(ctx);
+        if (stv[0] != 0.0) throw numeric_error(residue_message(stv[1], 1e-8));
+        if (b0 != ULLONG_MAX)  // require_finite(x, "admm_l2l2") (:185)
+            throw numeric_error("admm_l2l2: non-finite value at flat index " + std::to_string(b0));
+        d2h(ctx, x_r, x.p, x.bytes());
+        if (report) {
+            report->iterations = iters;
+            d2h(ctx, &report->initial_objective, init_obj.p, sizeof(double));
+            if (report->objective) d2h(ctx, report->objective, obj.p, iters * sizeof(double));
+            if (report->primal_residual) d2h(ctx, report->primal_residual, res.p, iters * sizeof(double));
+        }
+        sync(ctx);
+        if (report) report->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    });
 }
 
 int vsr_admm_tv(vsr_ctx* ctx, const size_t hr_dims[3], const size_t rates[3], const double* y_r,

@@ -649,6 +649,63 @@ def admm_tv(y, psf, spec: DecimationSpec, cfg: TvAdmmConfig, ctx=None):
     return out, report
 
 
+@dataclass
+class AdmmL2Options:
+    """solvers.hpp:58-62; warm_start = (x, v, dual) HR volumes or None."""
+    mu: float = 0.1
+    rel_tol: float = 1e-10
+    warm_start: Optional[tuple] = None
+
+
+class _L2Config(C.Structure):
+    _fields_ = [("mu", C.c_double), ("rel_tol", C.c_double), ("warm_x", C.c_void_p),
+                ("warm_v", C.c_void_p), ("warm_dual", C.c_void_p)]
+
+
+_sig("vsr_admm_l2l2", [_vp, _szp, _szp, _dp, _dp, C.c_double, _dp, C.c_size_t, C.POINTER(_L2Config), _dp,
+                       C.POINTER(_Report)])
+
+
+def admm_l2l2(y, lam, spec, cfg: TikhonovConfig, max_iters: int, opts: Optional[AdmmL2Options] = None, ctx=None):
+    """solvers.hpp:67-70 / solvers.cpp:95-189 -> (x, SolveReport)."""
+    opts = opts or AdmmL2Options()
+    require_positive(cfg.lambda_, "lambda")
+    require_positive(opts.mu, "mu")
+    a = _real(y)
+    require_same_dims(dims_of(a), spec.lr, "admm_l2l2")
+    if cfg.xbar is None:
+        raise ShapeError("admm_l2l2: xbar: dims mismatch")
+    xb = _real(cfg.xbar)
+    require_same_dims(dims_of(xb), spec.hr, "admm_l2l2: xbar")
+    if max_iters < 1:
+        raise ValueError("admm_l2l2: max_iters must be >= 1")
+    L = _cplx(lam)
+    require_same_dims(dims_of(L), spec.hr, "admm_l2l2: lambda")
+    c = _L2Config(float(opts.mu), float(opts.rel_tol), None, None, None)
+    keep = []
+    if opts.warm_start is not None:
+        ws = [_real(w) for w in opts.warm_start]
+        for w in ws:
+            require_same_dims(dims_of(w), spec.hr, "admm_l2l2: warm start")
+        keep = ws
+        c.warm_x, c.warm_v, c.warm_dual = (w.ctypes.data for w in ws)
+    obj = np.zeros(max_iters)
+    res = np.zeros(max_iters)
+    rep = _Report()
+    rep.objective = _p(obj)
+    rep.primal_residual = _p(res)
+    out = np.empty(shape_of(spec.hr))
+    check(_lib.vsr_admm_l2l2(_ctx(ctx), _dims_arr(spec.hr), _dims_arr(spec.rates), _p(a),
+                             _p(L.view(np.float64)), float(cfg.lambda_), _p(xb), C.c_size_t(max_iters),
+                             C.byref(c), _p(out), C.byref(rep)))
+    del keep
+    it = int(rep.iterations)
+    report = SolveReport(iterations=it, initial_objective=float(rep.initial_objective),
+                         objective=obj[:it].tolist(), primal_residual=res[:it].tolist(),
+                         seconds=float(rep.seconds))
+    return out, report
+
+
 def tikhonov_algorithmic_bytes(hr_dims, rates) -> float:
     return float(_lib.vsr_tikhonov_algorithmic_bytes(_dims_arr(hr_dims), _dims_arr(rates)))
 

@@ -151,3 +151,32 @@ def test_gpu_objective_golden(V):
     hr, rates = tup(g["hr"]), tup(g["rates"])
     v = V.objective_tv(g["x"], g["y"], V.psf_to_spectrum(g["psf"]), V.DecimationSpec(hr, rates), float(g["w"]))
     assert abs(v - float(g["value"])) < 1e-12 * abs(float(g["value"]))
+
+
+# ------------------------------------------------------------------ admm_l2l2
+def _l2_cases():
+    g = load("admm_l2l2")
+    for i in range(2):
+        yield (tup(g[f"c{i}_hr"]), tup(g[f"c{i}_rates"]), int(g[f"c{i}_iters"]), g[f"c{i}_lam"], g[f"c{i}_xbar"],
+               g[f"c{i}_y"], g[f"c{i}_x"], g[f"c{i}_objective"], g[f"c{i}_residual"], float(g[f"c{i}_init_obj"]))
+
+
+def test_oracle_admm_l2l2_golden(O):
+    for hr, rates, it, lam, xbar, y, x, obj, res, init in _l2_cases():
+        xo, rep = O.admm_l2l2(y, lam, O.DecimationSpec(hr, rates), 0.05, xbar, it, mu=0.3, rel_tol=0.0)
+        assert rel_err(xo, x) < 1e-13
+        np.testing.assert_allclose(rep.objective, obj, rtol=1e-13)
+        np.testing.assert_allclose(rep.primal_residual, res, rtol=1e-12)
+        assert abs(rep.initial_objective - init) <= 1e-13 * abs(init)
+
+
+@pytest.mark.gpu
+def test_gpu_admm_l2l2_golden(V):
+    for hr, rates, it, lam, xbar, y, x, obj, res, init in _l2_cases():
+        xg, rep = V.admm_l2l2(y, lam, V.DecimationSpec(hr, rates), V.TikhonovConfig(0.05, xbar), it,
+                              V.AdmmL2Options(mu=0.3, rel_tol=0.0))
+        assert rep.iterations == it
+        assert rel_err(xg, x) < 1e-10
+        np.testing.assert_allclose(rep.objective, obj, rtol=1e-10)
+        np.testing.assert_allclose(rep.primal_residual, res, rtol=1e-9)
+        assert abs(rep.initial_objective - init) <= 1e-10 * abs(init)

@@ -494,3 +494,84 @@ def test_env_variants(env, dims, rates):
     r = subprocess.run([sys.executable, "-c", code], env={**os.environ, **env}, capture_output=True, text=True,
                        timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+# ------------------------------------------------------------------ admm_l2l2
+L2_CASES = [((8, 8, 8), (2, 2, 2), 6), ((12, 10, 8), (2, 2, 2), 5), ((16, 16, 16), (4, 4, 4), 8),
+            ((32, 16, 8), (2, 1, 2), 5), ((64, 64, 32), (2, 2, 2), 4)]
+
+
+@pytest.mark.parametrize("dims,rates,iters", L2_CASES)
+def test_admm_l2l2_vs_oracle(V, O, dims, rates, iters):
+    """solvers.cpp:95-189, fixed iteration count (rel_tol = 0)."""
+    rng = np.random.default_rng(31)
+    spec, ospec = V.DecimationSpec(dims, rates), O.DecimationSpec(dims, rates)
+    lam = O.psf_to_spectrum(random_psf(dims, 3, rng))
+    xbar = random_volume(dims, rng)
+    y = random_volume(spec.lr, rng)
+    x, rep = V.admm_l2l2(y, lam, spec, V.TikhonovConfig(0.05, xbar), iters, V.AdmmL2Options(mu=0.3, rel_tol=0.0))
+    xo, orep = O.admm_l2l2(y, lam, ospec, 0.05, xbar, iters, mu=0.3, rel_tol=0.0)
+    assert rep.iterations == orep.iterations == iters
+    assert rel_err(x, xo) < TOL
+    assert abs(rep.initial_objective - orep.initial_objective) <= 1e-12 * abs(orep.initial_objective)
+    np.testing.assert_allclose(rep.objective, orep.objective, rtol=1e-10)
+    np.testing.assert_allclose(rep.primal_residual, orep.primal_residual, rtol=1e-9)
+
+
+def test_admm_l2l2_fixed_point(V, O):
+    """test_solvers.cpp:194-222: warm start at the exact minimizer stays there."""
+    rng = np.random.default_rng(7)
+    d = (8, 8, 8)
+    spec, ospec = V.DecimationSpec(d, (2, 2, 2)), O.DecimationSpec(d, (2, 2, 2))
+    lam = O.psf_to_spectrum(random_psf(d, 3, rng))
+    xbar = random_volume(d, rng)
+    y = random_volume(spec.lr, rng)
+    xstar = O.tikhonov_fast(y, lam, ospec, 0.05, xbar)
+    v = O.blur_apply(xstar, lam)
+    r = O.decimate(v, ospec) - y
+    dual = O.decimate_adjoint(r, ospec) / 0.3
+    x1, rep = V.admm_l2l2(y, lam, spec, V.TikhonovConfig(0.05, xbar), 1,
+                          V.AdmmL2Options(mu=0.3, rel_tol=0.0, warm_start=(xstar, v, dual)))
+    assert rep.iterations == 1
+    assert rel_err(x1, xstar) < TOL
+
+
+def test_admm_l2l2_converges_to_closed_form(V, O):
+    """test_solvers.cpp:224-260: converges (rel_tol stop) to the tikhonov_fast minimizer."""
+    rng = np.random.default_rng(8)
+    d = (16, 16, 16)
+    spec, ospec = V.DecimationSpec(d, (2, 2, 2)), O.DecimationSpec(d, (2, 2, 2))
+    lam = O.psf_to_spectrum(O.make_gaussian_psf((5, 5, 5), (1.5, 1.5, 1.5), d))
+    y = random_volume(spec.lr, rng, 0.0, 1.0)
+    xbar = O.zero_fill_upsample(y, ospec)
+    cfg = V.TikhonovConfig(0.01, xbar)
+    fast = V.tikhonov_fast(y, lam, spec, cfg)
+    it, rep = V.admm_l2l2(y, lam, spec, cfg, 4000, V.AdmmL2Options(mu=0.1, rel_tol=1e-11))
+    assert rep.iterations < 4000
+
+    def objective(x):
+        z = O.decimate(O.blur_apply(x, lam), ospec)
+        return 0.5 * float(np.sum((y - z) ** 2)) + 0.01 * float(np.sum((x - xbar) ** 2))
+
+    assert abs(rep.objective[-1] - objective(fast)) <= 1e-8 * objective(fast)
+    assert rel_err(it, fast) < 1e-5
+
+
+def test_admm_l2l2_errors_and_determinism(V):
+    d = (8, 8, 8)
+    spec = V.DecimationSpec(d, (2, 2, 2))
+    lam = np.ones(V.shape_of(d), complex)
+    xbar = np.zeros(V.shape_of(d))
+    y = np.ones(V.shape_of(spec.lr))
+    with pytest.raises(ValueError, match="mu must be positive"):
+        V.admm_l2l2(y, lam, spec, V.TikhonovConfig(0.1, xbar), 3, V.AdmmL2Options(mu=0.0))
+    with pytest.raises(ValueError, match="max_iters"):
+        V.admm_l2l2(y, lam, spec, V.TikhonovConfig(0.1, xbar), 0)
+    with pytest.raises(V.ShapeError):
+        V.admm_l2l2(np.ones((2, 2, 2)), lam, spec, V.TikhonovConfig(0.1, xbar), 3)
+    with pytest.raises(V.ShapeError, match="warm start"):
+        V.admm_l2l2(y, lam, spec, V.TikhonovConfig(0.1, xbar), 3,
+                    V.AdmmL2Options(warm_start=(xbar, xbar, np.zeros((2, 2, 2)))))
+    a, _ = V.admm_l2l2(y, lam, spec, V.TikhonovConfig(0.1, xbar), 5, V.AdmmL2Options(rel_tol=0.0))
+    b, _ = V.admm_l2l2(y, lam, spec, V.TikhonovConfig(0.1, xbar), 5, V.AdmmL2Options(rel_tol=0.0))
+    assert a.tobytes() == b.tobytes()

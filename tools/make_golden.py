@@ -97,5 +97,39 @@ def main():
          value=R.objective_tv(x, y, R.psf_to_spectrum(psf), hr, rates, 0.3))
 
 
+
+def admm_l2l2_golden():
+    """admm_l2l2 (solvers.cpp:95-189) on two small problems, fixed iteration
+    counts, from the reference itself."""
+    assert R.available(), "build oracle/_ref first (make -C oracle)"
+    rng = np.random.default_rng(95189)
+    out = {}
+    for i, (hr, rates, iters) in enumerate([((8, 8, 8), (2, 2, 2), 6), ((12, 10, 8), (2, 1, 2), 5)]):
+        m, n, s = hr
+        w = rng.uniform(0.0, 1.0, 27)
+        psf = np.zeros((s, n, m))
+        k = 0
+        for dz in (-1, 0, 1):
+            for dy in (-1, 0, 1):
+                for dx in (-1, 0, 1):
+                    psf[dz % s, dy % n, dx % m] = w[k]
+                    k += 1
+        psf /= psf.sum()
+        lam = R.fft3(psf) * np.sqrt(m * n * s)  # unnormalised DFT of the wrapped PSF
+        xbar = rng.uniform(-1, 1, (s, n, m))
+        lr = (m // rates[0], n // rates[1], s // rates[2])
+        y = rng.uniform(-1, 1, (lr[2], lr[1], lr[0]))
+        x, rep = R.admm_l2l2(y, lam, hr, rates, 0.05, xbar, iters, mu=0.3, rel_tol=0.0)
+        out.update({f"c{i}_hr": np.array(hr), f"c{i}_rates": np.array(rates), f"c{i}_iters": iters,
+                    f"c{i}_lam": lam, f"c{i}_xbar": xbar, f"c{i}_y": y, f"c{i}_x": x,
+                    f"c{i}_objective": rep["objective"], f"c{i}_residual": rep["primal_residual"],
+                    f"c{i}_init_obj": rep["initial_objective"]})
+    save("admm_l2l2", **out)
+
+
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 1 and sys.argv[1] == "admm_l2l2":
+        admm_l2l2_golden()
+    else:
+        main()
+        admm_l2l2_golden()
