@@ -205,6 +205,33 @@ int main() {
         CHECK(a.first.data() == b.first.data());
         CHECK(a.second.objective == b.second.objective);
     }
+    {  // test_solvers.cpp:194-222 admm_l2l2 stays at the exact fixed point
+        std::mt19937_64 rng(7);
+        const Dims3 d{8, 8, 8};
+        const DecimationSpec spec(d, {2, 2, 2});
+        const Volume3D psf = make_gaussian_psf(PsfSpec::gaussian({3, 3, 3}, {1, 1, 1}), d);
+        const SpectrumDiag lam = psf_to_spectrum(psf);
+        TikhonovConfig cfg;
+        cfg.lambda = 0.05;
+        cfg.xbar = random_volume(d, rng, -1.0, 1.0);
+        const Volume3D y = random_volume(spec.lr(), rng, -1.0, 1.0);
+        const Volume3D xstar = tikhonov_fast(y, lam, spec, cfg);
+        AdmmL2Options opts;
+        opts.mu = 0.3;
+        opts.rel_tol = 0.0;
+        AdmmL2State state;
+        state.x = xstar;
+        state.v = blur_apply(xstar, lam);
+        Volume3D r = decimate(state.v, spec);
+        for (std::size_t g = 0; g < r.size(); ++g) r[g] -= y[g];
+        state.dual = decimate_adjoint(r, spec);
+        for (std::size_t p = 0; p < state.dual.size(); ++p) state.dual[p] /= opts.mu;
+        opts.warm_start = state;
+        auto [x1, report] = admm_l2l2(y, lam, spec, cfg, 1, opts);
+        CHECK(report.iterations == 1);
+        CHECK(rel_err(x1, xstar) < 1e-10);
+        CHECK(throws<std::invalid_argument>([&] { admm_l2l2(y, lam, spec, cfg, 0); }));
+    }
     std::printf("checks: %d failed: %d\n", g_checks, g_fail);
     return g_fail ? 1 : 0;
 }
