@@ -6,6 +6,8 @@
 // through shared memory for the divergence, and rho_z of the previous plane
 // stays in a register.  Every HBM byte of x, dual, dual' and theta is touched
 // once per iteration (halo re-reads hit L2).
+#include <type_traits>
+
 #include "tv.cuh"
 
 namespace vsr {
@@ -362,13 +364,20 @@ __global__ void __launch_bounds__(STH)
     double acc_res = 0.0, acc_tv = 0.0, acc_dx = 0.0, acc_xp = 0.0;
     double rz_prev = 0.0;
     long long zo = zp(k0 - 1);
-    for (int k = k0 - 1; k < k1; ++k) {
+    // The march is unrolled by 6 (lcm of the x ring of 3 slots and the dual ring
+    // of 2), so every slot is a compile-time offset of the shared-memory base.
+    auto step = [&](int k, auto x0, auto x1, auto x2, auto d0, auto d1) {
+        double* const XS0 = sm + decltype(x0)::value * FXS;
+        double* const XS1 = sm + decltype(x1)::value * FXS;
+        double* const XS2 = sm + decltype(x2)::value * FXS;
+        double* const DS0 = sm + 3 * FXS + decltype(d0)::value * FDS;
+        double* const DS1 = sm + 3 * FXS + decltype(d1)::value * FDS;
         // registers -> smem for step k+1, then request x(k+3), dual(k+2)
-        if (k + 2 <= k1 && xa) *reinterpret_cast<double2*>(xsl[2] + xsm) = rxv;
+        if (k + 2 <= k1 && xa) *reinterpret_cast<double2*>(XS2 + xsm) = rxv;
         if (!INIT && k + 1 <= k1 - 1) {
 #pragma unroll
             for (int q = 0; q < 2; ++q)
-                if (da[q]) *reinterpret_cast<double2*>(dsl[1] + dsm[q]) = rdv[q];
+                if (da[q]) *reinterpret_cast<double2*>(DS1 + dsm[q]) = rdv[q];
         }
         if (k + 3 <= k1) {
             zx += plane;
@@ -384,9 +393,9 @@ __global__ void __launch_bounds__(STH)
         }
         __syncthreads();
         const bool warm = k < k0;
-        const double* X0 = xsl[0];
-        const double* X1 = xsl[1];
-        const double* D0 = dsl[0];
+        const double* X0 = XS0;
+        const double* X1 = XS1;
+        [[maybe_unused]] const double* D0 = DS0;
 
         const double xc = X0[xi];
         const double l0 = X0[xi + 1] - xc;
@@ -440,7 +449,7 @@ __global__ void __launch_bounds__(STH)
                 const double hc = X0[hx];
                 const double h0 = X0[hx + 1] - hc;
                 const double h1 = X0[hx + FXW] - hc;
-                const double h2 = X1[hx] - hc;
+                [[maybe_unused]] const double h2 = X1[hx] - hc;
                 double q0, q1;
                 if constexpr (INIT) {
                     q0 = h0;
@@ -467,15 +476,19 @@ __global__ void __launch_bounds__(STH)
         }
         rz_prev = r2;
         // rotate the rings: x slots (k, k+1, k+2) -> (k+1, k+2, k+3); dual (k, k+1) -> (k+1, k+2)
-        double* t0 = xsl[0];
-        xsl[0] = xsl[1];
-        xsl[1] = xsl[2];
-        xsl[2] = t0;
-        double* t1 = dsl[0];
-        dsl[0] = dsl[1];
-        dsl[1] = t1;
         zo += plane;
         if (!halo && zo >= plane * s) zo -= plane * s;
+    };
+    using I0 = std::integral_constant<int, 0>;
+    using I1 = std::integral_constant<int, 1>;
+    using I2 = std::integral_constant<int, 2>;
+    for (int k = k0 - 1; k < k1; k += 6) {
+        step(k, I0{}, I1{}, I2{}, I0{}, I1{});
+        if (k + 1 < k1) step(k + 1, I1{}, I2{}, I0{}, I1{}, I0{});
+        if (k + 2 < k1) step(k + 2, I2{}, I0{}, I1{}, I0{}, I1{});
+        if (k + 3 < k1) step(k + 3, I0{}, I1{}, I2{}, I1{}, I0{});
+        if (k + 4 < k1) step(k + 4, I1{}, I2{}, I0{}, I0{}, I1{});
+        if (k + 5 < k1) step(k + 5, I2{}, I0{}, I1{}, I1{}, I0{});
     }
 
     double v[4] = {acc_res, acc_tv, acc_dx, acc_xp};
