@@ -13,19 +13,20 @@ from paper_2010_15491_b200 import volsr as V  # noqa: E402
 def main(mode="all", reps=2):
     ctx = V.default_context()
     rng = np.random.default_rng(0)
-    if mode in ("all", "tik", "tiklat"):
+    if mode in ("all", "tik", "tiklat", "bench"):
         hr, rates = (256, 256, 256), (2, 2, 2)
         spec = V.DecimationSpec(hr, rates)
         psf = V.make_gaussian_psf((13, 13, 13), (1.5, 1.5, 1.5), hr)
         lam = V.psf_to_spectrum(psf)
         y = rng.uniform(0, 1, V.shape_of(spec.lr))
         # tiklat: the CLI-default lattice prior (spatial-expansion solve)
-        xbar = V.zero_fill_upsample(y, spec) if mode == "tiklat" else rng.uniform(0, 1, V.shape_of(hr))
+        lat = mode in ("tiklat", "bench")
+        xbar = V.zero_fill_upsample(y, spec) if lat else rng.uniform(0, 1, V.shape_of(hr))
         op = V.TikhonovOperator(lam, spec, V.TikhonovConfig(1e-3, xbar))
         for _ in range(reps):
             op.solve(y)
         op.close()
-    if mode in ("all", "tv"):
+    if mode in ("all", "tv", "bench"):
         hr, rates = (256, 256, 256), (4, 4, 4)
         spec = V.DecimationSpec(hr, rates)
         psf = V.make_gaussian_psf((13, 13, 13), (1.5, 1.5, 1.5), hr)
