@@ -517,10 +517,12 @@ def bench_sharded(args, ctx, V, synth, torch, rank, world, local):
     if dist_on:
         tdist.barrier()
     torch.cuda.synchronize()
+    ctx.synchronize()
+    lib = torch.cuda.ExternalStream(ctx.stream(), device=dev)  # the stream the slab stages run on
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    tv.iterate(k)
-    e1.record()
+    e0.record(lib)
+    tv.iterate(k)  # ends with the scalar gather on the library stream
+    e1.record(lib)
     e1.synchronize()
     ms = e0.elapsed_time(e1) / k
     if dist_on:

@@ -80,6 +80,9 @@ class LocalExchange:
     def __init__(self, P: int):
         self.world = P
         self.ranks = list(range(P))
+        # several virtual ranks own different streams: exchanges synchronise
+        # them on the host; a single one keeps everything on its stream
+        self.ordered = P == 1
 
     def all_to_all(self, send: Dict[int, torch.Tensor], recv: Dict[int, torch.Tensor]):
         P = self.world
@@ -102,7 +105,13 @@ class LocalExchange:
 
 
 class TorchExchange:
-    """One rank per process over torch.distributed (NCCL for CUDA, gloo for CPU)."""
+    """One rank per process over torch.distributed (NCCL for CUDA, gloo for CPU).
+
+    `ordered`: the rank's device work, copies and collectives are all issued on
+    the rank's library stream (NCCL orders itself against the current stream),
+    so a TV iteration needs no host synchronisation."""
+
+    ordered = True
 
     def __init__(self):
         import torch.distributed as dist
@@ -252,7 +261,15 @@ class _Base:
         self._exchange(self.send, out)
         self._each(lambda r: self.st.axis3(r, self.g, out[r], False, scale))
 
+    def _ordered(self):
+        return getattr(self.ex, "ordered", False) and len(self.ranks) == 1
+
     def _exchange(self, send, recv):
+        if self._ordered():
+            r = self.ranks[0]
+            with self.st.stream(r):
+                self.ex.all_to_all(send, recv)
+            return
         for r in self.ranks:
             self.st.synchronize(r)
         self.ex.all_to_all(send, recv)
@@ -373,32 +390,53 @@ class SlabADMMTV(_Base):
 
     def _halo_x(self):
         g, pl = self.g, self.g.plane
-        self._sync_all()
+        ordered = self._ordered()
+        if not ordered:
+            self._sync_all()
         lo_src = {r: self.x_ext[r][pl:2 * pl] for r in self.ranks}                    # first slab plane
         hi_src = {r: self.x_ext[r][g.sz * pl:(g.sz + 1) * pl] for r in self.ranks}     # last slab plane
-        self.ex.ring_shift(hi_src, self.halo_lo, lo_src, self.halo_hi)
-        for r in self.ranks:
-            self.x_ext[r][0:pl].copy_(self.halo_lo[r])
-            self.x_ext[r][(g.sz + 1) * pl:(g.sz + 2) * pl].copy_(self.halo_hi[r])
-        self._torch_sync()
+
+        def body():
+            self.ex.ring_shift(hi_src, self.halo_lo, lo_src, self.halo_hi)
+            for r in self.ranks:
+                self.x_ext[r][0:pl].copy_(self.halo_lo[r])
+                self.x_ext[r][(g.sz + 1) * pl:(g.sz + 2) * pl].copy_(self.halo_hi[r])
+        if ordered:
+            with self.st.stream(self.ranks[0]):
+                body()
+        else:
+            body()
+            self._torch_sync()
 
     def _halo_dual(self, d):
         g, pl = self.g, self.g.plane
         ext = (g.sz + 1) * pl
-        self._sync_all()
-        for r in self.ranks:
-            for c in range(3):
-                self.dhalo_out[r][c * pl:(c + 1) * pl].copy_(d[r][c * ext + g.sz * pl:c * ext + (g.sz + 1) * pl])
-        self.ex.ring_shift(self.dhalo_out, self.dhalo_in)
-        for r in self.ranks:
-            for c in range(3):
-                d[r][c * ext:c * ext + pl].copy_(self.dhalo_in[r][c * pl:(c + 1) * pl])
-        self._torch_sync()
+        ordered = self._ordered()
+        if not ordered:
+            self._sync_all()
+
+        def body():
+            for r in self.ranks:
+                for c in range(3):
+                    self.dhalo_out[r][c * pl:(c + 1) * pl].copy_(
+                        d[r][c * ext + g.sz * pl:c * ext + (g.sz + 1) * pl])
+            self.ex.ring_shift(self.dhalo_out, self.dhalo_in)
+            for r in self.ranks:
+                for c in range(3):
+                    d[r][c * ext:c * ext + pl].copy_(self.dhalo_in[r][c * pl:(c + 1) * pl])
+        if ordered:
+            with self.st.stream(self.ranks[0]):
+                body()
+        else:
+            body()
+            self._torch_sync()
 
     def iterate(self, k: int = 1):
         g, pl = self.g, self.g.plane
         s = 1.0 / math.sqrt(g.N)
-        for _ in range(k):
+        # per-iteration scalars stay on the device (fit, residual^2, TV); gathered once after the loop
+        hist = {r: self.st.zeros(r, 3 * k) for r in self.ranks}
+        for it in range(k):
             self.forward3_theta()
             self._each(lambda r: self.st.tv_fold(r, g, self.Yl[r], self.lam[r], self.W[r], self.mu, self.tau, s,
                                                  self.s_fit[r]))
@@ -412,10 +450,21 @@ class SlabADMMTV(_Base):
             self._each(lambda r: self.st.stencil(r, g, False, self.x_ext[r], din[r], dout[r], self.theta[r],
                                                  self.lam_tv / self.mu, self.s_st[r]))
             self.cur = 1 - self.cur
-            fit = sum(float(v[0]) for v in self.ex.gather(self.s_fit))
-            stv = self.ex.gather(self.s_st)
-            res2 = sum(float(v[0]) for v in stv)
-            tv = sum(float(v[1]) for v in stv)
+
+            def keep(r, it=it):
+                hist[r][3 * it:3 * it + 1].copy_(self.s_fit[r][0:1])
+                hist[r][3 * it + 1:3 * it + 3].copy_(self.s_st[r][0:2])
+            self._each(keep)
+        if self._ordered():  # the history was written on the rank's stream
+            with self.st.stream(self.ranks[0]):
+                h = self.ex.gather(hist)
+        else:
+            self._sync_all()
+            h = self.ex.gather(hist)  # rank order: deterministic sums for a given P
+        for it in range(k):
+            fit = sum(float(v[3 * it]) for v in h)
+            res2 = sum(float(v[3 * it + 1]) for v in h)
+            tv = sum(float(v[3 * it + 2]) for v in h)
             self.objective.append(0.5 * fit + self.lam_tv * tv)
             self.primal_residual.append(math.sqrt(res2))
 
