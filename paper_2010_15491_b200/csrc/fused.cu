@@ -182,107 +182,6 @@ __global__ void __launch_bounds__(FShape<L, A>::THREADS, (512 / FShape<L, A>::TH
     }
 }
 
-// ---------------------------------------------------------------- Tikhonov v2
-// Same fold + inverse axis-3 FFT with the register profile of the plain
-// strided pass (16 values per thread, 128-thread CTAs, ~5 CTAs/SM): Lambda is
-// parked in this thread's own slots of the FFT exchange buffer while the fold
-// runs (same thread writes and reads them, so no barrier), and the buffer is
-// reused by the transform afterwards.
-template <int L, int A, int DS, int T>
-__global__ void __launch_bounds__(T * A * (L / 16), (512 / (T * A * (L / 16))) > 0 ? 512 / (T * A * (L / 16)) : 1)
-    tik_fold_ax3_v2_kernel(FoldGeom G, const double2* __restrict__ Yl, const double2* __restrict__ lam,
-                           const double2* __restrict__ xbh, double2* __restrict__ out, double reg2, double shift,
-                           double inv2l, double invsqrtd, const double2* __restrict__ tw) {
-    using Pl = fftc::Plan<L, 16>;
-    constexpr int R = Pl::R, P = Pl::P, NLN = T * A, RD = R / DS;
-    static_assert(R % DS == 0, "ds must divide 16");
-    extern __shared__ double2 sm[];
-    const int tid = threadIdx.x;
-    const int ln = tid % NLN, t = tid / NLN;
-    const int ti = ln % T, a = ln / T;
-    const int br = a % G.dr, bc = a / G.dr;
-    const long long tpr = G.ml / T;
-    const long long g1 = (blockIdx.x % tpr) * T + ti, g2 = blockIdx.x / tpr;
-    const long long f1 = g1 + br * G.ml, f2 = g2 + bc * G.nl;
-    const long long base = f1 + G.m * f2, stride = G.m * G.n;
-    auto sidx = [&](int q) { return q * NLN + ln; };
-    double2 v[R];
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-        const long long off = base + stride * (t + P * r);
-        v[r] = __ldg(xbh + off);
-        sm[sidx(t + P * r)] = __ldg(lam + off);
-    }
-    const double2* Yrow = Yl + g1 + G.ml * g2;
-    const long long Ystride = G.ml * G.nl;
-#pragma unroll
-    for (int rr = 0; rr < RD; ++rr) {
-        const double2 yv = cscale(__ldg(Yrow + Ystride * (t + P * rr)), invsqrtd);
-        double Sx = 0.0, Sy = 0.0, gram = 0.0;
-#pragma unroll
-        for (int bs = 0; bs < DS; ++bs) {
-            const int r = rr + RD * bs;
-            const double2 Lr = sm[sidx(t + P * r)];
-            v[r] = cadd(cmulc(Lr, yv), cscale(v[r], reg2));  // k (solvers.cpp:53-54)
-            gram += cnorm(Lr);
-            const double2 pr = cmul(Lr, v[r]);
-            Sx += pr.x;
-            Sy += pr.y;
-        }
-        Sx = lanes_sum<T, A>(Sx);
-        Sy = lanes_sum<T, A>(Sy);
-        gram = lanes_sum<T, A>(gram);
-        const double den = gram + shift;
-        const double2 w = make_double2(Sx / den, Sy / den);
-#pragma unroll
-        for (int bs = 0; bs < DS; ++bs) {
-            const int r = rr + RD * bs;
-            const double2 Lr = sm[sidx(t + P * r)];
-            v[r] = cscale(csub(v[r], cmulc(Lr, w)), inv2l);  // x̂ (solvers.cpp:60-62)
-        }
-    }
-    __syncthreads();  // the exchange buffer changes hands
-    fftc::stockham<L, true, decltype(sidx), 16>(v, t, sm, sidx, tw);
-#pragma unroll
-    for (int j = 0; j < R; ++j) out[base + stride * Pl::out_q(t, j)] = v[j];
-}
-
-template <int L, int A, int DS, int T>
-void launch_tik_v2(const FoldGeom& G, const double2* Yl, const double2* lam, const double2* xbh, double2* out,
-                   double reg, cudaStream_t st) {
-    auto kern = tik_fold_ax3_v2_kernel<L, A, DS, T>;
-    const int threads = T * A * (L / 16);
-    const size_t smem = (size_t)T * A * L * sizeof(double2);
-    if (smem > 48 * 1024)
-        VSR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    const unsigned grid = (unsigned)((G.ml / T) * G.nl);
-    kern<<<grid, threads, smem, st>>>(G, Yl, lam, xbh, out, 2.0 * reg, 2.0 * reg * (double)G.d, 1.0 / (2.0 * reg),
-                                      1.0 / std::sqrt((double)G.d), fft_engine().twiddles((size_t)L));
-    VSR_LAUNCH_CHECK();
-}
-
-bool dispatch_tik_v2(const FoldGeom& G, const double2* Yl, const double2* lam, const double2* xbh, double2* out,
-                     double reg, cudaStream_t st) {
-    const int A = G.dr * G.dc;
-    static const int vt = [] {
-        const char* e = std::getenv("VSR_TIK_V2_T");
-        return e ? std::atoi(e) : 2;
-    }();
-    if (A == 4 && G.ds == 2 && G.ml % 2 == 0) {
-        switch (G.s) {
-            case 256:
-                if (vt == 8 && G.ml % 8 == 0) launch_tik_v2<256, 4, 2, 8>(G, Yl, lam, xbh, out, reg, st);
-                else if (vt == 4 && G.ml % 4 == 0) launch_tik_v2<256, 4, 2, 4>(G, Yl, lam, xbh, out, reg, st);
-                else launch_tik_v2<256, 4, 2, 2>(G, Yl, lam, xbh, out, reg, st);
-                return true;
-            case 512: launch_tik_v2<512, 4, 2, 2>(G, Yl, lam, xbh, out, reg, st); return true;
-            case 1024: launch_tik_v2<1024, 4, 2, 2>(G, Yl, lam, xbh, out, reg, st); return true;
-            default: return false;
-        }
-    }
-    return false;
-}
-
 // ---------------------------------------------------------------- fold + axis 1
 // The fold fused with the contiguous axis-1 pass.  A CTA owns T consecutive
 // g2 x the A = dc*ds alias rows (g2 + bc nl, g3 + bs sl) of one g3, full rows
@@ -713,11 +612,6 @@ void launch_tik_fold_ifft3(const FoldGeom& G, const double2* Yl, const double2* 
     GammaTables none{nullptr, nullptr, nullptr, 0.0};
     const double shift = 2.0 * reg * (double)G.d;  // solvers.cpp:43
     const double inv2l = 1.0 / (2.0 * reg);         // solvers.cpp:59
-    static const bool v2 = [] {
-        const char* e = std::getenv("VSR_TIK_V2");
-        return e && e[0] == '1';
-    }();
-    if (v2 && dispatch_tik_v2(G, Yl, lam, xbh, out, reg, st)) return;
     if (!dispatch<false, false>(G, Yl, lam, sep, xbh, Zl, nullptr, out, none, 2.0 * reg, shift, inv2l, 1.0,
                                 nullptr, st))
         throw std::logic_error("launch_tik_fold_ifft3: unsupported geometry");
