@@ -1414,6 +1414,12 @@ struct vsr_tv {
     SepState sep;
     DevBuf<double> gw;  // LR table sum_b Gamma_b |Lambda_b|^2 (axis-1 sandwich)
     DevBuf<double2> W2;  // sandwich output on the half-spectrum path (m x n x (s/2+1))
+    DevBuf<int> iter_dev;  // iteration index read by the finalize kernel (graph replay)
+    cudaGraphExec_t gexec = nullptr;  // two consecutive iterations (one dual ping-pong period)
+    uint64_t g_kernels = 0;
+    ~vsr_tv() {
+        if (gexec) cudaGraphExecDestroy(gexec);
+    }
     size_t iters_done = 0;
     bool dual_in_a = true;
     bool stopped = false;
@@ -1494,6 +1500,8 @@ static vsr_tv* tv_build(vsr_ctx* ctx, const Spec& sp, const double* y_dev, const
         h->rel.alloc(h->max_iters);
         h->status.alloc(4);
         h->init_obj.alloc(1);
+        h->iter_dev.alloc(1);
+        VSR_CUDA(cudaMemsetAsync(h->iter_dev.p, 0, sizeof(int), st));
         const double st_init[4] = {-1.0, 0.0, 0.0, 0.0};
         h2d(ctx, h->status.p, st_init, sizeof(st_init));
         VSR_CUDA(cudaMemsetAsync(h->bad.p, 0xff, sizeof(unsigned long long), st));
@@ -1621,7 +1629,7 @@ static void tv_step(vsr_tv* h) {
                           h->rel_tol > 0.0 ? h->xprev.p : nullptr, h->stp.p, st);
     }
     h->dual_in_a = !h->dual_in_a;
-    TvIterScalars sc{h->obj.p, h->res.p, h->rel.p, h->status.p};
+    TvIterScalars sc{h->obj.p, h->res.p, h->rel.p, h->status.p, h->iter_dev.p};
     {
         ProfScope ps(prof, "tv_finalize", st);
         launch_tv_finalize((int)h->iters_done, h->fitp.p,
@@ -1635,8 +1643,56 @@ static void tv_step(vsr_tv* h) {
     ++h->iters_done;
 }
 
+// Fixed-count iterations (rel_tol = 0, profiler off) replay a CUDA graph of
+// two consecutive iterations (the dual buffers ping-pong with period 2; the
+// iteration index lives on the device).  VSR_NO_GRAPH=1 keeps eager launches.
 static void tv_iterate(vsr_tv* h, size_t iters) {
-    for (size_t k = 0; k < iters && !h->stopped && h->iters_done < h->max_iters; ++k) {
+    static const bool no_graph = [] {
+        const char* e = std::getenv("VSR_NO_GRAPH");
+        return e && e[0] == '1';
+    }();
+    size_t k = 0;
+    const bool graphs = !no_graph && h->rel_tol <= 0.0 && h->ctx->prof() == nullptr;
+    if (graphs) {
+        cudaStream_t st = h->ctx->stream;
+        while (k + 2 <= iters && h->iters_done + 2 <= h->max_iters) {
+            if (!h->dual_in_a || h->iters_done == 0) {  // align to the captured parity / warm up
+                tv_step(h);
+                ++k;
+                continue;
+            }
+            if (!h->gexec) {
+                const uint64_t l0 = g_launches.load(), f0 = g_fwd.load(), i0 = g_inv.load();
+                const size_t it0 = h->iters_done;
+                cudaGraph_t graph = nullptr;
+                VSR_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+                try {
+                    tv_step(h);
+                    tv_step(h);
+                } catch (...) {
+                    cudaStreamEndCapture(st, &graph);
+                    if (graph) cudaGraphDestroy(graph);
+                    throw;
+                }
+                VSR_CUDA(cudaStreamEndCapture(st, &graph));
+                const cudaError_t e = cudaGraphInstantiate(&h->gexec, graph, 0);
+                cudaGraphDestroy(graph);
+                VSR_CUDA(e);
+                h->g_kernels = g_launches.load() - l0;
+                g_launches.fetch_sub(h->g_kernels);  // counted when the graph runs
+                g_fwd.fetch_sub(g_fwd.load() - f0);
+                g_inv.fetch_sub(g_inv.load() - i0);
+                h->iters_done = it0;  // the captured steps have not run yet
+            }
+            VSR_CUDA(cudaGraphLaunch(h->gexec, st));
+            g_launches.fetch_add(h->g_kernels);
+            g_fwd += 2;
+            g_inv += 2;
+            h->iters_done += 2;
+            k += 2;
+        }
+    }
+    for (; k < iters && !h->stopped && h->iters_done < h->max_iters; ++k) {
         tv_step(h);
         if (h->rel_tol > 0.0) {  // stop test (:405) needs the scalar now
             double rc = 0.0;

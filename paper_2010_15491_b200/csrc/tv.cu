@@ -529,6 +529,7 @@ __global__ void __launch_bounds__(1024)
         if (init_obj) {
             *init_obj = obj;
         } else {
+            if (sc.iter_dev) iter = (*sc.iter_dev)++;
             sc.objective[iter] = obj;
             sc.primal_residual[iter] = sqrt(resid);
             sc.rel_change[iter] = sqrt(dx2) / fmax(sqrt(xp2), 1e-300);

@@ -43,6 +43,8 @@ struct TvIterScalars {
     double* primal_residual;  // [max_iters]
     double* rel_change;       // [max_iters]
     double* status;           // [4]: first residue violation iter (-1 none), its ratio, last ratio, pad
+    int* iter_dev = nullptr;  // optional device iteration counter (read and advanced by the finalize),
+                              // so a captured iteration replays without new kernel arguments
 };
 void launch_tv_finalize(int iter, const double* fit_partials, size_t fit_blocks,
                         const double* st_partials, size_t st_blocks, const double* res_partials,
