@@ -946,6 +946,7 @@ static void tik_spatial(vsr_tikhonov* t, cudaStream_t st) {
     std::vector<double> kp;
     spatial_phase_taps(t->sp.rates, p.h, p.dmin, taps, p.dm, kp);
     taps.swap(kp);
+    p.kp_host = taps;
     t->sp_taps.alloc(taps.size());
     t->sp_s1.alloc(s1.size());
     t->sp_s2.alloc(s2.size());

@@ -344,6 +344,294 @@ __global__ void __launch_bounds__(SP_THREADS, (DM <= 8 ? 8 : 6)) spatial_expand_
     }
 }
 
+// ------------------------------------------------ expand kernel, z march
+// Same polyphase correlation, reordered so the output-heavy axis runs last
+// from registers: a CTA owns a CX x CY LR column (output W x H per plane) and
+// marches along z through its chunk of LR planes.  Four stages per LR plane:
+//   a. the prefetched LR tile (LY x LX with the x/y halo) is parked in smem and
+//      the next plane's tile is fetched into registers;
+//   b. stage x: one LR row, two LR cells x R1 phases per item (pair loads);
+//   c. stage y: one output column, two LR cells x R2 phases per item;
+//   d. stage z: each thread keeps the last DM xy-expanded planes of its
+//      column pairs in a register ring (slot = plane mod DM, compile-time via
+//      the DM-fold unroll) and writes R3 output planes, 16-B stores.
+// The stages are software-pipelined: phase p parks plane p, runs stage x on
+// plane p - 1, y on p - 2 and z on p - 3 out of double-buffered tiles, so a
+// phase holds four independent pieces of work and ends in ONE barrier.
+// No z halo is re-read except the DM - 1 warm-up planes of each chunk; taps
+// are kernel parameters (constant-bank operands of the DFMAs).  Finiteness:
+// fma(v, 0, chk) turns any inf/nan into a NaN chk; a thread that sees one
+// rescans its own outputs for the first bad flat index.
+constexpr int MX_CX = 16, MX_CY = 4, MX_THREADS = 128, MX_KMAX = 64;
+constexpr int MX_ZCMAX = 64;
+constexpr int MX_PD = 3;  // LR plane tiles in flight (cp.async ring depth - 2)  // LR planes per CTA chunk (bounds the prior's smem stage)
+
+struct MarchArgs {
+    int m, n, s, ml, nl, sl;
+    int dmin1, dmin2, dmin3;
+    int zc;  // LR planes per CTA
+    double k1[MX_KMAX], k2[MX_KMAX], k3[MX_KMAX];
+    const double* u;
+    const double* z;
+    double* x;
+    unsigned long long* bad;
+};
+
+template <int DM, int R1, int R2, int R3, int CY>
+__global__ void __launch_bounds__(MX_THREADS, 4) spatial_march_kernel(const __grid_constant__ MarchArgs A) {
+    static_assert(R1 == 2, "stage z pairs (2c, 2c + 1) assume the lattice column is the even one");
+    constexpr int CX = MX_CX, NT = MX_THREADS;
+    constexpr int LX = CX + DM - 1, LY = CY + DM - 1;
+    constexpr int LXP = LX + (LX & 1);  // even pitch: 16-B aligned pair loads
+    constexpr int W = R1 * CX, H = R2 * CY;
+    constexpr int NLD = (LY * LX + NT - 1) / NT;
+    constexpr int NXI = LY * (CX / 2), NYI = W * (CY / 2);
+    constexpr int NPAIR = (DM + 2) / 2;  // pair loads covering DM + 1 inputs
+    constexpr int CPR = W / 2, RG = NT / CPR, RPT = H / RG;
+    static_assert(NT % CPR == 0 && H % RG == 0, "stage-z thread map");
+    constexpr int NB = MX_PD + 2, LTB = LY * LXP + 2;  // + pad slot (keeps 16-B alignment)
+    __shared__ __align__(16) double lt[NB][LTB];
+    constexpr int NZB = MX_PD + 4;  // prior ring: fetched PD phases before plane q lands, read 3 after
+    __shared__ __align__(16) double zs[NZB][CY * CX];
+    __shared__ __align__(16) double ex[2][LY * W];
+    __shared__ __align__(16) double ey[2][H * W];
+    __shared__ int xoff[LX], yoff[LY];
+
+    const int tid = threadIdx.x;
+    const int cx0 = blockIdx.x * CX, cy0 = blockIdx.y * CY;
+    const int c30 = blockIdx.z * A.zc;
+    const int nz = min(A.zc, A.sl - c30);
+    if (tid < LX)
+        xoff[tid] = wrap_idx(cx0 + A.dmin1 + tid, A.ml);
+    else if (tid >= 32 && tid < 32 + LY)
+        yoff[tid - 32] = wrap_idx(cy0 + A.dmin2 + tid - 32, A.nl) * A.ml;
+    __syncthreads();
+    // loads past the tile read offset 0 and park in the pad slot (never read),
+    // so the prefetch is unconditional: no select keeps a register waiting on it
+    int loff[NLD], lsm[NLD];
+#pragma unroll
+    for (int k = 0; k < NLD; ++k) {
+        const int e = tid + NT * k;
+        if (e < LY * LX) {
+            const int qy = e / LX, qx = e - qy * LX;
+            loff[k] = yoff[qy] + xoff[qx];
+            lsm[k] = qy * LXP + qx;
+        } else {
+            loff[k] = 0;
+            lsm[k] = LY * LXP;
+        }
+    }
+    const long long plane = (long long)A.ml * A.nl;
+    const int jend = nz + DM - 1;  // LR planes the chunk reads
+    int zq = wrap_idx(c30 + A.dmin3, A.sl);  // LR z of the next plane to fetch
+    const int cp = tid % CPR, rg = tid / CPR;
+    const int X0 = cx0 * R1, Y0 = cy0 * R2;
+    double2 ring[RPT][DM];
+    double chk = 0.0;
+    // LR plane tiles: cp.async ring of NB buffers, MX_PD planes in flight
+    // per-element shared addresses of buffer 0 and global pointers of LR z = 0
+    unsigned lsa[NLD];
+    const double* lgp[NLD];
+#pragma unroll
+    for (int k = 0; k < NLD; ++k) {
+        lsa[k] = (unsigned)__cvta_generic_to_shared(&lt[0][lsm[k]]);
+        lgp[k] = A.u + loff[k];
+    }
+    int qb = 0;  // ring buffer of the next fetch
+    auto fetch = [&](int q) {
+        if (q < jend) {
+            const long long zo = zq * plane;
+            const unsigned bo = (unsigned)(qb * LTB) * 8u;
+#pragma unroll
+            for (int k = 0; k < NLD; ++k)
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(lsa[k] + bo), "l"(lgp[k] + zo)
+                             : "memory");
+            zq = zq + 1 == A.sl ? 0 : zq + 1;
+            qb = qb + 1 == NB ? 0 : qb + 1;
+        }
+        // the lattice prior of output plane c3 (its last LR plane is q): cold in
+        // HBM, so it rides in the same group, DM + 2 phases before stage z reads it
+        const int oz = q - (DM - 1);
+        if (A.z && oz >= 0 && oz < nz && tid < CY * (CX / 2)) {
+            const int h = tid % (CX / 2), y = tid / (CX / 2);
+            const double* g = A.z + ((long long)(c30 + oz) * A.nl + cy0 + y) * A.ml + cx0 + 2 * h;
+            const unsigned sa = (unsigned)__cvta_generic_to_shared(&zs[oz % NZB][2 * tid]);
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(g) : "memory");
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");  // (empty past the chunk: uniform counting)
+    };
+    for (int q = 0; q < MX_PD; ++q) fetch(q);
+    const long long hplane = (long long)A.n * A.m;
+    double* const xrow = A.x + (long long)(Y0 + rg * RPT) * A.m + X0 + 2 * cp;
+    for (int pb = 0; pb < jend + 3; pb += DM) {
+#pragma unroll
+        for (int s = 0; s < DM; ++s) {
+            const int p = pb + s;
+            if (p >= jend + 3) break;
+            // a. fetch plane p + PD; plane p must land before this phase's barrier
+            fetch(p + MX_PD);
+            // d. stage z on plane p - 3 (issued first: its loads and stores
+            //    overlap the smem work of stages x and y below)
+            const int jz = p - 3;
+            if (jz >= 0) {
+                const double* eb = ey[jz & 1];
+                const int slot = ((s - 3) % DM + DM) % DM;  // compile-time after the unroll
+#pragma unroll
+                for (int rr = 0; rr < RPT; ++rr)
+                    ring[rr][slot] = *reinterpret_cast<const double2*>(eb + (rg * RPT + rr) * W + 2 * cp);
+                if (jz >= DM - 1) {
+                    const int c3 = c30 + jz - (DM - 1);  // LR plane of the outputs
+                    double zv[RPT];
+#pragma unroll
+                    for (int rr = 0; rr < RPT; ++rr) {
+                        const int row = rg * RPT + rr;
+                        zv[rr] = (A.z && row % R2 == 0) ? zs[(c3 - c30) % NZB][(row / R2) * CX + cp] : 0.0;
+                    }
+#pragma unroll
+                    for (int ph = 0; ph < R3; ++ph) {
+                        double* xp = xrow + (long long)(R3 * c3 + ph) * hplane;
+#pragma unroll
+                        for (int rr = 0; rr < RPT; ++rr) {
+                            double ax = 0.0, ay = 0.0;
+#pragma unroll
+                            for (int i = 0; i < DM; ++i) {
+                                const double2 v = ring[rr][(slot + 1 + i) % DM];
+                                ax = fma(A.k3[ph * DM + i], v.x, ax);
+                                ay = fma(A.k3[ph * DM + i], v.y, ay);
+                            }
+                            if (ph == 0) ax += zv[rr];
+                            chk = fma(ax, 0.0, chk);
+                            chk = fma(ay, 0.0, chk);
+                            __stcs(reinterpret_cast<double2*>(xp + (long long)rr * A.m), make_double2(ax, ay));  // streaming: x must not evict u
+                        }
+                    }
+                }
+            }
+            // b. stage x on plane p - 1
+            const int jx = p - 1;
+            if (jx >= 0 && jx < jend) {
+                const double* lb = lt[jx % NB];
+                double* xb = ex[jx & 1];
+                for (int it = tid; it < NXI; it += NT) {
+                    const int qy = it / (CX / 2), c = 2 * (it - qy * (CX / 2));
+                    const double* row = lb + qy * LXP + c;
+                    double in[2 * NPAIR];
+#pragma unroll
+                    for (int i = 0; i < NPAIR; ++i) {
+                        const double2 v = *reinterpret_cast<const double2*>(row + 2 * i);
+                        in[2 * i] = v.x;
+                        in[2 * i + 1] = v.y;
+                    }
+                    double o[2 * R1];
+#pragma unroll
+                    for (int cell = 0; cell < 2; ++cell)
+#pragma unroll
+                        for (int ph = 0; ph < R1; ++ph) {
+                            double acc = 0.0;
+#pragma unroll
+                            for (int i = 0; i < DM; ++i) acc = fma(A.k1[ph * DM + i], in[cell + i], acc);
+                            o[cell * R1 + ph] = acc;
+                        }
+                    double* dst = xb + qy * W + R1 * c;
+#pragma unroll
+                    for (int i = 0; i < 2 * R1; i += 2)
+                        *reinterpret_cast<double2*>(dst + i) = make_double2(o[i], o[i + 1]);
+                }
+            }
+            // c. stage y on plane p - 2
+            const int jy = p - 2;
+            if (jy >= 0 && jy < jend) {
+                const double* xb = ex[jy & 1];
+                double* yb = ey[jy & 1];
+                for (int it = tid; it < NYI; it += NT) {
+                    const int cy = 2 * (it / W), n = it % W;
+                    double in[DM + 1];
+#pragma unroll
+                    for (int i = 0; i < DM + 1; ++i) in[i] = xb[(cy + i) * W + n];
+#pragma unroll
+                    for (int cell = 0; cell < 2; ++cell)
+#pragma unroll
+                        for (int ph = 0; ph < R2; ++ph) {
+                            double acc = 0.0;
+#pragma unroll
+                            for (int i = 0; i < DM; ++i) acc = fma(A.k2[ph * DM + i], in[cell + i], acc);
+                            yb[(R2 * (cy + cell) + ph) * W + n] = acc;
+                        }
+                }
+            }
+            asm volatile("cp.async.wait_group %0;" ::"n"(MX_PD) : "memory");  // plane p (and the prior) landed
+            __syncthreads();
+        }
+    }
+    if (chk != chk) {  // some output is inf/nan: find this thread's first one
+        unsigned long long best = ~0ull;
+        for (int c3 = c30; c3 < c30 + nz; ++c3)
+            for (int ph = 0; ph < R3; ++ph)
+                for (int rr = 0; rr < RPT; ++rr)
+                    for (int e = 0; e < 2; ++e) {
+                        const unsigned long long idx =
+                            ((unsigned long long)(R3 * c3 + ph) * A.n + Y0 + rg * RPT + rr) * A.m + X0 + 2 * cp + e;
+                        if (!isfinite(A.x[idx]) && idx < best) best = idx;
+                    }
+        atomicMin(A.bad, best);
+    }
+}
+
+template <int DM, int R3, int CY>
+static void launch_march_cy(MarchArgs& A, unsigned tx, unsigned ty, cudaStream_t st) {
+    auto kern = spatial_march_kernel<DM, 2, 2, R3, CY>;
+    int dev = 0, sms = 0;
+    VSR_CUDA(cudaGetDevice(&dev));
+    VSR_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    // z chunk length: minimise waves x (planes per CTA incl. the DM - 1 warm-up
+    // planes and 3 pipeline phases); ties: the longer chunk
+    const long long cols = (long long)tx * ty;
+    static long long memo_key = -1;  // per instantiation: last (sl, cols, prior) and its choice
+    static int memo_zc = 0;
+    const long long key = ((long long)A.sl << 33) ^ (cols << 1) ^ (A.z ? 1 : 0);
+    int zc = std::min(A.sl, MX_ZCMAX);
+    double best = 1e300;
+    int occ = 0;
+    if (memo_key != key) VSR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, MX_THREADS, 0));
+    for (int c = memo_key == key ? 0 : std::min(A.sl, MX_ZCMAX); c >= 4; --c) {
+        const long long ctas = cols * ((A.sl + c - 1) / c), slots = (long long)std::max(occ, 1) * sms;
+        const double cost = (double)((ctas + slots - 1) / slots) * (c + DM + 2);
+        if (cost < best) best = cost, zc = c;
+    }
+    if (memo_key == key)
+        zc = memo_zc;
+    else
+        memo_key = key, memo_zc = zc;
+    if (const char* e = std::getenv("VSR_MARCH_ZC")) zc = std::max(1, std::atoi(e));
+    zc = std::min(std::min(zc, A.sl), MX_ZCMAX);
+    A.zc = zc;
+    const unsigned tz = (unsigned)((A.sl + zc - 1) / zc);
+    kern<<<dim3(tx, ty, tz), MX_THREADS, 0, st>>>(A);
+    VSR_LAUNCH_CHECK();
+}
+
+template <int DM, int R3>
+static void launch_march_k(MarchArgs& A, unsigned tx, unsigned ty, cudaStream_t st) {
+    static const bool cy8 = [] {
+        const char* e = std::getenv("VSR_MARCH_CY");  // 8-row column tiles unless VSR_MARCH_CY=4
+        return !(e && e[0] == '4');
+    }();
+    if (cy8 && ty % 2 == 0)
+        launch_march_cy<DM, R3, 8>(A, tx, ty / 2, st);
+    else
+        launch_march_cy<DM, R3, 4>(A, tx, ty, st);
+}
+
+// The march kernel serves rates (2, 2, 2|4) with a tile-aligned LR grid.
+static bool march_ok(const Dims& hr, const int rates[3], int dm) {
+    if (rates[0] != 2 || rates[1] != 2 || (rates[2] != 2 && rates[2] != 4)) return false;
+    if (dm != 4 && dm != 5 && dm != 7 && dm != 8) return false;
+    if (hr.s / rates[2] < 1) return false;
+    const char* e = std::getenv("VSR_NO_MARCH");
+    if (e && e[0] == '1') return false;
+    return (hr.m / 2) % MX_CX == 0 && (hr.n / 2) % MX_CY == 0 && rates[2] * dm <= MX_KMAX;
+}
+
 static const int kDms[] = {4, 5, 7, 8, 12, 16};  // 5, 7: the 9- and 13-tap PSFs at rate 2
 
 // DM (padded taps per phase) serving every axis, 0 if the support is too wide.
@@ -393,6 +681,26 @@ void launch_spatial_expand(const Dims& hr, const int rates[3], const SpatialPlan
     const int dm = spatial_tile(p, rates);
     if (!dm) throw std::logic_error("spatial_expand: support too wide for the tile budget");
     if (dm != p.dm) throw std::logic_error("spatial_expand: plan taps built for another width");
+    if (march_ok(hr, rates, dm) && p.kp_host.size() == (size_t)(rates[0] + rates[1] + rates[2]) * dm) {
+        MarchArgs M{};
+        M.m = (int)hr.m, M.n = (int)hr.n, M.s = (int)hr.s;
+        M.ml = M.m / 2, M.nl = M.n / 2, M.sl = M.s / rates[2];
+        M.dmin1 = p.dmin[0], M.dmin2 = p.dmin[1], M.dmin3 = p.dmin[2];
+        const double* kp = p.kp_host.data();
+        for (int i = 0; i < 2 * dm; ++i) M.k1[i] = kp[i];
+        for (int i = 0; i < 2 * dm; ++i) M.k2[i] = kp[2 * dm + i];
+        for (int i = 0; i < rates[2] * dm; ++i) M.k3[i] = kp[4 * dm + i];
+        M.u = u, M.z = z, M.x = x, M.bad = bad;
+        const unsigned tx = (unsigned)(M.ml / MX_CX), ty = (unsigned)(M.nl / MX_CY);
+        const bool r4 = rates[2] == 4;
+        switch (dm) {
+            case 4: r4 ? launch_march_k<4, 4>(M, tx, ty, st) : launch_march_k<4, 2>(M, tx, ty, st); break;
+            case 5: r4 ? launch_march_k<5, 4>(M, tx, ty, st) : launch_march_k<5, 2>(M, tx, ty, st); break;
+            case 7: r4 ? launch_march_k<7, 4>(M, tx, ty, st) : launch_march_k<7, 2>(M, tx, ty, st); break;
+            default: r4 ? launch_march_k<8, 4>(M, tx, ty, st) : launch_march_k<8, 2>(M, tx, ty, st); break;
+        }
+        return;
+    }
     ExpandArgs A;
     A.m = (int)hr.m, A.n = (int)hr.n, A.s = (int)hr.s;
     A.ml = A.m / rates[0], A.nl = A.n / rates[1], A.sl = A.s / rates[2];

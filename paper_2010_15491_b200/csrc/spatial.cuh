@@ -29,6 +29,7 @@ struct SpatialPlan {
     int ndelta[3] = {0, 0, 0};            // LR offsets a phase can touch
     int dm = 0;                           // padded taps per phase (kernel template width)
     const double* kp = nullptr;           // device phase-padded taps (spatial_phase_taps)
+    std::vector<double> kp_host;          // the same taps on the host (march kernel: kernel parameters)
     // per-axis alias sums of the spectral tables (device): A1, A2 (ml), B1, B2 (nl), C1, C2 (sl)
     const double2* s1[3] = {nullptr, nullptr, nullptr};
     const double* s2[3] = {nullptr, nullptr, nullptr};

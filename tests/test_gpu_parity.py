@@ -160,7 +160,10 @@ SPATIAL_CASES = [((64, 64, 64), (2, 2, 2), (9, 9, 9), (1.0, 1.0, 1.0)),
                  ((40, 24, 16), (2, 2, 2), (7, 5, 5), (1.3, 1.1, 0.9)),
                  ((6, 4, 4), (3, 2, 1), (3, 3, 3), (1.0, 1.0, 1.0)),
                  ((128, 32, 64), (2, 1, 2), (15, 15, 9), (1.2, 1.2, 2.0)),
-                 ((96, 16, 8), (3, 2, 2), (9, 7, 7), (1.4, 1.0, 1.0))]
+                 ((96, 16, 8), (3, 2, 2), (9, 7, 7), (1.4, 1.0, 1.0)),
+                 # z-march expand kernel: 13-tap (DM 7) at rate 2, config-3-like (DM 8, r3 = 4)
+                 ((64, 32, 48), (2, 2, 2), (13, 13, 13), (1.5, 1.5, 1.5)),
+                 ((32, 16, 40), (2, 2, 4), (15, 15, 21), (1.2, 1.2, 2.0))]
 
 
 @pytest.mark.parametrize("dims,rates,ksz,sigma", SPATIAL_CASES)
@@ -483,6 +486,10 @@ print("ok", op.path())
     ({"VSR_NO_GRAPH": "1"}, (64, 64, 32), (2, 2, 2)),
     ({"VSR_A1_RM": "8"}, (64, 64, 64), (4, 4, 4)),
     ({"VSR_A1_PERSIST": "1"}, (64, 64, 64), (4, 4, 4)),
+    ({"VSR_NO_MARCH": "1"}, (64, 64, 32), (2, 2, 2)),
+    ({"VSR_MARCH_ZC": "5"}, (64, 64, 32), (2, 2, 2)),
+    ({"VSR_MARCH_ZC": "1"}, (64, 64, 32), (2, 2, 2)),
+    ({"VSR_MARCH_CY": "4"}, (64, 64, 32), (2, 2, 2)),
 ])
 def test_env_variants(env, dims, rates):
     import os
