@@ -395,6 +395,8 @@ def run_b200(args, rank, world, local):
 
     if not args.no_tv:
         line["tv"] = bench_tv(args, ctx, V, synth, torch, stream, local, hbm)
+    if not args.no_fft_path:
+        line["fft3_vs_cufft"] = bench_fft_compare(args, ctx, V, torch, stream, local, hbm)
     if world > 1 or args.sharded:
         line["sharded"] = bench_sharded(args, ctx, V, synth, torch, rank, world, local)
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -428,6 +430,57 @@ def tik_fft_path_ms(args, ctx, V, spec, lam_d, cfg, xbar_d, y_d, x_d, stream, to
     op.check()
     op.close()
     return tot / args.steps
+
+
+def bench_fft_compare(args, ctx, V, torch, stream, local, hbm, edge=256):
+    """The hand-written fp64 3D FFT engine (vsr_fft3_d: unitary C2C, three
+    axis passes) next to cuFFT (torch.fft.fftn, norm="ortho") on the same
+    256^3 complex128 buffer; cuFFT is timed only as a comparison (BASELINE
+    north_star).  Inputs exceed L2 (268 MB), so no flush is needed."""
+    import ctypes as C
+    dev = torch.device("cuda", local)
+    n = edge ** 3
+    g = torch.Generator(device=dev).manual_seed(5)
+    x = torch.complex(torch.rand(n, generator=g, device=dev, dtype=torch.float64),
+                      torch.rand(n, generator=g, device=dev, dtype=torch.float64))
+    ours = torch.empty_like(x)
+    dims = (C.c_size_t * 3)(edge, edge, edge)
+    scale = 1.0 / math.sqrt(n)
+
+    def run_ours():
+        V.check(V._lib.vsr_fft3_d(ctx.handle, dims, C.c_void_p(x.data_ptr()), 0, C.c_void_p(ours.data_ptr()),
+                                  scale))
+
+    def run_cufft():
+        return torch.fft.fftn(x.view(edge, edge, edge), norm="ortho")
+
+    def timed(fn, st):
+        for _ in range(3):
+            with torch.cuda.stream(st):
+                fn()
+        torch.cuda.synchronize()
+        tot = 0.0
+        reps = max(5, args.steps)
+        for _ in range(reps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            with torch.cuda.stream(st):
+                a.record(st)
+                fn()
+                b.record(st)
+            b.synchronize()
+            tot += a.elapsed_time(b)
+        return tot / reps
+
+    ms_ours = timed(run_ours, stream)
+    ms_cufft = timed(run_cufft, torch.cuda.current_stream(dev))
+    ref = run_cufft().reshape(-1)
+    torch.cuda.synchronize()
+    err = float(torch.linalg.vector_norm(ours - ref) / torch.linalg.vector_norm(ref))
+    alg = 32.0 * n  # read + write 16 B per point, once (SURVEY 8(d) compulsory model)
+    return {"workload": f"unitary forward 3D C2C FFT, complex128 {edge}^3 (out of place)",
+            "ms_ours": ms_ours, "ms_cufft": ms_cufft, "speedup_vs_cufft": ms_cufft / ms_ours,
+            "ours_gbs_compulsory": alg / (ms_ours * 1e-3) / 1e9, "ours_frac": alg / (ms_ours * 1e-3) / 1e9 / hbm,
+            "rel_l2_vs_cufft": err, "cufft": "torch.fft.fftn (cuFFT, library) -- comparison only"}
 
 
 def bench_tv(args, ctx, V, synth, torch, stream, local, hbm):

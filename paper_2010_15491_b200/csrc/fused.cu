@@ -256,6 +256,33 @@ __device__ __forceinline__ void fold_axis1_tile(int tile, FoldGeom G, const doub
     }
     __syncthreads();
     auto row_base = [&](int j) { return rowbase_s[j]; };
+    // TV: the per-position tables (blur factor a, Gamma row term, Gw row) go to
+    // shared memory by cp.async now, and the per-line scalars to registers, so
+    // their latency hides under the W load and the forward FFT
+    __shared__ __align__(16) double2 sa_s[TV ? L : 1];
+    __shared__ __align__(16) double nr_s[TV ? L : 1];
+    __shared__ __align__(16) double gw_s[TV ? T * (L / DR) : 1];  // one Gw row per LR g2 of the tile
+    double2 bc_ = make_double2(0.0, 0.0);
+    double base_g = 0.0;
+    if constexpr (TV) {
+        if (sep.a) {
+            for (int i = tid; i < L; i += THREADS)
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(sa_s + i)),
+                             "l"(sep.a + i) : "memory");
+            bc_ = cmul(__ldg(sep.b + f2), __ldg(sep.c + f3));
+        }
+        for (int i = tid; i < L; i += THREADS)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(nr_s + i)),
+                         "l"(tabs.nr + i) : "memory");
+        if (tabs.gw)
+            for (int i = tid; i < T * (L / DR); i += THREADS) {
+                const long long gi2 = (long long)bx2 * T + i / (L / DR);
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(gw_s + i)),
+                             "l"(tabs.gw + G.ml * (gi2 + G.nl * g3) + i % (L / DR)) : "memory");
+            }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        base_g = __ldg(tabs.nc + f2) + __ldg(tabs.ns + f3);
+    }
     double2 v[R];
     // LR spectrum of y for this row: issued first so its latency overlaps the
     // forward transform
@@ -291,7 +318,8 @@ __device__ __forceinline__ void fold_axis1_tile(int tile, FoldGeom G, const doub
         fftc::to_natural<L, RM>(v);
 #pragma unroll
         for (int r = 0; r < R; ++r) v[r] = cscale(v[r], fwd_scale);
-        __syncthreads();  // exchange buffer reused for Lambda below
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        __syncthreads();  // exchange buffer reused for Lambda below; tables landed
     } else if (Zl) {
         const double2* zrow = Zl + G.ml * (g2 + G.nl * g3);
 #pragma unroll
@@ -306,15 +334,18 @@ __device__ __forceinline__ void fold_axis1_tile(int tile, FoldGeom G, const doub
     }
 #pragma unroll
     if (sep.a) {
-        const double2 bc_ = cmul(__ldg(sep.b + f2), __ldg(sep.c + f3));
+        if constexpr (TV) {
 #pragma unroll
-        for (int r = 0; r < R; ++r) sm[sidx(t + P * r)] = cmul(__ldg(sep.a + (t + P * r)), bc_);
+            for (int r = 0; r < R; ++r) sm[sidx(t + P * r)] = cmul(sa_s[t + P * r], bc_);
+        } else {
+            const double2 bcv = cmul(__ldg(sep.b + f2), __ldg(sep.c + f3));
+#pragma unroll
+            for (int r = 0; r < R; ++r) sm[sidx(t + P * r)] = cmul(__ldg(sep.a + (t + P * r)), bcv);
+        }
     } else {
 #pragma unroll
         for (int r = 0; r < R; ++r) sm[sidx(t + P * r)] = __ldg(lam + rowb + t + P * r);
     }
-    double base_g = 0.0;
-    if constexpr (TV) base_g = __ldg(tabs.nc + f2) + __ldg(tabs.ns + f3);
     double fit = 0.0;
     if constexpr (TV) {
         if (tabs.gw) {
@@ -323,7 +354,7 @@ __device__ __forceinline__ void fold_axis1_tile(int tile, FoldGeom G, const doub
             // sum_b Lambda_b x̂_b = (S - Gw w) / mu
             double gwv[RD];
 #pragma unroll
-            for (int rr = 0; rr < RD; ++rr) gwv[rr] = __ldg(tabs.gw + (Yrow - Yl) + t + P * rr);
+            for (int rr = 0; rr < RD; ++rr) gwv[rr] = gw_s[ti * (L / DR) + t + P * rr];
 #pragma unroll
             for (int rr = 0; rr < RD; ++rr) {
                 const double2 yraw = yr[rr];
@@ -334,7 +365,7 @@ __device__ __forceinline__ void fold_axis1_tile(int tile, FoldGeom G, const doub
                 for (int br = 0; br < DR; ++br) {
                     const int r = rr + RD * br;
                     const double2 Lr = sm[sidx(t + P * r)];
-                    Gg[br] = fast_rcp((__ldg(tabs.nr + (t + P * r)) + base_g) + tabs.tau);
+                    Gg[br] = fast_rcp((nr_s[t + P * r] + base_g) + tabs.tau);
                     v[r] = cscale(cadd(cmulc(Lr, yv), cscale(v[r], cA)), Gg[br]);
                     const double2 pr = cmul(Lr, v[r]);
                     Sx += pr.x;
@@ -373,7 +404,7 @@ __device__ __forceinline__ void fold_axis1_tile(int tile, FoldGeom G, const doub
             const int r = rr + RD * br;
             const double2 Lr = sm[sidx(t + P * r)];
             if constexpr (TV) {
-                Gg[br] = 1.0 / ((__ldg(tabs.nr + (t + P * r)) + base_g) + tabs.tau);
+                Gg[br] = 1.0 / ((nr_s[t + P * r] + base_g) + tabs.tau);
                 v[r] = cscale(cadd(cmulc(Lr, yv), cscale(v[r], cA)), Gg[br]);
                 gram += Gg[br] * cnorm(Lr);
             } else {
