@@ -130,7 +130,7 @@ def decimate(x: np.ndarray, rates) -> np.ndarray:
 def degrade(x: np.ndarray, psf: np.ndarray, rates, bsnr_db: Optional[float], seed: int):
     """y = D H x + n (reference sim.cpp:106-127 conventions, numpy host side)."""
     lam = np.fft.rfftn(psf)
-    hx = np.fft.irfftn(np.fft.rfftn(x) * lam, s=x.shape)
+    hx = np.fft.irfftn(np.fft.rfftn(x) * lam, s=x.shape, axes=(0, 1, 2))
     y = decimate(hx, rates)
     sigma = 0.0
     if bsnr_db is not None:
