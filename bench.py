@@ -402,6 +402,8 @@ def run_b200(args, rank, world, local):
     if rank == 0 and world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(cfg, inp)
     op.close()
+    if world == 1 and not args.no_config4:
+        line["config4"] = bench_config4(args, ctx, V, synth, torch, stream, local, hbm)
     if rank == 0:
         print(json.dumps(line), flush=True)
     return 0
@@ -481,6 +483,108 @@ def bench_fft_compare(args, ctx, V, torch, stream, local, hbm, edge=256):
             "ms_ours": ms_ours, "ms_cufft": ms_cufft, "speedup_vs_cufft": ms_cufft / ms_ours,
             "ours_gbs_compulsory": alg / (ms_ours * 1e-3) / 1e9, "ours_frac": alg / (ms_ours * 1e-3) / 1e9 / hbm,
             "rel_l2_vs_cufft": err, "cufft": "torch.fft.fftn (cuFFT, library) -- comparison only"}
+
+
+class _Dev:
+    """A torch device tensor seen through the C ABI's device-pointer entry points."""
+
+    def __init__(self, t):
+        import ctypes as C
+        self.t = t
+        self.ptr = C.c_void_p(t.data_ptr())
+
+
+def bench_config4(args, ctx, V, synth, torch, stream, local, hbm):
+    """configs[4] on ONE GPU (the P = 1 point of its slab-sharded run): HR
+    1024^3 -> LR 512^3 (d = 8), sigma 1.5 13^3 PSF; one Tikhonov solve
+    (tau 1e-3, CLI-default lattice prior) then 20 ADMM-TV iterations (lambda
+    2e-3, mu 0.05).  Timing only: y is a seeded uniform LR volume generated on
+    the device (the kernels' work is value-independent; parity at this size is
+    tests/test_full_configs.py).  Needs ~135 GB of device memory."""
+    import ctypes as C
+    cfg = synth.CONFIGS[4]
+    dev = torch.device("cuda", local)
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    free, _ = torch.cuda.mem_get_info(dev)
+    if free < 150e9:
+        return {"skipped": f"needs ~150 GB free device memory, {free / 1e9:.0f} GB free"}
+    m, n, s = cfg.hr
+    N = m * n * s
+    d = int(np.prod(cfg.rates))
+    r1, r2, r3 = cfg.rates
+    spec = V.DecimationSpec(cfg.hr, cfg.rates)
+    g = torch.Generator(device=dev).manual_seed(cfg.seeds[-1])
+    y = torch.rand(s // r3, n // r2, m // r1, generator=g, device=dev, dtype=torch.float64)
+    kern = torch.from_numpy(np.ascontiguousarray(V.make_gaussian_psf(cfg.psf_size, cfg.psf_sigma,
+                                                                     cfg.psf_size))).to(dev)
+    psf = torch.zeros(s, n, m, device=dev, dtype=torch.float64)
+    idx = []
+    for k, L in zip(kern.shape, (s, n, m)):
+        i = torch.arange(k, device=dev)
+        idx.append(torch.where(i <= k // 2, i, i - k) % L)
+    psf[idx[0][:, None, None], idx[1][None, :, None], idx[2][None, None, :]] = kern
+    out = {"workload": "config4 on 1 GPU: HR 1024^3 -> LR 512^3 (d=8), PSF sigma 1.5 13^3, Tikhonov tau 1e-3 "
+                       "then 20 ADMM-TV iterations (lambda 2e-3, mu 0.05, tau 1e-3*mu)",
+           "data": "seeded uniform LR y generated on the device (timing only)"}
+
+    def ev_time(fn, reps):
+        tot = 0.0
+        for _ in range(reps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            fn()
+            b.record(stream)
+            b.synchronize()
+            tot += a.elapsed_time(b)
+        return tot / reps
+
+    # Tikhonov: Lambda on the device (unnormalised DFT of the PSF), lattice prior d D^H y
+    lam = torch.empty(N, device=dev, dtype=torch.complex128)
+    dims = (C.c_size_t * 3)(m, n, s)
+    torch.cuda.synchronize()
+    V.check(V._lib.vsr_fft3_d(ctx.handle, dims, C.c_void_p(psf.data_ptr()), 1, C.c_void_p(lam.data_ptr()), 1.0))
+    ctx.synchronize()
+    xbar = torch.zeros(s, n, m, device=dev, dtype=torch.float64)
+    xbar[::r3, ::r2, ::r1] = d * y
+    x = torch.empty(s, n, m, device=dev, dtype=torch.float64)
+    torch.cuda.synchronize()
+    op = V.TikhonovDevice(ctx, spec, _Dev(lam), cfg.reg, _Dev(xbar))
+    for _ in range(3):
+        op.solve_d(_Dev(y), _Dev(x))
+    ms_tik = ev_time(lambda: op.solve_d(_Dev(y), _Dev(x)), max(3, min(args.steps, 10)))
+    op.check()
+    out["tikhonov_ms"] = ms_tik
+    out["tikhonov_value"] = N / (ms_tik * 1e-3)
+    out["tikhonov_spatial_path"] = op.spatial()
+    op.close()
+    del lam, xbar, x
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    # ADMM-TV: construction timed separately (setup: Lambda, tables, init)
+    iters = 20
+    tcfg = V.TvAdmmConfig(lambda_=cfg.tv_lambda, mu=cfg.tv_mu, max_iters=iters + 4, rel_tol=0.0,
+                          tau=1e-3 * cfg.tv_mu, init=V.INIT_UPSAMPLED)
+    t0 = time.perf_counter()
+    tv = V.TvDevice(ctx, spec, _Dev(y), _Dev(psf), tcfg)
+    ctx.synchronize()
+    out["tv_setup_s"] = time.perf_counter() - t0
+    tv.iterate(2)
+    k = 4
+    ms_it = ev_time(lambda: tv.iterate(k), 1) / k
+    rep = tv.report()
+    tv.close()
+    out["tv_ms_per_iter"] = ms_it
+    out["tv_value"] = N / (ms_it * 1e-3)
+    out["tv_iters_timed"] = k
+    out["objective_last"] = rep.objective[-1]
+    out["job_ms"] = ms_tik + iters * ms_it
+    out["job_note"] = "one Tikhonov solve + 20 ADMM-TV iterations, device-resident inputs, setup excluded"
+    out["tik_frac_general_model"] = V.tikhonov_algorithmic_bytes(cfg.hr, cfg.rates) / (ms_tik * 1e-3) / 1e9 / hbm
+    out["tv_frac_model"] = V.tv_algorithmic_bytes(cfg.hr, cfg.rates) / (ms_it * 1e-3) / 1e9 / hbm
+    del psf, y
+    torch.cuda.empty_cache()
+    return out
 
 
 def bench_tv(args, ctx, V, synth, torch, stream, local, hbm):
@@ -598,6 +702,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-tv", action="store_true")
+    ap.add_argument("--no-config4", action="store_true", help="skip the 1024^3 single-GPU config-4 timing")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-fft-path", action="store_true", help="skip timing the general FFT-path solve")
     ap.add_argument("--sharded", action="store_true", help="also time the slab-sharded config-3 path at N=1")
