@@ -688,11 +688,29 @@ def bench_sharded(args, ctx, V, synth, torch, rank, world, local):
         ms = float(t.item())
     N = g.N
     a2a = 2 * 16 * (N // world) * (world - 1) / world
-    return {"workload": "config3: ADMM-TV fp64 512x512x256 -> 256x256x64 (d=2,2,4), slab-sharded over "
-                        f"{world} GPU(s): NCCL all-to-all FFT transposes + ring halos",
-            "value": N / (ms * 1e-3), "unit": "HR voxels/s per ADMM-TV iteration", "ms_per_iter": ms,
-            "iters_timed": k, "scaling": "strong", "alltoall_bytes_per_rank_per_iter": a2a,
-            "note": "host-orchestrated stages (python), exchanges synchronous"}
+    out = {"workload": "config3: ADMM-TV fp64 512x512x256 -> 256x256x64 (d=2,2,4), slab-sharded over "
+                       f"{world} GPU(s): NCCL all-to-all FFT transposes + ring halos",
+           "value": N / (ms * 1e-3), "unit": "HR voxels/s per ADMM-TV iteration", "ms_per_iter": ms,
+           "iters_timed": k, "scaling": "strong", "alltoall_bytes_per_rank_per_iter": a2a,
+           "note": "host-orchestrated stages (python), exchanges synchronous"}
+    del tv
+    if world == 1:
+        # the same config through the single-GPU path (half-spectrum fused kernels, graph replay)
+        V = __import__("paper_2010_15491_b200.volsr", fromlist=["volsr"])
+        spec = V.DecimationSpec(hr, rates)
+        psf_d = torch.from_numpy(np.ascontiguousarray(psf)).reshape(-1).to(dev)
+        tcfg = V.TvAdmmConfig(lambda_=cfg.tv_lambda, mu=cfg.tv_mu, max_iters=k + 4, rel_tol=0.0,
+                              tau=1e-3 * cfg.tv_mu, init=V.INIT_UPSAMPLED)
+        one = V.TvDevice(ctx, spec, _Dev(y), _Dev(psf_d), tcfg)
+        one.iterate(2)
+        ctx.synchronize()
+        e0.record(lib)
+        one.iterate(k)
+        e1.record(lib)
+        e1.synchronize()
+        one.close()
+        out["single_gpu_path_ms_per_iter"] = e0.elapsed_time(e1) / k
+    return out
 
 
 def main():

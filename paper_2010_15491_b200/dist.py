@@ -246,8 +246,11 @@ class _Base:
         self.ranks = exchange.ranks
         g = self.g
         self.work = {r: stages.zeros(r, 2 * g.slab_elems) for r in self.ranks}
-        self.send = {r: stages.zeros(r, 2 * g.slab_elems) for r in self.ranks}
-        self.recv = {r: stages.zeros(r, 2 * g.slab_elems) for r in self.ranks}
+        # one rank: the all-to-all is the identity, so the xy stage packs straight
+        # into the spectral buffer and the inverse unpacks straight from it
+        self.solo = exchange.world == 1
+        self.send = {} if self.solo else {r: stages.zeros(r, 2 * g.slab_elems) for r in self.ranks}
+        self.recv = {} if self.solo else {r: stages.zeros(r, 2 * g.slab_elems) for r in self.ranks}
 
     def _each(self, fn):
         for r in self.ranks:
@@ -257,8 +260,10 @@ class _Base:
     def forward3(self, slabs: Dict[int, torch.Tensor], real: bool, scale: float,
                  out: Dict[int, torch.Tensor]):
         """Distributed forward 3D FFT: z-slabs -> local spectral layout (m, n/P, s)."""
-        self._each(lambda r: self.st.fwd_xy_pack(r, self.g, slabs[r], real, self.work[r], self.send[r]))
-        self._exchange(self.send, out)
+        dst = out if self.solo else self.send
+        self._each(lambda r: self.st.fwd_xy_pack(r, self.g, slabs[r], real, self.work[r], dst[r]))
+        if not self.solo:
+            self._exchange(self.send, out)
         self._each(lambda r: self.st.axis3(r, self.g, out[r], False, scale))
 
     def _ordered(self):
@@ -289,8 +294,10 @@ class _Base:
         self._each(f)
 
     def _inverse_to_slabs(self, W, out_slabs, scale, sums, bad):
-        self._exchange(W, self.recv)
-        self._each(lambda r: self.st.unpack_inv_xy(r, self.g, self.recv[r], self.work[r], out_slabs[r], scale,
+        src = W if self.solo else self.recv
+        if not self.solo:
+            self._exchange(W, self.recv)
+        self._each(lambda r: self.st.unpack_inv_xy(r, self.g, src[r], self.work[r], out_slabs[r], scale,
                                                    sums[r], bad[r]))
 
 
@@ -470,8 +477,10 @@ class SlabADMMTV(_Base):
 
     def forward3_theta(self):
         g = self.g
-        self._each(lambda r: self.st.fwd_xy_pack(r, g, self.theta[r], True, self.work[r], self.send[r]))
-        self._exchange(self.send, self.W)
+        dst = self.W if self.solo else self.send
+        self._each(lambda r: self.st.fwd_xy_pack(r, g, self.theta[r], True, self.work[r], dst[r]))
+        if not self.solo:
+            self._exchange(self.send, self.W)
 
     def x_slab(self, r):
         pl = self.g.plane
