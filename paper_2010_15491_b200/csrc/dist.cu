@@ -10,7 +10,9 @@
 // host orchestrator (paper_2010_15491_b200/dist.py) with NCCL through
 // torch.distributed; these functions are the device work between them, all
 // enqueued on the context stream.
+#include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <functional>
 #include <string>
 #include <vector>
@@ -164,6 +166,63 @@ struct DevGuard {
 };
 }  // namespace
 
+namespace {
+// Per-rank constant state of the TV fold, built on the first call for a given
+// (context, Lambda slice, geometry, rank) and reused by every iteration: the
+// Gamma tables (global rows/slices, local columns), the fit partials, and -
+// when this rank's Lambda slice is separable, Lambda = a[f1] b[jl] c[f3] -
+// the local 1-D factors, so the fused fold rebuilds Lambda instead of
+// streaming 16 N / P bytes per iteration.  lam_loc must stay constant while
+// it is used (the slab ADMM-TV program computes it once).
+struct TvFoldState {
+    const void* ctx = nullptr;
+    const double* lam = nullptr;
+    long long m = 0, nP = 0, s = 0, rank = -1, P = 0;
+    int rates[3] = {0, 0, 0};
+    double* nr = nullptr;
+    double* nc = nullptr;
+    double* ns = nullptr;
+    double* fitp = nullptr;
+    double2* sep = nullptr;  // a (m) | b (nP) | c (s), or nullptr
+    size_t nb = 0;
+};
+
+TvFoldState& tv_fold_state(vsr_ctx* ctx, const Slab& g, int rank, const double* lam_loc, const FoldGeom& G,
+                           cudaStream_t st) {
+    static std::vector<TvFoldState> cache;
+    for (auto& e : cache)
+        if (e.ctx == ctx && e.lam == lam_loc && e.m == g.m && e.nP == g.nP && e.s == g.s && e.rank == rank &&
+            e.P == g.P && e.rates[0] == g.rates[0] && e.rates[1] == g.rates[1] && e.rates[2] == g.rates[2])
+            return e;
+    TvFoldState e;
+    e.ctx = ctx, e.lam = lam_loc, e.m = g.m, e.nP = g.nP, e.s = g.s, e.rank = rank, e.P = g.P;
+    for (int a = 0; a < 3; ++a) e.rates[a] = g.rates[a];
+    const auto nr = diff_norm_table(g.m), ns = diff_norm_table(g.s), ncg = diff_norm_table(g.n);
+    std::vector<double> nc((size_t)g.nP);
+    for (long long jl = 0; jl < g.nP; ++jl) nc[(size_t)jl] = ncg[(size_t)row_of(jl, rank, g.nlP, g.nl)];
+    VSR_CUDA(cudaMalloc(&e.nr, nr.size() * sizeof(double)));
+    VSR_CUDA(cudaMalloc(&e.nc, nc.size() * sizeof(double)));
+    VSR_CUDA(cudaMalloc(&e.ns, ns.size() * sizeof(double)));
+    VSR_CUDA(cudaMemcpyAsync(e.nr, nr.data(), nr.size() * sizeof(double), cudaMemcpyHostToDevice, st));
+    VSR_CUDA(cudaMemcpyAsync(e.nc, nc.data(), nc.size() * sizeof(double), cudaMemcpyHostToDevice, st));
+    VSR_CUDA(cudaMemcpyAsync(e.ns, ns.data(), ns.size() * sizeof(double), cudaMemcpyHostToDevice, st));
+    e.nb = fused_axis3_ok(G) ? tv_sandwich_blocks(G) : tv_fold_blocks(G);
+    VSR_CUDA(cudaMalloc(&e.fitp, std::max<size_t>(e.nb, 1) * sizeof(double)));
+    if (fused_axis3_ok(G)) {
+        const Dims ld{(size_t)g.m, (size_t)g.nP, (size_t)g.s};
+        VSR_CUDA(cudaMalloc(&e.sep, (ld.m + ld.n + ld.s) * sizeof(double2)));
+        if (!detect_separable(ld, reinterpret_cast<const double2*>(lam_loc), e.sep, e.sep + ld.m,
+                              e.sep + ld.m + ld.n, 1e-13, st)) {
+            VSR_CUDA(cudaFree(e.sep));
+            e.sep = nullptr;
+        }
+    }
+    cache.push_back(e);
+    return cache.back();
+}
+
+}  // namespace
+
 extern "C" {
 
 int vsr_fft3_d(vsr_ctx* ctx, const size_t dims[3], const double* in, int in_real, double* out_c,
@@ -250,40 +309,23 @@ int vsr_slab_tv_fold_d(vsr_ctx* ctx, const size_t hr[3], const size_t rates[3], 
         const Slab g = make_slab(hr, rates, P);
         const FoldGeom G = local_geom(g);
         cudaStream_t st = vsr_capi::stream_of(ctx);
-        // Gamma tables: global rows/slices, local columns (rows of this rank's set)
-        const auto nr = diff_norm_table(g.m), ns = diff_norm_table(g.s), ncg = diff_norm_table(g.n);
-        std::vector<double> nc((size_t)g.nP);
-        for (long long jl = 0; jl < g.nP; ++jl) nc[(size_t)jl] = ncg[(size_t)row_of(jl, rank, g.nlP, g.nl)];
-        double *dnr = nullptr, *dnc = nullptr, *dns = nullptr, *fitp = nullptr;
-        VSR_CUDA(cudaMallocAsync(&dnr, nr.size() * sizeof(double), st));
-        VSR_CUDA(cudaMallocAsync(&dnc, nc.size() * sizeof(double), st));
-        VSR_CUDA(cudaMallocAsync(&dns, ns.size() * sizeof(double), st));
-        VSR_CUDA(cudaMemcpyAsync(dnr, nr.data(), nr.size() * sizeof(double), cudaMemcpyHostToDevice, st));
-        VSR_CUDA(cudaMemcpyAsync(dnc, nc.data(), nc.size() * sizeof(double), cudaMemcpyHostToDevice, st));
-        VSR_CUDA(cudaMemcpyAsync(dns, ns.data(), ns.size() * sizeof(double), cudaMemcpyHostToDevice, st));
-        GammaTables tabs{dnr, dnc, dns, tau};
+        const TvFoldState& fs = tv_fold_state(ctx, g, rank, lam_loc, G, st);
+        GammaTables tabs{fs.nr, fs.nc, fs.ns, tau};
         auto* Wc = reinterpret_cast<double2*>(W);
         const auto* Y = reinterpret_cast<const double2*>(Yl_loc);
         const auto* L = reinterpret_cast<const double2*>(lam_loc);
         const Dims ld{(size_t)g.m, (size_t)g.nP, (size_t)g.s};
-        size_t nb;
         if (fused_axis3_ok(G)) {
-            nb = tv_sandwich_blocks(G);
-            VSR_CUDA(cudaMallocAsync(&fitp, std::max<size_t>(nb, 1) * sizeof(double), st));
-            launch_tv_sandwich(G, Y, L, Wc, tabs, mu, fwd_scale, fitp, st);
+            SepTables sep;
+            if (fs.sep) sep = SepTables{fs.sep, fs.sep + ld.m, fs.sep + ld.m + ld.n};
+            launch_tv_sandwich(G, Y, L, Wc, tabs, mu, fwd_scale, fs.fitp, st, sep);
         } else {
-            nb = tv_fold_blocks(G);
-            VSR_CUDA(cudaMallocAsync(&fitp, std::max<size_t>(nb, 1) * sizeof(double), st));
             fft_engine().axis_pass(ld, 2, false, Wc, IN_COMPLEX, Wc, OUT_COMPLEX, fwd_scale, nullptr, st);
-            launch_tv_fold(G, Y, L, Wc, Wc, nullptr, tabs, mu, fitp, st);
+            launch_tv_fold(G, Y, L, Wc, Wc, nullptr, tabs, mu, fs.fitp, st);
             fft_engine().axis_pass(ld, 2, true, Wc, IN_COMPLEX, Wc, OUT_COMPLEX, 1.0, nullptr, st);
         }
-        sum_partials_kernel<<<1, 1024, 0, st>>>(fitp, 1, 1, (long long)nb, fit_out);
+        sum_partials_kernel<<<1, 1024, 0, st>>>(fs.fitp, 1, 1, (long long)fs.nb, fit_out);
         VSR_LAUNCH_CHECK();
-        cudaFreeAsync(fitp, st);
-        cudaFreeAsync(dnr, st);
-        cudaFreeAsync(dnc, st);
-        cudaFreeAsync(dns, st);
     });
 }
 

@@ -126,7 +126,7 @@ __global__ void __launch_bounds__(FShape<L, A>::THREADS, (512 / FShape<L, A>::TH
             const int r = rr + RD * bs;
             if constexpr (TV) {
                 // k = conj(L) F D^H y + mu theta_hat (solvers.cpp:342-344,375); ĝ = Γ k (:223)
-                Gg[bs] = 1.0 / ((base_g + __ldg(tabs.ns + (t + P * r))) + tabs.tau);
+                Gg[bs] = fast_rcp((base_g + __ldg(tabs.ns + (t + P * r))) + tabs.tau);
                 v[r] = cscale(cadd(cmulc(Lm[r], yv), cscale(v[r], cA)), Gg[bs]);
                 gram += Gg[bs] * cnorm(Lm[r]);
             } else {
@@ -142,7 +142,13 @@ __global__ void __launch_bounds__(FShape<L, A>::THREADS, (512 / FShape<L, A>::TH
         Sy = lanes_sum<T, A>(Sy);
         gram = lanes_sum<T, A>(gram);
         const double den = gram + shift;
-        const double2 w = make_double2(Sx / den, Sy / den);
+        double2 w;
+        if constexpr (TV) {
+            const double iden = fast_rcp(den);
+            w = make_double2(Sx * iden, Sy * iden);
+        } else {
+            w = make_double2(Sx / den, Sy / den);
+        }
         double ax = 0.0, ay = 0.0;
 #pragma unroll
         for (int bs = 0; bs < DS; ++bs) {
