@@ -121,6 +121,7 @@ inline void check(int rc) {
         case VSR_ERR_INVALID: throw std::invalid_argument(m);
         case VSR_ERR_NUMERIC: throw numeric_error(m);
         case VSR_ERR_OUT_OF_RANGE: throw std::out_of_range(m);
+        case VSR_ERR_IO: throw io_error(m);
         default: throw std::runtime_error(m);
     }
 }
@@ -271,6 +272,34 @@ inline Volume3D make_gaussian_psf(const PsfSpec& spec, const Dims3& hr) {
                 psf.at(i, j, l) += k[a + kr * b + kr * kc * c];
             }
     return psf;
+}
+
+// ------------------------------------------------------------- volume_io.hpp
+enum class VolumeDType { f32, f64 };
+
+inline std::string strip_volume_extension(const std::string& path) {
+    auto ends = [&](const char* e) {
+        const std::string x(e);
+        return path.size() >= x.size() && path.compare(path.size() - x.size(), x.size(), x) == 0;
+    };
+    if (ends(".volhdr")) return path.substr(0, path.size() - 7);
+    if (ends(".vol")) return path.substr(0, path.size() - 4);
+    return path;
+}
+
+inline void save_volume(const Volume3D& v, const std::string& base, VolumeDType dtype = VolumeDType::f64) {
+    const detail::D3 d(v.dims());
+    detail::check(vsr_save_volume(base.c_str(), d.v, v.data().data(),
+                                  dtype == VolumeDType::f32 ? VSR_DTYPE_F32 : VSR_DTYPE_F64));
+}
+
+inline Volume3D load_volume(const std::string& base) {
+    std::size_t d[3];
+    int t = 0;
+    detail::check(vsr_volume_header(base.c_str(), d, &t));
+    Volume3D v(Dims3{d[0], d[1], d[2]});
+    detail::check(vsr_load_volume(base.c_str(), v.data().data(), v.size()));
+    return v;
 }
 
 inline SpectrumDiag psf_to_spectrum(const Volume3D& psf) { return SpectrumDiag{dft3_unnormalized(psf)}; }

@@ -37,6 +37,7 @@ extern "C" {
 #define VSR_ERR_OUT_OF_RANGE 4 /* std::out_of_range */
 #define VSR_ERR_CUDA 5         /* device / runtime failure (no reference analogue) */
 #define VSR_ERR_INTERNAL 6
+#define VSR_ERR_IO 7           /* volsr::io_error (volume files) */
 
 typedef struct vsr_ctx vsr_ctx;
 typedef struct vsr_tikhonov vsr_tikhonov;
@@ -52,6 +53,23 @@ int vsr_ctx_destroy(vsr_ctx* ctx);
 int vsr_ctx_synchronize(vsr_ctx* ctx);
 void* vsr_ctx_stream(vsr_ctx* ctx); /* cudaStream_t */
 int vsr_ctx_device(vsr_ctx* ctx);
+
+/* ---- volume files: replaces volsr::load_volume / save_volume /
+ *      strip_volume_extension (src/volume_io.cpp:27-131, include/volsr/volume_io.hpp).
+ *      <base>.volhdr (dims=m,n,s / dtype=f32|f64 / order=lex) + <base>.vol (raw
+ *      little-endian scalars, lexicographic).  `path` may carry either extension.
+ *      Errors: VSR_ERR_IO (io_error text of the reference), VSR_ERR_SHAPE (buffer
+ *      size), VSR_ERR_NUMERIC (save of a non-finite value).  The _d variants
+ *      stream the payload between the file and device memory in 32 MB chunks
+ *      through two pinned buffers (f32 crosses PCIe narrow and is converted on
+ *      the device; the non-finite check runs on the device). */
+#define VSR_DTYPE_F64 0
+#define VSR_DTYPE_F32 1
+int vsr_volume_header(const char* path, size_t dims_out[3], int* dtype_out);
+int vsr_load_volume(const char* path, double* out, size_t count);
+int vsr_save_volume(const char* path, const size_t dims[3], const double* v, int dtype);
+int vsr_load_volume_d(vsr_ctx* ctx, const char* path, double* dev_out, size_t count);
+int vsr_save_volume_d(vsr_ctx* ctx, const char* path, const size_t dims[3], const double* dev_in, int dtype);
 
 /* pinned host / device memory helpers (for end-to-end staging) */
 int vsr_host_alloc(size_t bytes, void** out);

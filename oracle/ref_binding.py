@@ -49,6 +49,8 @@ def _setup():
                               C.c_int, C.c_double, C.c_int, _dp, _dp, _dp, _dp, _sz, _dp, _dp]
     L.ref_admm_l2l2.argtypes = [_sz, _sz, _dp, _dp, C.c_double, _dp, C.c_size_t, C.c_double, C.c_double,
                                 _dp, _dp, _dp, _sz, _dp]
+    L.ref_save_volume.argtypes = [C.c_char_p, _sz, _dp, C.c_int]
+    L.ref_load_volume.argtypes = [C.c_char_p, _sz, _dp, C.c_size_t]
 
 
 class RefError(RuntimeError):
@@ -198,3 +200,18 @@ def admm_l2l2(y, lam, hr, rates, reg, xbar, max_iters, mu=0.1, rel_tol=1e-10):
     k = iters.value
     return x, {"iterations": k, "initial_objective": init_obj.value, "objective": obj[:k],
                "primal_residual": res[:k]}
+
+
+def save_volume(base, v, f32=False):
+    """reference volsr::save_volume (volume_io.cpp:34-57)."""
+    v = np.ascontiguousarray(v, dtype=np.float64)
+    _chk(_lib.ref_save_volume(str(base).encode(), _d(_dims(v)), _p(v), int(bool(f32))))
+
+
+def load_volume(base, cap=1 << 20):
+    """reference volsr::load_volume (volume_io.cpp:61-131); returns (s, n, m) array."""
+    d = (C.c_size_t * 3)()
+    out = np.empty(cap)
+    _chk(_lib.ref_load_volume(str(base).encode(), d, _p(out), cap))
+    m, n, s = int(d[0]), int(d[1]), int(d[2])
+    return out[:m * n * s].reshape(s, n, m).copy()

@@ -12,6 +12,7 @@
 #include "volsr/operators.hpp"
 #include "volsr/solvers.hpp"
 #include "volsr/spectral.hpp"
+#include "volsr/volume_io.hpp"
 
 using namespace volsr;
 
@@ -193,6 +194,22 @@ int ref_admm_l2l2(const size_t hr[3], const size_t rates[3], const double* y, co
         }
         *iters = rep.iterations;
         *init_obj = rep.initial_objective;
+    });
+}
+
+// volume_io.cpp:34-131 (save_volume / load_volume) for the file-format goldens
+int ref_save_volume(const char* base, const size_t d[3], const double* v, int f32) {
+    return wrap([&] {
+        Volume3D vol(Dims3{d[0], d[1], d[2]}, std::vector<double>(v, v + d[0] * d[1] * d[2]));
+        save_volume(vol, base, f32 ? VolumeDType::f32 : VolumeDType::f64);
+    });
+}
+int ref_load_volume(const char* base, size_t d_out[3], double* out, size_t cap) {
+    return wrap([&] {
+        const Volume3D v = load_volume(base);
+        d_out[0] = v.dims().m, d_out[1] = v.dims().n, d_out[2] = v.dims().s;
+        if (v.size() > cap) throw std::invalid_argument("ref_load_volume: buffer too small");
+        put(v, out);
     });
 }
 

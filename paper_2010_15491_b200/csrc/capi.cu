@@ -119,6 +119,9 @@ int guarded(F&& f) {
     } catch (const vsr::cuda_error& e) {
         g_last_error = e.what();
         return VSR_ERR_CUDA;
+    } catch (const vsr::io_error& e) {
+        g_last_error = e.what();
+        return VSR_ERR_IO;
     } catch (const std::exception& e) {
         g_last_error = e.what();
         return VSR_ERR_INTERNAL;

@@ -24,6 +24,9 @@ struct numeric_error : std::runtime_error {
 struct cuda_error : std::runtime_error {
     using std::runtime_error::runtime_error;
 };
+struct io_error : std::runtime_error {  // volume.hpp:22 (volume files)
+    using std::runtime_error::runtime_error;
+};
 
 #define VSR_CUDA(call)                                                                   \
     do {                                                                                 \

@@ -34,6 +34,8 @@ import numpy as np
 _LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libvsr_b200.so"
 
 VSR_OK, VSR_ERR_SHAPE, VSR_ERR_INVALID, VSR_ERR_NUMERIC, VSR_ERR_OUT_OF_RANGE, VSR_ERR_CUDA = range(6)
+VSR_ERR_IO = 7
+VSR_DTYPE_F64, VSR_DTYPE_F32 = 0, 1
 INIT_ZERO, INIT_UPSAMPLED, INIT_PROVIDED = 0, 1, 2
 
 
@@ -47,6 +49,10 @@ class NumericError(RuntimeError):
 
 class DeviceError(RuntimeError):
     """CUDA/runtime failure inside the library."""
+
+
+class VolumeIOError(OSError):
+    """volsr::io_error (volume files), volume.hpp:22-24."""
 
 
 def load_library() -> C.CDLL:
@@ -146,6 +152,8 @@ def check(rc: int):
         raise NumericError(msg)
     if rc == VSR_ERR_OUT_OF_RANGE:
         raise IndexError(msg)
+    if rc == VSR_ERR_IO:
+        raise VolumeIOError(msg)
     raise DeviceError(msg)
 
 
@@ -888,3 +896,55 @@ class TvDevice:
         if self.handle:
             _lib.vsr_tv_destroy(self.handle)
             self.handle = None
+
+
+# ---------------------------------------------------------------- volume files
+_sig("vsr_volume_header", [C.c_char_p, _szp, C.POINTER(C.c_int)])
+_sig("vsr_load_volume", [C.c_char_p, _vp, C.c_size_t])
+_sig("vsr_save_volume", [C.c_char_p, _szp, _vp, C.c_int])
+_sig("vsr_load_volume_d", [_vp, C.c_char_p, _vp, C.c_size_t])
+_sig("vsr_save_volume_d", [_vp, C.c_char_p, _szp, _vp, C.c_int])
+
+
+def strip_volume_extension(path: str) -> str:
+    """volume_io.cpp:27-31."""
+    for ext in (".volhdr", ".vol"):
+        if path.endswith(ext):
+            return path[: -len(ext)]
+    return path
+
+
+def volume_header(path: str):
+    """(dims (m, n, s), dtype "f32" | "f64") of <base>.volhdr."""
+    d = (C.c_size_t * 3)()
+    t = C.c_int()
+    check(_lib.vsr_volume_header(str(path).encode(), d, C.byref(t)))
+    return (int(d[0]), int(d[1]), int(d[2])), ("f32" if t.value == VSR_DTYPE_F32 else "f64")
+
+
+def load_volume(path: str) -> np.ndarray:
+    """volsr::load_volume (volume_io.cpp:61-131): array of shape (s, n, m)."""
+    dims, _ = volume_header(path)
+    out = np.empty(shape_of(dims))
+    check(_lib.vsr_load_volume(str(path).encode(), _p(out), out.size))
+    return out
+
+
+def save_volume(v: np.ndarray, path: str, dtype: str = "f64"):
+    """volsr::save_volume (volume_io.cpp:34-57); v has shape (s, n, m)."""
+    a = _real(v)
+    check(_lib.vsr_save_volume(str(path).encode(), _dims_arr(dims_of(a)), _p(a),
+                               VSR_DTYPE_F32 if dtype == "f32" else VSR_DTYPE_F64))
+
+
+def load_volume_device(path: str, out_dev, ctx=None):
+    """Streams <base>.vol into a device buffer (object with .ptr) of dims.count() doubles."""
+    dims, _ = volume_header(path)
+    check(_lib.vsr_load_volume_d(_ctx(ctx), str(path).encode(), out_dev.ptr, dims[0] * dims[1] * dims[2]))
+    return dims
+
+
+def save_volume_device(in_dev, dims, path: str, dtype: str = "f64", ctx=None):
+    """Streams a device volume (object with .ptr) to <base>.volhdr/.vol."""
+    check(_lib.vsr_save_volume_d(_ctx(ctx), str(path).encode(), _dims_arr(tuple(dims)), in_dev.ptr,
+                                 VSR_DTYPE_F32 if dtype == "f32" else VSR_DTYPE_F64))

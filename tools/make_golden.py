@@ -127,9 +127,46 @@ def admm_l2l2_golden():
     save("admm_l2l2", **out)
 
 
+def volio_golden():
+    """Volume files (volume_io.cpp:34-131) written and read by the reference:
+    its f64 / f32 files byte for byte, and its error text for the malformed
+    cases of tests/volio_cases.py."""
+    import tempfile
+    sys.path.insert(0, str(ROOT / "tests"))
+    import volio_cases as VC
+    assert R.available(), "build oracle/_ref first (make -C oracle)"
+    out = {}
+    with tempfile.TemporaryDirectory() as td:
+        d = Path(td)
+        for f32 in (False, True):
+            tag = "f32" if f32 else "f64"
+            R.save_volume(d / f"w_{tag}", VC.VALS, f32=f32)
+            out[f"{tag}_hdr"] = np.frombuffer((d / f"w_{tag}.volhdr").read_bytes(), dtype=np.uint8)
+            out[f"{tag}_raw"] = np.frombuffer((d / f"w_{tag}.vol").read_bytes(), dtype=np.uint8)
+        for name, base in VC.cases(d).items():
+            try:
+                v = R.load_volume(base)
+                out[f"case_{name}"] = np.array("OK")
+                out[f"case_{name}_vals"] = v
+            except R.RefError as e:
+                msg = str(e).split("] ", 1)[1]
+                out[f"case_{name}"] = np.array(VC.norm(msg, d))
+        bad = VC.VALS.copy()
+        bad[2, 0, 1] = np.inf
+        try:
+            R.save_volume(d / "save_bad", bad)
+            out["save_non_finite"] = np.array("OK")
+        except R.RefError as e:
+            out["save_non_finite"] = np.array(str(e).split("] ", 1)[1])
+    save("volio", vals=VC.VALS, **out)
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "admm_l2l2":
         admm_l2l2_golden()
+    elif len(sys.argv) > 1 and sys.argv[1] == "volio":
+        volio_golden()
     else:
         main()
         admm_l2l2_golden()
+        volio_golden()
