@@ -274,6 +274,29 @@ inline Volume3D make_gaussian_psf(const PsfSpec& spec, const Dims3& hr) {
     return psf;
 }
 
+// ------------------------------------------------------------- sim.hpp:26-41
+struct DegradationRecipe {
+    PsfSpec psf;
+    DecimationSpec spec;
+    std::optional<double> bsnr_db;
+    std::uint64_t rng_seed = 0;
+};
+struct DegradeResult {
+    Volume3D y;
+    double noise_sigma = 0.0;
+};
+inline DegradeResult degrade(const Volume3D& x, const DegradationRecipe& recipe) {
+    require_same_dims(x.dims(), recipe.spec.hr(), "degrade");
+    const Volume3D psf = make_gaussian_psf(recipe.psf, recipe.spec.hr());
+    const detail::D3 hr(recipe.spec.hr());
+    const std::size_t r[3] = {recipe.spec.dr(), recipe.spec.dc(), recipe.spec.ds()};
+    DegradeResult out;
+    out.y = Volume3D(recipe.spec.lr());
+    detail::check(vsr_degrade(detail::ctx(), hr.v, r, x.data().data(), psf.data().data(), recipe.bsnr_db.has_value(),
+                              recipe.bsnr_db.value_or(0.0), recipe.rng_seed, out.y.data().data(), &out.noise_sigma));
+    return out;
+}
+
 // ------------------------------------------------------------- volume_io.hpp
 enum class VolumeDType { f32, f64 };
 

@@ -54,6 +54,16 @@ int vsr_ctx_synchronize(vsr_ctx* ctx);
 void* vsr_ctx_stream(vsr_ctx* ctx); /* cudaStream_t */
 int vsr_ctx_device(vsr_ctx* ctx);
 
+/* ---- degrade: replaces volsr::degrade (src/sim.cpp:106-127) and its
+ *      gaussian_noise (:88-104).  y = decimate(blur(x, Lambda(psf))) + sigma n
+ *      with sigma^2 = var(y) / 10^(bsnr_db / 10) (only when has_bsnr), n the
+ *      reference's mt19937_64 + Box-Muller stream for `seed`.  x, psf: HR host
+ *      volumes (psf as make_gaussian_psf lays it out); y_out: LR host volume;
+ *      sigma_out: the noise sigma (0 without bsnr).  Errors as the reference:
+ *      numeric_error for a non-finite y, the ifft3_real residue check. */
+int vsr_degrade(vsr_ctx* ctx, const size_t hr_dims[3], const size_t rates[3], const double* x, const double* psf,
+                int has_bsnr, double bsnr_db, uint64_t seed, double* y_out, double* sigma_out);
+
 /* ---- volume files: replaces volsr::load_volume / save_volume /
  *      strip_volume_extension (src/volume_io.cpp:27-131, include/volsr/volume_io.hpp).
  *      <base>.volhdr (dims=m,n,s / dtype=f32|f64 / order=lex) + <base>.vol (raw

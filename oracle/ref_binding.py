@@ -50,6 +50,7 @@ def _setup():
     L.ref_admm_l2l2.argtypes = [_sz, _sz, _dp, _dp, C.c_double, _dp, C.c_size_t, C.c_double, C.c_double,
                                 _dp, _dp, _dp, _sz, _dp]
     L.ref_save_volume.argtypes = [C.c_char_p, _sz, _dp, C.c_int]
+    L.ref_degrade.argtypes = [_sz, _sz, _dp, _sz, _dp, C.c_int, C.c_double, C.c_ulonglong, _dp, _dp]
     L.ref_load_volume.argtypes = [C.c_char_p, _sz, _dp, C.c_size_t]
 
 
@@ -215,3 +216,14 @@ def load_volume(base, cap=1 << 20):
     _chk(_lib.ref_load_volume(str(base).encode(), d, _p(out), cap))
     m, n, s = int(d[0]), int(d[1]), int(d[2])
     return out[:m * n * s].reshape(s, n, m).copy()
+
+
+def degrade(x, psf_size, psf_sigma, rates, bsnr_db, seed):
+    """reference volsr::degrade (sim.cpp:106-127) with a Gaussian PsfSpec; returns (y, sigma)."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    m, n, s = _dims(x)
+    y = np.empty((s // rates[2], n // rates[1], m // rates[0]))
+    sig = C.c_double()
+    _chk(_lib.ref_degrade(_d((m, n, s)), _d(rates), _p(x), _d(psf_size), (C.c_double * 3)(*psf_sigma),
+                          int(bsnr_db is not None), float(bsnr_db or 0.0), int(seed), _p(y), C.byref(sig)))
+    return y, sig.value

@@ -13,6 +13,7 @@
 #include "volsr/solvers.hpp"
 #include "volsr/spectral.hpp"
 #include "volsr/volume_io.hpp"
+#include "volsr/sim.hpp"
 
 using namespace volsr;
 
@@ -194,6 +195,21 @@ int ref_admm_l2l2(const size_t hr[3], const size_t rates[3], const double* y, co
         }
         *iters = rep.iterations;
         *init_obj = rep.initial_objective;
+    });
+}
+
+// sim.cpp:106-127 (degrade with a Gaussian PsfSpec) for the degrade golden
+int ref_degrade(const size_t hr[3], const size_t rates[3], const double* x, const size_t psf_size[3],
+                const double psf_sigma[3], int has_bsnr, double bsnr_db, unsigned long long seed, double* y_out,
+                double* sigma_out) {
+    return wrap([&] {
+        DegradationRecipe r{PsfSpec::gaussian({psf_size[0], psf_size[1], psf_size[2]},
+                                              {psf_sigma[0], psf_sigma[1], psf_sigma[2]}),
+                            DecimationSpec(D(hr), {rates[0], rates[1], rates[2]}),
+                            has_bsnr ? std::optional<double>(bsnr_db) : std::nullopt, seed};
+        const DegradeResult res = degrade(vol(hr, x), r);
+        put(res.y, y_out);
+        *sigma_out = res.noise_sigma;
     });
 }
 

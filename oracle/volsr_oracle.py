@@ -728,3 +728,64 @@ def psnr(ref, x, peak=None):
     if e == 0.0:
         return math.inf
     return 10.0 * math.log10(pk * pk / e)
+
+
+# ---------------------------------------------------------------- input synthesis
+class _MT19937_64:
+    """std::mt19937_64 (the reference's noise generator, sim.cpp:88-104);
+    pure Python, for the small oracle cases only."""
+
+    def __init__(self, seed):
+        self.mt = [0] * 312
+        self.mt[0] = seed & 0xFFFFFFFFFFFFFFFF
+        for i in range(1, 312):
+            self.mt[i] = (6364136223846793005 * (self.mt[i - 1] ^ (self.mt[i - 1] >> 62)) + i) & 0xFFFFFFFFFFFFFFFF
+        self.i = 312
+
+    def __call__(self):
+        if self.i >= 312:
+            mt, um, lm = self.mt, 0xFFFFFFFF80000000, 0x7FFFFFFF
+            for k in range(312):
+                x = (mt[k] & um) | (mt[(k + 1) % 312] & lm)
+                xa = x >> 1
+                if x & 1:
+                    xa ^= 0xB5026F5AA96619E9
+                mt[k] = mt[(k + 156) % 312] ^ xa
+            self.i = 0
+        y = self.mt[self.i]
+        self.i += 1
+        y ^= (y >> 29) & 0x5555555555555555
+        y ^= (y << 17) & 0x71D67FFFEDA60000
+        y ^= (y << 37) & 0xFFF7EEE000000000
+        y ^= y >> 43
+        return y & 0xFFFFFFFFFFFFFFFF
+
+
+def gaussian_noise(dims, seed):
+    """reference src/sim.cpp:88-104 (mt19937_64 + Box-Muller, (r >> 11 + 1) 2^-53)."""
+    import math
+    m, n, s = dims
+    N = m * n * s
+    rng = _MT19937_64(seed)
+    out = np.empty(N)
+    for p in range(0, N, 2):
+        u1 = ((rng() >> 11) + 1.0) * 2.0 ** -53
+        u2 = ((rng() >> 11) + 1.0) * 2.0 ** -53
+        r = math.sqrt(-2.0 * math.log(u1))
+        out[p] = r * math.cos(2.0 * math.pi * u2)
+        if p + 1 < N:
+            out[p + 1] = r * math.sin(2.0 * math.pi * u2)
+    return out.reshape(s, n, m)
+
+
+def degrade(x, psf, spec, bsnr_db=None, seed=0):
+    """reference src/sim.cpp:106-127: y = D H x (+ noise at bsnr_db); returns (y, sigma)."""
+    y = decimate(blur_apply(x, psf_to_spectrum(psf)), spec)
+    sigma = 0.0
+    if bsnr_db is not None:
+        mean = float(np.sum(y)) / y.size
+        var = float(np.sum((y - mean) ** 2)) / y.size
+        sigma = float(np.sqrt(var / 10.0 ** (bsnr_db / 10.0)))
+        y = y + sigma * gaussian_noise(spec.lr, seed)
+    require_finite(y, "degrade")
+    return y, sigma

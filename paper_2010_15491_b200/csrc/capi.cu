@@ -4,6 +4,8 @@
 // cited beside it.  Nothing here falls back to the CPU: every numeric step
 // runs in a kernel on the context's device.
 #include <atomic>
+#include <random>
+#include <thread>
 #include <chrono>
 #include <climits>
 #include <cmath>
@@ -267,6 +269,29 @@ __global__ void off_lattice_kernel(long long m, long long n, long long N, int dr
     if ((i % dr || j % dc || k % ds) && x[p] != 0.0) *flag = 1;
 }
 
+// degrade (sim.cpp:106-127): per-block sums of y, then of (y - mean)^2
+__global__ void __launch_bounds__(256) blocksum_kernel(const double* __restrict__ y, long long n,
+                                                       const double* __restrict__ mean, double* __restrict__ partials) {
+    __shared__ double red[32];
+    double v[1] = {0.0};
+    const double mu = mean ? *mean : 0.0;
+    for (long long i = blockIdx.x * 256LL + threadIdx.x; i < n; i += (long long)gridDim.x * 256) {
+        const double t = y[i] - mu;
+        v[0] += mean ? t * t : y[i];
+    }
+    block_reduce_sum<1>(v, red);
+    if (threadIdx.x == 0) partials[blockIdx.x] = v[0];
+}
+__global__ void add_noise_kernel(double* __restrict__ y, const double* __restrict__ noise, long long n, double sigma,
+                                 unsigned long long* __restrict__ bad) {
+    for (long long i = blockIdx.x * 256LL + threadIdx.x; i < n; i += (long long)gridDim.x * 256) {
+        const double v = noise ? y[i] + sigma * noise[i] : y[i];
+        y[i] = v;
+        if (!isfinite(v)) atomicMin(bad, (unsigned long long)i);
+    }
+}
+
+__global__ void scale_kernel(double* v, double s) { *v *= s; }
 __global__ void cmul_kernel(long long n, double2* __restrict__ a, const double2* __restrict__ b,
                             bool conj_b) {
     const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -657,6 +682,101 @@ int vsr_blur_apply(vsr_ctx* ctx, const size_t dims[3], const double* x, const do
         if (status[0] != 0.0) throw numeric_error(residue_message(status[1], 1e-8));
         d2h(ctx, out, dx.p, dx.bytes());
         sync(ctx);
+    });
+}
+
+// ============================================================ degrade (input synthesis)
+namespace {
+// sim.cpp:88-104 gaussian_noise: the reference's sequential mt19937_64 +
+// Box-Muller stream, (u1, u2) = ((r >> 11) + 1) * 2^-53 per draw (host: the
+// generator is inherently serial; it runs on a host thread while the device
+// blurs and decimates)
+void gaussian_noise_host(size_t n, uint64_t seed, double* out) {
+    std::mt19937_64 rng(seed);
+    auto uniform = [&rng]() { return (static_cast<double>(rng() >> 11) + 1.0) * 0x1p-53; };
+    constexpr double two_pi = 2.0 * 3.141592653589793;  // 2 * std::numbers::pi
+    for (size_t p = 0; p < n; p += 2) {
+        const double u1 = uniform();
+        const double u2 = uniform();
+        const double r = std::sqrt(-2.0 * std::log(u1));
+        out[p] = r * std::cos(two_pi * u2);
+        if (p + 1 < n) out[p + 1] = r * std::sin(two_pi * u2);
+    }
+}
+}  // namespace
+
+// degrade (sim.cpp:106-127): y = decimate(blur_apply(x, Lambda(psf))) + sigma n,
+// sigma^2 = var(y) / 10^(bsnr/10) over the mean-removed noiseless y.  The
+// blur-and-decimate runs as ONE HR forward transform, the alias fold of
+// Lambda X (F_l(D v)[g] = d^-1/2 sum_b F(v)[g + b lr]) and ONE LR inverse.
+int vsr_degrade(vsr_ctx* ctx, const size_t hr_dims[3], const size_t rates[3], const double* x, const double* psf,
+                int has_bsnr, double bsnr_db, uint64_t seed, double* y_out, double* sigma_out) {
+    return guarded([&] {
+        require_ctx(ctx);
+        const Spec sp = make_spec(hr_dims, rates);
+        vsr_ctx::Guard g(ctx->device);
+        cudaStream_t st = ctx->stream;
+        const long long Nl = (long long)sp.lr.count();
+        std::vector<double> noise;
+        std::thread gen;
+        if (has_bsnr) {
+            noise.resize((size_t)Nl);
+            gen = std::thread([&] { gaussian_noise_host((size_t)Nl, seed, noise.data()); });
+        }
+        struct Join {
+            std::thread& t;
+            ~Join() {
+                if (t.joinable()) t.join();
+            }
+        } join{gen};
+        const FoldGeom G = make_geom(sp.hr, sp.rates);
+        DevBuf<double> dx(sp.hr.count()), y(sp.lr.count());
+        DevBuf<double2> X(sp.hr.count()), lam(sp.hr.count()), Yl(sp.lr.count());
+        h2d(ctx, dx.p, psf, dx.bytes());
+        fft_engine().forward3(sp.hr, dx.p, IN_REAL, lam.p, 1.0, st);  // Lambda: unnormalised DFT (operators.cpp:121-123)
+        h2d(ctx, dx.p, x, dx.bytes());
+        fft_engine().forward3(sp.hr, dx.p, IN_REAL, X.p, inv_sqrt_count(sp.hr), st);
+        g_fwd += 2;
+        launch_fold_apply(G, lam.p, nullptr, X.p, Yl.p, st);  // sum_b Lambda_b X_b
+        ResidueCheck rc(ctx, sp.lr);
+        fft_engine().inverse3(sp.lr, Yl.p, y.p, OUT_REAL, inv_sqrt_count(sp.lr) / std::sqrt((double)sp.rate()), &rc.red,
+                              st);
+        ++g_inv;
+        double status[4];
+        unsigned long long bad;
+        rc.finish(ctx, 1e-8, status, &bad);
+        if (status[0] != 0.0) throw numeric_error(residue_message(status[1], 1e-8));
+        double sigma = 0.0;
+        DevBuf<double> nz;
+        if (has_bsnr) {
+            const unsigned nb = (unsigned)std::min<long long>((Nl + 255) / 256, 148LL * 8);
+            DevBuf<double> part(nb), mv(2);
+            blocksum_kernel<<<nb, 256, 0, st>>>(y.p, Nl, nullptr, part.p);
+            VSR_LAUNCH_CHECK();
+            launch_finalize_sum(part.p, 1, 1, nb, mv.p, st);
+            scale_kernel<<<1, 1, 0, st>>>(mv.p, 1.0 / (double)Nl);
+            VSR_LAUNCH_CHECK();
+            blocksum_kernel<<<nb, 256, 0, st>>>(y.p, Nl, mv.p, part.p);
+            VSR_LAUNCH_CHECK();
+            launch_finalize_sum(part.p, 1, 1, nb, mv.p + 1, st);
+            double h[2];
+            d2h(ctx, h, mv.p, sizeof(h));
+            sync(ctx);
+            const double var = h[1] / (double)Nl;
+            sigma = std::sqrt(var / std::pow(10.0, bsnr_db / 10.0));
+            gen.join();
+            nz.alloc((size_t)Nl);
+            h2d(ctx, nz.p, noise.data(), nz.bytes());
+        }
+        VSR_CUDA(cudaMemsetAsync(ctx->bad.p, 0xff, sizeof(unsigned long long), st));
+        add_noise_kernel<<<(unsigned)std::min<long long>((Nl + 255) / 256, 148LL * 16), 256, 0, st>>>(
+            y.p, has_bsnr ? nz.p : nullptr, Nl, sigma, ctx->bad.p);
+        VSR_LAUNCH_CHECK();
+        d2h(ctx, &bad, ctx->bad.p, sizeof(bad));
+        d2h(ctx, y_out, y.p, y.bytes());
+        sync(ctx);
+        if (bad != ULLONG_MAX) throw numeric_error("degrade: non-finite value at flat index " + std::to_string(bad));
+        if (sigma_out) *sigma_out = sigma;
     });
 }
 

@@ -948,3 +948,21 @@ def save_volume_device(in_dev, dims, path: str, dtype: str = "f64", ctx=None):
     """Streams a device volume (object with .ptr) to <base>.volhdr/.vol."""
     check(_lib.vsr_save_volume_d(_ctx(ctx), str(path).encode(), _dims_arr(tuple(dims)), in_dev.ptr,
                                  VSR_DTYPE_F32 if dtype == "f32" else VSR_DTYPE_F64))
+
+
+# ---------------------------------------------------------------- degrade
+_sig("vsr_degrade", [_vp, _szp, _szp, _vp, _vp, C.c_int, C.c_double, C.c_uint64, _vp, C.POINTER(C.c_double)])
+
+
+def degrade(x, psf, spec: DecimationSpec, bsnr_db: Optional[float] = None, seed: int = 0, ctx=None):
+    """volsr::degrade (sim.cpp:106-127) on the GPU: y = D H x + sigma n with the
+    reference's mt19937_64 + Box-Muller noise stream.  psf: HR volume as
+    make_gaussian_psf builds it.  Returns (y, noise_sigma)."""
+    a, p = _real(x), _real(psf)
+    require_same_dims(dims_of(a), spec.hr, "degrade")
+    require_same_dims(dims_of(p), spec.hr, "degrade")
+    y = np.empty(shape_of(spec.lr))
+    sig = C.c_double()
+    check(_lib.vsr_degrade(_ctx(ctx), _dims_arr(spec.hr), _dims_arr(spec.rates), _p(a), _p(p),
+                           int(bsnr_db is not None), float(bsnr_db or 0.0), int(seed), _p(y), C.byref(sig)))
+    return y, sig.value

@@ -161,12 +161,34 @@ def volio_golden():
     save("volio", vals=VC.VALS, **out)
 
 
+def degrade_golden():
+    """degrade (sim.cpp:106-127) from the reference: Gaussian PsfSpec, BSNR
+    noise from its mt19937_64 + Box-Muller stream, and a noiseless case."""
+    assert R.available(), "build oracle/_ref first (make -C oracle)"
+    rng = np.random.default_rng(106127)
+    out = {}
+    cases = [((16, 12, 8), (2, 2, 2), (5, 5, 5), (1.0, 1.0, 1.0), 30.0, 7),
+             ((24, 16, 8), (2, 1, 2), (7, 5, 3), (1.3, 0.9, 0.7), 20.0, 123456789),
+             ((12, 12, 12), (3, 2, 4), (5, 5, 5), (1.0, 1.0, 1.0), None, 0)]
+    for i, (hr, rates, ksz, sig, bsnr, seed) in enumerate(cases):
+        x = rng.uniform(0, 1, (hr[2], hr[1], hr[0]))
+        y, sigma = R.degrade(x, ksz, sig, rates, bsnr, seed)
+        out.update({f"c{i}_hr": np.array(hr), f"c{i}_rates": np.array(rates), f"c{i}_ksz": np.array(ksz),
+                    f"c{i}_sigma_psf": np.array(sig), f"c{i}_bsnr": np.array(-1.0 if bsnr is None else bsnr),
+                    f"c{i}_seed": np.array(seed, dtype=np.uint64), f"c{i}_x": x, f"c{i}_y": y,
+                    f"c{i}_noise_sigma": np.array(sigma)})
+    save("degrade", n=np.array(len(cases)), **out)
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "admm_l2l2":
         admm_l2l2_golden()
     elif len(sys.argv) > 1 and sys.argv[1] == "volio":
         volio_golden()
+    elif len(sys.argv) > 1 and sys.argv[1] == "degrade":
+        degrade_golden()
     else:
         main()
         admm_l2l2_golden()
         volio_golden()
+        degrade_golden()
