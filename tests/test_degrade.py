@@ -74,3 +74,57 @@ def test_gpu_degrade_rejects_non_finite(V, O):
     x[3, 4, 5] = np.nan
     with pytest.raises(V.NumericError):
         V.degrade(x, O.make_gaussian_psf((5, 5, 5), (1.0, 1.0, 1.0), hr), V.DecimationSpec(hr, rates), 30.0, 1)
+
+
+# ------------------------------------------------ reference test_sim.cpp:59-130, restated
+@pytest.mark.gpu
+def test_gpu_degrade_trivial_operators(V, O):
+    """test_sim.cpp:59-68: 1x1x1 PSF, unit rates, no noise -> y = x (bit-exact there; here the
+    unitary transform pair leaves rounding, so <= 1e-15)."""
+    rng = np.random.default_rng(1)
+    d = (8, 8, 8)
+    x = rng.uniform(0, 1, d)
+    y, s = V.degrade(x, O.make_gaussian_psf((1, 1, 1), (0, 0, 0), d), V.DecimationSpec(d, (1, 1, 1)))
+    assert s == 0.0 and rel_err(y, x) < 1e-15
+
+
+@pytest.mark.gpu
+def test_gpu_degrade_noiseless_is_decimated_blur(V, O):
+    """test_sim.cpp:70-79."""
+    rng = np.random.default_rng(2)
+    d = (16, 16, 16)
+    psf = O.make_gaussian_psf((5, 5, 5), (1.5, 1.5, 1.5), d)
+    x = rng.uniform(0, 1, d)
+    y, s = V.degrade(x, psf, V.DecimationSpec(d, (2, 2, 2)))
+    want = O.decimate(O.blur_apply(x, O.psf_to_spectrum(psf)), O.DecimationSpec(d, (2, 2, 2)))
+    assert s == 0.0 and rel_err(y, want) < 1e-13
+
+
+@pytest.mark.gpu
+def test_gpu_degrade_bsnr_band(V, O):
+    """test_sim.cpp:81-118: the measured BSNR lands within 0.5 dB, noise zero-mean."""
+    from paper_2010_15491_b200 import synth
+    d = (64, 64, 64)
+    spec = V.DecimationSpec(d, (2, 2, 2))
+    psf = O.make_gaussian_psf((9, 9, 9), (3, 3, 3), d)
+    x = synth.ellipsoid_phantom(d, 0)
+    noisy, sig = V.degrade(x, psf, spec, 30.0, 11)
+    clean, _ = V.degrade(x, psf, spec, None, 11)
+    n = noisy - clean
+    bsnr = 10 * np.log10(np.mean((clean - clean.mean()) ** 2) / np.mean(n ** 2))
+    assert 29.5 < bsnr < 30.5
+    assert abs(n.mean()) < 4 * sig / np.sqrt(n.size)
+
+
+@pytest.mark.gpu
+def test_gpu_degrade_deterministic_per_seed(V, O):
+    """test_sim.cpp:120-130."""
+    rng = np.random.default_rng(5)
+    d = (16, 16, 16)
+    spec = V.DecimationSpec(d, (2, 2, 2))
+    psf = O.make_gaussian_psf((5, 5, 5), (1.2, 1.2, 1.2), d)
+    x = rng.uniform(0, 1, d)
+    a, _ = V.degrade(x, psf, spec, 25.0, 123)
+    b, _ = V.degrade(x, psf, spec, 25.0, 123)
+    c, _ = V.degrade(x, psf, spec, 25.0, 124)
+    assert a.tobytes() == b.tobytes() and np.abs(a - c).max() > 0
