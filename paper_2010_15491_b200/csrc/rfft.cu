@@ -18,9 +18,14 @@
 namespace vsr {
 namespace {
 
+#ifndef VSR_ROW_RMAX
+#define VSR_ROW_RMAX 8
+#endif
+constexpr int kRowR = VSR_ROW_RMAX;  // values per thread of a row transform
+
 template <int M>
 struct RowShape {
-    using Pl = fftc::Plan<M>;
+    using Pl = fftc::Plan<M, kRowR>;
     static constexpr int R = Pl::R, P = Pl::P;
     static constexpr int TG = P >= 128 ? 1 : 128 / P;  // rows per CTA
     static constexpr int THREADS = TG * P;
@@ -43,11 +48,12 @@ __global__ void __launch_bounds__(RowShape<M>::THREADS)
     double2 v[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) v[r] = active ? __ldg(z + t + P * r) : make_double2(0.0, 0.0);
-    fftc::stockham<M, false>(v, t, smr, [&](int q) { return ls * Sh::LPAD + q + q / R; }, twM);
+    auto sidx_r = [&](int q) { return ls * Sh::LPAD + q + q / R; };
+    fftc::stockham<M, false, decltype(sidx_r), kRowR>(v, t, smr, sidx_r, twM);
     __syncthreads();  // exchange buffer -> split buffer
     double2* buf = smr + ls * Sh::XPITCH;
 #pragma unroll
-    for (int j = 0; j < R; ++j) buf[fftc::Plan<M>::out_q(t, j)] = v[j];
+    for (int j = 0; j < R; ++j) buf[fftc::Plan<M, kRowR>::out_q(t, j)] = v[j];
     __syncthreads();
     if (!active) return;
     double2* out = X + row * Mp;
@@ -95,13 +101,14 @@ __global__ void __launch_bounds__(RowShape<M>::THREADS)
         v[r] = make_double2(s.x - wd.y, s.y + wd.x);            // s + i wd
     }
     __syncthreads();  // split buffer -> exchange buffer
-    fftc::stockham<M, true>(v, t, smr, [&](int q) { return ls * Sh::LPAD + q + q / R; }, twM);
+    auto sidx_r = [&](int q) { return ls * Sh::LPAD + q + q / R; };
+    fftc::stockham<M, true, decltype(sidx_r), kRowR>(v, t, smr, sidx_r, twM);
     if (!active) return;
     double2* outz = reinterpret_cast<double2*>(x) + row * M;
     const double2* subz = reinterpret_cast<const double2*>(sub) + row * M;
 #pragma unroll
     for (int j = 0; j < R; ++j) {
-        const int n = fftc::Plan<M>::out_q(t, j);
+        const int n = fftc::Plan<M, kRowR>::out_q(t, j);
         double2 r = cscale(v[j], scale);
         if (sub) {
             const double2 q = __ldg(subz + n);

@@ -48,9 +48,14 @@ void launch_spatial_v(const Dims& lr, int d, const SpatialPlan& p, const double2
 // forward axis-3 FFT, scale fs, U(g) as in spatial_u_kernel, inverse axis-3
 // FFT scaled by out_scale.  A CTA owns TG tiles of T consecutive inner
 // positions p = g1 + ml g2, each line held by P threads x R registers.
+#ifndef VSR_SW_RMAX
+#define VSR_SW_RMAX 8
+#endif
+constexpr int kSwR = VSR_SW_RMAX;  // values per thread of the LR axis-3 sandwich
+
 template <int L>
 struct SwShape {
-    using Pl = fftc::Plan<L>;
+    using Pl = fftc::Plan<L, kSwR>;
     static constexpr int R = Pl::R, P = Pl::P, T = 8;
     static constexpr int TG = (T * P) >= 128 ? 1 : 128 / (T * P);
     static constexpr int THREADS = TG * T * P;
@@ -83,8 +88,8 @@ __global__ void __launch_bounds__(SwShape<L>::THREADS, 512 / SwShape<L>::THREADS
 #pragma unroll
         for (int r = 0; r < R; ++r) asm volatile("prefetch.global.L2 [%0];" ::"l"(Zl + p + S * (t + P * r)));
     }
-    fftc::stockham<L, false>(v, t, smw, sidx, tw);
-    fftc::to_natural<L>(v);
+    fftc::stockham<L, false, decltype(sidx), kSwR>(v, t, smw, sidx, tw);
+    fftc::to_natural<L, kSwR>(v);
     // v[r] = F_l(y) at g3 = t + P r (times 1/fs)
     const int g1 = (int)(p % pitch), g2 = (int)(p / pitch);
     const double2 ab1 = Zl ? cmul(__ldg(a1 + g1), __ldg(b1 + g2)) : make_double2(0.0, 0.0);
@@ -97,7 +102,7 @@ __global__ void __launch_bounds__(SwShape<L>::THREADS, 512 / SwShape<L>::THREADS
         v[r] = cscale(num, 1.0 / (ab2 * __ldg(c2 + g3) + shift));
     }
     __syncthreads();  // the exchange buffer is reused by the inverse transform
-    fftc::stockham<L, true>(v, t, smw, sidx, tw);
+    fftc::stockham<L, true, decltype(sidx), kSwR>(v, t, smw, sidx, tw);
     if (active) {
 #pragma unroll
         for (int j = 0; j < R; ++j) Y[p + S * Pl::out_q(t, j)] = cscale(v[j], out_scale);
