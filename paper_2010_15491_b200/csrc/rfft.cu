@@ -18,14 +18,14 @@
 namespace vsr {
 namespace {
 
-#ifndef VSR_ROW_RMAX
-#define VSR_ROW_RMAX 8
-#endif
-constexpr int kRowR = VSR_ROW_RMAX;  // values per thread of a row transform
+// values per thread of a row transform: radix 8 for the short rows of the
+// latency-bound LR stages (M <= 64: 128^3 LR grids), 16 for longer rows
+template <int M>
+constexpr int row_r() { return M <= 64 ? 8 : 16; }
 
 template <int M>
 struct RowShape {
-    using Pl = fftc::Plan<M, kRowR>;
+    using Pl = fftc::Plan<M, row_r<M>()>;
     static constexpr int R = Pl::R, P = Pl::P;
     static constexpr int TG = P >= 128 ? 1 : 128 / P;  // rows per CTA
     static constexpr int THREADS = TG * P;
@@ -49,11 +49,11 @@ __global__ void __launch_bounds__(RowShape<M>::THREADS)
 #pragma unroll
     for (int r = 0; r < R; ++r) v[r] = active ? __ldg(z + t + P * r) : make_double2(0.0, 0.0);
     auto sidx_r = [&](int q) { return ls * Sh::LPAD + q + q / R; };
-    fftc::stockham<M, false, decltype(sidx_r), kRowR>(v, t, smr, sidx_r, twM);
+    fftc::stockham<M, false, decltype(sidx_r), row_r<M>()>(v, t, smr, sidx_r, twM);
     __syncthreads();  // exchange buffer -> split buffer
     double2* buf = smr + ls * Sh::XPITCH;
 #pragma unroll
-    for (int j = 0; j < R; ++j) buf[fftc::Plan<M, kRowR>::out_q(t, j)] = v[j];
+    for (int j = 0; j < R; ++j) buf[fftc::Plan<M, row_r<M>()>::out_q(t, j)] = v[j];
     __syncthreads();
     if (!active) return;
     double2* out = X + row * Mp;
@@ -102,13 +102,13 @@ __global__ void __launch_bounds__(RowShape<M>::THREADS)
     }
     __syncthreads();  // split buffer -> exchange buffer
     auto sidx_r = [&](int q) { return ls * Sh::LPAD + q + q / R; };
-    fftc::stockham<M, true, decltype(sidx_r), kRowR>(v, t, smr, sidx_r, twM);
+    fftc::stockham<M, true, decltype(sidx_r), row_r<M>()>(v, t, smr, sidx_r, twM);
     if (!active) return;
     double2* outz = reinterpret_cast<double2*>(x) + row * M;
     const double2* subz = reinterpret_cast<const double2*>(sub) + row * M;
 #pragma unroll
     for (int j = 0; j < R; ++j) {
-        const int n = fftc::Plan<M, kRowR>::out_q(t, j);
+        const int n = fftc::Plan<M, row_r<M>()>::out_q(t, j);
         double2 r = cscale(v[j], scale);
         if (sub) {
             const double2 q = __ldg(subz + n);
