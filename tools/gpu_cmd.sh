@@ -1,4 +1,7 @@
-timeout 600 python -m pytest tests/test_gpu_parity.py tests/test_full_configs.py -x -q -k "spatial or env_variants or rfft or half or config1 or config4" > gpurun_out/t2.log 2>&1; echo rc=$? >> gpurun_out/t2.log
-timeout 900 python bench.py --no-cpu --no-fft-path --no-tv > gpurun_out/b9.json 2> gpurun_out/b9.err
+timeout 600 python -m pytest tests/test_gpu_parity.py tests/test_golden.py -x -q -k "tv or admm or objective or env or rpair or half" > gpurun_out/t3.log 2>&1; echo rc=$? >> gpurun_out/t3.log
+rm -f gpurun_out/b3.txt
+for v in "" ""; do
+env $v timeout 600 python bench.py --no-cpu --no-fft-path --no-config4 --steps 10 > gpurun_out/b3.json 2> gpurun_out/b3.err
 python -c "
-import json;d=json.loads(open('gpurun_out/b9.json').read().strip().splitlines()[-1]);print(d['ms_per_step'], d['config4']['tikhonov_ms'])" > gpurun_out/b9.txt
+import json;d=json.loads(open('gpurun_out/b3.json').read().strip().splitlines()[-1]);print('$v', d['tv']['ms_per_iter'], {k:round(v['avg_us'],1) for k,v in d['tv']['stages'].items()})" >> gpurun_out/b3.txt
+done
