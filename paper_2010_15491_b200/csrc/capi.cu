@@ -1539,10 +1539,19 @@ struct vsr_tv {
     DevBuf<double> gw;  // LR table sum_b Gamma_b |Lambda_b|^2 (axis-1 sandwich)
     DevBuf<double2> W2;  // sandwich output on the half-spectrum path (m x n x (s/2+1))
     DevBuf<int> iter_dev;  // iteration index read by the finalize kernel (graph replay)
-    cudaGraphExec_t gexec = nullptr;  // two consecutive iterations (one dual ping-pong period)
+    cudaGraphExec_t gexec = nullptr;  // kGraphIters consecutive iterations (dual ping-pong period 2)
     uint64_t g_kernels = 0;
+    // fixed-count iterations: the scalar finalize runs on a side stream and
+    // overlaps the next iteration's forward passes; the next fold (which
+    // rewrites the partials) waits for it
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    bool fin_pending = false;
     ~vsr_tv() {
         if (gexec) cudaGraphExecDestroy(gexec);
+        if (side) cudaStreamDestroy(side);
+        if (ev_fork) cudaEventDestroy(ev_fork);
+        if (ev_join) cudaEventDestroy(ev_join);
     }
     size_t iters_done = 0;
     bool dual_in_a = true;
@@ -1669,6 +1678,21 @@ static vsr_tv* tv_build(vsr_ctx* ctx, const Spec& sp, const double* y_dev, const
     return h;
 }
 
+// iterations per captured TV graph: a multiple of the dual ping-pong period 2
+#ifndef VSR_TV_GRAPH_ITERS
+#define VSR_TV_GRAPH_ITERS 4
+#endif
+constexpr size_t kTvGraphIters = VSR_TV_GRAPH_ITERS;
+
+// the previous iteration's side-stream finalize must be done before the
+// partial buffers are rewritten (and before anything reads the report)
+static void tv_join(vsr_tv* h) {
+    if (h->fin_pending) {
+        VSR_CUDA(cudaStreamWaitEvent(h->ctx->stream, h->ev_join, 0));
+        h->fin_pending = false;
+    }
+}
+
 static void tv_step(vsr_tv* h) {
     cudaStream_t st = h->ctx->stream;
     const Dims& hr = h->sp.hr;
@@ -1692,6 +1716,7 @@ static void tv_step(vsr_tv* h) {
             ProfScope ps(prof, "fft_fwd_axis2_half", st);
             fft_engine().axis_pass(hrh, 1, false, h->W.p, IN_COMPLEX, h->W.p, OUT_COMPLEX, 1.0, nullptr, st);
         }
+        tv_join(h);
         ProfScope ps(prof, "tv_fft1_fold_ifft1_half", st);
         launch_tv_sandwich1(h->G, h->Yl.p, h->lam.p, h->W.p, tabs, h->mu, s, h->fitp.p, st, h->sep.t, h->W2.p);
     } else if (a1) {
@@ -1703,6 +1728,7 @@ static void tv_step(vsr_tv* h) {
             ProfScope ps(prof, "fft_fwd_axis2", st);
             fft_engine().axis_pass(hr, 1, false, h->W.p, IN_COMPLEX, h->W.p, OUT_COMPLEX, 1.0, nullptr, st);
         }
+        tv_join(h);
         ProfScope ps(prof, "tv_fft1_fold_ifft1", st);
         launch_tv_sandwich1(h->G, h->Yl.p, h->lam.p, h->W.p, tabs, h->mu, s, h->fitp.p, st, h->sep.t);
     } else if (fused) {
@@ -1712,10 +1738,12 @@ static void tv_step(vsr_tv* h) {
         } else {
             fft_engine().forward12(hr, h->theta.p, IN_REAL, h->W.p, st, prof);
         }
+        tv_join(h);
         ProfScope ps(prof, "tv_fft3_fold_ifft3", st);
         launch_tv_sandwich(h->G, h->Yl.p, h->lam.p, h->W.p, tabs, h->mu, s, h->fitp.p, st, h->sep.t);
     } else {
         fft_engine().forward3(hr, h->theta.p, IN_REAL, h->W.p, s, st, prof);
+        tv_join(h);
         ProfScope ps(prof, "tv_fold", st);
         launch_tv_fold(h->G, h->Yl.p, h->lam.p, h->W.p, h->W.p, nullptr, tabs, h->mu, h->fitp.p, st);
     }
@@ -1754,6 +1782,16 @@ static void tv_step(vsr_tv* h) {
     }
     h->dual_in_a = !h->dual_in_a;
     TvIterScalars sc{h->obj.p, h->res.p, h->rel.p, h->status.p, h->iter_dev.p};
+    const bool side = h->rel_tol <= 0.0 && prof == nullptr;
+    if (side) {
+        if (!h->side) {
+            VSR_CUDA(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
+            VSR_CUDA(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
+            VSR_CUDA(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
+        }
+        VSR_CUDA(cudaEventRecord(h->ev_fork, st));
+        VSR_CUDA(cudaStreamWaitEvent(h->side, h->ev_fork, 0));
+    }
     {
         ProfScope ps(prof, "tv_finalize", st);
         launch_tv_finalize((int)h->iters_done, h->fitp.p,
@@ -1762,7 +1800,11 @@ static void tv_step(vsr_tv* h) {
                            half ? fft_engine().half3_blocks(hr)
                                 : (a1 ? fft_engine().pass_blocks(hr, 2) : h->res_blocks),
                            h->lambda, 1e-8, sc, nullptr,
-                           st);
+                           side ? h->side : st);
+    }
+    if (side) {
+        VSR_CUDA(cudaEventRecord(h->ev_join, h->side));
+        h->fin_pending = true;
     }
     ++h->iters_done;
 }
@@ -1779,7 +1821,8 @@ static void tv_iterate(vsr_tv* h, size_t iters) {
     const bool graphs = !no_graph && h->rel_tol <= 0.0 && h->ctx->prof() == nullptr;
     if (graphs) {
         cudaStream_t st = h->ctx->stream;
-        while (k + 2 <= iters && h->iters_done + 2 <= h->max_iters) {
+        constexpr size_t G = kTvGraphIters;
+        while (k + G <= iters && h->iters_done + G <= h->max_iters) {
             if (!h->dual_in_a || h->iters_done == 0) {  // align to the captured parity / warm up
                 tv_step(h);
                 ++k;
@@ -1789,10 +1832,11 @@ static void tv_iterate(vsr_tv* h, size_t iters) {
                 const uint64_t l0 = g_launches.load(), f0 = g_fwd.load(), i0 = g_inv.load();
                 const size_t it0 = h->iters_done;
                 cudaGraph_t graph = nullptr;
+                tv_join(h);  // no cross-capture event waits
                 VSR_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
                 try {
-                    tv_step(h);
-                    tv_step(h);
+                    for (size_t q = 0; q < G; ++q) tv_step(h);
+                    tv_join(h);  // the side stream rejoins before the capture ends
                 } catch (...) {
                     cudaStreamEndCapture(st, &graph);
                     if (graph) cudaGraphDestroy(graph);
@@ -1808,12 +1852,13 @@ static void tv_iterate(vsr_tv* h, size_t iters) {
                 g_inv.fetch_sub(g_inv.load() - i0);
                 h->iters_done = it0;  // the captured steps have not run yet
             }
+            tv_join(h);  // an eager step's side-stream finalize precedes the graph's fold
             VSR_CUDA(cudaGraphLaunch(h->gexec, st));
             g_launches.fetch_add(h->g_kernels);
-            g_fwd += 2;
-            g_inv += 2;
-            h->iters_done += 2;
-            k += 2;
+            g_fwd += G;
+            g_inv += G;
+            h->iters_done += G;
+            k += G;
         }
     }
     for (; k < iters && !h->stopped && h->iters_done < h->max_iters; ++k) {
@@ -1825,6 +1870,7 @@ static void tv_iterate(vsr_tv* h, size_t iters) {
             if (rc < h->rel_tol) h->stopped = true;
         }
     }
+    tv_join(h);  // report readers on the main stream see the last iteration's scalars
 }
 
 static void tv_fill_report(vsr_tv* h, vsr_report* rep, const char* where) {
