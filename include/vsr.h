@@ -246,6 +246,8 @@ int vsr_slab_lr_slice_d(vsr_ctx* ctx, const size_t hr_dims[3], const size_t rate
 int vsr_slab_tik_fold_d(vsr_ctx* ctx, const size_t hr_dims[3], const size_t rates[3], int P,
                         const double* Yl_loc, const double* lam_loc, const double* xbh_loc, double reg,
                         double* W_out);
+int vsr_slab_tv_prepare_d(vsr_ctx* ctx, const size_t hr_dims[3], const size_t rates[3], int P, int rank,
+                          const double* lam_loc);
 int vsr_slab_tv_fold_d(vsr_ctx* ctx, const size_t hr_dims[3], const size_t rates[3], int P, int rank,
                        const double* Yl_loc, const double* lam_loc, double* W, double mu, double tau,
                        double fwd_scale, double* fit_out);

@@ -187,13 +187,26 @@ struct TvFoldState {
     size_t nb = 0;
 };
 
+void free_state(TvFoldState& e) {
+    cudaFree(e.nr), cudaFree(e.nc), cudaFree(e.ns), cudaFree(e.fitp);
+    if (e.sep) cudaFree(e.sep);
+}
+
+// rebuild = true (vsr_slab_tv_prepare_d): the Lambda slice behind lam_loc is new
 TvFoldState& tv_fold_state(vsr_ctx* ctx, const Slab& g, int rank, const double* lam_loc, const FoldGeom& G,
-                           cudaStream_t st) {
+                           cudaStream_t st, bool rebuild = false) {
     static std::vector<TvFoldState> cache;
-    for (auto& e : cache)
+    for (size_t i = 0; i < cache.size(); ++i) {
+        auto& e = cache[i];
         if (e.ctx == ctx && e.lam == lam_loc && e.m == g.m && e.nP == g.nP && e.s == g.s && e.rank == rank &&
-            e.P == g.P && e.rates[0] == g.rates[0] && e.rates[1] == g.rates[1] && e.rates[2] == g.rates[2])
-            return e;
+            e.P == g.P && e.rates[0] == g.rates[0] && e.rates[1] == g.rates[1] && e.rates[2] == g.rates[2]) {
+            if (!rebuild) return e;
+            VSR_CUDA(cudaStreamSynchronize(st));  // no queued fold still reads these tables
+            free_state(e);
+            cache.erase(cache.begin() + (long)i);
+            break;
+        }
+    }
     TvFoldState e;
     e.ctx = ctx, e.lam = lam_loc, e.m = g.m, e.nP = g.nP, e.s = g.s, e.rank = rank, e.P = g.P;
     for (int a = 0; a < 3; ++a) e.rates[a] = g.rates[a];
@@ -296,6 +309,17 @@ int vsr_slab_tik_fold_d(vsr_ctx* ctx, const size_t hr[3], const size_t rates[3],
 }
 
 // TV: forward axis-3 FFT (scaled) + fold + inverse axis-3 FFT in place on W;
+// (Re)builds the rank's cached fold tables for the Lambda slice at lam_loc
+// (call after computing it; a later fold with the same pointer reuses them).
+int vsr_slab_tv_prepare_d(vsr_ctx* ctx, const size_t hr[3], const size_t rates[3], int P, int rank,
+                          const double* lam_loc) {
+    return vsr_capi::guard_call([&] {
+        DevGuard dg(vsr_capi::device_of(ctx));
+        const Slab g = make_slab(hr, rates, P);
+        tv_fold_state(ctx, g, rank, lam_loc, local_geom(g), vsr_capi::stream_of(ctx), true);
+    });
+}
+
 // fit_out (device double) receives this rank's share of ||y - D H x||^2.
 int vsr_slab_tv_fold_d(vsr_ctx* ctx, const size_t hr[3], const size_t rates[3], int P, int rank,
                        const double* Yl_loc, const double* lam_loc, double* W, double mu, double tau,

@@ -206,6 +206,10 @@ class GpuStages:
         self._call("vsr_slab_tik_fold_d", self.ctx[rank].handle, hr, rt, g.P, self._d(Yl_loc), self._d(lam),
                    self._d(xbh), float(reg), self._d(W))
 
+    def tv_prepare(self, rank, g, lam):
+        hr, rt = self._geo(g)
+        self._call("vsr_slab_tv_prepare_d", self.ctx[rank].handle, hr, rt, g.P, rank, self._d(lam))
+
     def tv_fold(self, rank, g, Yl_loc, lam, W, mu, tau, fwd_scale, fit):
         hr, rt = self._geo(g)
         self._call("vsr_slab_tv_fold_d", self.ctx[rank].handle, hr, rt, g.P, rank, self._d(Yl_loc),
@@ -357,6 +361,7 @@ class SlabADMMTV(_Base):
         pl = g.plane
         self.lam = {r: stages.zeros(r, 2 * g.slab_elems) for r in self.ranks}
         self.forward3(psf_slabs, True, 1.0, self.lam)
+        self._each(lambda r: self.st.tv_prepare(r, g, self.lam[r]))  # fold tables for this Lambda
         self._lr_spectrum(y_full)
         self.x_ext = {r: stages.zeros(r, pl * (g.sz + 2)) for r in self.ranks}
         self.dual = [{r: stages.zeros(r, 3 * pl * (g.sz + 1)) for r in self.ranks} for _ in range(2)]

@@ -69,6 +69,9 @@ class NumpyStages:
         xh = (k - f.apply_adjoint(w)) * (1.0 / (2.0 * reg))
         _c(W, (g.s, g.nP, g.m))[...] = np.fft.ifft(xh, axis=0) * g.s
 
+    def tv_prepare(self, rank, g, lam):
+        pass  # the numpy fold has no cached tables
+
     def tv_fold(self, rank, g, Yl_loc, lam, W, mu, tau, fwd_scale, fit):
         sp = self._local(g)
         L = _c(lam, (g.s, g.nP, g.m))
