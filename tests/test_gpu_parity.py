@@ -365,7 +365,9 @@ TV_CASES = [((8, 8, 8), (2, 2, 2), 6), ((16, 16, 16), (4, 4, 4), 10), ((32, 32, 
             ((12, 10, 8), (2, 2, 2), 5), ((64, 64, 64), (4, 4, 4), 12), ((40, 24, 16), (2, 2, 2), 5),
             ((32, 32, 64), (2, 2, 4), 6), ((64, 32, 128), (2, 2, 2), 4), ((32, 32, 32), (1, 1, 1), 4),
             # half-spectrum mirror pairing: nl not a power of two, and sl = 4 (self-mirror planes 0, 2)
-            ((64, 48, 32), (4, 4, 4), 5), ((64, 64, 16), (4, 4, 4), 5), ((128, 64, 32), (4, 4, 2), 4)]
+            ((64, 48, 32), (4, 4, 4), 5), ((64, 64, 16), (4, 4, 4), 5), ((128, 64, 32), (4, 4, 2), 4),
+            # 1024-point axis-3 lines (paired real passes with 16-column tiles, as at config 4)
+            ((64, 8, 1024), (2, 2, 2), 3)]
 
 
 @pytest.mark.parametrize("dims,rates,iters", TV_CASES)
