@@ -145,11 +145,15 @@ __global__ void __launch_bounds__(PassShape<L, R, T, TG, CONTIG>::THREADS)
 //   inverse: Z[k] = X_c[k] + i X_{c+1}[k] (k > L/2 from conj X[L-k]); the real and
 //            imaginary parts of IDFT(Z) are the two real columns.
 // A CTA owns one tile of T = 8 columns (4 pairs), full lines.
+// real columns per tile of the paired passes, every L (1024: 128 KB of smem,
+// one CTA per SM); half3_blocks() sizes the residue partials from it too
+constexpr int kRPairCols = 16;
+
 template <int L>
 struct RPairShape {
     using Pl = fftc::Plan<L>;
     // 16 real columns per tile: 128-byte row segments in the real domain
-    static constexpr int R = Pl::R, P = Pl::P, T = L >= 1024 ? 8 : 16, TP = T / 2;
+    static constexpr int R = Pl::R, P = Pl::P, T = kRPairCols, TP = T / 2;
     static constexpr int TG = (TP * P) >= 128 ? 1 : 128 / (TP * P);  // tiles per CTA
     static constexpr int THREADS = TG * TP * P;
     static constexpr int SMEM = TG * TP * L;
@@ -550,7 +554,7 @@ bool FftEngine::half3_ok(const Dims& d) const {
 }
 
 size_t FftEngine::half3_blocks(const Dims& d) const {
-    const size_t T = d.s >= 1024 ? 8 : 16;
+    const size_t T = kRPairCols;
     const size_t P = d.s < 16 ? 1 : d.s / 16, tp = (T / 2) * P;
     const size_t tg = tp >= 128 ? 1 : 128 / tp;
     return (d.count() / (T * d.s) + tg - 1) / tg;
