@@ -337,12 +337,18 @@ __global__ void __launch_bounds__(256)
 }
 
 // ------------------------------------------------------------ dispatch
+// lines per tile of a strided pass (8: 128-B rows; whole lines sit in smem, so
+// lines of 1024+ points take 4 -- 8 at L = 1024 measured slower, 128 KB of
+// smem per CTA): the ONE definition the kernels, the block counts and the
+// geometry checks all use
+constexpr long long strided_cols(long long L) { return L >= 1024 ? 4 : 8; }
+
 template <int L>
 struct LCfg {
     static constexpr int R = L < 16 ? L : 16;
     static constexpr int P = L / R;
     // strided tile width and tiles per CTA (>= 128 threads per CTA)
-    static constexpr int TS = L >= 1024 ? 4 : 8;
+    static constexpr int TS = strided_cols(L);
     static constexpr int TGS = (TS * P) >= 128 ? 1 : (128 / (TS * P));
     // contiguous: lines per CTA
     static constexpr int TGC = P >= 128 ? 1 : (128 / P);
@@ -412,13 +418,13 @@ bool dispatch_L(size_t L, long long S, long long units, const void* in, void* ou
 template <bool CONTIG>
 long long pass_units(size_t L, long long S, long long total) {
     if (CONTIG) return total / (long long)L;
-    const size_t TS = L >= 1024 ? 4 : 8;
+    const size_t TS = (size_t)strided_cols((long long)L);
     return total / ((long long)TS * (long long)L);  // tiles of TS whole lines
 }
 
 size_t blocks_for(size_t L, bool contig, long long units) {
     size_t P = L < 16 ? 1 : L / 16;
-    size_t TS = L >= 1024 ? 4 : 8;
+    size_t TS = (size_t)strided_cols((long long)L);
     size_t tg;
     if (contig)
         tg = P >= 128 ? 1 : 128 / P;
@@ -430,7 +436,7 @@ size_t blocks_for(size_t L, bool contig, long long units) {
 bool tiled_ok(size_t L, int axis, long long S) {
     if (L < 2 || L > 2048 || !is_pow2(L)) return false;
     if (axis == 0) return true;
-    const long long TS = L >= 1024 ? 4 : 8;
+    const long long TS = strided_cols((long long)L);
     return S % TS == 0;
 }
 
