@@ -1,4 +1,7 @@
-timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/t3.log 2>&1; echo rc=$? >> gpurun_out/t3.log
-timeout 900 python bench.py --no-cpu > gpurun_out/b9.json 2> gpurun_out/b9.err
-python -c "
-import json;d=json.loads(open('gpurun_out/b9.json').read().strip().splitlines()[-1]);print(d['ms_per_step'], d['tv']['ms_per_iter'], d['config4']['tikhonov_ms'], d['config4']['tv_ms_per_iter'], d['fft3_vs_cufft'])" > gpurun_out/b9.txt
+timeout 600 python -m pytest tests/test_gpu_parity.py -x -q -k "spatial or env_variants" > gpurun_out/t2.log 2>&1; echo rc=$? >> gpurun_out/t2.log
+VSR_MARCH_YX=1 timeout 600 python -m pytest tests/test_gpu_parity.py tests/test_full_configs.py -x -q -k "spatial or config1 or config4" >> gpurun_out/t2.log 2>&1; echo rc=$? >> gpurun_out/t2.log
+rm -f gpurun_out/b2.log
+for v in "" "VSR_MARCH_YX=1" "" "VSR_MARCH_YX=1"; do
+  echo "== $v" >> gpurun_out/b2.log
+  env $v timeout 300 python bench.py --no-tv --no-cpu --no-fft-path --no-config4 --steps 30 --warmup 5 2>>gpurun_out/b2.err | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print(d['ms_per_step'], d['stages']['spatial_expand']['avg_us'])" >> gpurun_out/b2.log
+done
