@@ -146,3 +146,39 @@ def test_config4_tikhonov_properties_1024(V, O, synth):
     rhs = blur(up, True) + 2 * reg * xbar
     res = float(torch.linalg.vector_norm(lhs) / torch.linalg.vector_norm(rhs))
     assert res < 1e-9, res
+
+
+# ------------------------------------------------ against the reference itself
+# oracle/_ref (the reference's own sources, compiled with the FFTW3-API shim)
+# travels with the repo, so the GPU box can run the REFERENCE on the same
+# full-size inputs: config 1's solve and config 2's first ADMM-TV iterations.
+@pytest.fixture(scope="module")
+def R():
+    import ref_binding
+    if not ref_binding.available():
+        pytest.skip("oracle/_ref not built")
+    return ref_binding
+
+
+def test_config1_tikhonov_vs_reference_binary(V, R, synth):
+    cfg = synth.CONFIGS[1]
+    inp = synth.make_inputs(cfg, with_truth=False)
+    spec = V.DecimationSpec(cfg.hr, cfg.rates)
+    got = V.TikhonovOperator(V.psf_to_spectrum(inp.psf), spec, V.TikhonovConfig(cfg.reg, inp.xbar)).solve(inp.y)
+    want = R.TikhonovOperator(inp.psf, cfg.hr, cfg.rates, cfg.reg, inp.xbar).solve(inp.y)
+    assert rel_err(got, want) < TOL
+
+
+def test_config2_admm_tv_vs_reference_binary(V, R, synth):
+    cfg = synth.CONFIGS[2]
+    inp = synth.make_inputs(cfg, with_truth=False)
+    spec = V.DecimationSpec(cfg.hr, cfg.rates)
+    tau, iters = 1e-3 * cfg.tv_mu, 2
+    got, rep = V.admm_tv(inp.y, inp.psf, spec,
+                         V.TvAdmmConfig(lambda_=cfg.tv_lambda, mu=cfg.tv_mu, max_iters=iters, rel_tol=0.0, tau=tau,
+                                        init=V.INIT_PROVIDED, init_volume=inp.x0))
+    want, wrep = R.admm_tv(inp.y, inp.psf, cfg.hr, cfg.rates, cfg.tv_lambda, cfg.tv_mu, iters, 0.0, tau=tau,
+                           init=V.INIT_PROVIDED, init_volume=inp.x0)
+    assert rel_err(got, want) < TOL
+    assert rel_err(rep.objective, wrep["objective"]) < TOL
+    assert abs(rep.initial_objective - wrep["initial_objective"]) <= 1e-10 * abs(wrep["initial_objective"])
