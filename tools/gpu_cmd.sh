@@ -1,1 +1,1 @@
-timeout 1200 python -m pytest tests/test_full_configs.py -x -q -k "reference_binary" --durations=5 > gpurun_out/t10.log 2>&1; echo rc=$? >> gpurun_out/t10.log
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:fold_axis3 -s 1 -c 1 -o gpurun_out/fa3b python tools/prof_sharded.py 2 > gpurun_out/ncu_fa3.log 2>&1
