@@ -1,1 +1,3 @@
-timeout 600 ncu --set full --import-source on --clock-control none -k regex:fold_axis3 -s 1 -c 1 -o gpurun_out/fa3b python tools/prof_sharded.py 2 > gpurun_out/ncu_fa3.log 2>&1
+export VSR_NO_GRAPH=1
+timeout 900 ncu --set full --clock-control none -k regex:"fold_axis1|tv_stencil_fast|rpair_fwd|rpair_inv|fft_pass" -s 6 -c 6 -o gpurun_out/r01h_tv python tools/prof_step.py tv > gpurun_out/ncu_tv.log 2>&1
+tail -2 gpurun_out/ncu_tv.log
