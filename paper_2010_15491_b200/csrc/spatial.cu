@@ -43,6 +43,16 @@ void launch_spatial_v(const Dims& lr, int d, const SpatialPlan& p, const double2
     VSR_LAUNCH_CHECK();
 }
 
+// 1/x for finite x > 0: MUFU.RCP64H seed and two Newton steps (~1 ulp),
+// branch-free unlike the IEEE division sequence
+__device__ __forceinline__ double rcp_pos(double x) {
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    y = y * fma(-x, y, 2.0);
+    y = y * fma(-x, y, 2.0);
+    return y;
+}
+
 // --------------------------------------------------- LR axis-3 sandwich
 // In place on Y (LR spectrum after the forward axis-1/2 passes, unscaled):
 // forward axis-3 FFT, scale fs, U(g) as in spatial_u_kernel, inverse axis-3
@@ -99,7 +109,7 @@ __global__ void __launch_bounds__(SwShape<L>::THREADS, 512 / SwShape<L>::THREADS
         const int g3 = t + P * r;
         const double2 y = cscale(v[r], cy);
         const double2 num = Zl ? csub(y, cmul(__ldg(Zl + p + S * g3), cmul(ab1, __ldg(c1 + g3)))) : y;
-        v[r] = cscale(num, 1.0 / (ab2 * __ldg(c2 + g3) + shift));
+        v[r] = cscale(num, rcp_pos(ab2 * __ldg(c2 + g3) + shift));
     }
     __syncthreads();  // the exchange buffer is reused by the inverse transform
     fftc::stockham<L, true, decltype(sidx), kSwR>(v, t, smw, sidx, tw);

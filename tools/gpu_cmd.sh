@@ -1,3 +1,5 @@
-export VSR_NO_GRAPH=1
-timeout 900 ncu --set full --clock-control none -k regex:"fold_axis1|tv_stencil_fast|rpair_fwd|rpair_inv|fft_pass" -s 6 -c 6 -o gpurun_out/r01h_tv python tools/prof_step.py tv > gpurun_out/ncu_tv.log 2>&1
-tail -2 gpurun_out/ncu_tv.log
+timeout 600 python -m pytest tests/test_gpu_parity.py tests/test_golden.py -x -q -k "spatial or env_variants or tikhonov or config0" > gpurun_out/t2.log 2>&1; echo rc=$? >> gpurun_out/t2.log
+rm -f gpurun_out/b2.log
+for v in "" ""; do
+  env $v timeout 300 python bench.py --no-tv --no-cpu --no-fft-path --no-config4 --steps 30 --warmup 5 2>>gpurun_out/b2.err | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print(d['ms_per_step'], {k:round(v['avg_us'],1) for k,v in d['stages'].items()})" >> gpurun_out/b2.log
+done
