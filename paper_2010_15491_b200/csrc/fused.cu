@@ -147,7 +147,8 @@ __global__ void __launch_bounds__(FShape<L, A>::THREADS, (512 / FShape<L, A>::TH
             const double iden = fast_rcp(den);
             w = make_double2(Sx * iden, Sy * iden);
         } else {
-            w = make_double2(Sx / den, Sy / den);
+            const double iden = fast_rcp(den);
+            w = make_double2(Sx * iden, Sy * iden);
         }
         double ax = 0.0, ay = 0.0;
 #pragma unroll
