@@ -1,6 +1,5 @@
-nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,temperature.gpu,power.draw --format=csv > gpurun_out/smi2.txt
-for i in 1 2; do
-timeout 600 python bench.py --no-cpu --no-config4 --no-fft-path --steps 20 > gpurun_out/b9.json 2> gpurun_out/b9.err
-python -c "
-import json;d=json.loads(open('gpurun_out/b9.json').read().strip().splitlines()[-1]);print(d['ms_per_step'], d['tv']['ms_per_iter'], d['clocks'], {k:round(v['avg_us'],1) for k,v in d['tv']['stages'].items()})" >> gpurun_out/b10.txt
-done
+SECONDS=0
+timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/r01i_gputests.log 2>&1; echo "rc=$? t=$SECONDS" >> gpurun_out/r01i_gputests.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r01i_smoke.log 2>&1; echo "rc=$?" >> gpurun_out/r01i_smoke.log
+timeout 900 python bench.py > gpurun_out/r01i_bench.json 2> gpurun_out/r01i_bench.err
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file gpurun_out/r01i_launches.csv python bench.py --steps 3 --warmup 3 --no-cpu --no-config4 > gpurun_out/ncu_l.log 2>&1
