@@ -1,5 +1,5 @@
-SECONDS=0
-timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/r01i_gputests.log 2>&1; echo "rc=$? t=$SECONDS" >> gpurun_out/r01i_gputests.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r01i_smoke.log 2>&1; echo "rc=$?" >> gpurun_out/r01i_smoke.log
-timeout 900 python bench.py > gpurun_out/r01i_bench.json 2> gpurun_out/r01i_bench.err
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file gpurun_out/r01i_launches.csv python bench.py --steps 3 --warmup 3 --no-cpu --no-config4 > gpurun_out/ncu_l.log 2>&1
+timeout 600 python -m pytest tests/test_gpu_parity.py -x -q -k "spatial or env_variants or rfft" > gpurun_out/t2.log 2>&1; echo rc=$? >> gpurun_out/t2.log
+rm -f gpurun_out/b2.log
+for v in "" ""; do
+  env $v timeout 300 python bench.py --no-tv --no-cpu --no-fft-path --no-config4 --steps 30 --warmup 5 2>>gpurun_out/b2.err | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print(d['ms_per_step'], {k:round(v['avg_us'],1) for k,v in d['stages'].items()})" >> gpurun_out/b2.log
+done
