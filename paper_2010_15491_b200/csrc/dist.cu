@@ -14,6 +14,8 @@
 #include <cmath>
 #include <cstdlib>
 #include <functional>
+#include <list>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -195,15 +197,17 @@ void free_state(TvFoldState& e) {
 // rebuild = true (vsr_slab_tv_prepare_d): the Lambda slice behind lam_loc is new
 TvFoldState& tv_fold_state(vsr_ctx* ctx, const Slab& g, int rank, const double* lam_loc, const FoldGeom& G,
                            cudaStream_t st, bool rebuild = false) {
-    static std::vector<TvFoldState> cache;
-    for (size_t i = 0; i < cache.size(); ++i) {
-        auto& e = cache[i];
+    static std::list<TvFoldState> cache;  // references stay valid as entries come and go
+    static std::mutex mu;                  // several host threads may drive ranks of one process
+    std::lock_guard<std::mutex> lock(mu);
+    for (auto it = cache.begin(); it != cache.end(); ++it) {
+        auto& e = *it;
         if (e.ctx == ctx && e.lam == lam_loc && e.m == g.m && e.nP == g.nP && e.s == g.s && e.rank == rank &&
             e.P == g.P && e.rates[0] == g.rates[0] && e.rates[1] == g.rates[1] && e.rates[2] == g.rates[2]) {
             if (!rebuild) return e;
             VSR_CUDA(cudaStreamSynchronize(st));  // no queued fold still reads these tables
             free_state(e);
-            cache.erase(cache.begin() + (long)i);
+            cache.erase(it);
             break;
         }
     }
