@@ -248,6 +248,9 @@ int vsr_slab_tik_fold_d(vsr_ctx* ctx, const size_t hr_dims[3], const size_t rate
                         double* W_out);
 int vsr_slab_tv_prepare_d(vsr_ctx* ctx, const size_t hr_dims[3], const size_t rates[3], int P, int rank,
                           const double* lam_loc);
+/* frees the fold tables cached by vsr_slab_tv_prepare_d for lam_loc (NULL: all of
+ * this context's; vsr_ctx_destroy also frees them) */
+int vsr_slab_tv_release_d(vsr_ctx* ctx, const double* lam_loc);
 int vsr_slab_tv_fold_d(vsr_ctx* ctx, const size_t hr_dims[3], const size_t rates[3], int P, int rank,
                        const double* Yl_loc, const double* lam_loc, double* W, double mu, double tau,
                        double fwd_scale, double* fit_out);

@@ -23,7 +23,6 @@
 #include "spatial.cuh"
 #include "l2l2.cuh"
 #include "rfft.cuh"
-#include "chain.cuh"
 #include "tv.cuh"
 
 using namespace vsr;
@@ -367,17 +366,6 @@ void require_ctx(vsr_ctx* ctx) {
 
 double inv_sqrt_count(const Dims& d) { return 1.0 / std::sqrt((double)d.count()); }
 
-// Fused fold + axis-3 FFT kernels unless disabled (VSR_NO_FUSE=1, for A/B runs).
-// Chained in-plane passes (chain.cuh): opt-in (VSR_CHAIN=1) until they beat
-// two plain passes (measured r01: 201 us vs 173 us at 256^3).
-bool use_chain() {
-    static const bool on = [] {
-        const char* e = std::getenv("VSR_CHAIN");
-        return e && e[0] == '1';
-    }();
-    return on;
-}
-
 // Which pass the fold is fused with: 1 (contiguous rows), 3 (strided lines) or
 // 0 (none).  Measured at 256^3 (r01): Tikhonov fold+axis3 220 us vs
 // fold+axis1 285 us; TV sandwich on axis 1 358 us vs axis 3 470 us.  So the
@@ -430,6 +418,7 @@ bool use_fused(const FoldGeom& G) {
 
 // hooks for the other C-ABI translation units (dist.cu)
 namespace vsr_capi {
+void release_slab_state(vsr_ctx* ctx, const double* lam_loc);  // dist.cu
 cudaStream_t stream_of(vsr_ctx* ctx) {
     if (!ctx) throw std::invalid_argument("vsr: null context");
     return ctx->stream;
@@ -469,6 +458,7 @@ int vsr_ctx_destroy(vsr_ctx* ctx) {
         if (!ctx) return;
         vsr_ctx::Guard g(ctx->device);
         cudaStreamSynchronize(ctx->stream);
+        vsr_capi::release_slab_state(ctx, nullptr);  // slab TV fold tables cached for this context
         ctx->scal.release();
         ctx->bad.release();
         cudaStreamDestroy(ctx->stream);
@@ -953,9 +943,6 @@ struct vsr_tikhonov {
     }
     DevBuf<double2> sp_s1, U;
     DevBuf<unsigned long long> lrbad;
-    ChainPlan chain;                  // chained inverse axes 2 -> 1 (L2 ring)
-    DevBuf<double2> ring;
-    DevBuf<int> chain_ctr;
 };
 
 static void tik_reset_status(vsr_tikhonov* t) {
@@ -988,14 +975,6 @@ static vsr_tikhonov* tik_new(vsr_ctx* ctx, const size_t hr_dims[3], const size_t
     t->y.alloc(Nl);
     t->x.alloc(N);
     t->res_blocks = std::max(fft_engine().inverse_final_blocks(sp.hr), fft_engine().pass_blocks(sp.hr, 2));
-    if (use_chain() && use_fused(t->G)) {
-        t->chain = chain_plan(sp.hr);
-        if (t->chain.ok) {
-            t->ring.alloc(t->chain.scratch_elems);
-            t->chain_ctr.alloc(1 + 2 * t->chain.chunks);
-            t->res_blocks = std::max(t->res_blocks, t->chain.b_total());
-        }
-    }
     t->partials.alloc(2 * std::max<size_t>(t->res_blocks, 1));
     t->status.alloc(4);
     t->bad.alloc(1);
@@ -1097,13 +1076,19 @@ static void tik_spatial(vsr_tikhonov* t, cudaStream_t st) {
         VSR_CUDA(cudaMemsetAsync(yz.p, 0, yz.bytes(), st));
         launch_spatial_v(lr, t->sp.rate(), p, yz.p, t->Zl.p, t->reg, uq.p, st);  // -Z G1 / (G2 + s)
         t->q.alloc(Nl);
-        const size_t qb = fft_engine().inverse_final_blocks(lr);
-        DevBuf<double> qpart(2 * std::max<size_t>(qb, 1));
-        DevBuf<unsigned long long> qbad(1);
-        PassReduce qr{qpart.p, qbad.p};
+        // q is real by construction (Z is the spectrum of a real lattice
+        // prior, G1 and G2 are real even filters): check it like ifft3_real
+        // (fft.cpp:86-96) before it enters every solve
+        ResidueCheck qc(t->ctx, lr);
         fft_engine().inverse3(lr, uq.p, t->q.p, OUT_REAL,
-                              -inv_sqrt_count(lr) * std::sqrt((double)t->sp.rate()), &qr, st);
-        VSR_CUDA(cudaStreamSynchronize(st));
+                              -inv_sqrt_count(lr) * std::sqrt((double)t->sp.rate()), &qc.red, st);
+        double qstat[4];
+        unsigned long long qbad = 0;
+        qc.finish(t->ctx, 1e-8, qstat, &qbad);
+        if (qstat[0] != 0.0) throw numeric_error(residue_message(qstat[1], 1e-8));
+        if (qbad != ULLONG_MAX)
+            throw numeric_error("tikhonov_fast: non-finite value at flat index " + std::to_string(qbad) +
+                                " of the prior's LR term");
         t->half = true;
     } else if (!spatial_sandwich_ok(lr)) {
         t->U.alloc(lr.count());  // unfused LR stage: U kernel + inverse3
@@ -1272,14 +1257,7 @@ static void tik_enqueue(vsr_tikhonov* t, const double* y_dev, double* x_dev) {
             ProfScope ps(prof, "tik_fold_ifft_axis3", st);
             launch_tik_fold_ifft3(t->G, t->Yl.p, t->lam.p, t->xbh.p, t->xh.p, t->reg, st, t->sep.t, t->Zl.p);
         }
-        if (t->chain.ok) {
-            ProfScope ps(prof, "chain_inv_axis2_axis1_c2r", st);
-            ChainWork w{t->ring.p, t->chain_ctr.p};
-            launch_chain_inverse(t->sp.hr, t->chain, w, t->xh.p, x_dev, inv_sqrt_count(t->sp.hr), red, st);
-        } else {
-            fft_engine().inverse21(t->sp.hr, t->xh.p, x_dev, OUT_REAL, inv_sqrt_count(t->sp.hr), &red,
-                                   st, prof);
-        }
+        fft_engine().inverse21(t->sp.hr, t->xh.p, x_dev, OUT_REAL, inv_sqrt_count(t->sp.hr), &red, st, prof);
     } else {
         {
             ProfScope ps(prof, "tik_fold", st);
@@ -1293,8 +1271,7 @@ static void tik_enqueue(vsr_tikhonov* t, const double* y_dev, double* x_dev) {
         ProfScope ps(prof, "residue_status", st);
         const size_t nres = t->spl.ok ? fft_engine().pass_blocks(t->sp.lr, 0)
                             : fuse_axis(t->G, 3) == 1 ? fft_engine().pass_blocks(t->sp.hr, 2)
-                            : (use_fused(t->G) && t->chain.ok) ? t->chain.b_total()
-                                                               : fft_engine().inverse_final_blocks(t->sp.hr);
+                                                 : fft_engine().inverse_final_blocks(t->sp.hr);
         residue_status_kernel<<<1, 1024, 0, st>>>(t->partials.p, (long long)nres, 1e-8, t->status.p);
         VSR_LAUNCH_CHECK();
     }
@@ -1532,9 +1509,6 @@ struct vsr_tv {
     DevBuf<unsigned long long> bad;
     DevBuf<double> obj, res, rel, status, init_obj;
     size_t fit_blocks = 0, st_blocks = 0, res_blocks = 0;
-    ChainPlan chain;
-    DevBuf<double2> ring;
-    DevBuf<int> chain_ctr;
     SepState sep;
     DevBuf<double> gw;  // LR table sum_b Gamma_b |Lambda_b|^2 (axis-1 sandwich)
     DevBuf<double2> W2;  // sandwich output on the half-spectrum path (m x n x (s/2+1))
@@ -1611,14 +1585,6 @@ static vsr_tv* tv_build(vsr_ctx* ctx, const Spec& sp, const double* y_dev, const
         h->fit_blocks = tv_fold_blocks(h->G);
         h->st_blocks = stencil_geom(hr).blocks();
         h->res_blocks = fft_engine().inverse_final_blocks(hr);
-        if (use_chain() && use_fused(h->G)) {
-            h->chain = chain_plan(hr);
-            if (h->chain.ok) {
-                h->ring.alloc(h->chain.scratch_elems);
-                h->chain_ctr.alloc(1 + 2 * h->chain.chunks);
-                h->res_blocks = h->chain.b_total();
-            }
-        }
         h->fitp.alloc(std::max<size_t>(
             std::max(std::max(std::max(h->fit_blocks, fit_blocks(h->G)), tv_sandwich_blocks(h->G)),
                      tv_sandwich1_blocks(h->G)),
@@ -1701,7 +1667,6 @@ static void tv_step(vsr_tv* h) {
     Profiler* prof = h->ctx->prof();
     GammaTables tabs{h->tnr.p, h->tnc.p, h->tns.p, h->tau, h->gw.p};
     const bool fused = use_fused(h->G);
-    ChainWork cw{h->ring.p, h->chain_ctr.p};
     const bool a1 = fuse_axis(h->G, 1) == 1;
     // Hermitian half spectrum along axis 3 (theta is real): planes 0..s/2 only
     const bool half = a1 && tv_half(hr);
@@ -1732,12 +1697,7 @@ static void tv_step(vsr_tv* h) {
         ProfScope ps(prof, "tv_fft1_fold_ifft1", st);
         launch_tv_sandwich1(h->G, h->Yl.p, h->lam.p, h->W.p, tabs, h->mu, s, h->fitp.p, st, h->sep.t);
     } else if (fused) {
-        if (h->chain.ok) {
-            ProfScope ps(prof, "chain_fwd_axis1_r2c_axis2", st);
-            launch_chain_forward(hr, h->chain, cw, h->theta.p, h->W.p, st);
-        } else {
-            fft_engine().forward12(hr, h->theta.p, IN_REAL, h->W.p, st, prof);
-        }
+        fft_engine().forward12(hr, h->theta.p, IN_REAL, h->W.p, st, prof);
         tv_join(h);
         ProfScope ps(prof, "tv_fft3_fold_ifft3", st);
         launch_tv_sandwich(h->G, h->Yl.p, h->lam.p, h->W.p, tabs, h->mu, s, h->fitp.p, st, h->sep.t);
@@ -1763,9 +1723,6 @@ static void tv_step(vsr_tv* h) {
         }
         ProfScope ps(prof, "fft_inv_axis3_c2r", st);
         fft_engine().axis_pass(hr, 2, true, h->W.p, IN_COMPLEX, h->x.p, OUT_REAL, s, &red, st);
-    } else if (fused && h->chain.ok) {
-        ProfScope ps(prof, "chain_inv_axis2_axis1_c2r", st);
-        launch_chain_inverse(hr, h->chain, cw, h->W.p, h->x.p, s, red, st);
     } else if (fused)
         fft_engine().inverse21(hr, h->W.p, h->x.p, OUT_REAL, s, &red, st, prof);
     else
@@ -1810,7 +1767,7 @@ static void tv_step(vsr_tv* h) {
 }
 
 // Fixed-count iterations (rel_tol = 0, profiler off) replay a CUDA graph of
-// two consecutive iterations (the dual buffers ping-pong with period 2; the
+// kTvGraphIters consecutive iterations (a multiple of the ping-pong period 2) (the dual buffers ping-pong with period 2; the
 // iteration index lives on the device).  VSR_NO_GRAPH=1 keeps eager launches.
 static void tv_iterate(vsr_tv* h, size_t iters) {
     static const bool no_graph = [] {

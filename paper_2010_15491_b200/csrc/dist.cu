@@ -194,12 +194,20 @@ void free_state(TvFoldState& e) {
     if (e.sep) cudaFree(e.sep);
 }
 
+std::list<TvFoldState>& state_cache() {
+    static std::list<TvFoldState> cache;  // references stay valid as entries come and go
+    return cache;
+}
+std::mutex& state_mutex() {
+    static std::mutex mu;  // several host threads may drive ranks of one process
+    return mu;
+}
+
 // rebuild = true (vsr_slab_tv_prepare_d): the Lambda slice behind lam_loc is new
 TvFoldState& tv_fold_state(vsr_ctx* ctx, const Slab& g, int rank, const double* lam_loc, const FoldGeom& G,
                            cudaStream_t st, bool rebuild = false) {
-    static std::list<TvFoldState> cache;  // references stay valid as entries come and go
-    static std::mutex mu;                  // several host threads may drive ranks of one process
-    std::lock_guard<std::mutex> lock(mu);
+    auto& cache = state_cache();
+    std::lock_guard<std::mutex> lock(state_mutex());
     for (auto it = cache.begin(); it != cache.end(); ++it) {
         auto& e = *it;
         if (e.ctx == ctx && e.lam == lam_loc && e.m == g.m && e.nP == g.nP && e.s == g.s && e.rank == rank &&
@@ -239,6 +247,24 @@ TvFoldState& tv_fold_state(vsr_ctx* ctx, const Slab& g, int rank, const double* 
 }
 
 }  // namespace
+
+// Frees the cached fold tables of one context (vsr_ctx_destroy), or of one
+// Lambda slice of it (lam_loc != nullptr; vsr_slab_tv_release_d, called when a
+// slab ADMM-TV program is torn down).
+namespace vsr_capi {
+void release_slab_state(vsr_ctx* ctx, const double* lam_loc) {
+    auto& cache = state_cache();
+    std::lock_guard<std::mutex> lock(state_mutex());
+    for (auto it = cache.begin(); it != cache.end();) {
+        if (it->ctx == ctx && (lam_loc == nullptr || it->lam == lam_loc)) {
+            free_state(*it);
+            it = cache.erase(it);
+        } else {
+            ++it;
+        }
+    }
+}
+}  // namespace vsr_capi
 
 extern "C" {
 
@@ -309,6 +335,15 @@ int vsr_slab_tik_fold_d(vsr_ctx* ctx, const size_t hr[3], const size_t rates[3],
             const Dims ld{(size_t)g.m, (size_t)g.nP, (size_t)g.s};
             fft_engine().axis_pass(ld, 2, true, out, IN_COMPLEX, out, OUT_COMPLEX, 1.0, nullptr, st);
         }
+    });
+}
+
+
+int vsr_slab_tv_release_d(vsr_ctx* ctx, const double* lam_loc) {
+    return vsr_capi::guard_call([&] {
+        DevGuard dg(vsr_capi::device_of(ctx));
+        VSR_CUDA(cudaStreamSynchronize(vsr_capi::stream_of(ctx)));  // no queued fold still reads them
+        vsr_capi::release_slab_state(ctx, lam_loc);
     });
 }
 

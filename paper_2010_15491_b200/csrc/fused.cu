@@ -31,15 +31,6 @@ struct FShape {
 // xor-butterfly over the A alias lanes (lane stride T): every lane ends with
 // the bit-identical total (fp addition is commutative, so each level combines
 // identical operand pairs on both partners).
-// 1/x for finite x > 0 (Gamma denominators): MUFU.RCP64H seed and two Newton
-// steps (~1 ulp), branch-free unlike the IEEE division sequence.
-__device__ __forceinline__ double fast_rcp(double x) {
-    double y;
-    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-    y = y * fma(-x, y, 2.0);
-    y = y * fma(-x, y, 2.0);
-    return y;
-}
 
 template <int T, int A>
 __device__ __forceinline__ double lanes_sum(double v) {
@@ -126,7 +117,7 @@ __global__ void __launch_bounds__(FShape<L, A>::THREADS, (512 / FShape<L, A>::TH
             const int r = rr + RD * bs;
             if constexpr (TV) {
                 // k = conj(L) F D^H y + mu theta_hat (solvers.cpp:342-344,375); ĝ = Γ k (:223)
-                Gg[bs] = fast_rcp((base_g + __ldg(tabs.ns + (t + P * r))) + tabs.tau);
+                Gg[bs] = rcp_pos((base_g + __ldg(tabs.ns + (t + P * r))) + tabs.tau);
                 v[r] = cscale(cadd(cmulc(Lm[r], yv), cscale(v[r], cA)), Gg[bs]);
                 gram += Gg[bs] * cnorm(Lm[r]);
             } else {
@@ -144,10 +135,10 @@ __global__ void __launch_bounds__(FShape<L, A>::THREADS, (512 / FShape<L, A>::TH
         const double den = gram + shift;
         double2 w;
         if constexpr (TV) {
-            const double iden = fast_rcp(den);
+            const double iden = rcp_pos(den);
             w = make_double2(Sx * iden, Sy * iden);
         } else {
-            const double iden = fast_rcp(den);
+            const double iden = rcp_pos(den);
             w = make_double2(Sx * iden, Sy * iden);
         }
         double ax = 0.0, ay = 0.0;
@@ -372,7 +363,7 @@ __device__ __forceinline__ void fold_axis1_tile(int tile, FoldGeom G, const doub
                 for (int br = 0; br < DR; ++br) {
                     const int r = rr + RD * br;
                     const double2 Lr = sm[sidx(t + P * r)];
-                    Gg[br] = fast_rcp((nr_s[t + P * r] + base_g) + tabs.tau);
+                    Gg[br] = rcp_pos((nr_s[t + P * r] + base_g) + tabs.tau);
                     v[r] = cscale(cadd(cmulc(Lr, yv), cscale(v[r], cA)), Gg[br]);
                     const double2 pr = cmul(Lr, v[r]);
                     Sx += pr.x;
@@ -380,7 +371,7 @@ __device__ __forceinline__ void fold_axis1_tile(int tile, FoldGeom G, const doub
                 }
                 Sx = lanes_sum<1, A>(Sx);
                 Sy = lanes_sum<1, A>(Sy);
-                const double iden = fast_rcp(gwv[rr] + shift);
+                const double iden = rcp_pos(gwv[rr] + shift);
                 const double2 w = make_double2(Sx * iden, Sy * iden);
 #pragma unroll
                 for (int br = 0; br < DR; ++br) {
@@ -539,18 +530,7 @@ void launch_a1(const FoldGeom& G, const double2* Yl, const double2* lam, const S
     if (Sh::SMEM > 48 * 1024)
         VSR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Sh::SMEM));
     const int ntiles = (int)((G.nl / Sh::T) * G.sl);
-    static const bool persist = [] {
-        const char* e = std::getenv("VSR_A1_PERSIST");  // opt-in: measured slower (254 vs 241 us)
-        return e && e[0] == '1';
-    }();
-    unsigned grid = (unsigned)ntiles;
-    if (persist) {
-        int per_sm = 0, dev = 0, sms = 0;
-        VSR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, Sh::THREADS, Sh::SMEM));
-        VSR_CUDA(cudaGetDevice(&dev));
-        VSR_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        grid = (unsigned)std::min<long long>(ntiles, (long long)std::max(per_sm, 1) * sms);
-    }
+    const unsigned grid = (unsigned)ntiles;
     kern<<<grid, Sh::THREADS, Sh::SMEM, st>>>(ntiles, G, Yl, lam, sep, xbh, Zl, W, out, tabs, cA, shift, inv_scale,
                                               1.0 / std::sqrt((double)G.d), fwd_scale,
                                               fft_engine().twiddles((size_t)L), fit);
@@ -569,18 +549,10 @@ bool dispatch_a1(const FoldGeom& G, const double2* Yl, const double2* lam, const
                  const double2* xbh, const double2* Zl, double2* W, double2* out, const GammaTables& tabs, double cA, double shift,
                  double inv_scale, double fwd_scale, double* fit, cudaStream_t st) {
     const int A = G.dc * G.ds;
-    static const int rm = [] {
-        const char* e = std::getenv("VSR_A1_RM");
-        return e ? std::atoi(e) : 16;
-    }();
 #define VSR_X(LL, AA, DD)                                                                           \
     if (G.m == LL && A == AA && G.dr == DD && G.nl % A1Shape<LL, AA, DD>::T == 0) {                  \
-        if (rm == 8 && DD <= 8 && A1Shape<LL, AA, DD, 8>::T == A1Shape<LL, AA, DD>::T)               \
-            launch_a1<LL, AA, DD, TV, FIT, 8>(G, Yl, lam, sep, xbh, Zl, W, out, tabs, cA, shift, inv_scale, \
-                                              fwd_scale, fit, st);                                  \
-        else                                                                                        \
-            launch_a1<LL, AA, DD, TV, FIT>(G, Yl, lam, sep, xbh, Zl, W, out, tabs, cA, shift, inv_scale, \
-                                           fwd_scale, fit, st);                                     \
+        launch_a1<LL, AA, DD, TV, FIT>(G, Yl, lam, sep, xbh, Zl, W, out, tabs, cA, shift, inv_scale,   \
+                                       fwd_scale, fit, st);                                         \
         return true;                                                                                \
     }
     VSR_A1_TABLE(VSR_X)

@@ -43,16 +43,6 @@ void launch_spatial_v(const Dims& lr, int d, const SpatialPlan& p, const double2
     VSR_LAUNCH_CHECK();
 }
 
-// 1/x for finite x > 0: MUFU.RCP64H seed and two Newton steps (~1 ulp),
-// branch-free unlike the IEEE division sequence
-__device__ __forceinline__ double rcp_pos(double x) {
-    double y;
-    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-    y = y * fma(-x, y, 2.0);
-    y = y * fma(-x, y, 2.0);
-    return y;
-}
-
 // --------------------------------------------------- LR axis-3 sandwich
 // In place on Y (LR spectrum after the forward axis-1/2 passes, unscaled):
 // forward axis-3 FFT, scale fs, U(g) as in spatial_u_kernel, inverse axis-3

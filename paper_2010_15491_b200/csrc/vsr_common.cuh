@@ -118,4 +118,18 @@ __device__ __forceinline__ void block_reduce_sum(double (&v)[NV], double* smem /
     }
 }
 
+// ------------------------------------------------- reciprocal of a positive
+// 1/x for x > 0: MUFU.RCP64H seed and two Newton steps (~1 ulp), cheaper than
+// the IEEE division sequence.  The seed flushes subnormal x to 0 (-> inf), so
+// x below DBL_MIN (a denominator |Lambda|^2 + 2 reg d with a subnormal reg)
+// takes the IEEE division instead.
+__device__ __forceinline__ double rcp_pos(double x) {
+    if (x < 2.2250738585072014e-308) return 1.0 / x;
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    y = y * fma(-x, y, 2.0);
+    y = y * fma(-x, y, 2.0);
+    return y;
+}
+
 }  // namespace vsr

@@ -166,7 +166,10 @@ class GpuStages:
 
     # buffers
     def zeros(self, rank, n, dtype=torch.float64):
-        return torch.zeros(n, dtype=dtype, device=self.device[rank])
+        # zero-filled on the rank's library stream, so the fill is ordered
+        # before every library kernel that later writes or reads the buffer
+        with self.stream(rank):
+            return torch.zeros(n, dtype=dtype, device=self.device[rank])
 
     def stream(self, rank):
         return torch.cuda.stream(self.streams[rank])
@@ -210,6 +213,9 @@ class GpuStages:
         hr, rt = self._geo(g)
         self._call("vsr_slab_tv_prepare_d", self.ctx[rank].handle, hr, rt, g.P, rank, self._d(lam))
 
+    def tv_release(self, rank, lam):
+        self._call("vsr_slab_tv_release_d", self.ctx[rank].handle, self._d(lam))
+
     def tv_fold(self, rank, g, Yl_loc, lam, W, mu, tau, fwd_scale, fit):
         hr, rt = self._geo(g)
         self._call("vsr_slab_tv_fold_d", self.ctx[rank].handle, hr, rt, g.P, rank, self._d(Yl_loc),
@@ -237,7 +243,8 @@ class GpuStages:
 
 def _ulong_max_tensor(st, rank):
     t = st.zeros(rank, 1, dtype=torch.int64)
-    t.fill_(-1)  # all ones == ULLONG_MAX
+    with st.stream(rank):
+        t.fill_(-1)  # all ones == ULLONG_MAX
     return t
 
 
@@ -260,6 +267,20 @@ class _Base:
         for r in self.ranks:
             with self.st.stream(r):
                 fn(r)
+
+    def _sync_all(self):
+        for r in self.ranks:
+            self.st.synchronize(r)
+
+    def _gather(self, vals):
+        """All-gather of per-rank device scalars, issued on the rank's library
+        stream (NCCL orders itself against the current stream) so it reads the
+        values the rank's kernels wrote."""
+        if self._ordered():
+            with self.st.stream(self.ranks[0]):
+                return self.ex.gather(vals)
+        self._sync_all()
+        return self.ex.gather(vals)
 
     def forward3(self, slabs: Dict[int, torch.Tensor], real: bool, scale: float,
                  out: Dict[int, torch.Tensor]):
@@ -304,6 +325,25 @@ class _Base:
         self._each(lambda r: self.st.unpack_inv_xy(r, self.g, src[r], self.work[r], out_slabs[r], scale,
                                                    sums[r], bad[r]))
 
+    def _check_status(self, sums_by_rank, where):
+        """Imaginary-residue ratio (fft.cpp:89-93) and first non-finite index
+        (volume.cpp:31-36) of the last inverse, summed over ranks in rank order.
+        Every rank's work is complete when this returns (x is safe to read on
+        any stream)."""
+        g = self.g
+        self._sync_all()
+        sums = self._gather(sums_by_rank)
+        im2 = sum(float(s[0]) for s in sums)
+        tot2 = sum(float(s[1]) for s in sums)
+        from .volsr import NumericError
+        if tot2 > 0.0 and math.sqrt(im2 / tot2) > 1e-8:
+            raise NumericError(f"ifft3_real: imaginary residue {math.sqrt(im2 / tot2):f} exceeds 0.000000 "
+                               "(spectral bookkeeping bug?)")
+        bads = [int(b[0]) for b in self._gather(self.bad)]
+        for p, b in enumerate(bads):
+            if b != -1:
+                raise NumericError(f"{where}: non-finite value at flat index {p * g.slab_elems + b}")
+
 
 class SlabTikhonov(_Base):
     """Distributed TikhonovOperator (solvers.cpp:36-67): Lambda and fft3(xbar)
@@ -327,22 +367,9 @@ class SlabTikhonov(_Base):
         g = self.g
         self._lr_spectrum(y_full)
         self._each(lambda r: self.st.tik_fold(r, g, self.Yl[r], self.lam[r], self.xbh[r], self.reg, self.W[r]))
-        for r in self.ranks:
-            self.bad[r].fill_(-1)
+        self._each(lambda r: self.bad[r].fill_(-1))  # on the rank stream, ahead of the unpack that sets it
         self._inverse_to_slabs(self.W, x_slabs, 1.0 / math.sqrt(g.N), self.sums, self.bad)
-        sums = self.ex.gather(self.sums)
-        im2 = sum(float(s[0]) for s in sums)
-        tot2 = sum(float(s[1]) for s in sums)
-        if tot2 > 0.0 and math.sqrt(im2 / tot2) > 1e-8:
-            from .volsr import NumericError
-            raise NumericError(f"ifft3_real: imaginary residue {math.sqrt(im2 / tot2):f} exceeds 0.000000 "
-                               "(spectral bookkeeping bug?)")
-        bads = [int(b[0]) for b in self.ex.gather(self.bad)]
-        for p, b in enumerate(bads):
-            if b != -1:
-                from .volsr import NumericError
-                raise NumericError(f"tikhonov_fast: non-finite value at flat index {p * g.slab_elems + b}")
-
+        self._check_status(self.sums, "tikhonov_fast")
 
 class SlabADMMTV(_Base):
     """Distributed admm_tv (solvers.cpp:321-411) with rel_tol = 0 semantics
@@ -376,9 +403,10 @@ class SlabADMMTV(_Base):
         self.halo_hi = {r: stages.zeros(r, pl) for r in self.ranks}
         self.dhalo_out = {r: stages.zeros(r, 3 * pl) for r in self.ranks}
         self.dhalo_in = {r: stages.zeros(r, 3 * pl) for r in self.ranks}
-        for r in self.ranks:
-            self.x_ext[r][pl:pl * (g.sz + 1)].copy_(x0_slabs[r].reshape(-1))
+        # buffers above were zeroed on torch's current stream: order the rank
+        # stream after them before any library kernel touches them
         self._torch_sync()
+        self._each(lambda r: self.x_ext[r][pl:pl * (g.sz + 1)].copy_(x0_slabs[r].reshape(-1)))
         # initial objective: data term from fft3(x0), TV from the init stencil
         self.forward3({r: self.x_ext[r][pl:pl * (g.sz + 1)] for r in self.ranks}, True, 1.0 / math.sqrt(g.N),
                       self.W)
@@ -386,14 +414,10 @@ class SlabADMMTV(_Base):
         self._halo_x()
         self._each(lambda r: self.st.stencil(r, g, True, self.x_ext[r], None, self.dual[0][r], self.theta[r],
                                              lam_tv / mu, self.s_st[r]))
-        fit = sum(float(v[0]) for v in self.ex.gather(self.s_fit))
-        tv = sum(float(v[1]) for v in self.ex.gather(self.s_st))
+        fit = sum(float(v[0]) for v in self._gather(self.s_fit))
+        tv = sum(float(v[1]) for v in self._gather(self.s_st))
         self.initial_objective = 0.5 * fit + lam_tv * tv
         self.objective, self.primal_residual = [], []
-
-    def _sync_all(self):
-        for r in self.ranks:
-            self.st.synchronize(r)
 
     def _torch_sync(self):
         for r in self.ranks:
@@ -447,13 +471,13 @@ class SlabADMMTV(_Base):
         g, pl = self.g, self.g.plane
         s = 1.0 / math.sqrt(g.N)
         # per-iteration scalars stay on the device (fit, residual^2, TV); gathered once after the loop
-        hist = {r: self.st.zeros(r, 3 * k) for r in self.ranks}
+        hist = {}
+        self._each(lambda r: hist.__setitem__(r, self.st.zeros(r, 3 * k)))
         for it in range(k):
             self.forward3_theta()
             self._each(lambda r: self.st.tv_fold(r, g, self.Yl[r], self.lam[r], self.W[r], self.mu, self.tau, s,
                                                  self.s_fit[r]))
-            for r in self.ranks:
-                self.bad[r].fill_(-1)
+            self._each(lambda r: self.bad[r].fill_(-1))
             self._inverse_to_slabs(self.W, {r: self.x_ext[r][pl:pl * (g.sz + 1)] for r in self.ranks}, s,
                                    self.s_res, self.bad)
             self._halo_x()
@@ -467,18 +491,29 @@ class SlabADMMTV(_Base):
                 hist[r][3 * it:3 * it + 1].copy_(self.s_fit[r][0:1])
                 hist[r][3 * it + 1:3 * it + 3].copy_(self.s_st[r][0:2])
             self._each(keep)
-        if self._ordered():  # the history was written on the rank's stream
-            with self.st.stream(self.ranks[0]):
-                h = self.ex.gather(hist)
-        else:
-            self._sync_all()
-            h = self.ex.gather(hist)  # rank order: deterministic sums for a given P
+        h = self._gather(hist)  # rank order: deterministic sums for a given P
+        # solvers.cpp:408 require_finite(x, "admm_tv"), plus the residue check of
+        # the last inverse (fft.cpp:89-93), as the single-GPU path does
+        self._check_status(self.s_res, "admm_tv")
         for it in range(k):
             fit = sum(float(v[3 * it]) for v in h)
             res2 = sum(float(v[3 * it + 1]) for v in h)
             tv = sum(float(v[3 * it + 2]) for v in h)
             self.objective.append(0.5 * fit + self.lam_tv * tv)
             self.primal_residual.append(math.sqrt(res2))
+
+    def close(self):
+        """Frees the rank's cached fold tables (vsr_slab_tv_prepare_d)."""
+        lam, self.lam = getattr(self, "lam", None), None
+        if lam:
+            for r in self.ranks:
+                self.st.tv_release(r, lam[r])
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
     def forward3_theta(self):
         g = self.g

@@ -729,6 +729,7 @@ _sig("vsr_slab_axis3_d", [_vp, _szp, _szp, C.c_int, _vp, C.c_int, C.c_double])
 _sig("vsr_slab_lr_slice_d", [_vp, _szp, _szp, C.c_int, C.c_int, _vp, _vp])
 _sig("vsr_slab_tik_fold_d", [_vp, _szp, _szp, C.c_int, _vp, _vp, _vp, C.c_double, _vp])
 _sig("vsr_slab_tv_prepare_d", [_vp, _szp, _szp, C.c_int, C.c_int, _vp])
+_sig("vsr_slab_tv_release_d", [_vp, _vp])
 _sig("vsr_slab_tv_fold_d", [_vp, _szp, _szp, C.c_int, C.c_int, _vp, _vp, _vp, C.c_double, C.c_double,
                             C.c_double, _vp])
 _sig("vsr_slab_unpack_inv_xy_d", [_vp, _szp, _szp, C.c_int, _vp, _vp, _vp, C.c_double, _vp, _vp])
