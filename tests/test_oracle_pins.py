@@ -413,3 +413,32 @@ def test_admm_l2l2_fixed_point(O):
     x1, rep = O.admm_l2l2(y, lam, spec, 0.05, xbar, 1, mu=0.3, rel_tol=0.0, warm_start=(xs, v, dual))
     assert rep.iterations == 1
     assert rel_err(x1, xs) < 1e-10
+
+
+# ------------------------------------------------------------------ lean oracle
+# oracle/lean_oracle.py (the config-4 checker, memory-lean) pinned to the
+# line-by-line oracle and to the reference binary (oracle/_ref) where built.
+@pytest.mark.parametrize("dims,rates", [((32, 32, 32), (2, 2, 2)), ((32, 16, 24), (2, 2, 4)),
+                                        ((16, 16, 16), (4, 4, 4)), ((20, 12, 6), (5, 3, 2))])
+def test_lean_oracle_pinned(O, dims, rates):
+    import lean_oracle as LO
+    import ref_binding as R
+    rng = np.random.default_rng(77)
+    spec = O.DecimationSpec(dims, rates)
+    psf = O.make_gaussian_psf((5, 5, 3), (1.2, 1.0, 0.8), dims)
+    y = random_volume(spec.lr, rng, 0.0, 1.0)
+    xbar = O.zero_fill_upsample(y, spec)
+    want = O.tikhonov_fast(y, O.psf_to_spectrum(psf), spec, 1e-3, xbar)
+    assert rel_err(LO.tikhonov_fast(y, psf, spec, 1e-3, xbar), want) < 1e-13
+    for init in (O.INIT_ZERO, O.INIT_UPSAMPLED):
+        xa, ra = O.admm_tv(y, psf, spec, lam_tv=2e-3, mu=0.05, max_iters=3, rel_tol=0.0, tau=5e-5, init=init)
+        xb, rb = LO.admm_tv(y, psf, spec, 2e-3, 0.05, 3, tau=5e-5, init=init)
+        assert rel_err(xb, xa) < 1e-10
+        assert abs(rb.initial_objective - ra.initial_objective) <= 1e-13 * abs(ra.initial_objective)
+        np.testing.assert_allclose(rb.objective, ra.objective, rtol=1e-13)
+        np.testing.assert_allclose(rb.primal_residual, ra.primal_residual, rtol=1e-13)
+        if R.available():
+            xr, rr = R.admm_tv(y, psf, dims, rates, 2e-3, 0.05, 3, 0.0, tau=5e-5, init=init)
+            assert rel_err(xb, xr) < 1e-10
+            np.testing.assert_allclose(rb.objective, rr["objective"], rtol=1e-12)
+            np.testing.assert_allclose(rb.primal_residual, rr["primal_residual"], rtol=1e-12)
