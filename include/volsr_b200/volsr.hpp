@@ -89,6 +89,8 @@ public:
     std::size_t size() const { return data_.size(); }
     value_type operator[](std::size_t p) const { return data_[p]; }
     value_type& operator[](std::size_t p) { return data_[p]; }
+    value_type at(std::size_t i, std::size_t j, std::size_t k) const { return data_[lex_index(i, j, k, dims_)]; }
+    value_type& at(std::size_t i, std::size_t j, std::size_t k) { return data_[lex_index(i, j, k, dims_)]; }
     const std::vector<value_type>& data() const { return data_; }
     std::vector<value_type>& data() { return data_; }
 
@@ -99,6 +101,37 @@ private:
 
 inline void require_same_dims(const Dims3& a, const Dims3& b, const char* where) {
     if (!(a == b)) throw shape_error(std::string(where) + ": dims mismatch, " + to_string(a) + " vs " + to_string(b));
+}
+
+// volume.hpp:106-116: value-type helpers on host containers (caller-side
+// checks and norms of returned volumes; the solvers never route through them)
+inline void require_finite(const Volume3D& v, const char* where) {
+    for (std::size_t p = 0; p < v.size(); ++p)
+        if (!std::isfinite(v[p]))
+            throw numeric_error(std::string(where) + ": non-finite value at flat index " + std::to_string(p));
+}
+inline double dot(const Volume3D& a, const Volume3D& b) {
+    require_same_dims(a.dims(), b.dims(), "dot");
+    double acc = 0.0;
+    for (std::size_t p = 0; p < a.size(); ++p) acc += a[p] * b[p];
+    return acc;
+}
+inline double norm2(const Volume3D& a) { return std::sqrt(dot(a, a)); }
+inline std::complex<double> dot(const ComplexVolume3D& a, const ComplexVolume3D& b) {  // conj(a) . b
+    require_same_dims(a.dims(), b.dims(), "dot");
+    std::complex<double> acc = 0.0;
+    for (std::size_t p = 0; p < a.size(); ++p) acc += std::conj(a[p]) * b[p];
+    return acc;
+}
+inline double norm2(const ComplexVolume3D& a) {
+    double acc = 0.0;
+    for (std::size_t p = 0; p < a.size(); ++p) acc += std::norm(a[p]);
+    return std::sqrt(acc);
+}
+inline ComplexVolume3D to_complex(const Volume3D& v) {
+    ComplexVolume3D out(v.dims());
+    for (std::size_t p = 0; p < v.size(); ++p) out[p] = v[p];
+    return out;
 }
 
 // ------------------------------------------------------------- C ABI plumbing
@@ -348,6 +381,13 @@ inline Volume3D decimate_adjoint(const Volume3D& y, const DecimationSpec& spec) 
                                        x.data().data()));
     return x;
 }
+inline Volume3D nn_upsample(const Volume3D& y, const DecimationSpec& spec) {
+    require_same_dims(y.dims(), spec.lr(), "nn_upsample");
+    Volume3D x(spec.hr());
+    detail::check(vsr_nn_upsample(detail::ctx(), detail::D3(spec.hr()).v, spec.rates_ptr(), y.data().data(),
+                                  x.data().data()));
+    return x;
+}
 inline Volume3D zero_fill_upsample(const Volume3D& y, const DecimationSpec& spec) {
     Volume3D x = decimate_adjoint(y, spec);
     const double d = static_cast<double>(spec.rate());
@@ -367,6 +407,35 @@ inline Volume3D diff_adjoint(const Volume3D& x, Axis a) {
     return out;
 }
 
+// operators.hpp:79-87
+struct DiffSpectra {
+    SpectrumDiag rows, cols, slices;
+    const SpectrumDiag& along(Axis a) const { return a == Axis::Rows ? rows : (a == Axis::Cols ? cols : slices); }
+};
+inline DiffSpectra finite_diff_spectra(const Dims3& hr) {
+    DiffSpectra d{SpectrumDiag{ComplexVolume3D(hr)}, SpectrumDiag{ComplexVolume3D(hr)},
+                  SpectrumDiag{ComplexVolume3D(hr)}};
+    detail::check(vsr_finite_diff_spectra(detail::ctx(), detail::D3(hr).v, detail::cp(d.rows.values),
+                                          detail::cp(d.cols.values), detail::cp(d.slices.values)));
+    return d;
+}
+
+// ------------------------------------------------------------- spectral.hpp:12-19
+inline ComplexVolume3D alias_fold(const ComplexVolume3D& hr, const DecimationSpec& spec) {
+    require_same_dims(hr.dims(), spec.hr(), "alias_fold");
+    ComplexVolume3D out(spec.lr());
+    detail::check(vsr_alias_fold(detail::ctx(), detail::D3(spec.hr()).v, spec.rates_ptr(), detail::cp(hr),
+                                 detail::cp(out)));
+    return out;
+}
+inline ComplexVolume3D alias_expand(const ComplexVolume3D& lr, const DecimationSpec& spec) {
+    require_same_dims(lr.dims(), spec.lr(), "alias_expand");
+    ComplexVolume3D out(spec.hr());
+    detail::check(vsr_alias_expand(detail::ctx(), detail::D3(spec.hr()).v, spec.rates_ptr(), detail::cp(lr),
+                                   detail::cp(out)));
+    return out;
+}
+
 // ------------------------------------------------------------- spectral.hpp:21-68
 class FoldedSpectrum {
 public:
@@ -375,9 +444,27 @@ public:
         detail::check(vsr_folded_create(detail::ctx(), detail::D3(spec.hr()).v, spec.rates_ptr(),
                                         detail::cp(lambda.values), &h_));
     }
-    FoldedSpectrum(const FoldedSpectrum&) = delete;
-    FoldedSpectrum& operator=(const FoldedSpectrum&) = delete;
-    ~FoldedSpectrum() { vsr_folded_destroy(h_); }
+    // a value type, as in the reference: copies own an independent device copy of Lambda
+    FoldedSpectrum(const FoldedSpectrum& o) : spec_(o.spec_) { detail::check(vsr_folded_clone(o.h_, &h_)); }
+    FoldedSpectrum(FoldedSpectrum&& o) noexcept : spec_(o.spec_), h_(o.h_) { o.h_ = nullptr; }
+    FoldedSpectrum& operator=(const FoldedSpectrum& o) {
+        if (this != &o) {
+            vsr_folded* h = nullptr;
+            detail::check(vsr_folded_clone(o.h_, &h));
+            vsr_folded_destroy(h_);
+            h_ = h;
+            spec_ = o.spec_;
+        }
+        return *this;
+    }
+    FoldedSpectrum& operator=(FoldedSpectrum&& o) noexcept {
+        std::swap(h_, o.h_);
+        spec_ = o.spec_;
+        return *this;
+    }
+    ~FoldedSpectrum() {
+        if (h_) vsr_folded_destroy(h_);
+    }
     const DecimationSpec& spec() const { return spec_; }
     std::complex<double> block_value(std::size_t br, std::size_t bc, std::size_t bs, std::size_t g) const {
         double v[2];
@@ -396,6 +483,20 @@ public:
         detail::check(vsr_folded_apply_adjoint(h_, detail::cp(lr), detail::cp(out)));
         return out;
     }
+    ComplexVolume3D apply_weighted(const ComplexVolume3D& hr, const Volume3D& w) const {
+        require_same_dims(hr.dims(), spec_.hr(), "FoldedSpectrum::apply_weighted");
+        require_same_dims(w.dims(), spec_.hr(), "FoldedSpectrum::apply_weighted: weights");
+        ComplexVolume3D out(spec_.lr());
+        detail::check(vsr_folded_apply_weighted(h_, detail::cp(hr), w.data().data(), detail::cp(out)));
+        return out;
+    }
+    ComplexVolume3D apply_adjoint_weighted(const ComplexVolume3D& lr, const Volume3D& w) const {
+        require_same_dims(lr.dims(), spec_.lr(), "FoldedSpectrum::apply_adjoint_weighted");
+        require_same_dims(w.dims(), spec_.hr(), "FoldedSpectrum::apply_adjoint_weighted: weights");
+        ComplexVolume3D out(spec_.hr());
+        detail::check(vsr_folded_apply_adjoint_weighted(h_, detail::cp(lr), w.data().data(), detail::cp(out)));
+        return out;
+    }
     void swap_blocks_for_fault_injection() { detail::check(vsr_folded_swap_blocks_for_fault_injection(h_)); }
     vsr_folded* handle() const { return h_; }
 
@@ -404,9 +505,19 @@ private:
     vsr_folded* h_ = nullptr;
 };
 
+inline FoldedSpectrum fold_lambda(const SpectrumDiag& lambda, const DecimationSpec& spec) {  // spectral.hpp:54
+    return FoldedSpectrum(lambda, spec);
+}
+
 inline Volume3D gram_diag(const FoldedSpectrum& f) {
     Volume3D out(f.spec().lr());
     detail::check(vsr_folded_gram_diag(f.handle(), out.data().data()));
+    return out;
+}
+inline Volume3D gram_diag_weighted(const FoldedSpectrum& f, const Volume3D& w) {
+    require_same_dims(w.dims(), f.spec().hr(), "gram_diag_weighted");
+    Volume3D out(f.spec().lr());
+    detail::check(vsr_folded_gram_diag_weighted(f.handle(), w.data().data(), out.data().data()));
     return out;
 }
 
@@ -511,9 +622,15 @@ struct TvAdmmConfig {
     Volume3D init_volume;
 };
 
-inline Volume3D make_gamma(const Dims3& hr, double tau) {
+// solvers.hpp:117 make_gamma(const DiffSpectra&, double)
+inline Volume3D make_gamma(const DiffSpectra& diffs, double tau) {
+    const Dims3& hr = diffs.rows.dims();
+    require_same_dims(diffs.cols.dims(), hr, "make_gamma");
+    require_same_dims(diffs.slices.dims(), hr, "make_gamma");
     Volume3D g(hr);
-    detail::check(vsr_make_gamma(detail::ctx(), detail::D3(hr).v, tau, g.data().data()));
+    detail::check(vsr_make_gamma_spectra(detail::ctx(), detail::D3(hr).v, detail::cp(diffs.rows.values),
+                                         detail::cp(diffs.cols.values), detail::cp(diffs.slices.values), tau,
+                                         g.data().data()));
     return g;
 }
 

@@ -108,6 +108,12 @@ int vsr_decimate(vsr_ctx* ctx, const size_t hr_dims[3], const size_t rates[3], c
                  double* y);                                      /* operators.cpp:133-142 */
 int vsr_decimate_adjoint(vsr_ctx* ctx, const size_t hr_dims[3], const size_t rates[3],
                          const double* y, double* x);             /* operators.cpp:144-153 */
+int vsr_nn_upsample(vsr_ctx* ctx, const size_t hr_dims[3], const size_t rates[3], const double* y,
+                    double* x);                                   /* operators.cpp:155-164 */
+/* DiffSpectra finite_diff_spectra(hr) (operators.hpp:79-87, operators.cpp:225-243):
+ * three complex HR volumes (rows, cols, slices), exactly 0 at DC */
+int vsr_finite_diff_spectra(vsr_ctx* ctx, const size_t hr_dims[3], double* rows_c, double* cols_c,
+                            double* slices_c);
 int vsr_diff_forward(vsr_ctx* ctx, const size_t dims[3], int axis, const double* x,
                      double* out);                                /* operators.cpp:191-206 */
 int vsr_diff_adjoint(vsr_ctx* ctx, const size_t dims[3], int axis, const double* x,
@@ -124,6 +130,8 @@ int vsr_alias_expand(vsr_ctx* ctx, const size_t hr_dims[3], const size_t rates[3
 int vsr_folded_create(vsr_ctx* ctx, const size_t hr_dims[3], const size_t rates[3],
                       const double* lambda_c, vsr_folded** out);
 int vsr_folded_destroy(vsr_folded* f);
+/* independent copy of a FoldedSpectrum (the reference type is copyable) */
+int vsr_folded_clone(const vsr_folded* src, vsr_folded** out);
 int vsr_folded_block_value(vsr_folded* f, size_t br, size_t bc, size_t bs, size_t g,
                            double out_c[2]);
 int vsr_folded_apply(vsr_folded* f, const double* hr_c, double* lr_c);
@@ -164,6 +172,10 @@ double vsr_tikhonov_algorithmic_bytes(const size_t hr_dims[3], const size_t rate
  *      tv_x_update (:89-91, :245-259), tv_shrink (:100-101, :286-301),
  *      objective_tv (:111-112, :303-319). */
 int vsr_make_gamma(vsr_ctx* ctx, const size_t hr_dims[3], double tau, double* gamma_r);
+/* make_gamma(const DiffSpectra&, tau) (solvers.hpp:117) from explicit spectra;
+ * VSR_ERR_NUMERIC with the reference text when a denominator is not positive */
+int vsr_make_gamma_spectra(vsr_ctx* ctx, const size_t hr_dims[3], const double* rows_c, const double* cols_c,
+                           const double* slices_c, double tau, double* gamma_r);
 int vsr_tv_x_update(vsr_ctx* ctx, const size_t hr_dims[3], const size_t rates[3],
                     const double* y_r, const double* lambda_c, double mu,
                     const double* theta_hat_c, const double* gamma_r, double* x_r);

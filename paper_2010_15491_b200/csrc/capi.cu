@@ -290,6 +290,49 @@ __global__ void add_noise_kernel(double* __restrict__ y, const double* __restric
     }
 }
 
+// nn_upsample (operators.cpp:155-164): x[i,j,k] = y[i/dr, j/dc, k/ds]
+__global__ void nn_upsample_kernel(long long m, long long n, long long N, int dr, int dc, int ds, long long ml,
+                                   long long nl, const double* __restrict__ y, double* __restrict__ x) {
+    const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= N) return;
+    const long long i = p % m, j = (p / m) % n, k = p / (m * n);
+    x[p] = y[(i / dr) + ml * ((j / dc) + nl * (k / ds))];
+}
+
+// finite_diff_spectra (operators.cpp:225-243): (cos(2 pi f/len) - 1, sin(2 pi f/len)),
+// exactly 0 at f = 0, per axis over the whole HR grid
+__global__ void diff_spectra_kernel(long long m, long long n, long long N, long long s, double2* __restrict__ rows,
+                                    double2* __restrict__ cols, double2* __restrict__ slices) {
+    const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= N) return;
+    const long long f[3] = {p % m, (p / m) % n, p / (m * n)};
+    const long long len[3] = {m, n, s};
+    double2* out[3] = {rows, cols, slices};
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        double2 v = make_double2(0.0, 0.0);
+        if (f[a] != 0) {
+            const double ang = 6.283185307179586 * (double)f[a] / (double)len[a];  // 2 * std::numbers::pi
+            v = make_double2(cos(ang) - 1.0, sin(ang));
+        }
+        out[a][p] = v;
+    }
+}
+
+// make_gamma (solvers.cpp:191-205) from three given difference spectra:
+// gamma = 1 / (|r|^2 + |c|^2 + |s|^2 + tau); the first non-positive
+// denominator's index goes to *bad (atomicMin)
+__global__ void gamma_spectra_kernel(long long N, const double2* __restrict__ r, const double2* __restrict__ c,
+                                     const double2* __restrict__ s, double tau, double* __restrict__ g,
+                                     unsigned long long* __restrict__ bad) {
+    const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= N) return;
+    const double2 a = r[p], b = c[p], e = s[p];
+    const double den = (((a.x * a.x + a.y * a.y) + (b.x * b.x + b.y * b.y)) + (e.x * e.x + e.y * e.y)) + tau;
+    if (!(den > 0.0)) atomicMin(bad, (unsigned long long)p);
+    g[p] = 1.0 / den;
+}
+
 __global__ void scale_kernel(double* v, double s) { *v *= s; }
 __global__ void cmul_kernel(long long n, double2* __restrict__ a, const double2* __restrict__ b,
                             bool conj_b) {
@@ -626,6 +669,76 @@ int vsr_decimate_adjoint(vsr_ctx* ctx, const size_t hr_dims[3], const size_t rat
     });
 }
 
+int vsr_nn_upsample(vsr_ctx* ctx, const size_t hr_dims[3], const size_t rates[3], const double* y, double* x) {
+    return guarded([&] {
+        require_ctx(ctx);
+        const Spec sp = make_spec(hr_dims, rates);
+        vsr_ctx::Guard g(ctx->device);
+        DevBuf<double> dx(sp.hr.count()), dy(sp.lr.count());
+        h2d(ctx, dy.p, y, dy.bytes());
+        const long long N = (long long)sp.hr.count();
+        if (N) {
+            nn_upsample_kernel<<<(unsigned)((N + 255) / 256), 256, 0, ctx->stream>>>(
+                (long long)sp.hr.m, (long long)sp.hr.n, N, sp.rates[0], sp.rates[1], sp.rates[2],
+                (long long)sp.lr.m, (long long)sp.lr.n, dy.p, dx.p);
+            VSR_LAUNCH_CHECK();
+        }
+        d2h(ctx, x, dx.p, dx.bytes());
+        sync(ctx);
+    });
+}
+
+int vsr_finite_diff_spectra(vsr_ctx* ctx, const size_t hr_dims[3], double* rows_c, double* cols_c,
+                            double* slices_c) {
+    return guarded([&] {
+        require_ctx(ctx);
+        const Dims d = to_dims(hr_dims);
+        vsr_ctx::Guard g(ctx->device);
+        const long long N = (long long)d.count();
+        DevBuf<double2> r(d.count()), c(d.count()), z(d.count());
+        if (N) {
+            diff_spectra_kernel<<<(unsigned)((N + 255) / 256), 256, 0, ctx->stream>>>(
+                (long long)d.m, (long long)d.n, N, (long long)d.s, r.p, c.p, z.p);
+            VSR_LAUNCH_CHECK();
+        }
+        d2h(ctx, rows_c, r.p, r.bytes());
+        d2h(ctx, cols_c, c.p, c.bytes());
+        d2h(ctx, slices_c, z.p, z.bytes());
+        sync(ctx);
+    });
+}
+
+int vsr_make_gamma_spectra(vsr_ctx* ctx, const size_t hr_dims[3], const double* rows_c, const double* cols_c,
+                           const double* slices_c, double tau, double* gamma_r) {
+    return guarded([&] {
+        require_ctx(ctx);
+        if (tau < 0.0) throw std::invalid_argument("make_gamma: tau must be nonnegative");  // solvers.cpp:192
+        const Dims d = to_dims(hr_dims);
+        vsr_ctx::Guard g(ctx->device);
+        const long long N = (long long)d.count();
+        DevBuf<double2> r(d.count()), c(d.count()), z(d.count());
+        DevBuf<double> out(d.count());
+        h2d(ctx, r.p, rows_c, r.bytes());
+        h2d(ctx, c.p, cols_c, c.bytes());
+        h2d(ctx, z.p, slices_c, z.bytes());
+        VSR_CUDA(cudaMemsetAsync(ctx->bad.p, 0xff, sizeof(unsigned long long), ctx->stream));
+        if (N) {
+            gamma_spectra_kernel<<<(unsigned)((N + 255) / 256), 256, 0, ctx->stream>>>(N, r.p, c.p, z.p, tau, out.p,
+                                                                                      ctx->bad.p);
+            VSR_LAUNCH_CHECK();
+        }
+        unsigned long long bad = 0;
+        d2h(ctx, &bad, ctx->bad.p, sizeof(bad));
+        sync(ctx);
+        if (bad != ULLONG_MAX)
+            throw numeric_error(
+                "make_gamma: difference-operator gram is singular at the zero frequency (DC); "
+                "a positive tau floor is required");
+        d2h(ctx, gamma_r, out.p, out.bytes());
+        sync(ctx);
+    });
+}
+
 static int diff_host(vsr_ctx* ctx, const size_t dims[3], int axis, const double* x, double* out,
                      bool adjoint) {
     return guarded([&] {
@@ -821,6 +934,22 @@ int vsr_folded_create(vsr_ctx* ctx, const size_t hr_dims[3], const size_t rates[
         f->lam.alloc(sp.hr.count());
         h2d(ctx, f->lam.p, lambda_c, f->lam.bytes());
         sync(ctx);
+        *out = f;
+    });
+}
+
+// an independent copy (FoldedSpectrum is a value type in the reference)
+int vsr_folded_clone(const vsr_folded* src, vsr_folded** out) {
+    return guarded([&] {
+        if (!src || !out) throw std::invalid_argument("vsr_folded_clone: null handle");
+        vsr_ctx::Guard g(src->ctx->device);
+        auto* f = new vsr_folded();
+        f->ctx = src->ctx;
+        f->sp = src->sp;
+        f->G = src->G;
+        f->lam.alloc(src->sp.hr.count());
+        VSR_CUDA(cudaMemcpyAsync(f->lam.p, src->lam.p, f->lam.bytes(), cudaMemcpyDeviceToDevice, src->ctx->stream));
+        sync(src->ctx);
         *out = f;
     });
 }

@@ -159,7 +159,7 @@ int main() {
         CHECK(throws<std::invalid_argument>([&] { tv_shrink(one(1.0), one(0.0), one(0.0), -0.5); }));
     }
     {  // test_solvers.cpp:369-384 DC-singular gamma
-        CHECK(throws<numeric_error>([&] { make_gamma(Dims3{4, 4, 4}, 0.0); }));
+        CHECK(throws<numeric_error>([&] { make_gamma(finite_diff_spectra(Dims3{4, 4, 4}), 0.0); }));
     }
     {  // test_solvers.cpp:386-401 near-identity ADMM-TV
         std::mt19937_64 rng(12);
