@@ -133,7 +133,9 @@ def cpu_baseline(cfg, inp, budget_s: float = 25.0):
             op.solve(inp.y)
             times.append(time.perf_counter() - t0)
         kind, sample = "reference", (f"reference volsr TikhonovOperator::solve (oracle/_ref, FFTW3-API shim), "
-                                     f"config1 256^3, {len(times)} solves, best")
+                                     f"config1 256^3, {len(times)} solves, best; the shim's FFT is a radix-2 "
+                                     f"row-column transform, slower than real FFTW, so this overstates the "
+                                     f"reference's CPU time (the survey estimates ~3 s per solve with FFTW)")
     else:
         import volsr_oracle as O
         spec = O.DecimationSpec(cfg.hr, cfg.rates)
@@ -168,7 +170,8 @@ def run_reference(args, rank, world):
     if ref is not None:
         op = ref.TikhonovOperator(inp.psf, cfg.hr, cfg.rates, cfg.reg, inp.xbar)
         kind = "reference"
-        sample = "reference volsr TikhonovOperator::solve (oracle/_ref, FFTW3-API shim), config1, 1 thread"
+        sample = ("reference volsr TikhonovOperator::solve (oracle/_ref, FFTW3-API shim), config1, 1 thread; "
+                  "the shim's radix-2 FFT is slower than real FFTW (overstates the reference CPU time)")
     else:
         import volsr_oracle as O
         spec = O.DecimationSpec(cfg.hr, cfg.rates)
@@ -214,8 +217,6 @@ STAGE_BYTES = {
     # TV on the Hermitian half spectrum along axis 3 (planes 0..s/2)
     "fft_fwd_axis3_r2c_half": (16, 0), "fft_fwd_axis2_half": (16, 0), "tv_fft1_fold_ifft1_half": (32, 16),
     "fft_inv_axis2_half": (16, 0), "fft_inv_axis3_c2r_half": (16, 0),
-    # chained in-plane passes: one HBM read of the input, one write of the output
-    "chain_inv_axis2_axis1_c2r": (24, 0), "chain_fwd_axis1_r2c_axis2": (24, 0),
     # spatial-expansion Tikhonov: LR transforms (r2c 24 + 2 x 32), LR pointwise
     # U (Yl, Zl in, U out), expansion (x out, u and decimate(xbar) in)
     "lr_fft3": (0, 88), "lr_ifft3": (0, 88), "spatial_u": (0, 48), "spatial_expand": (8, 16),
@@ -380,9 +381,16 @@ def run_b200(args, rank, world, local):
     try:
         prof = json.loads((ROOT / "profiles" / "traffic.json").read_text())
         if dom in prof:
-            roofline["traffic"] = prof[dom]
+            roofline["traffic"] = prof[dom]["bytes"] if isinstance(prof[dom], dict) else prof[dom]
+            roofline["traffic_source"] = (prof.get("_source") or "committed ncu capture") + \
+                " -- dram__bytes_read.sum + dram__bytes_write.sum of this kernel from the capture, not this run"
     except Exception:
         pass
+    # the spatial path's own compulsory bytes: read y, write x
+    comp = 8 * N + 8 * Nl
+    roofline["path_compulsory"] = {"bytes": comp, "achieved": comp / (ms * 1e-3) / 1e9,
+                                   "frac": comp / (ms * 1e-3) / 1e9 / hbm,
+                                   "model": "(8 N + 8 N/d) bytes per solve: y in, x out"}
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
@@ -393,8 +401,13 @@ def run_b200(args, rank, world, local):
             "timing": "per-solve CUDA events on the library stream, L2 flushed between solves; headline pass "
                       "runs the user path (CUDA-graph replay), stage table from a second profiled pass"}
 
+    line["config0"] = bench_tik_config(args, ctx, V, synth, torch, stream, local, hbm, 0)
     if not args.no_tv:
-        line["tv"] = bench_tv(args, ctx, V, synth, torch, stream, local, hbm)
+        line["tv"] = bench_tv(args, ctx, V, synth, torch, stream, local, hbm, 2)
+        line["config3"] = bench_tv(args, ctx, V, synth, torch, stream, local, hbm, 3)
+        if rank == 0 and world == 1 and not args.no_cpu:
+            line["tv"]["cpu_baseline"] = cpu_baseline_tv(synth.CONFIGS[2], synth.make_inputs(synth.CONFIGS[2],
+                                                                                          with_truth=False))
     if not args.no_fft_path:
         line["fft3_vs_cufft"] = bench_fft_compare(args, ctx, V, torch, stream, local, hbm)
     if world > 1 or args.sharded:
@@ -587,9 +600,10 @@ def bench_config4(args, ctx, V, synth, torch, stream, local, hbm):
     return out
 
 
-def bench_tv(args, ctx, V, synth, torch, stream, local, hbm):
-    """ADMM-TV iteration throughput on configs[2] (256^3, d = 64)."""
-    cfg = synth.CONFIGS[2]
+def bench_tv(args, ctx, V, synth, torch, stream, local, hbm, idx=2):
+    """ADMM-TV iteration throughput on configs[2] (256^3, d = 64) or configs[3]
+    (512x512x256, d = (2,2,4)) through the single-GPU path."""
+    cfg = synth.CONFIGS[idx]
     inp = synth.make_inputs(cfg, with_truth=False)
     N = cfg.voxels
     spec = V.DecimationSpec(cfg.hr, cfg.rates)
@@ -597,12 +611,14 @@ def bench_tv(args, ctx, V, synth, torch, stream, local, hbm):
     y_d.upload(inp.y)
     p_d = V.DeviceBuffer(ctx, inp.psf.nbytes)
     p_d.upload(inp.psf)
-    x0_d = V.DeviceBuffer(ctx, inp.x0.nbytes)
-    x0_d.upload(inp.x0)
+    x0_d = None
+    if inp.x0 is not None:
+        x0_d = V.DeviceBuffer(ctx, inp.x0.nbytes)
+        x0_d.upload(inp.x0)
     k = max(args.steps, 10)
     iters = 2 * k + max(args.warmup, 3)
     tcfg = V.TvAdmmConfig(lambda_=cfg.tv_lambda, mu=cfg.tv_mu, max_iters=iters, rel_tol=0.0,
-                          tau=1e-3 * cfg.tv_mu, init=V.INIT_PROVIDED)
+                          tau=1e-3 * cfg.tv_mu, init=V.INIT_PROVIDED if x0_d is not None else V.INIT_UPSAMPLED)
     tv = V.TvDevice(ctx, spec, y_d, p_d, tcfg, x0_d)
     tv.iterate(max(args.warmup, 3))
     ctx.synchronize()
@@ -638,11 +654,73 @@ def bench_tv(args, ctx, V, synth, torch, stream, local, hbm):
             r["gbs"] = byts / (avg * 1e-3) / 1e9
             r["frac"] = r["gbs"] / hbm
         rows[name] = r
-    return {"workload": "config2: ADMM-TV fp64 256^3 -> 64^3 (d=64), lambda 2e-3, mu 0.05, tau 1e-3*mu",
+    hr, lr = cfg.hr, cfg.lr
+    return {"workload": f"config{idx}: ADMM-TV fp64 {hr[0]}x{hr[1]}x{hr[2]} -> {lr[0]}x{lr[1]}x{lr[2]} "
+                        f"(d={cfg.d}), lambda {cfg.tv_lambda:g}, mu {cfg.tv_mu:g}, tau 1e-3*mu, single GPU",
             "value": N / (ms * 1e-3), "unit": "HR voxels/s per ADMM-TV iteration", "ms_per_iter": ms,
             "iters_timed": k, "path_frac": path / (ms * 1e-3) / 1e9 / hbm, "lambda_separable": tv_sep,
             "path_model": "(160 + 16/d) N bytes per iteration", "objective_last": rep.objective[-1],
             "stages": rows, "stages_ms_per_iter": ms_prof}
+
+
+def bench_tik_config(args, ctx, V, synth, torch, stream, local, hbm, idx=0):
+    """configs[0] (64^3 -> 32^3, d = 8): the same device Tikhonov solve at the
+    reference's CPU-runnable size.  L2-resident and launch-bound (SURVEY
+    8(d)): reported, but its roofline fraction is not meaningful."""
+    cfg = synth.CONFIGS[idx]
+    inp = synth.make_inputs(cfg, with_truth=False)
+    spec = V.DecimationSpec(cfg.hr, cfg.rates)
+    lam = V.psf_to_spectrum(inp.psf, ctx)
+    lam_d = V.DeviceBuffer(ctx, lam.nbytes)
+    lam_d.upload(lam)
+    xbar_d = V.DeviceBuffer(ctx, inp.xbar.nbytes)
+    xbar_d.upload(inp.xbar)
+    y_d = V.DeviceBuffer(ctx, inp.y.nbytes)
+    y_d.upload(inp.y)
+    x_d = V.DeviceBuffer(ctx, cfg.voxels * 8)
+    op = V.TikhonovDevice(ctx, spec, lam_d, cfg.reg, xbar_d)
+    for _ in range(max(args.warmup, 3)):
+        op.solve_d(y_d, x_d)
+    op.check()
+    ctx.synchronize()
+    k = max(args.steps, 20)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(k):
+        op.solve_d(y_d, x_d)
+    e1.record(stream)
+    e1.synchronize()
+    op.check()
+    ms = e0.elapsed_time(e1) / k
+    path = {"spatial": op.spatial(), "separable": op.separable(), "lattice_prior": op.lattice_prior()}
+    op.close()
+    return {"workload": f"config{idx}: closed-form Tikhonov SR fp64 64^3 -> 32^3 (d=8), back-to-back solves "
+                        "(graph replay; inputs L2-resident: launch-bound)",
+            "value": cfg.voxels / (ms * 1e-3), "unit": UNIT, "ms_per_solve": ms, "solves_timed": k,
+            "path": path}
+
+
+def cpu_baseline_tv(cfg, inp, iters=2):
+    """The reference admm_tv (oracle/_ref, one thread) on configs[2] at
+    rel_tol = 0: report.seconds / iterations (solvers.cpp:409), which includes
+    its precompute and the 2 objective FFTs per iteration; bounded to `iters`
+    iterations."""
+    sys.path.insert(0, str(ROOT / "oracle"))
+    try:
+        import ref_binding
+        if not ref_binding.available():
+            return None
+    except Exception:
+        return None
+    os.environ["VSR_SHIM_THREADS"] = "1"
+    x, rep = ref_binding.admm_tv(inp.y, inp.psf, cfg.hr, cfg.rates, cfg.tv_lambda, cfg.tv_mu, iters, 0.0,
+                                 tau=1e-3 * cfg.tv_mu, init=2 if inp.x0 is not None else 1, init_volume=inp.x0)
+    per = rep["seconds"] / rep["iterations"]
+    return {"value": cfg.voxels / per, "unit": "HR voxels/s per ADMM-TV iteration", "cores": 1, "kind": "reference",
+            "seconds_per_iteration": per,
+            "sample": f"reference volsr admm_tv (oracle/_ref) config{cfg.idx}, {rep['iterations']} iterations at "
+                      "rel_tol 0, report.seconds / iterations (includes its precompute); FFTW3-API shim = radix-2 "
+                      "row-column FFT, slower than real FFTW, so this overstates the reference's CPU time"}
 
 
 def bench_sharded(args, ctx, V, synth, torch, rank, world, local):
