@@ -13,7 +13,8 @@ One step = one TikhonovOperator::solve (reference src/solvers.cpp:48-67).
 
 Run: python bench.py [--gpus N --steps K --warmup W] [--impl reference]
 For N > 1 (torchrun) every rank solves its own config-1 volume (replicas,
-weak scaling); the slab-sharded path is not part of this line.
+weak scaling) for the headline; the `sharded` / `sharded_config4` blocks time
+configs 3 and 4 slab-sharded over all N GPUs (strong scaling).
 """
 from __future__ import annotations
 
@@ -410,13 +411,15 @@ def run_b200(args, rank, world, local):
                                                                                           with_truth=False))
     if not args.no_fft_path:
         line["fft3_vs_cufft"] = bench_fft_compare(args, ctx, V, torch, stream, local, hbm)
-    if world > 1 or args.sharded:
-        line["sharded"] = bench_sharded(args, ctx, V, synth, torch, rank, world, local)
+    if not args.no_sharded:
+        line["sharded"] = bench_sharded(args, ctx, V, synth, torch, rank, world, local, 3)
     if rank == 0 and world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(cfg, inp)
     op.close()
     if world == 1 and not args.no_config4:
         line["config4"] = bench_config4(args, ctx, V, synth, torch, stream, local, hbm)
+    if not args.no_sharded and not args.no_config4:
+        line["sharded_config4"] = bench_sharded(args, ctx, V, synth, torch, rank, world, local, 4, iters=3)
     if rank == 0:
         print(json.dumps(line), flush=True)
     return 0
@@ -723,72 +726,72 @@ def cpu_baseline_tv(cfg, inp, iters=2):
                       "row-column FFT, slower than real FFTW, so this overstates the reference's CPU time"}
 
 
-def bench_sharded(args, ctx, V, synth, torch, rank, world, local):
-    """configs[3] ADMM-TV (512x512x256, d = (2,2,4)) slab-decomposed over all
-    ranks: NCCL all-to-all transposes + ring halos (paper_2010_15491_b200/dist.py).
-    Seeded random data of the config's shapes (values do not change the work)."""
+def bench_sharded(args, ctx, V, synth, torch, rank, world, local, idx=3, iters=None):
+    """configs[3] (512x512x256, d = (2,2,4)) or configs[4] (1024^3, d = 8)
+    ADMM-TV, slab-sharded over all ranks (csrc/slab.cu through the C ABI):
+    y-slabs, the axis-3 half spectrum split by plane over conjugate LR class
+    pairs, the exchanges as the kernels' own NVLink peer stores / loads
+    between stream-ordered NCCL barriers (N > 1), P = 1 on one GPU.  Strong
+    scaling: the whole volume is split over the N ranks."""
     import torch.distributed as tdist
     from paper_2010_15491_b200 import dist as D
-    cfg = synth.CONFIGS[3]
+    cfg = synth.CONFIGS[idx]
     hr, rates = cfg.hr, cfg.rates
     m, n, s = hr
+    N = m * n * s
+    free = torch.cuda.mem_get_info(local)[0]
+    need = 110.0 * N / world + 24.0 * N  # per rank: slab state ~96 N / P + the setup's full Lambda
+    if free < need:
+        return {"skipped": f"needs ~{need / 1e9:.0f} GB of free device memory per GPU ({free / 1e9:.0f} GB free)"}
+    dist_on = world > 1 and tdist.is_available() and tdist.is_initialized()
+    comm = D.SlabComm.nccl(ctx) if dist_on else D.SlabComm.local(1, ctx)
     psf = synth.make_gaussian_psf(cfg.psf_size, cfg.psf_sigma, hr)
-    g = D.SlabGeometry(hr, rates, world)
-    dev = torch.device("cuda", local)
-    gen = torch.Generator(device=dev).manual_seed(1234 + rank)
-    sz = g.sz
-    psf_slab = torch.from_numpy(np.ascontiguousarray(psf[rank * sz:(rank + 1) * sz])).reshape(-1).to(dev)
-    gy = torch.Generator(device=dev).manual_seed(99)
-    y = torch.rand(g.sl * g.nl * g.ml, generator=gy, device=dev, dtype=torch.float64)
-    x0 = torch.rand(g.slab_elems, generator=gen, device=dev, dtype=torch.float64)
-    dist_on = tdist.is_available() and tdist.is_initialized()
-    ex = D.TorchExchange() if dist_on else D.LocalExchange(1)
-    st = D.GpuStages({rank if dist_on else 0: ctx})
-    r0 = rank if dist_on else 0
-    tv = D.SlabADMMTV(st, ex, hr, rates, {r0: psf_slab}, {r0: y}, {r0: x0}, cfg.tv_lambda, cfg.tv_mu,
-                      tau=1e-3 * cfg.tv_mu)
+    rng = np.random.default_rng(99)
+    y = rng.uniform(0.0, 1.0, V.shape_of(cfg.lr))  # the work is value-independent; parity: tests/test_dist.py
+    k = iters or max(3, min(args.steps, 10))
+    spec = V.DecimationSpec(hr, rates)
+    tcfg = V.TvAdmmConfig(lambda_=cfg.tv_lambda, mu=cfg.tv_mu, max_iters=k + 2, rel_tol=0.0,
+                          tau=1e-3 * cfg.tv_mu, init=V.INIT_UPSAMPLED)
+    tv = D.SlabADMMTV(comm, y, psf, spec, tcfg)
+    del psf
     tv.iterate(2)
-    k = max(3, min(args.steps, 10))
+    dev = torch.device("cuda", local)
+    lib = torch.cuda.ExternalStream(ctx.stream(), device=dev)  # the stream the slab stages run on
     if dist_on:
         tdist.barrier()
-    torch.cuda.synchronize()
     ctx.synchronize()
-    lib = torch.cuda.ExternalStream(ctx.stream(), device=dev)  # the stream the slab stages run on
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    l0 = V.launch_count()
     e0.record(lib)
-    tv.iterate(k)  # ends with the scalar gather on the library stream
+    tv.iterate(k)
     e1.record(lib)
     e1.synchronize()
+    launches = V.launch_count() - l0
     ms = e0.elapsed_time(e1) / k
+    _, rep = tv.finish()
+    tv.close()
+    comm.close()
     if dist_on:
         t = torch.tensor([ms], device=dev, dtype=torch.float64)
         tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
         ms = float(t.item())
-    N = g.N
-    a2a = 2 * 16 * (N // world) * (world - 1) / world
-    out = {"workload": "config3: ADMM-TV fp64 512x512x256 -> 256x256x64 (d=2,2,4), slab-sharded over "
-                       f"{world} GPU(s): NCCL all-to-all FFT transposes + ring halos",
-           "value": N / (ms * 1e-3), "unit": "HR voxels/s per ADMM-TV iteration", "ms_per_iter": ms,
-           "iters_timed": k, "scaling": "strong", "alltoall_bytes_per_rank_per_iter": a2a,
-           "note": "host-orchestrated stages (python), exchanges synchronous"}
-    del tv
-    if world == 1:
-        # the same config through the single-GPU path (half-spectrum fused kernels, graph replay)
-        V = __import__("paper_2010_15491_b200.volsr", fromlist=["volsr"])
-        spec = V.DecimationSpec(hr, rates)
-        psf_d = torch.from_numpy(np.ascontiguousarray(psf)).reshape(-1).to(dev)
-        tcfg = V.TvAdmmConfig(lambda_=cfg.tv_lambda, mu=cfg.tv_mu, max_iters=k + 4, rel_tol=0.0,
-                              tau=1e-3 * cfg.tv_mu, init=V.INIT_UPSAMPLED)
-        one = V.TvDevice(ctx, spec, _Dev(y), _Dev(psf_d), tcfg)
-        one.iterate(2)
-        ctx.synchronize()
-        e0.record(lib)
-        one.iterate(k)
-        e1.record(lib)
-        e1.synchronize()
-        one.close()
-        out["single_gpu_path_ms_per_iter"] = e0.elapsed_time(e1) / k
-    return out
+    # peer traffic per rank per iteration: its rows of the half planes it does
+    # not own, out (r2c stores) and back (c2r loads), plus 5 halo rows per plane
+    half_bytes = 16.0 * m * (n // world) * (s // 2 + 1)
+    peer = 2 * half_bytes * (world - 1) / world + 5 * 8.0 * m * s * (world > 1)
+    hbm = load_peaks().get("hbm_gbs") or 6650.0
+    path = V.tv_algorithmic_bytes(hr, rates)
+    return {"workload": f"config{idx}: ADMM-TV fp64 {m}x{n}x{s} -> {cfg.lr[0]}x{cfg.lr[1]}x{cfg.lr[2]} "
+                        f"(d={cfg.d}), slab-sharded over {world} GPU(s)",
+            "value": N / (ms * 1e-3), "unit": "HR voxels/s per ADMM-TV iteration", "ms_per_iter": ms,
+            "iters_timed": k, "scaling": "strong", "gpu_launches_per_iter": launches / k,
+            "per_gpu_hbm_frac_of_model": path / world / (ms * 1e-3) / 1e9 / hbm,
+            "peer_bytes_per_rank_per_iter": peer,
+            "peer_gbs_per_rank": peer / (ms * 1e-3) / 1e9 if world > 1 else 0.0,
+            "peer_frac_of_nvlink_900": peer / (ms * 1e-3) / 1e9 / 900.0 if world > 1 else 0.0,
+            "objective_last": rep.objective[-1],
+            "design": "exchange = r2c peer stores / c2r peer loads over NVLink (CUDA IPC), 3 stream-ordered "
+                      "barriers per iteration; no pack/unpack passes; half-spectrum planes only"}
 
 
 def main():
@@ -801,7 +804,7 @@ def main():
     ap.add_argument("--no-config4", action="store_true", help="skip the 1024^3 single-GPU config-4 timing")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-fft-path", action="store_true", help="skip timing the general FFT-path solve")
-    ap.add_argument("--sharded", action="store_true", help="also time the slab-sharded config-3 path at N=1")
+    ap.add_argument("--no-sharded", action="store_true", help="skip the slab-sharded config-3/4 timings")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     rank = int(os.environ.get("RANK", "0"))

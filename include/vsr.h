@@ -240,40 +240,61 @@ int vsr_tv_report(vsr_tv* h, vsr_report* report); /* synchronizes */
 int vsr_tv_destroy(vsr_tv* h);
 double vsr_tv_algorithmic_bytes(const size_t hr_dims[3], const size_t rates[3]);
 
-/* ---- slab-decomposed distributed path; per-rank device stages.
- *      A rank holds z-slab p (s/P planes) of spatial volumes and, spectrally,
- *      the alias-closed row set {g2 + bc*nl : g2 in [p nl/P, (p+1) nl/P)} in
- *      the local layout [f3][jl][f1] (dims m x n/P x s).  The host exchanges
- *      (all-to-all, halos, scalar gathers) between these calls
- *      (paper_2010_15491_b200/dist.py).  All pointers are device pointers on
- *      the context's device; work is ordered on the context stream. */
+/* unitary-scaled forward 3D FFT of device data (the engine alone; bench/tests) */
 int vsr_fft3_d(vsr_ctx* ctx, const size_t dims[3], const double* in, int in_real, double* out_c,
                double scale);
-int vsr_slab_fwd_xy_pack_d(vsr_ctx* ctx, const size_t hr_dims[3], const size_t rates[3], int P,
-                           const double* in, int in_real, double* work_c, double* send_c);
-int vsr_slab_axis3_d(vsr_ctx* ctx, const size_t hr_dims[3], const size_t rates[3], int P, double* W,
-                     int inverse, double scale);
-int vsr_slab_lr_slice_d(vsr_ctx* ctx, const size_t hr_dims[3], const size_t rates[3], int P, int rank,
-                        const double* Yl_full, double* Yl_loc);
-int vsr_slab_tik_fold_d(vsr_ctx* ctx, const size_t hr_dims[3], const size_t rates[3], int P,
-                        const double* Yl_loc, const double* lam_loc, const double* xbh_loc, double reg,
-                        double* W_out);
-int vsr_slab_tv_prepare_d(vsr_ctx* ctx, const size_t hr_dims[3], const size_t rates[3], int P, int rank,
-                          const double* lam_loc);
-/* frees the fold tables cached by vsr_slab_tv_prepare_d for lam_loc (NULL: all of
- * this context's; vsr_ctx_destroy also frees them) */
-int vsr_slab_tv_release_d(vsr_ctx* ctx, const double* lam_loc);
-int vsr_slab_tv_fold_d(vsr_ctx* ctx, const size_t hr_dims[3], const size_t rates[3], int P, int rank,
-                       const double* Yl_loc, const double* lam_loc, double* W, double mu, double tau,
-                       double fwd_scale, double* fit_out);
-int vsr_slab_unpack_inv_xy_d(vsr_ctx* ctx, const size_t hr_dims[3], const size_t rates[3], int P,
-                             const double* recv_c, double* work_c, double* out_real, double scale,
-                             double* sums_out, unsigned long long* bad_out);
-int vsr_slab_tv_stencil_d(vsr_ctx* ctx, const size_t hr_dims[3], const size_t rates[3], int P, int init,
-                          const double* x_ext, const double* dual_in_ext, double* dual_out_ext,
-                          double* theta, double thr, double* sums_out);
-int vsr_slab_fit_d(vsr_ctx* ctx, const size_t hr_dims[3], const size_t rates[3], int P,
-                   const double* Yl_loc, const double* lam_loc, const double* xh_loc, double* fit_out);
+
+/* ---- slab-sharded solvers over P ranks, one GPU per rank.
+ *      Rank p owns HR rows y in [p n/P, (p+1) n/P) of every plane: a slab is
+ *      an (m, n/P, s) array.  Spectrally the axis-3 half spectrum is split by
+ *      plane over conjugate LR class pairs, so every fold alias set is local;
+ *      the exchanges are the kernels' own NVLink peer loads/stores (CUDA IPC)
+ *      between stream-ordered barriers.  y (LR) and the PSF / Lambda are
+ *      passed in full on every rank; slab arguments are arrays with one entry
+ *      per LOCAL rank (1 for NCCL / host comms, P for a local comm).  Every
+ *      call is collective over the comm.  Host buffers unless marked _d. */
+typedef struct vsr_comm vsr_comm;
+typedef struct vsr_slab_tv vsr_slab_tv;
+typedef struct vsr_slab_tikhonov vsr_slab_tikhonov;
+/* caller-provided exchange (e.g. a gloo process group): both return 0 on success */
+typedef struct vsr_host_exchange {
+    int (*barrier)(void* user);                                          /* all ranks reached it */
+    int (*all_gather)(void* user, const void* send, void* recv, size_t bytes); /* rank order */
+} vsr_host_exchange;
+/* P virtual ranks in this process on the context's device (stage by stage, stream order) */
+int vsr_comm_local(vsr_ctx* ctx, int nranks, vsr_comm** out);
+/* one process per GPU over NCCL (libnccl.so.2 loaded at run time); rank 0's id to all */
+int vsr_nccl_unique_id(unsigned char out[128]);
+int vsr_comm_nccl(vsr_ctx* ctx, int nranks, int rank, const unsigned char id[128], vsr_comm** out);
+int vsr_comm_host(vsr_ctx* ctx, int nranks, int rank, const vsr_host_exchange* ops, void* user, vsr_comm** out);
+int vsr_comm_destroy(vsr_comm* comm);
+int vsr_comm_info(vsr_comm* comm, int* nranks, int* rank /* -1: local comm */, int* local_ranks);
+/* plane ownership: owner_half[f3] for f3 = 0..s/2 (may be NULL), planes owned by `rank` */
+int vsr_slab_plan(const size_t hr_dims[3], const size_t rates[3], int nranks, int rank, int* owner_half,
+                  int* nplanes);
+/* admm_tv (solvers.hpp:106-107, solvers.cpp:321-411): cfg->init_volume is
+ * ignored, init_slabs carries the Provided init; x_slabs receive x. */
+int vsr_slab_admm_tv(vsr_comm* comm, const size_t hr_dims[3], const size_t rates[3], const double* y_r,
+                     const double* psf_r, const vsr_tv_config* cfg, const double* const* init_slabs,
+                     double* const* x_slabs, vsr_report* report);
+int vsr_slab_tv_create(vsr_comm* comm, const size_t hr_dims[3], const size_t rates[3], const double* y_r,
+                       const double* psf_r, const vsr_tv_config* cfg, const double* const* init_slabs,
+                       vsr_slab_tv** out);
+int vsr_slab_tv_iterate(vsr_slab_tv* h, size_t iters);
+int vsr_slab_tv_local_ranks(vsr_slab_tv* h, int* count);
+int vsr_slab_tv_x_d(vsr_slab_tv* h, int local, const double** x_dev);
+/* require_finite + x slabs (may be NULL) + report (may be NULL); synchronizes */
+int vsr_slab_tv_finish(vsr_slab_tv* h, double* const* x_slabs, vsr_report* report);
+int vsr_slab_tv_destroy(vsr_slab_tv* h);
+/* TikhonovOperator (solvers.hpp:27-43): full Lambda (complex HR) on every rank */
+int vsr_slab_tikhonov_create(vsr_comm* comm, const size_t hr_dims[3], const size_t rates[3],
+                             const double* lambda_c, double reg, const double* const* xbar_slabs,
+                             vsr_slab_tikhonov** out);
+int vsr_slab_tikhonov_solve(vsr_slab_tikhonov* h, const double* y_r, double* const* x_slabs);
+int vsr_slab_tikhonov_solve_d(vsr_slab_tikhonov* h, const double* y_dev);
+int vsr_slab_tikhonov_check(vsr_slab_tikhonov* h);
+int vsr_slab_tikhonov_x_d(vsr_slab_tikhonov* h, int local, const double** x_dev);
+int vsr_slab_tikhonov_destroy(vsr_slab_tikhonov* h);
 
 /* 1 when the operator's blur spectrum was detected separable, Lambda(f) =
  * a[f1] b[f2] c[f3] (any Gaussian PSF): the fused folds then rebuild Lambda

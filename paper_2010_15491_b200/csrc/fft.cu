@@ -162,7 +162,7 @@ struct RPairShape {
 template <int L>
 __global__ void __launch_bounds__(RPairShape<L>::THREADS)
     rpair_fwd_kernel(const double* __restrict__ in, double2* __restrict__ out, long long S, long long tiles,
-                     const double2* __restrict__ tw) {
+                     const double2* __restrict__ tw, RemotePlanes rp) {
     using Sh = RPairShape<L>;
     constexpr int R = Sh::R, P = Sh::P, T = Sh::T, TP = Sh::TP;
     extern __shared__ double2 sm[];
@@ -189,17 +189,20 @@ __global__ void __launch_bounds__(RPairShape<L>::THREADS)
         const double2 a = sm[sidx(k)], b = sm[sidx((L - k) & (L - 1))];
         const double2 xa = make_double2(0.5 * (a.x + b.x), 0.5 * (a.y - b.y));
         const double2 xb = make_double2(0.5 * (a.y + b.y), -0.5 * (a.x - b.x));
-        double2* d = dst + S * k;
+        // slab-sharded: plane k goes straight to its owner's spectral buffer
+        // (peer memory over NVLink), rows of this rank's y range
+        double2* d = rp.peer ? rp.peer[rp.owner[k]] + rp.off[k] + c : dst + S * k;
         d[0] = xa;
         d[1] = xb;
     }
+    if (rp.peer) __threadfence_system();
 }
 
 template <int L>
 __global__ void __launch_bounds__(RPairShape<L>::THREADS)
     rpair_inv_kernel(const double2* __restrict__ in, double* __restrict__ out, long long S, long long tiles,
                      const double2* __restrict__ tw, double scale, double* __restrict__ partials,
-                     unsigned long long* __restrict__ bad_index) {
+                     unsigned long long* __restrict__ bad_index, RemotePlanes rp) {
     using Sh = RPairShape<L>;
     constexpr int R = Sh::R, P = Sh::P, T = Sh::T, TP = Sh::TP;
     extern __shared__ double2 sm[];
@@ -214,7 +217,8 @@ __global__ void __launch_bounds__(RPairShape<L>::THREADS)
     for (int r = 0; r < R; ++r) {
         const int q = t + P * r;
         const bool lo = q <= L / 2;
-        const double2* p = src + S * (lo ? q : L - q);
+        const int pq = lo ? q : L - q;
+        const double2* p = rp.peer ? rp.peer[rp.owner[pq]] + rp.off[pq] + c : src + S * pq;
         double2 A = active ? __ldg(p) : make_double2(0.0, 0.0), B = active ? __ldg(p + 1) : make_double2(0.0, 0.0);
         if (!lo) A.y = -A.y, B.y = -B.y;
         v[r] = make_double2(A.x - B.y, A.y + B.x);  // A + i B
@@ -248,7 +252,7 @@ __global__ void __launch_bounds__(RPairShape<L>::THREADS)
 
 template <int L>
 bool launch_rpair(bool fwd, const void* in, void* out, long long S, long long total, const double2* tw,
-                  double scale, const PassReduce* red, cudaStream_t st) {
+                  double scale, const PassReduce* red, cudaStream_t st, const RemotePlanes& rp) {
     using Sh = RPairShape<L>;
     const long long tiles = total / ((long long)Sh::T * L);
     const unsigned blocks = (unsigned)((tiles + Sh::TG - 1) / Sh::TG);
@@ -257,29 +261,29 @@ bool launch_rpair(bool fwd, const void* in, void* out, long long S, long long to
         auto kern = rpair_fwd_kernel<L>;
         if (smem > 48 * 1024) VSR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         kern<<<blocks, Sh::THREADS, smem, st>>>(static_cast<const double*>(in), static_cast<double2*>(out), S,
-                                                       tiles, tw);
+                                                       tiles, tw, rp);
     } else {
         auto kern = rpair_inv_kernel<L>;
         if (smem > 48 * 1024) VSR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         kern<<<blocks, Sh::THREADS, smem, st>>>(static_cast<const double2*>(in), static_cast<double*>(out), S,
                                                        tiles, tw, scale, red ? red->partials : nullptr,
-                                                       red ? red->bad_index : nullptr);
+                                                       red ? red->bad_index : nullptr, rp);
     }
     VSR_LAUNCH_CHECK();
     return true;
 }
 
 bool dispatch_rpair(bool fwd, size_t L, const void* in, void* out, long long S, long long total, const double2* tw,
-                    double scale, const PassReduce* red, cudaStream_t st) {
+                    double scale, const PassReduce* red, cudaStream_t st, const RemotePlanes& rp = RemotePlanes{}) {
     switch (L) {
-        case 8: return launch_rpair<8>(fwd, in, out, S, total, tw, scale, red, st);
-        case 16: return launch_rpair<16>(fwd, in, out, S, total, tw, scale, red, st);
-        case 32: return launch_rpair<32>(fwd, in, out, S, total, tw, scale, red, st);
-        case 64: return launch_rpair<64>(fwd, in, out, S, total, tw, scale, red, st);
-        case 128: return launch_rpair<128>(fwd, in, out, S, total, tw, scale, red, st);
-        case 256: return launch_rpair<256>(fwd, in, out, S, total, tw, scale, red, st);
-        case 512: return launch_rpair<512>(fwd, in, out, S, total, tw, scale, red, st);
-        case 1024: return launch_rpair<1024>(fwd, in, out, S, total, tw, scale, red, st);
+        case 8: return launch_rpair<8>(fwd, in, out, S, total, tw, scale, red, st, rp);
+        case 16: return launch_rpair<16>(fwd, in, out, S, total, tw, scale, red, st, rp);
+        case 32: return launch_rpair<32>(fwd, in, out, S, total, tw, scale, red, st, rp);
+        case 64: return launch_rpair<64>(fwd, in, out, S, total, tw, scale, red, st, rp);
+        case 128: return launch_rpair<128>(fwd, in, out, S, total, tw, scale, red, st, rp);
+        case 256: return launch_rpair<256>(fwd, in, out, S, total, tw, scale, red, st, rp);
+        case 512: return launch_rpair<512>(fwd, in, out, S, total, tw, scale, red, st, rp);
+        case 1024: return launch_rpair<1024>(fwd, in, out, S, total, tw, scale, red, st, rp);
         default: return false;
     }
 }
@@ -572,6 +576,23 @@ void FftEngine::r2c_axis3_half(const Dims& d, const double* in, double2* out, cu
     if (!half3_ok(d)) throw std::logic_error("r2c_axis3_half: unsupported geometry");
     if (!dispatch_rpair(true, (size_t)L, in, out, S, total, twiddles((size_t)L), 1.0, nullptr, st))
         throw std::logic_error("r2c_axis3_half: unsupported length");
+}
+
+void FftEngine::r2c_axis3_half_remote(const Dims& d, const double* in, const RemotePlanes& rp, cudaStream_t st) {
+    long long S, L, total;
+    axis_geometry(d, 2, S, L, total);
+    if (!half3_ok(d)) throw std::logic_error("r2c_axis3_half: unsupported geometry");
+    if (!dispatch_rpair(true, (size_t)L, in, nullptr, S, total, twiddles((size_t)L), 1.0, nullptr, st, rp))
+        throw std::logic_error("r2c_axis3_half: unsupported length");
+}
+
+void FftEngine::c2r_axis3_half_remote(const Dims& d, const RemotePlanes& rp, double* out, double scale,
+                                      const PassReduce* red, cudaStream_t st) {
+    long long S, L, total;
+    axis_geometry(d, 2, S, L, total);
+    if (!half3_ok(d)) throw std::logic_error("c2r_axis3_half: unsupported geometry");
+    if (!dispatch_rpair(false, (size_t)L, nullptr, out, S, total, twiddles((size_t)L), scale, red, st, rp))
+        throw std::logic_error("c2r_axis3_half: unsupported length");
 }
 
 void FftEngine::c2r_axis3_half(const Dims& d, const double2* in, double* out, double scale, const PassReduce* red,

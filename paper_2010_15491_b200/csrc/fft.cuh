@@ -33,6 +33,15 @@ struct PassReduce {
     unsigned long long* bad_index = nullptr;  // atomicMin target (init ULLONG_MAX)
 };
 
+// Slab-sharded half-spectrum planes (slab.cu): plane k of an axis-3 r2c lives
+// at peer[owner[k]] + off[k] (complex elements; the rank's rows of that plane
+// are contiguous there).  peer == nullptr: the local (m, n, s/2+1) layout.
+struct RemotePlanes {
+    double2* const* peer = nullptr;
+    const int* owner = nullptr;
+    const long long* off = nullptr;
+};
+
 class FftEngine {
 public:
     // Device twiddle table exp(-2*pi*i*j/L), j in [0, L), cached per L.
@@ -70,6 +79,12 @@ public:
     void r2c_axis3_half(const Dims& d, const double* in, double2* out, cudaStream_t st);
     void c2r_axis3_half(const Dims& d, const double2* in, double* out, double scale, const PassReduce* red,
                         cudaStream_t st);
+    // the same passes with the half-spectrum planes on their owner ranks: the
+    // r2c stores each plane into its owner's buffer (peer stores over NVLink),
+    // the c2r pulls each plane from its owner (peer loads)
+    void r2c_axis3_half_remote(const Dims& d, const double* in, const RemotePlanes& rp, cudaStream_t st);
+    void c2r_axis3_half_remote(const Dims& d, const RemotePlanes& rp, double* out, double scale,
+                               const PassReduce* red, cudaStream_t st);
 
     // Blocks of the final (axis-1) pass of inverse3.
     size_t inverse_final_blocks(const Dims& d) const { return pass_blocks(d, 0); }

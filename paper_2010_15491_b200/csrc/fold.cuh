@@ -48,6 +48,19 @@ struct GammaTables {
     // 1: W holds only planes f3 <= s/2 of a Hermitian spectrum (axis 3 r2c);
     // alias rows with f3 > s/2 are read as conj(row(-f2, s - f3)) and not stored
     int half3 = 0;
+    // slab-sharded sandwich (slab.cu, half3 only): a rank holds a subset of
+    // the half-spectrum planes.  wplane[f3] (f3 <= s/2) is the local plane of
+    // W / the output, lplane[f3] (f3 < s) the local plane of a dense Lambda,
+    // and tiles[i] = (g2 block, g3) the tiles this launch runs (ntiles of
+    // them).  nullptr: identity / every tile.
+    const int* wplane = nullptr;
+    const int* lplane = nullptr;
+    const int2* tiles = nullptr;
+    int ntiles = 0;
+    // 1: the axis-1 TV sandwich only reports the data fit of its INPUT
+    // spectrum, ||Yl - (1/sqrt d) sum_b Lambda_b W_b||^2 per tile, and writes
+    // nothing (the initial objective of a slab-sharded admm_tv)
+    int fit_only = 0;
 };
 
 // Gw(g) = sum_b Gamma_b |Lambda_b|^2 over the d aliases of every LR frequency

@@ -207,14 +207,21 @@ __device__ __forceinline__ void fold_axis1_tile(int tile, FoldGeom G, const doub
     const int a = ln % A, ti = ln / A;
     const int bc = a % G.dc, bs = a / G.dc;
     const int ng2 = (int)(G.nl / T);
-    const int bx2 = tile % ng2, bx3 = tile / ng2;
+    int bx2 = tile % ng2, bx3 = tile / ng2;
+    if (TV && tabs.tiles) {  // slab-sharded: this rank's tile list
+        const int2 tt = tabs.tiles[tile];
+        bx2 = tt.x, bx3 = tt.y;
+    }
     const long long g2 = (long long)bx2 * T + ti, g3 = bx3;
     const long long f2 = g2 + bc * G.nl, f3 = g3 + bs * G.sl;
-    const long long rowb = G.m * (f2 + G.n * f3);
+    // W / output rows live on local planes (wplane), dense Lambda rows on lplane
+    auto wpl = [&](long long z) -> long long { return (TV && tabs.wplane) ? (long long)tabs.wplane[z] : z; };
+    const long long rowb = (TV && tabs.lplane) ? G.m * (f2 + G.n * (long long)tabs.lplane[f3]) : G.m * (f2 + G.n * f3);
     // half-spectrum W (tabs.half3): rows past the Nyquist plane are mirrors
     const bool mir = TV && tabs.half3 && 2 * f3 > G.s;
     const long long nf2 = f2 == 0 ? 0 : G.n - f2;  // -f2 mod n (0 <= f2 < n)
-    const long long rowb_rd = mir ? G.m * (nf2 + G.n * (G.s - f3)) : rowb;
+    const long long roww = mir ? 0 : G.m * (f2 + G.n * wpl(f3));
+    const long long rowb_rd = mir ? G.m * (nf2 + G.n * wpl(G.s - f3)) : roww;
     // Mirror pairing (half3, one LR column per tile): the alias set of LR
     // (g2, g3) and that of (-g2, -g3) give conjugate rows, so only one of the
     // pair runs (role 1) and also stores the other's rows, conjugated; a
@@ -234,8 +241,8 @@ __device__ __forceinline__ void fold_axis1_tile(int tile, FoldGeom G, const doub
         return;
     }
     // second copy of a row on the Nyquist/zero planes (its mirror is also <= s/2)
-    const long long mrow = G.m * (nf2 + G.n * f3);
-    const long long sec = (role == 1 && !mir && (f3 == 0 || 2 * f3 == G.s) && mrow != rowb) ? mrow : -1;
+    const long long mrow = G.m * (nf2 + G.n * wpl(f3));
+    const long long sec = (role == 1 && !mir && (f3 == 0 || 2 * f3 == G.s) && mrow != roww) ? mrow : -1;
     // line-interleaved: a quarter-warp (8 lines at one position) is one 128-B row
     auto sidx = [&](int q) { return q * NLN + ln; };
     // Staged HBM I/O: whole rows move through shared memory (pitch L + 1, bank-
@@ -345,6 +352,33 @@ __device__ __forceinline__ void fold_axis1_tile(int tile, FoldGeom G, const doub
         for (int r = 0; r < R; ++r) sm[sidx(t + P * r)] = __ldg(lam + rowb + t + P * r);
     }
     double fit = 0.0;
+    if constexpr (TV && FIT) {
+        if (tabs.fit_only) {  // data fit of the input spectrum only (uniform per launch)
+#pragma unroll
+            for (int rr = 0; rr < RD; ++rr) {
+                double ax = 0.0, ay = 0.0;
+#pragma unroll
+                for (int br = 0; br < DR; ++br) {
+                    const int r = rr + RD * br;
+                    const double2 pr = cmul(sm[sidx(t + P * r)], v[r]);
+                    ax += pr.x;
+                    ay += pr.y;
+                }
+                ax = lanes_sum<1, A>(ax);
+                ay = lanes_sum<1, A>(ay);
+                if (a == 0) {
+                    const double rx = yr[rr].x - invsqrtd * ax, ry = yr[rr].y - invsqrtd * ay;
+                    fit += rx * rx + ry * ry;
+                }
+            }
+            if (role == 1) fit *= 2.0;
+            __shared__ double red0[32];
+            double vv[1] = {fit};
+            block_reduce_sum<1>(vv, red0);
+            if (tid == 0) fit_partials[tile] = vv[0];
+            return;
+        }
+    }
     if constexpr (TV) {
         if (tabs.gw) {
             // one cross-alias sum: S = sum_b Lambda_b g_b with g_b = Gamma_b k_b; the
@@ -467,7 +501,7 @@ folded:
         for (int j = 0; j < R; ++j) {
             const double2 val = v[j];
             if (!mir)
-                dst[rowb + Pl::out_q(t, j)] = val;
+                dst[(TV ? roww : rowb) + Pl::out_q(t, j)] = val;
             else if (role == 1)
                 dst[rowb_rd + Pl::out_q(t, j)] = make_double2(val.x, -val.y);
             if (sec >= 0) dst[sec + Pl::out_q(t, j)] = make_double2(val.x, -val.y);
@@ -529,7 +563,8 @@ void launch_a1(const FoldGeom& G, const double2* Yl, const double2* lam, const S
     auto kern = fold_axis1_kernel<L, A, DR, Sh::T, TV, FIT, RM>;
     if (Sh::SMEM > 48 * 1024)
         VSR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Sh::SMEM));
-    const int ntiles = (int)((G.nl / Sh::T) * G.sl);
+    const int ntiles = (TV && tabs.tiles) ? tabs.ntiles : (int)((G.nl / Sh::T) * G.sl);
+    if (ntiles == 0) return;
     const unsigned grid = (unsigned)ntiles;
     kern<<<grid, Sh::THREADS, Sh::SMEM, st>>>(ntiles, G, Yl, lam, sep, xbh, Zl, W, out, tabs, cA, shift, inv_scale,
                                               1.0 / std::sqrt((double)G.d), fwd_scale,
@@ -664,6 +699,15 @@ void launch_tik_fold_ifft1(const FoldGeom& G, const double2* Yl, const double2* 
     if (!dispatch_a1<false, false>(G, Yl, lam, sep, xbh, Zl, nullptr, out, none, 2.0 * reg, 2.0 * reg * (double)G.d,
                                    1.0 / (2.0 * reg), 1.0, nullptr, st))
         throw std::logic_error("launch_tik_fold_ifft1: unsupported geometry");
+}
+
+int tv_sandwich1_tile_g2(const FoldGeom& G) {
+    const int A = G.dc * G.ds;
+#define VSR_X(LL, AA, DD) \
+    if (G.m == LL && A == AA && G.dr == DD) return A1Shape<LL, AA, DD>::T;
+    VSR_A1_TABLE(VSR_X)
+#undef VSR_X
+    return 0;
 }
 
 size_t tv_sandwich1_blocks(const FoldGeom& G) {

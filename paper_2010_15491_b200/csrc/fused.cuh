@@ -42,6 +42,8 @@ void launch_tik_fold_ifft1(const FoldGeom& G, const double2* Yl, const double2* 
                            double2* out, double reg, cudaStream_t st, const SepTables& sep = SepTables{},
                            const double2* Zl = nullptr);
 size_t tv_sandwich1_blocks(const FoldGeom& G);
+// consecutive g2 per tile of the axis-1 sandwich (tile = (g2 / T, g3)); 0 if unsupported
+int tv_sandwich1_tile_g2(const FoldGeom& G);
 // Wout (optional): write x̂ there instead of in place (required with
 // tabs.half3, where lines read other tiles' rows as conjugate mirrors).
 void launch_tv_sandwich1(const FoldGeom& G, const double2* Yl, const double2* lam, double2* W,

@@ -280,7 +280,9 @@ __global__ void __launch_bounds__(STH)
     tv_stencil_fast_kernel(int m, int n, int s, int KC, const double* __restrict__ x,
                            const double* __restrict__ dual_in, double* __restrict__ dual_out,
                            double* __restrict__ theta, double thr, const double* __restrict__ xprev,
-                           double* __restrict__ partials, int halo, long long dsi, long long dso) {
+                           double* __restrict__ partials, int halo, long long dsi, long long dso,
+                           const double* __restrict__ ylo_x = nullptr, const double* __restrict__ yhi_x = nullptr,
+                           const double* __restrict__ ylo_d = nullptr) {
     extern __shared__ double sm[];
     double* rx = sm + 3 * FXS + 2 * FDS;  // [TY][TX+1]
     double* ry = rx + TY * (TX + 1);       // [TY+1][TX]
@@ -299,24 +301,44 @@ __global__ void __launch_bounds__(STH)
         v %= len;
         return v < 0 ? v + len : v;
     };
+    // y-slab mode (slab.cu: ylo_x set): axis 2 is not periodic here; the halo
+    // rows -1 and n come from the neighbouring ranks' x (and dual) slabs, read
+    // in place over NVLink peer memory (row n-1 of the lower one, row 0 of the
+    // upper one; same plane stride)
+    const bool yslab = ylo_x != nullptr;
+    auto yrow = [&](int jr, const double*& base, const double* lo, const double* hi) {
+        if (!yslab) return wrap(jr, n);
+        if (jr < 0) {
+            base = lo;
+            return n - 1;
+        }
+        if (jr >= n) {
+            base = hi;
+            return 0;
+        }
+        return jr;
+    };
     // load assignments: one x pair (tid < FXP), up to two dual pairs
     const bool xa = tid < FXP;
     int xoff = 0, xsm = 0;
+    const double* xsrc = x;
     if (xa) {
         const int row = tid / (FXW / 2), pc = tid % (FXW / 2);
-        xoff = wrap(i0 - 2 + 2 * pc, m) + m * wrap(j0 - 1 + row, n);
+        xoff = wrap(i0 - 2 + 2 * pc, m) + m * yrow(j0 - 1 + row, xsrc, ylo_x, yhi_x);
         xsm = row * FXW + 2 * pc;
     }
     bool da[2];
     long long doff[2];
     int dsm[2];
+    const double* dsrc[2] = {dual_in, dual_in};
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
         const int e = tid + q * STH;
         da[q] = !INIT && e < 3 * FDP;
         const int c = da[q] ? e / FDP : 0, rem = da[q] ? e % FDP : 0;
         const int row = rem / (FDW / 2), pc = rem % (FDW / 2);
-        doff[q] = (long long)c * dsi + wrap(i0 - 2 + 2 * pc, m) + (long long)m * wrap(j0 - 1 + row, n);
+        doff[q] = (long long)c * dsi + wrap(i0 - 2 + 2 * pc, m) +
+                  (long long)m * yrow(j0 - 1 + row, dsrc[q], ylo_d, nullptr);
         dsm[q] = c * FDH * FDW + row * FDW + 2 * pc;
     }
     // plane pointers advance by one plane per step; in periodic mode they wrap
@@ -330,23 +352,23 @@ __global__ void __launch_bounds__(STH)
 
     double2 rxv = make_double2(0.0, 0.0), rdv[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
     // prologue: x(k0-1), x(k0), dual(k0-1) resident; x(k0+1), dual(k0) in registers
-    if (xa) *reinterpret_cast<double2*>(xsl[0] + xsm) = __ldg(reinterpret_cast<const double2*>(x + zp(k0 - 1) + xoff));
+    if (xa) *reinterpret_cast<double2*>(xsl[0] + xsm) = __ldg(reinterpret_cast<const double2*>(xsrc + zp(k0 - 1) + xoff));
     if (!INIT) {
         const long long zo = zp(k0 - 1);
 #pragma unroll
         for (int q = 0; q < 2; ++q)
             if (da[q]) *reinterpret_cast<double2*>(dsl[0] + dsm[q]) =
-                __ldg(reinterpret_cast<const double2*>(dual_in + zo + doff[q]));
+                __ldg(reinterpret_cast<const double2*>(dsrc[q] + zo + doff[q]));
     }
-    if (xa) *reinterpret_cast<double2*>(xsl[1] + xsm) = __ldg(reinterpret_cast<const double2*>(x + zp(k0) + xoff));
-    const double* xnext = x + xoff;       // advanced below; holds plane k+3 at step k
-    const double* dnext = dual_in;        // plane k+2 at step k
+    if (xa) *reinterpret_cast<double2*>(xsl[1] + xsm) = __ldg(reinterpret_cast<const double2*>(xsrc + zp(k0) + xoff));
+    const double* xnext = xsrc + xoff;    // advanced below; holds plane k+3 at step k
+    const double* dnext[2] = {dsrc[0] + doff[0], dsrc[1] + doff[1]};  // plane k+2 at step k
     long long zx = zp(k0 + 1), zd = zp(k0);
     if (xa && k0 + 1 <= k1) rxv = __ldg(reinterpret_cast<const double2*>(xnext + zx));
     if (!INIT && k0 < k1) {
 #pragma unroll
         for (int q = 0; q < 2; ++q)
-            if (da[q]) rdv[q] = __ldg(reinterpret_cast<const double2*>(dnext + zd + doff[q]));
+            if (da[q]) rdv[q] = __ldg(reinterpret_cast<const double2*>(dnext[q] + zd));
     }
     // halo points (rho_x at ii = -1 for TY rows, rho_y at jj = -1 for TX columns)
     // packed into whole warps: warp 0 takes the TX row points, warp 1 the TY
@@ -389,7 +411,7 @@ __global__ void __launch_bounds__(STH)
             if (!halo && zd >= plane * s) zd -= plane * s;
 #pragma unroll
             for (int q = 0; q < 2; ++q)
-                if (da[q]) rdv[q] = __ldg(reinterpret_cast<const double2*>(dnext + zd + doff[q]));
+                if (da[q]) rdv[q] = __ldg(reinterpret_cast<const double2*>(dnext[q] + zd));
         }
         __syncthreads();
         const bool warm = k < k0;
@@ -755,25 +777,24 @@ void launch_tv_norm(const Dims& d, const double* x, double* partials, cudaStream
     VSR_LAUNCH_CHECK();
 }
 
-void launch_tv_stencil_slab(const Dims& slab, bool init, const double* x_ext, const double* dual_in_ext,
-                            double* dual_out_ext, double* theta, double thr, double* partials,
-                            cudaStream_t st) {
-    if (slab.m % 2 != 0) throw std::invalid_argument("slab stencil: axis 1 must be even");
-    const StencilGeom g = stencil_geom(slab);
-    const int m = (int)slab.m, n = (int)slab.n, s = (int)slab.s;
-    const long long plane = (long long)m * n;
-    const long long dstride = plane * (s + 1);  // components of the halo-extended dual arrays
+void launch_tv_stencil_yslab(const Dims& loc, bool init, const double* x, const double* dual_in, double* dual_out,
+                             double* theta, double thr, const double* xprev, double* partials, const double* ylo_x,
+                             const double* yhi_x, const double* ylo_d, cudaStream_t st) {
+    if (loc.m % 2 != 0) throw std::invalid_argument("slab stencil: axis 1 must be even");
+    const StencilGeom g = stencil_geom(loc);
+    const int m = (int)loc.m, n = (int)loc.n, s = (int)loc.s;
+    const long long N = (long long)loc.count();
     const size_t smem = fast_smem_doubles() * sizeof(double);
-    // x_ext planes: [z0-1, slab, z1] -> pass plane 0 of the slab; dual ext: [z0-1, slab]
-    const double* x0 = x_ext + plane;
-    const double* d0 = dual_in_ext ? dual_in_ext + plane : nullptr;
-    double* o0 = dual_out_ext + plane;
+#define VSR_FAST(I, R)                                                                                          \
+    tv_stencil_fast_kernel<I, R><<<g.grid, STH, smem, st>>>(m, n, s, g.kc, x, dual_in, dual_out, theta, thr, xprev, \
+                                                            partials, 0, N, N, ylo_x, yhi_x, ylo_d)
     if (init)
-        tv_stencil_fast_kernel<true, false><<<g.grid, STH, smem, st>>>(m, n, s, g.kc, x0, d0, o0, theta, thr,
-                                                                       nullptr, partials, 1, dstride, dstride);
+        VSR_FAST(true, false);
+    else if (xprev)
+        VSR_FAST(false, true);
     else
-        tv_stencil_fast_kernel<false, false><<<g.grid, STH, smem, st>>>(m, n, s, g.kc, x0, d0, o0, theta, thr,
-                                                                        nullptr, partials, 1, dstride, dstride);
+        VSR_FAST(false, false);
+#undef VSR_FAST
     VSR_LAUNCH_CHECK();
 }
 

@@ -28,13 +28,14 @@ void launch_tv_stencil(const Dims& d, bool init, const double* x, const double* 
                        double* dual_out, double* theta, double thr, const double* xprev,
                        double* partials, cudaStream_t st);
 
-// Slab of a z-distributed volume: x_ext has the slab's planes plus one halo
-// plane on each side ([z0-1, slab..., z1]); dual ext arrays hold 3 components
-// of (slab planes + 1) with the low halo plane first.  Writes dual_out_ext's
-// slab planes and theta (slab planes).  axis 1 must be even.
-void launch_tv_stencil_slab(const Dims& slab, bool init, const double* x_ext, const double* dual_in_ext,
-                            double* dual_out_ext, double* theta, double thr, double* partials,
-                            cudaStream_t st);
+// Slab of a y-distributed volume (slab.cu): local dims (m, n/P, s), z
+// periodic; the halo rows -1 / n/P come from the neighbouring ranks' x
+// (ylo_x: row n/P - 1 of the rank below, yhi_x: row 0 of the rank above)
+// and dual_in (ylo_d), read in place (NVLink peer memory); the dual arrays
+// hold 3 components of the local volume.  axis 1 must be even.
+void launch_tv_stencil_yslab(const Dims& loc, bool init, const double* x, const double* dual_in, double* dual_out,
+                             double* theta, double thr, const double* xprev, double* partials, const double* ylo_x,
+                             const double* yhi_x, const double* ylo_d, cudaStream_t st);
 
 // Per-iteration scalar reduction for admm_tv (fixed order, single CTA):
 // report[iter] objective / primal residual / rel change, residue check.

@@ -724,17 +724,6 @@ def tv_algorithmic_bytes(hr_dims, rates) -> float:
 
 # ---------------------------------------------------------------- slab stages (dist.py)
 _sig("vsr_fft3_d", [_vp, _szp, _vp, C.c_int, _vp, C.c_double])
-_sig("vsr_slab_fwd_xy_pack_d", [_vp, _szp, _szp, C.c_int, _vp, C.c_int, _vp, _vp])
-_sig("vsr_slab_axis3_d", [_vp, _szp, _szp, C.c_int, _vp, C.c_int, C.c_double])
-_sig("vsr_slab_lr_slice_d", [_vp, _szp, _szp, C.c_int, C.c_int, _vp, _vp])
-_sig("vsr_slab_tik_fold_d", [_vp, _szp, _szp, C.c_int, _vp, _vp, _vp, C.c_double, _vp])
-_sig("vsr_slab_tv_prepare_d", [_vp, _szp, _szp, C.c_int, C.c_int, _vp])
-_sig("vsr_slab_tv_release_d", [_vp, _vp])
-_sig("vsr_slab_tv_fold_d", [_vp, _szp, _szp, C.c_int, C.c_int, _vp, _vp, _vp, C.c_double, C.c_double,
-                            C.c_double, _vp])
-_sig("vsr_slab_unpack_inv_xy_d", [_vp, _szp, _szp, C.c_int, _vp, _vp, _vp, C.c_double, _vp, _vp])
-_sig("vsr_slab_tv_stencil_d", [_vp, _szp, _szp, C.c_int, C.c_int, _vp, _vp, _vp, _vp, C.c_double, _vp])
-_sig("vsr_slab_fit_d", [_vp, _szp, _szp, C.c_int, _vp, _vp, _vp, _vp])
 
 
 # ---------------------------------------------------------------- instrumentation
