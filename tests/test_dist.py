@@ -178,7 +178,7 @@ def test_numpy_decomposition_two_gloo_processes(tmp_path, hr, rates):
 
 
 # ------------------------------------------------------------------ GPU: local comm (P virtual ranks)
-GPU_CASES = [((32, 32, 32), (2, 2, 2)), ((64, 64, 64), (4, 4, 4)), ((64, 32, 64), (2, 2, 4))]
+GPU_CASES = [((64, 32, 32), (2, 2, 2)), ((64, 64, 64), (4, 4, 4)), ((64, 32, 64), (2, 2, 4))]
 
 
 @pytest.mark.gpu
@@ -241,11 +241,11 @@ def test_slab_tikhonov_local_ranks(V, hr, rates, P):
 @pytest.mark.gpu
 def test_slab_dense_lambda_and_errors(V):
     """A non-separable (random) PSF: the dense Lambda planes of each rank's classes."""
-    hr, rates = (32, 32, 32), (2, 2, 2)
+    hr, rates = (64, 32, 32), (2, 2, 2)
     rng = np.random.default_rng(4)
     w = rng.uniform(0, 1, 27)
     psf = O.make_gaussian_psf((3, 3, 3), (0, 0, 0), hr, weights=w)
-    y = rng.uniform(0, 1, (16, 16, 16))
+    y = rng.uniform(0, 1, (16, 16, 32))
     spec, ospec = V.DecimationSpec(hr, rates), O.DecimationSpec(hr, rates)
     cfg = V.TvAdmmConfig(lambda_=2e-3, mu=0.05, max_iters=2, rel_tol=0.0, tau=5e-5, init=V.INIT_UPSAMPLED)
     xs, _ = D.admm_tv(D.SlabComm.local(4), y, psf, spec, cfg)
@@ -323,7 +323,7 @@ dist.destroy_process_group()
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("hr,rates", [((32, 32, 32), (2, 2, 2)), ((64, 64, 64), (4, 4, 4))])
+@pytest.mark.parametrize("hr,rates", [((64, 32, 32), (2, 2, 2)), ((64, 64, 64), (4, 4, 4))])
 def test_slab_two_processes_one_gpu_host_comm(tmp_path, hr, rates):
     """Two ranks as two processes on one GPU: buffers shared by CUDA IPC, the
     kernels' peer stores/loads cross process boundaries, barriers on the host
