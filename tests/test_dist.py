@@ -211,9 +211,9 @@ def test_slab_admm_tv_inits_and_rel_tol(V, init):
     psf, y, _ = _case(hr, rates, seed=3)
     spec, ospec = V.DecimationSpec(hr, rates), O.DecimationSpec(hr, rates)
     mode = V.INIT_ZERO if init == "zero" else V.INIT_UPSAMPLED
-    cfg = V.TvAdmmConfig(lambda_=2e-3, mu=0.05, max_iters=40, rel_tol=2e-3, tau=5e-5, init=mode)
+    cfg = V.TvAdmmConfig(lambda_=2e-3, mu=0.05, max_iters=40, rel_tol=1e-2, tau=5e-5, init=mode)
     xs, rep = D.admm_tv(D.SlabComm.local(2), y, psf, spec, cfg)
-    want, wrep = O.admm_tv(y, psf, ospec, lam_tv=2e-3, mu=0.05, max_iters=40, rel_tol=2e-3, tau=5e-5, init=mode)
+    want, wrep = O.admm_tv(y, psf, ospec, lam_tv=2e-3, mu=0.05, max_iters=40, rel_tol=1e-2, tau=5e-5, init=mode)
     assert rep.iterations == wrep.iterations < 40  # the same stop iteration (solvers.cpp:405)
     assert rel_err(D.join_slabs(xs), want) < TOL
     np.testing.assert_allclose(rep.objective, wrep.objective, rtol=TOL)
