@@ -1543,6 +1543,8 @@ struct vsr_tv {
     SepState sep;
     DevBuf<double> gw;  // LR table sum_b Gamma_b |Lambda_b|^2 (axis-1 sandwich)
     DevBuf<double2> W2;  // sandwich output on the half-spectrum path (m x n x (s/2+1))
+    DevBuf<int2> tiles;  // half-spectrum sandwich: the tiles that do work (one per conjugate pair)
+    int ntiles = 0;
     DevBuf<int> iter_dev;  // iteration index read by the finalize kernel (graph replay)
     cudaGraphExec_t gexec = nullptr;  // kGraphIters consecutive iterations (dual ping-pong period 2)
     uint64_t g_kernels = 0;
@@ -1642,7 +1644,15 @@ static vsr_tv* tv_build(vsr_ctx* ctx, const Spec& sp, const double* y_dev, const
         g_fwd += 2;
         h->sep.detect(hr, h->lam.p, st);
         if (fuse_axis(h->G, 1) == 1) {
-            if (tv_half(hr)) h->W2.alloc(hr.m * hr.n * (hr.s / 2 + 1));
+            if (tv_half(hr)) {
+                h->W2.alloc(hr.m * hr.n * (hr.s / 2 + 1));
+                if (tv_sandwich1_tile_g2(h->G) == 1) {
+                    const std::vector<int2> tl = tv_sandwich1_active_tiles(h->G);
+                    h->ntiles = (int)tl.size();
+                    h->tiles.alloc(tl.size());
+                    h2d(ctx, h->tiles.p, tl.data(), h->tiles.bytes());
+                }
+            }
             h->gw.alloc(Nl);
             GammaTables tabs{h->tnr.p, h->tnc.p, h->tns.p, h->tau};
             launch_tv_gram(h->G, h->lam.p, h->sep.t, tabs, h->gw.p, st);
@@ -1704,6 +1714,8 @@ static void tv_step(vsr_tv* h) {
     const Dims hrh{hr.m, hr.n, hr.s / 2 + 1};
     if (half) {
         tabs.half3 = 1;
+        tabs.tiles = h->ntiles ? h->tiles.p : nullptr;
+        tabs.ntiles = h->ntiles;
         {
             ProfScope ps(prof, "fft_fwd_axis3_r2c_half", st);
             fft_engine().r2c_axis3_half(hr, h->theta.p, h->W.p, st);
@@ -1783,7 +1795,9 @@ static void tv_step(vsr_tv* h) {
     {
         ProfScope ps(prof, "tv_finalize", st);
         launch_tv_finalize((int)h->iters_done, h->fitp.p,
-                           a1 ? tv_sandwich1_blocks(h->G) : (fused ? tv_sandwich_blocks(h->G) : h->fit_blocks),
+                           half && h->ntiles ? (size_t)h->ntiles
+                                             : (a1 ? tv_sandwich1_blocks(h->G)
+                                                   : (fused ? tv_sandwich_blocks(h->G) : h->fit_blocks)),
                            h->stp.p, h->st_blocks, h->resp.p,
                            half ? fft_engine().half3_blocks(hr)
                                 : (a1 ? fft_engine().pass_blocks(hr, 2) : h->res_blocks),

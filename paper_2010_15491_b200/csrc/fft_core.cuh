@@ -78,6 +78,20 @@ __device__ __forceinline__ void dft_reg(double2* a) {
 
 __host__ __device__ constexpr int ilog2(int v) { return v <= 1 ? 0 : 1 + ilog2(v >> 1); }
 
+// Barrier used between Stockham stages: the whole CTA by default; the
+// pipelined sandwich (sandwich.cu) passes a named barrier per thread group.
+struct CtaSync {
+    __device__ __forceinline__ void operator()() const { __syncthreads(); }
+};
+
+// Twiddle table access: a global table through the read-only path, or a
+// copy in shared memory (TwShared).
+struct TwShared {
+    const double2* p;
+};
+__device__ __forceinline__ double2 tw_at(const double2* __restrict__ p, int i) { return __ldg(p + i); }
+__device__ __forceinline__ double2 tw_at(const TwShared& s, int i) { return s.p[i]; }
+
 template <int L, int RMAX = 16>
 struct Plan {
     static constexpr int R = L < RMAX ? L : RMAX;
@@ -97,9 +111,9 @@ struct Plan {
 
 // Full line transform.  All threads of the CTA must call it (it syncs when
 // NSTAGE > 1).  sidx(q) maps a line position to this thread's line slot in sm.
-template <int L, bool INV, class SIdx, int RMAX = 16>
-__device__ __forceinline__ void stockham(double2* v, int t, double2* sm, const SIdx& sidx,
-                                         const double2* __restrict__ tw) {
+template <int L, bool INV, class SIdx, int RMAX = 16, class Sync = CtaSync, class Tw = const double2*>
+__device__ __forceinline__ void stockham(double2* v, int t, double2* sm, const SIdx& sidx, Tw tw,
+                                         const Sync& sync = Sync()) {
     using Pl = Plan<L, RMAX>;
     constexpr int R = Pl::R, P = Pl::P;
     int Ns = 1;
@@ -117,7 +131,7 @@ __device__ __forceinline__ void stockham(double2* v, int t, double2* sm, const S
 #pragma unroll
                 for (int r = 1; r < R; ++r) {
                     if (r < RS) {
-                        const double2 w = __ldg(tw + ((r * k * tstride) & (L - 1)));
+                        const double2 w = tw_at(tw, (r * k * tstride) & (L - 1));
                         const double2 a = v[vv * RS + r];
                         v[vv * RS + r] = INV ? cmulc(w, a) : cmul(w, a);
                     }
@@ -138,7 +152,7 @@ __device__ __forceinline__ void stockham(double2* v, int t, double2* sm, const S
                 for (int r = 0; r < R; ++r)
                     if (r < RS) sm[sidx(ob + r * Ns)] = v[vv * RS + r];
             }
-            __syncthreads();
+            sync();
             Ns *= RS;
             const int RSn = (stage + 1 < Pl::K) ? R : Pl::RL;
             const int NBn = R / RSn;
@@ -149,7 +163,7 @@ __device__ __forceinline__ void stockham(double2* v, int t, double2* sm, const S
                 for (int r = 0; r < R; ++r)
                     if (r < RSn) v[vv * RSn + r] = sm[sidx(u + (L / RSn) * r)];
             }
-            __syncthreads();
+            sync();
         } else {
             Ns *= RS;
         }

@@ -723,6 +723,9 @@ void launch_tv_sandwich1(const FoldGeom& G, const double2* Yl, const double2* la
                          const GammaTables& tabs, double mu, double fwd_scale, double* fit_partials,
                          cudaStream_t st, const SepTables& sep, double2* Wout) {
     const double shift = mu * (double)G.d, inv_mu = 1.0 / mu;
+    static const bool no_pipe = std::getenv("VSR_NO_PIPE") != nullptr;
+    if (!no_pipe && tv_sandwich_pipe(G, Yl, sep, W, Wout, tabs, mu, shift, inv_mu, fwd_scale, fit_partials, st))
+        return;
     const bool ok = fit_partials ? dispatch_a1<true, true>(G, Yl, lam, sep, nullptr, nullptr, W, Wout, tabs, mu, shift,
                                                            inv_mu, fwd_scale, fit_partials, st)
                                  : dispatch_a1<true, false>(G, Yl, lam, sep, nullptr, nullptr, W, Wout, tabs, mu, shift,

@@ -11,6 +11,8 @@
 
 #include "fold.cuh"
 
+#include <vector>
+
 namespace vsr {
 
 // Whether the fused kernels cover this geometry (otherwise callers use the
@@ -49,5 +51,16 @@ int tv_sandwich1_tile_g2(const FoldGeom& G);
 void launch_tv_sandwich1(const FoldGeom& G, const double2* Yl, const double2* lam, double2* W,
                          const GammaTables& tabs, double mu, double fwd_scale, double* fit_partials,
                          cudaStream_t st, const SepTables& sep = SepTables{}, double2* Wout = nullptr);
+
+// The pipelined variant of the half-spectrum TV sandwich (sandwich.cu):
+// persistent CTAs, bulk-copy row loads into a 3-buffer ring, separable Lambda
+// and the Gw table required, out != W, an explicit tile list (tabs.tiles).
+// Returns false (nothing launched) when it does not cover the call.
+bool tv_sandwich_pipe(const FoldGeom& G, const double2* Yl, const SepTables& sep, const double2* W, double2* out,
+                      const GammaTables& tabs, double cA, double shift, double inv_scale, double fwd_scale,
+                      double* fit_partials, cudaStream_t st);
+// The tiles (g2, g3) of the half-spectrum axis-1 sandwich that do work (one
+// of each conjugate pair of alias sets; tile = one LR (g2, g3)), g3-major.
+std::vector<int2> tv_sandwich1_active_tiles(const FoldGeom& G);
 
 }  // namespace vsr

@@ -465,7 +465,11 @@ TV_CASES = [((8, 8, 8), (2, 2, 2), 6), ((16, 16, 16), (4, 4, 4), 10), ((32, 32, 
             # half-spectrum mirror pairing: nl not a power of two, and sl = 4 (self-mirror planes 0, 2)
             ((64, 48, 32), (4, 4, 4), 5), ((64, 64, 16), (4, 4, 4), 5), ((128, 64, 32), (4, 4, 2), 4),
             # 1024-point axis-3 lines (paired real passes with 16-column tiles, as at config 4)
-            ((64, 8, 1024), (2, 2, 2), 3)]
+            ((64, 8, 1024), (2, 2, 2), 3),
+            # the pipelined half-spectrum sandwich (sandwich.cu) at the configs' row geometries:
+            # (m, dc*ds, dr) = (256, 16, 4) config 2, (512, 8, 2) config 3, (1024, 4, 2) config 4
+            ((256, 32, 32), (4, 4, 4), 3), ((512, 16, 32), (2, 2, 4), 3), ((1024, 16, 8), (2, 2, 2), 3),
+            ((128, 32, 32), (2, 2, 2), 3)]
 
 
 @pytest.mark.parametrize("dims,rates,iters", TV_CASES)
@@ -595,6 +599,8 @@ print("ok", op.path())
     ({"VSR_MARCH_ZC": "5"}, (64, 64, 32), (2, 2, 2)),
     ({"VSR_MARCH_ZC": "1"}, (64, 64, 32), (2, 2, 2)),
     ({"VSR_MARCH_CY": "4"}, (64, 64, 32), (2, 2, 2)),
+    ({"VSR_NO_PIPE": "1"}, (256, 32, 32), (4, 4, 4)),
+    ({"VSR_NO_PIPE": "1"}, (512, 16, 32), (2, 2, 4)),
 ])
 def test_env_variants(env, dims, rates):
     import os

@@ -1,5 +1,2 @@
 mkdir -p gpurun_out
-nvidia-smi > gpurun_out/smi.txt 2>&1
-timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/gputest.log 2>&1; echo rc=$? >> gpurun_out/gputest.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo rc=$? >> gpurun_out/smoke.log
-timeout 900 python bench.py --steps 20 --warmup 5 > gpurun_out/bench.json 2> gpurun_out/bench.err; echo rc=$? >> gpurun_out/bench.err
+for e in 0 1 2 4 5 7; do VSR_PIPE_EXP=$e timeout 600 python bench.py --steps 10 --warmup 3 --no-config4 --no-cpu --no-sharded --no-fft-path > gpurun_out/bench_e$e.json 2> gpurun_out/bench_e$e.err; done
