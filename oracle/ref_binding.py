@@ -52,6 +52,7 @@ def _setup():
     L.ref_save_volume.argtypes = [C.c_char_p, _sz, _dp, C.c_int]
     L.ref_degrade.argtypes = [_sz, _sz, _dp, _sz, _dp, C.c_int, C.c_double, C.c_ulonglong, _dp, _dp]
     L.ref_load_volume.argtypes = [C.c_char_p, _sz, _dp, C.c_size_t]
+    L.ref_make_phantom.argtypes = [_sz, C.c_int, C.c_ulonglong, _dp]
 
 
 class RefError(RuntimeError):
@@ -227,3 +228,10 @@ def degrade(x, psf_size, psf_sigma, rates, bsnr_db, seed):
     _chk(_lib.ref_degrade(_d((m, n, s)), _d(rates), _p(x), _d(psf_size), (C.c_double * 3)(*psf_sigma),
                           int(bsnr_db is not None), float(bsnr_db or 0.0), int(seed), _p(y), C.byref(sig)))
     return y, sig.value
+
+
+def make_phantom(hr, kind=0, seed=0):
+    """Reference make_phantom (sim.cpp:23-73); kind 0 NestedEllipsoids, 1 RandomSmooth, 2 Constant."""
+    out = np.empty((hr[2], hr[1], hr[0]))
+    _chk(_lib.ref_make_phantom(_d(hr), kind, seed, _p(out)))
+    return out

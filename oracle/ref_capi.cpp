@@ -229,4 +229,14 @@ int ref_load_volume(const char* base, size_t d_out[3], double* out, size_t cap) 
     });
 }
 
+// sim.cpp:23-73 (make_phantom) and metrics.cpp (psnr) for the acceptance
+// criterion-3 test (acceptance_main.cpp:118-153)
+int ref_make_phantom(const size_t d[3], int kind, unsigned long long seed, double* out) {
+    return wrap([&] {
+        const PhantomKind k = kind == 0 ? PhantomKind::NestedEllipsoids
+                                        : (kind == 1 ? PhantomKind::RandomSmooth : PhantomKind::Constant);
+        put(make_phantom(D(d), k, seed), out);
+    });
+}
+
 }  // extern "C"
