@@ -199,7 +199,15 @@ typedef struct vsr_tv_config {
     double tau;
     int init;            /* VSR_INIT_* */
     const double* init_volume; /* HR real, when init == VSR_INIT_PROVIDED */
+    int precision;       /* VSR_PRECISION_F64 (reference, default) or VSR_PRECISION_F32: the
+                            iteration state (x, dual, theta, spectra) in fp32 and the transforms
+                            and fold in fp32 arithmetic, LR frequency 0 in fp64; needs a
+                            separable PSF spectrum and a half-spectrum geometry (no reference
+                            analogue: BASELINE north_star's optional fp32 mode) */
 } vsr_tv_config;
+
+#define VSR_PRECISION_F64 0
+#define VSR_PRECISION_F32 1
 
 typedef struct vsr_report {
     size_t iterations;
@@ -235,7 +243,8 @@ int vsr_tv_create_d(vsr_ctx* ctx, const size_t hr_dims[3], const size_t rates[3]
                     const double* y_r_dev, const double* psf_r_dev, const vsr_tv_config* cfg,
                     vsr_tv** out);
 int vsr_tv_iterate_d(vsr_tv* h, size_t iters);
-int vsr_tv_x_d(vsr_tv* h, const double** x_dev);
+int vsr_tv_x_d(vsr_tv* h, const double** x_dev);  /* fp32 mode: x widened into a handle-owned fp64 buffer */
+int vsr_tv_x_f32_d(vsr_tv* h, const float** x_dev); /* fp32 mode only: the fp32 iterate itself */
 int vsr_tv_report(vsr_tv* h, vsr_report* report); /* synchronizes */
 int vsr_tv_destroy(vsr_tv* h);
 double vsr_tv_algorithmic_bytes(const size_t hr_dims[3], const size_t rates[3]);

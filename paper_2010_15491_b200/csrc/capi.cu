@@ -234,12 +234,33 @@ __global__ void gamma_spectra_kernel(long long N, const double2* __restrict__ r,
 }
 
 __global__ void scale_kernel(double* v, double s) { *v *= s; }
+__global__ void narrow_f64_kernel(const double* __restrict__ in, float* __restrict__ out, long long n) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        out[i] = (float)in[i];
+}
+__global__ void widen_f32_kernel(const float* __restrict__ in, double* __restrict__ out, long long n) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        out[i] = (double)in[i];
+}
 __global__ void cmul_kernel(long long n, double2* __restrict__ a, const double2* __restrict__ b,
                             bool conj_b) {
     const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= n) return;
     const double2 bb = conj_b ? make_double2(b[p].x, -b[p].y) : b[p];
     a[p] = cmul(a[p], bb);  // operators.cpp:129 xh[p] *= lambda[p]
+}
+
+void launch_narrow(const double* in, float* out, size_t n, cudaStream_t st) {
+    if (!n) return;
+    const unsigned b = (unsigned)std::min<size_t>((n + 255) / 256, 148 * 16);
+    narrow_f64_kernel<<<b, 256, 0, st>>>(in, out, (long long)n);
+    VSR_LAUNCH_CHECK();
+}
+void launch_widen(const float* in, double* out, size_t n, cudaStream_t st) {
+    if (!n) return;
+    const unsigned b = (unsigned)std::min<size_t>((n + 255) / 256, 148 * 16);
+    widen_f32_kernel<<<b, 256, 0, st>>>(in, out, (long long)n);
+    VSR_LAUNCH_CHECK();
 }
 
 }  // namespace
@@ -1543,6 +1564,11 @@ struct vsr_tv {
     SepState sep;
     DevBuf<double> gw;  // LR table sum_b Gamma_b |Lambda_b|^2 (axis-1 sandwich)
     DevBuf<double2> W2;  // sandwich output on the half-spectrum path (m x n x (s/2+1))
+    // fp32 mode (cfg->precision): fp32 iteration state; x stays fp64 for the
+    // initial objective and the widened result
+    bool f32 = false;
+    DevBuf<float> xf, xprevf, thetaf, dualAf, dualBf;
+    DevBuf<float2> Wf, W2f;
     DevBuf<int2> tiles;  // half-spectrum sandwich: the tiles that do work (one per conjugate pair)
     int ntiles = 0;
     DevBuf<int> iter_dev;  // iteration index read by the finalize kernel (graph replay)
@@ -1600,14 +1626,19 @@ static vsr_tv* tv_build(vsr_ctx* ctx, const Spec& sp, const double* y_dev, const
         const Dims& hr = sp.hr;
         const size_t N = hr.count(), Nl = sp.lr.count();
         cudaStream_t st = ctx->stream;
+        h->f32 = cfg->precision == VSR_PRECISION_F32;
+        if (cfg->precision != VSR_PRECISION_F64 && !h->f32)
+            throw std::invalid_argument("admm_tv: unknown precision");
         h->lam.alloc(N);
         h->Yl.alloc(Nl);
-        h->W.alloc(N);
+        h->W.alloc(N);  // fp32 mode: the initial objective's full spectrum only (freed after setup)
         h->x.alloc(N);
-        if (h->rel_tol > 0.0) h->xprev.alloc(N);
-        h->theta.alloc(N);
-        h->dualA.alloc(3 * N);
-        h->dualB.alloc(3 * N);
+        if (!h->f32) {
+            if (h->rel_tol > 0.0) h->xprev.alloc(N);
+            h->theta.alloc(N);
+            h->dualA.alloc(3 * N);
+            h->dualB.alloc(3 * N);
+        }
         const auto nr = diff_norm_table(hr.m), nc = diff_norm_table(hr.n), ns = diff_norm_table(hr.s);
         h->tnr.alloc(hr.m);
         h->tnc.alloc(hr.n);
@@ -1643,9 +1674,24 @@ static vsr_tv* tv_build(vsr_ctx* ctx, const Spec& sp, const double* y_dev, const
         fft_engine().forward3(sp.lr, y_dev, IN_REAL, h->Yl.p, inv_sqrt_count(sp.lr), st);
         g_fwd += 2;
         h->sep.detect(hr, h->lam.p, st);
+        if (h->f32) {
+            if (!(fuse_axis(h->G, 1) == 1 && tv_half(hr) && h->sep.t.a && hr.m % 2 == 0 &&
+                  tv_sandwich_pipe_ok(h->G)))
+                throw std::invalid_argument(
+                    "admm_tv: fp32 mode needs a separable PSF spectrum and a half-spectrum geometry "
+                    "(power-of-two axis 3, even axis 1, a pipelined axis-1 sandwich shape)");
+            const size_t Nh = hr.m * hr.n * (hr.s / 2 + 1);
+            h->xf.alloc(N);
+            if (h->rel_tol > 0.0) h->xprevf.alloc(N);
+            h->thetaf.alloc(N);
+            h->dualAf.alloc(3 * N);
+            h->dualBf.alloc(3 * N);
+            h->Wf.alloc(Nh);
+            h->W2f.alloc(Nh);
+        }
         if (fuse_axis(h->G, 1) == 1) {
             if (tv_half(hr)) {
-                h->W2.alloc(hr.m * hr.n * (hr.s / 2 + 1));
+                if (!h->f32) h->W2.alloc(hr.m * hr.n * (hr.s / 2 + 1));
                 if (tv_sandwich1_tile_g2(h->G) == 1) {
                     const std::vector<int2> tl = tv_sandwich1_active_tiles(h->G);
                     h->ntiles = (int)tl.size();
@@ -1669,8 +1715,14 @@ static vsr_tv* tv_build(vsr_ctx* ctx, const Spec& sp, const double* y_dev, const
             throw std::invalid_argument("admm_tv: unknown init mode");
         }
         // u0 = L x0, dual0 = 0 (:356-358) -> theta for iteration 1; TV(x0)
-        launch_tv_stencil(hr, true, h->x.p, nullptr, h->dualA.p, h->theta.p, h->lambda / h->mu,
-                          nullptr, h->stp.p, st);
+        if (h->f32) {
+            launch_narrow(h->x.p, h->xf.p, N, st);
+            launch_tv_stencil_f32(hr, true, h->xf.p, nullptr, h->dualAf.p, h->thetaf.p, h->lambda / h->mu, nullptr,
+                                  h->stp.p, st);
+        } else {
+            launch_tv_stencil(hr, true, h->x.p, nullptr, h->dualA.p, h->theta.p, h->lambda / h->mu,
+                              nullptr, h->stp.p, st);
+        }
         // initial objective (:361): data term by LR Parseval from fft3(x0)
         fft_engine().forward3(hr, h->x.p, IN_REAL, h->W.p, inv_sqrt_count(hr), st);
         ++g_fwd;
@@ -1678,6 +1730,11 @@ static vsr_tv* tv_build(vsr_ctx* ctx, const Spec& sp, const double* y_dev, const
         TvIterScalars sc{h->obj.p, h->res.p, h->rel.p, h->status.p};
         launch_tv_finalize(0, h->fitp.p, fit_blocks(h->G), h->stp.p, h->st_blocks, nullptr, 0,
                            h->lambda, 1e-8, sc, h->init_obj.p, st);
+        if (h->f32) {  // the fp64 spectra served the setup only
+            sync(ctx);
+            h->W.release();
+            h->lam.release();
+        }
     } catch (...) {
         delete h;
         throw;
@@ -1700,6 +1757,8 @@ static void tv_join(vsr_tv* h) {
     }
 }
 
+static void tv_finalize_step(vsr_tv* h, Profiler* prof, bool a1, bool half, cudaStream_t st);
+
 static void tv_step(vsr_tv* h) {
     cudaStream_t st = h->ctx->stream;
     const Dims& hr = h->sp.hr;
@@ -1712,6 +1771,48 @@ static void tv_step(vsr_tv* h) {
     // Hermitian half spectrum along axis 3 (theta is real): planes 0..s/2 only
     const bool half = a1 && tv_half(hr);
     const Dims hrh{hr.m, hr.n, hr.s / 2 + 1};
+    if (h->f32) {  // fp32 mode: the half-spectrum route on fp32 state (tv_build checked the geometry)
+        tabs.half3 = 1;
+        tabs.tiles = h->tiles.p;
+        tabs.ntiles = h->ntiles;
+        {
+            ProfScope ps(prof, "fft_fwd_axis3_r2c_half", st);
+            fft_engine().r2c_axis3_half_f(hr, h->thetaf.p, h->Wf.p, st);
+        }
+        {
+            ProfScope ps(prof, "fft_fwd_axis2_half", st);
+            fft_engine().axis_pass_cf(hrh, 1, false, h->Wf.p, st);
+        }
+        tv_join(h);
+        {
+            ProfScope ps(prof, "tv_fft1_fold_ifft1_half", st);
+            if (!tv_sandwich_pipe_f32(h->G, h->Yl.p, h->sep.t, h->Wf.p, h->W2f.p, tabs, h->mu, h->mu * (double)h->G.d,
+                                      1.0 / h->mu, s, h->fitp.p, st))
+                throw std::logic_error("admm_tv fp32: sandwich geometry");
+        }
+        if (h->rel_tol > 0.0) std::swap(h->xf, h->xprevf);  // x_prev = x (:364)
+        PassReduce red{h->resp.p, h->bad.p};
+        {
+            ProfScope ps(prof, "fft_inv_axis2_half", st);
+            fft_engine().axis_pass_cf(hrh, 1, true, h->W2f.p, st);
+        }
+        {
+            ProfScope ps(prof, "fft_inv_axis3_c2r_half", st);
+            fft_engine().c2r_axis3_half_f(hr, h->W2f.p, h->xf.p, s, &red, st);
+        }
+        g_fwd += 1;
+        g_inv += 1;
+        float* din = h->dual_in_a ? h->dualAf.p : h->dualBf.p;
+        float* dout = h->dual_in_a ? h->dualBf.p : h->dualAf.p;
+        {
+            ProfScope ps(prof, "tv_stencil", st);
+            launch_tv_stencil_f32(hr, false, h->xf.p, din, dout, h->thetaf.p, h->lambda / h->mu,
+                                  h->rel_tol > 0.0 ? h->xprevf.p : nullptr, h->stp.p, st);
+        }
+        h->dual_in_a = !h->dual_in_a;
+        tv_finalize_step(h, prof, true, true, st);
+        return;
+    }
     if (half) {
         tabs.half3 = 1;
         tabs.tiles = h->ntiles ? h->tiles.p : nullptr;
@@ -1781,6 +1882,14 @@ static void tv_step(vsr_tv* h) {
                           h->rel_tol > 0.0 ? h->xprev.p : nullptr, h->stp.p, st);
     }
     h->dual_in_a = !h->dual_in_a;
+    tv_finalize_step(h, prof, a1, half, st);
+}
+
+// the iteration's scalar finalize (objective, residual, rel change, residue
+// status), on a side stream for fixed-count runs
+static void tv_finalize_step(vsr_tv* h, Profiler* prof, bool a1, bool half, cudaStream_t st) {
+    const Dims& hr = h->sp.hr;
+    const bool fused = use_fused(h->G);
     TvIterScalars sc{h->obj.p, h->res.p, h->rel.p, h->status.p, h->iter_dev.p};
     const bool side = h->rel_tol <= 0.0 && prof == nullptr;
     if (side) {
@@ -1873,6 +1982,12 @@ static void tv_iterate(vsr_tv* h, size_t iters) {
         }
     }
     tv_join(h);  // report readers on the main stream see the last iteration's scalars
+}
+
+// the iterate as fp64 (fp32 mode: widened on the stream into the fp64 x buffer)
+static const double* tv_x_fp64(vsr_tv* h) {
+    if (h->f32) launch_widen(h->xf.p, h->x.p, h->x.n, h->ctx->stream);
+    return h->x.p;
 }
 
 static void tv_fill_report(vsr_tv* h, vsr_report* rep, const char* where) {
@@ -2021,7 +2136,7 @@ int vsr_admm_tv(vsr_ctx* ctx, const size_t hr_dims[3], const size_t rates[3], co
         try {
             tv_iterate(h, h->max_iters);
             tv_fill_report(h, report, "admm_tv");
-            d2h(ctx, x_r, h->x.p, h->x.bytes());
+            d2h(ctx, x_r, tv_x_fp64(h), h->x.bytes());
             sync(ctx);
             if (report) report->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - h->t0).count();
         } catch (...) {
@@ -2053,7 +2168,17 @@ int vsr_tv_iterate_d(vsr_tv* h, size_t iters) {
 }
 
 int vsr_tv_x_d(vsr_tv* h, const double** x_dev) {
-    return guarded([&] { *x_dev = h->x.p; });
+    return guarded([&] {
+        vsr_ctx::Guard g(h->ctx->device);
+        *x_dev = tv_x_fp64(h);
+    });
+}
+
+int vsr_tv_x_f32_d(vsr_tv* h, const float** x_dev) {
+    return guarded([&] {
+        if (!h->f32) throw std::invalid_argument("admm_tv: not an fp32-mode handle");
+        *x_dev = h->xf.p;
+    });
 }
 
 int vsr_tv_report(vsr_tv* h, vsr_report* report) {

@@ -7,6 +7,7 @@
 //   * ifft3_real reduces sum(imag^2) and sum(|z|^2) for the residue check (:84-93).
 #include <climits>
 #include <cmath>
+#include <type_traits>
 
 #include "fft.cuh"
 #include "fft_core.cuh"
@@ -43,14 +44,16 @@ struct PassShape {
     }
 };
 
-template <int L, int R, int T, int TG, bool CONTIG, bool INV, int IK, int OK>
+template <int L, int R, int T, int TG, bool CONTIG, bool INV, int IK, int OK, class C = double2>
 __global__ void __launch_bounds__(PassShape<L, R, T, TG, CONTIG>::THREADS)
     fft_pass_kernel(const void* in_, void* out_, long long S,
-                    long long nlines_or_tiles, const double2* __restrict__ tw, double scale,
+                    long long nlines_or_tiles, const C* __restrict__ tw, double scale,
                     double* __restrict__ partials, unsigned long long* __restrict__ bad_index) {
     using Sh = PassShape<L, R, T, TG, CONTIG>;
+    using RT = typename CplxT<C>::real;
     constexpr int P = Sh::P;
-    extern __shared__ double2 sm[];
+    extern __shared__ double2 sm_raw[];
+    C* sm = reinterpret_cast<C*>(sm_raw);
 
     const int tid = threadIdx.x;
     int ls, t;  // line slot in CTA, thread index within its line
@@ -79,29 +82,29 @@ __global__ void __launch_bounds__(PassShape<L, R, T, TG, CONTIG>::THREADS)
         estride = S;
     }
 
-    double2 v[R];
+    C v[R];
     // ---- load: first stage (radix R, Ns = 1) reads q = t + P * r
     if (active) {
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             const long long off = base + estride * (long long)(t + P * r);
             if constexpr (IK == IN_REAL) {
-                v[r] = make_double2(reinterpret_cast<const double*>(in_)[off], 0.0);
+                v[r] = cmake<C>(reinterpret_cast<const RT*>(in_)[off], (RT)0);
             } else if constexpr (IK == IN_HALF) {
                 const int q = t + P * r;
                 if (q <= L / 2) {
-                    v[r] = reinterpret_cast<const double2*>(in_)[off];
+                    v[r] = reinterpret_cast<const C*>(in_)[off];
                 } else {
-                    const double2 h = reinterpret_cast<const double2*>(in_)[base + estride * (long long)(L - q)];
-                    v[r] = make_double2(h.x, -h.y);
+                    const C h = reinterpret_cast<const C*>(in_)[base + estride * (long long)(L - q)];
+                    v[r] = cmake<C>(h.x, -h.y);
                 }
             } else {
-                v[r] = reinterpret_cast<const double2*>(in_)[off];
+                v[r] = reinterpret_cast<const C*>(in_)[off];
             }
         }
     } else {
 #pragma unroll
-        for (int r = 0; r < R; ++r) v[r] = make_double2(0.0, 0.0);
+        for (int r = 0; r < R; ++r) v[r] = cmake<C>((RT)0, (RT)0);
     }
 
     fftc::stockham<L, INV>(v, t, sm, [&](int q) { return Sh::sidx(ls, q); }, tw);
@@ -113,16 +116,16 @@ __global__ void __launch_bounds__(PassShape<L, R, T, TG, CONTIG>::THREADS)
         for (int j = 0; j < R; ++j) {
             const int q = fftc::Plan<L>::out_q(t, j);
             const long long off = base + estride * (long long)q;
-            const double2 z = cscale(v[j], scale);
+            const C z = cscale(v[j], (RT)scale);
             if constexpr (OK == OUT_REAL) {
-                acc_im += z.y * z.y;
-                acc_tot += z.x * z.x + z.y * z.y;
-                reinterpret_cast<double*>(out_)[off] = z.x;
+                acc_im += (double)z.y * z.y;
+                acc_tot += (double)z.x * z.x + (double)z.y * z.y;
+                reinterpret_cast<RT*>(out_)[off] = z.x;
                 if (!isfinite(z.x)) atomicMin(bad_index, (unsigned long long)off);
             } else if constexpr (OK == OUT_HALF) {
-                if (q <= L / 2) reinterpret_cast<double2*>(out_)[off] = z;
+                if (q <= L / 2) reinterpret_cast<C*>(out_)[off] = z;
             } else {
-                reinterpret_cast<double2*>(out_)[off] = z;
+                reinterpret_cast<C*>(out_)[off] = z;
             }
         }
     }
@@ -159,80 +162,89 @@ struct RPairShape {
     static constexpr int SMEM = TG * TP * L;
 };
 
-template <int L>
+template <int L, class C = double2>
 __global__ void __launch_bounds__(RPairShape<L>::THREADS)
-    rpair_fwd_kernel(const double* __restrict__ in, double2* __restrict__ out, long long S, long long tiles,
-                     const double2* __restrict__ tw, RemotePlanes rp) {
+    rpair_fwd_kernel(const typename CplxT<C>::real* __restrict__ in, C* __restrict__ out, long long S,
+                     long long tiles, const C* __restrict__ tw, RemotePlanes rp) {
     using Sh = RPairShape<L>;
+    using RT = typename CplxT<C>::real;
     constexpr int R = Sh::R, P = Sh::P, T = Sh::T, TP = Sh::TP;
-    extern __shared__ double2 sm[];
+    extern __shared__ double2 sm_raw[];
+    C* sm = reinterpret_cast<C*>(sm_raw);
     const int tid = threadIdx.x, g = tid / (TP * P), rem = tid % (TP * P), lp = rem % TP, t = rem / TP;
     const long long tile = (long long)blockIdx.x * Sh::TG + g;
     const bool active = tile < tiles;
     const long long tpo = S / T, o = active ? tile / tpo : 0, c = active ? (tile % tpo) * T + 2 * lp : 0;
     auto sidx = [&](int q) { return g * (L * TP) + q * TP + lp; };
-    const double2* src = reinterpret_cast<const double2*>(in + c + S * (long long)L * o);
+    const C* src = reinterpret_cast<const C*>(in + c + S * (long long)L * o);
     const long long S2 = S / 2;
-    double2 v[R];
+    C v[R];
 #pragma unroll
-    for (int r = 0; r < R; ++r) v[r] = active ? __ldg(src + S2 * (t + P * r)) : make_double2(0.0, 0.0);
+    for (int r = 0; r < R; ++r) v[r] = active ? __ldg(src + S2 * (t + P * r)) : cmake<C>((RT)0, (RT)0);
     fftc::stockham<L, false>(v, t, sm, sidx, tw);
     __syncthreads();
 #pragma unroll
     for (int j = 0; j < R; ++j) sm[sidx(fftc::Plan<L>::out_q(t, j))] = v[j];
     __syncthreads();
-    double2* dst = out + c + S * (long long)(L / 2 + 1) * o;
+    C* dst = out + c + S * (long long)(L / 2 + 1) * o;
+    const RT half = (RT)0.5;
 #pragma unroll
     for (int j = 0; j < R; ++j) {
         const int k = t + P * j;
         if (k > L / 2 || !active) continue;
-        const double2 a = sm[sidx(k)], b = sm[sidx((L - k) & (L - 1))];
-        const double2 xa = make_double2(0.5 * (a.x + b.x), 0.5 * (a.y - b.y));
-        const double2 xb = make_double2(0.5 * (a.y + b.y), -0.5 * (a.x - b.x));
+        const C a = sm[sidx(k)], b = sm[sidx((L - k) & (L - 1))];
+        const C xa = cmake<C>(half * (a.x + b.x), half * (a.y - b.y));
+        const C xb = cmake<C>(half * (a.y + b.y), -half * (a.x - b.x));
         // slab-sharded: plane k goes straight to its owner's spectral buffer
-        // (peer memory over NVLink), rows of this rank's y range
-        double2* d = rp.peer ? rp.peer[rp.owner[k]] + rp.off[k] + c : dst + S * k;
+        // (peer memory over NVLink), rows of this rank's y range (fp64 only)
+        C* d = dst + S * k;
+        if constexpr (std::is_same<C, double2>::value)
+            if (rp.peer) d = rp.peer[rp.owner[k]] + rp.off[k] + c;
         d[0] = xa;
         d[1] = xb;
     }
     if (rp.peer) __threadfence_system();
 }
 
-template <int L>
+template <int L, class C = double2>
 __global__ void __launch_bounds__(RPairShape<L>::THREADS)
-    rpair_inv_kernel(const double2* __restrict__ in, double* __restrict__ out, long long S, long long tiles,
-                     const double2* __restrict__ tw, double scale, double* __restrict__ partials,
+    rpair_inv_kernel(const C* __restrict__ in, typename CplxT<C>::real* __restrict__ out, long long S,
+                     long long tiles, const C* __restrict__ tw, double scale, double* __restrict__ partials,
                      unsigned long long* __restrict__ bad_index, RemotePlanes rp) {
     using Sh = RPairShape<L>;
+    using RT = typename CplxT<C>::real;
     constexpr int R = Sh::R, P = Sh::P, T = Sh::T, TP = Sh::TP;
-    extern __shared__ double2 sm[];
+    extern __shared__ double2 sm_raw[];
+    C* sm = reinterpret_cast<C*>(sm_raw);
     const int tid = threadIdx.x, g = tid / (TP * P), rem = tid % (TP * P), lp = rem % TP, t = rem / TP;
     const long long tile = (long long)blockIdx.x * Sh::TG + g;
     const bool active = tile < tiles;
     const long long tpo = S / T, o = active ? tile / tpo : 0, c = active ? (tile % tpo) * T + 2 * lp : 0;
     auto sidx = [&](int q) { return g * (L * TP) + q * TP + lp; };
-    const double2* src = in + c + S * (long long)(L / 2 + 1) * o;
-    double2 v[R];
+    const C* src = in + c + S * (long long)(L / 2 + 1) * o;
+    C v[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
         const int q = t + P * r;
         const bool lo = q <= L / 2;
         const int pq = lo ? q : L - q;
-        const double2* p = rp.peer ? rp.peer[rp.owner[pq]] + rp.off[pq] + c : src + S * pq;
-        double2 A = active ? __ldg(p) : make_double2(0.0, 0.0), B = active ? __ldg(p + 1) : make_double2(0.0, 0.0);
+        const C* p = src + S * pq;
+        if constexpr (std::is_same<C, double2>::value)
+            if (rp.peer) p = rp.peer[rp.owner[pq]] + rp.off[pq] + c;
+        C A = active ? __ldg(p) : cmake<C>((RT)0, (RT)0), B = active ? __ldg(p + 1) : cmake<C>((RT)0, (RT)0);
         if (!lo) A.y = -A.y, B.y = -B.y;
-        v[r] = make_double2(A.x - B.y, A.y + B.x);  // A + i B
+        v[r] = cmake<C>(A.x - B.y, A.y + B.x);  // A + i B
     }
     fftc::stockham<L, true>(v, t, sm, sidx, tw);
-    double2* dst = reinterpret_cast<double2*>(out + c + S * (long long)L * o);
+    C* dst = reinterpret_cast<C*>(out + c + S * (long long)L * o);
     const long long S2 = S / 2;
     double acc = 0.0;
 #pragma unroll
     for (int j = 0; j < R; ++j) {
         const int q = fftc::Plan<L>::out_q(t, j);
-        const double2 z = cscale(v[j], scale);
+        const C z = cscale(v[j], (RT)scale);
         if (!active) continue;
-        acc += z.x * z.x + z.y * z.y;
+        acc += (double)z.x * z.x + (double)z.y * z.y;
         dst[S2 * q] = z;
         if (!isfinite(z.x) || !isfinite(z.y)) {
             const unsigned long long e = (unsigned long long)(c + S * (long long)L * o + S * (long long)q);
@@ -250,40 +262,41 @@ __global__ void __launch_bounds__(RPairShape<L>::THREADS)
     }
 }
 
-template <int L>
-bool launch_rpair(bool fwd, const void* in, void* out, long long S, long long total, const double2* tw,
+template <int L, class C>
+bool launch_rpair(bool fwd, const void* in, void* out, long long S, long long total, const C* tw,
                   double scale, const PassReduce* red, cudaStream_t st, const RemotePlanes& rp) {
     using Sh = RPairShape<L>;
+    using RT = typename CplxT<C>::real;
     const long long tiles = total / ((long long)Sh::T * L);
     const unsigned blocks = (unsigned)((tiles + Sh::TG - 1) / Sh::TG);
-    const size_t smem = (size_t)Sh::SMEM * sizeof(double2);
+    const size_t smem = (size_t)Sh::SMEM * sizeof(C);
     if (fwd) {
-        auto kern = rpair_fwd_kernel<L>;
+        auto kern = rpair_fwd_kernel<L, C>;
         if (smem > 48 * 1024) VSR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        kern<<<blocks, Sh::THREADS, smem, st>>>(static_cast<const double*>(in), static_cast<double2*>(out), S,
-                                                       tiles, tw, rp);
+        kern<<<blocks, Sh::THREADS, smem, st>>>(static_cast<const RT*>(in), static_cast<C*>(out), S, tiles, tw, rp);
     } else {
-        auto kern = rpair_inv_kernel<L>;
+        auto kern = rpair_inv_kernel<L, C>;
         if (smem > 48 * 1024) VSR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        kern<<<blocks, Sh::THREADS, smem, st>>>(static_cast<const double2*>(in), static_cast<double*>(out), S,
-                                                       tiles, tw, scale, red ? red->partials : nullptr,
-                                                       red ? red->bad_index : nullptr, rp);
+        kern<<<blocks, Sh::THREADS, smem, st>>>(static_cast<const C*>(in), static_cast<RT*>(out), S, tiles, tw,
+                                                scale, red ? red->partials : nullptr,
+                                                red ? red->bad_index : nullptr, rp);
     }
     VSR_LAUNCH_CHECK();
     return true;
 }
 
-bool dispatch_rpair(bool fwd, size_t L, const void* in, void* out, long long S, long long total, const double2* tw,
+template <class C>
+bool dispatch_rpair(bool fwd, size_t L, const void* in, void* out, long long S, long long total, const C* tw,
                     double scale, const PassReduce* red, cudaStream_t st, const RemotePlanes& rp = RemotePlanes{}) {
     switch (L) {
-        case 8: return launch_rpair<8>(fwd, in, out, S, total, tw, scale, red, st, rp);
-        case 16: return launch_rpair<16>(fwd, in, out, S, total, tw, scale, red, st, rp);
-        case 32: return launch_rpair<32>(fwd, in, out, S, total, tw, scale, red, st, rp);
-        case 64: return launch_rpair<64>(fwd, in, out, S, total, tw, scale, red, st, rp);
-        case 128: return launch_rpair<128>(fwd, in, out, S, total, tw, scale, red, st, rp);
-        case 256: return launch_rpair<256>(fwd, in, out, S, total, tw, scale, red, st, rp);
-        case 512: return launch_rpair<512>(fwd, in, out, S, total, tw, scale, red, st, rp);
-        case 1024: return launch_rpair<1024>(fwd, in, out, S, total, tw, scale, red, st, rp);
+        case 8: return launch_rpair<8, C>(fwd, in, out, S, total, tw, scale, red, st, rp);
+        case 16: return launch_rpair<16, C>(fwd, in, out, S, total, tw, scale, red, st, rp);
+        case 32: return launch_rpair<32, C>(fwd, in, out, S, total, tw, scale, red, st, rp);
+        case 64: return launch_rpair<64, C>(fwd, in, out, S, total, tw, scale, red, st, rp);
+        case 128: return launch_rpair<128, C>(fwd, in, out, S, total, tw, scale, red, st, rp);
+        case 256: return launch_rpair<256, C>(fwd, in, out, S, total, tw, scale, red, st, rp);
+        case 512: return launch_rpair<512, C>(fwd, in, out, S, total, tw, scale, red, st, rp);
+        case 1024: return launch_rpair<1024, C>(fwd, in, out, S, total, tw, scale, red, st, rp);
         default: return false;
     }
 }
@@ -363,7 +376,7 @@ struct Launch {
     size_t smem;
 };
 
-template <int L, bool CONTIG>
+template <int L, bool CONTIG, class CT = double2>
 Launch pass_geometry(long long S, long long lines_or_tiles) {
     using C = LCfg<L>;
     constexpr int T = CONTIG ? 1 : C::TS;
@@ -372,18 +385,18 @@ Launch pass_geometry(long long S, long long lines_or_tiles) {
     Launch g;
     g.block = dim3(Sh::THREADS);
     g.grid = dim3((unsigned)((lines_or_tiles + TG - 1) / TG));
-    g.smem = (size_t)Sh::SMEM_ELEMS * sizeof(double2);
+    g.smem = (size_t)Sh::SMEM_ELEMS * sizeof(CT);
     return g;
 }
 
-template <int L, bool CONTIG, bool INV, int IK, int OK>
-void launch_pass(long long S, long long units, const void* in, void* out, const double2* tw,
+template <int L, bool CONTIG, bool INV, int IK, int OK, class CT = double2>
+void launch_pass(long long S, long long units, const void* in, void* out, const CT* tw,
                  double scale, const PassReduce* red, cudaStream_t st) {
     using C = LCfg<L>;
     constexpr int T = CONTIG ? 1 : C::TS;
     constexpr int TG = CONTIG ? C::TGC : C::TGS;
-    auto kern = fft_pass_kernel<L, C::R, T, TG, CONTIG, INV, IK, OK>;
-    Launch g = pass_geometry<L, CONTIG>(S, units);
+    auto kern = fft_pass_kernel<L, C::R, T, TG, CONTIG, INV, IK, OK, CT>;
+    Launch g = pass_geometry<L, CONTIG, CT>(S, units);
     if (g.smem > 48 * 1024) {
         VSR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)g.smem));
@@ -394,13 +407,13 @@ void launch_pass(long long S, long long units, const void* in, void* out, const 
     VSR_LAUNCH_CHECK();
 }
 
-template <bool CONTIG, bool INV, int IK, int OK>
+template <bool CONTIG, bool INV, int IK, int OK, class CT = double2>
 bool dispatch_L(size_t L, long long S, long long units, const void* in, void* out,
-                const double2* tw, double scale, const PassReduce* red, cudaStream_t st) {
+                const CT* tw, double scale, const PassReduce* red, cudaStream_t st) {
     switch (L) {
 #define VSR_CASE(LL)                                                                       \
     case LL:                                                                               \
-        launch_pass<LL, CONTIG, INV, IK, OK>(S, units, in, out, tw, scale, red, st);       \
+        launch_pass<LL, CONTIG, INV, IK, OK, CT>(S, units, in, out, tw, scale, red, st);   \
         return true;
         VSR_CASE(2)
         VSR_CASE(4)
@@ -470,6 +483,26 @@ const double2* FftEngine::twiddles(size_t L) {
     VSR_CUDA(cudaMalloc(&d, L * sizeof(double2)));
     VSR_CUDA(cudaMemcpy(d, h.data(), L * sizeof(double2), cudaMemcpyHostToDevice));
     tw_[key] = d;
+    return d;
+}
+
+const float2* FftEngine::twiddles_f(size_t L) {
+    int dev = 0;
+    VSR_CUDA(cudaGetDevice(&dev));
+    const size_t key = ((size_t)dev << 40) | L;
+    std::lock_guard<std::mutex> lock(mu_);
+    auto it = twf_.find(key);
+    if (it != twf_.end()) return it->second;
+    std::vector<float2> h(L);
+    for (size_t j = 0; j < L; ++j) {
+        const long double ang = 2.0L * 3.141592653589793238462643383279502884L *
+                                (long double)j / (long double)L;
+        h[j] = make_float2((float)cosl(ang), (float)-sinl(ang));
+    }
+    float2* d = nullptr;
+    VSR_CUDA(cudaMalloc(&d, L * sizeof(float2)));
+    VSR_CUDA(cudaMemcpy(d, h.data(), L * sizeof(float2), cudaMemcpyHostToDevice));
+    twf_[key] = d;
     return d;
 }
 
@@ -601,6 +634,40 @@ void FftEngine::c2r_axis3_half(const Dims& d, const double2* in, double* out, do
     axis_geometry(d, 2, S, L, total);
     if (!half3_ok(d)) throw std::logic_error("c2r_axis3_half: unsupported geometry");
     if (!dispatch_rpair(false, (size_t)L, in, out, S, total, twiddles((size_t)L), scale, red, st))
+        throw std::logic_error("c2r_axis3_half: unsupported length");
+}
+
+// ---- fp32 mode (float2 spectra, fp32 arithmetic): the half-spectrum passes of
+// the ADMM-TV iteration
+void FftEngine::axis_pass_cf(const Dims& d, int axis, bool inverse, float2* inout, cudaStream_t st) {
+    long long S, L, total;
+    axis_geometry(d, axis, S, L, total);
+    if (total == 0) return;
+    if (axis == 0 || !tiled_ok((size_t)L, axis, S)) throw std::logic_error("fp32 axis pass: unsupported geometry");
+    const long long units = pass_units<false>(L, S, total);
+    const float2* tw = twiddles_f((size_t)L);
+    const bool done =
+        inverse ? dispatch_L<false, true, IN_COMPLEX, OUT_COMPLEX, float2>(L, S, units, inout, inout, tw, 1.0,
+                                                                          nullptr, st)
+                : dispatch_L<false, false, IN_COMPLEX, OUT_COMPLEX, float2>(L, S, units, inout, inout, tw, 1.0,
+                                                                           nullptr, st);
+    if (!done) throw std::logic_error("fp32 axis pass: unsupported length");
+}
+
+void FftEngine::r2c_axis3_half_f(const Dims& d, const float* in, float2* out, cudaStream_t st) {
+    long long S, L, total;
+    axis_geometry(d, 2, S, L, total);
+    if (!half3_ok(d)) throw std::logic_error("r2c_axis3_half: unsupported geometry");
+    if (!dispatch_rpair<float2>(true, (size_t)L, in, out, S, total, twiddles_f((size_t)L), 1.0, nullptr, st))
+        throw std::logic_error("r2c_axis3_half: unsupported length");
+}
+
+void FftEngine::c2r_axis3_half_f(const Dims& d, const float2* in, float* out, double scale, const PassReduce* red,
+                                 cudaStream_t st) {
+    long long S, L, total;
+    axis_geometry(d, 2, S, L, total);
+    if (!half3_ok(d)) throw std::logic_error("c2r_axis3_half: unsupported geometry");
+    if (!dispatch_rpair<float2>(false, (size_t)L, in, out, S, total, twiddles_f((size_t)L), scale, red, st))
         throw std::logic_error("c2r_axis3_half: unsupported length");
 }
 

@@ -89,9 +89,18 @@ public:
     // Blocks of the final (axis-1) pass of inverse3.
     size_t inverse_final_blocks(const Dims& d) const { return pass_blocks(d, 0); }
 
+    // ---- fp32 mode: float2 twiddles, the strided complex pass in place, and
+    // the half-spectrum r2c / c2r along axis 3 (fp32 arithmetic)
+    const float2* twiddles_f(size_t L);
+    void axis_pass_cf(const Dims& d, int axis, bool inverse, float2* inout, cudaStream_t st);
+    void r2c_axis3_half_f(const Dims& d, const float* in, float2* out, cudaStream_t st);
+    void c2r_axis3_half_f(const Dims& d, const float2* in, float* out, double scale, const PassReduce* red,
+                          cudaStream_t st);
+
 private:
     std::mutex mu_;
     std::map<size_t, double2*> tw_;
+    std::map<size_t, float2*> twf_;
 };
 
 FftEngine& fft_engine();

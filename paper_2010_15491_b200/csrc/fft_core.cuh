@@ -24,21 +24,22 @@ __device__ constexpr double kC8[8] = {1.0,
                                       0.19509032201612828};
 
 // exp(-+2 pi i k / 32) * v, k in [0, 16); k is a compile-time constant after
-// unrolling so every branch folds away.
-template <bool INV>
-__device__ __forceinline__ double2 twiddle32(double2 v, int k) {
+// unrolling so every branch folds away.  C = double2 or float2 (fp32 mode).
+template <bool INV, class C>
+__device__ __forceinline__ C twiddle32(C v, int k) {
+    using T = typename CplxT<C>::real;
     if (k == 0) return v;
-    if (k == 8) return INV ? make_double2(-v.y, v.x) : make_double2(v.y, -v.x);
-    double c, s;  // cos, sin of 2*pi*k/32
+    if (k == 8) return INV ? cmake<C>(-v.y, v.x) : cmake<C>(v.y, -v.x);
+    T c, s;  // cos, sin of 2*pi*k/32
     if (k < 8) {
-        c = kC8[k];
-        s = kC8[8 - k];
+        c = (T)kC8[k];
+        s = (T)kC8[8 - k];
     } else {
-        c = -kC8[16 - k];
-        s = kC8[k - 8];
+        c = -(T)kC8[16 - k];
+        s = (T)kC8[k - 8];
     }
-    if (INV) return make_double2(v.x * c - v.y * s, v.y * c + v.x * s);
-    return make_double2(v.x * c + v.y * s, v.y * c - v.x * s);
+    if (INV) return cmake<C>(v.x * c - v.y * s, v.y * c + v.x * s);
+    return cmake<C>(v.x * c + v.y * s, v.y * c - v.x * s);
 }
 
 template <int R>
@@ -52,10 +53,10 @@ __host__ __device__ constexpr int bitrev(int i) {
 }
 
 // In-register radix-R DFT (R = 1..32, power of two), natural order in/out.
-template <int R, bool INV>
-__device__ __forceinline__ void dft_reg(double2* a) {
+template <int R, bool INV, class C>
+__device__ __forceinline__ void dft_reg(C* a) {
     if constexpr (R > 1) {
-        double2 b[R];
+        C b[R];
 #pragma unroll
         for (int i = 0; i < R; ++i) b[bitrev<R>(i)] = a[i];
 #pragma unroll
@@ -64,8 +65,8 @@ __device__ __forceinline__ void dft_reg(double2* a) {
             for (int i = 0; i < R; i += 2 * h) {
 #pragma unroll
                 for (int j = 0; j < h; ++j) {
-                    const double2 u = b[i + j];
-                    const double2 t = twiddle32<INV>(b[i + j + h], j * (16 / h));
+                    const C u = b[i + j];
+                    const C t = twiddle32<INV>(b[i + j + h], j * (16 / h));
                     b[i + j] = cadd(u, t);
                     b[i + j + h] = csub(u, t);
                 }
@@ -86,11 +87,14 @@ struct CtaSync {
 
 // Twiddle table access: a global table through the read-only path, or a
 // copy in shared memory (TwShared).
+template <class C = double2>
 struct TwShared {
-    const double2* p;
+    const C* p;
 };
 __device__ __forceinline__ double2 tw_at(const double2* __restrict__ p, int i) { return __ldg(p + i); }
-__device__ __forceinline__ double2 tw_at(const TwShared& s, int i) { return s.p[i]; }
+__device__ __forceinline__ float2 tw_at(const float2* __restrict__ p, int i) { return __ldg(p + i); }
+template <class C>
+__device__ __forceinline__ C tw_at(const TwShared<C>& s, int i) { return s.p[i]; }
 
 template <int L, int RMAX = 16>
 struct Plan {
@@ -111,9 +115,8 @@ struct Plan {
 
 // Full line transform.  All threads of the CTA must call it (it syncs when
 // NSTAGE > 1).  sidx(q) maps a line position to this thread's line slot in sm.
-template <int L, bool INV, class SIdx, int RMAX = 16, class Sync = CtaSync, class Tw = const double2*>
-__device__ __forceinline__ void stockham(double2* v, int t, double2* sm, const SIdx& sidx, Tw tw,
-                                         const Sync& sync = Sync()) {
+template <int L, bool INV, class SIdx, int RMAX = 16, class Sync = CtaSync, class Tw = const double2*, class C>
+__device__ __forceinline__ void stockham(C* v, int t, C* sm, const SIdx& sidx, Tw tw, const Sync& sync = Sync()) {
     using Pl = Plan<L, RMAX>;
     constexpr int R = Pl::R, P = Pl::P;
     int Ns = 1;
@@ -131,8 +134,8 @@ __device__ __forceinline__ void stockham(double2* v, int t, double2* sm, const S
 #pragma unroll
                 for (int r = 1; r < R; ++r) {
                     if (r < RS) {
-                        const double2 w = tw_at(tw, (r * k * tstride) & (L - 1));
-                        const double2 a = v[vv * RS + r];
+                        const C w = tw_at(tw, (r * k * tstride) & (L - 1));
+                        const C a = v[vv * RS + r];
                         v[vv * RS + r] = INV ? cmulc(w, a) : cmul(w, a);
                     }
                 }
@@ -171,11 +174,11 @@ __device__ __forceinline__ void stockham(double2* v, int t, double2* sm, const S
 }
 
 // Output order -> natural order (v[k] = X[t + P k]); compile-time permutation.
-template <int L, int RMAX = 16>
-__device__ __forceinline__ void to_natural(double2* v) {
+template <int L, int RMAX = 16, class C>
+__device__ __forceinline__ void to_natural(C* v) {
     using Pl = Plan<L, RMAX>;
     if constexpr (Pl::RL > 1) {
-        double2 o[Pl::R];
+        C o[Pl::R];
 #pragma unroll
         for (int j = 0; j < Pl::R; ++j) o[(j / Pl::RSL) + Pl::NBL * (j % Pl::RSL)] = v[j];
 #pragma unroll

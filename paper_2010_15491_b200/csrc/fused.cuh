@@ -59,6 +59,13 @@ void launch_tv_sandwich1(const FoldGeom& G, const double2* Yl, const double2* la
 bool tv_sandwich_pipe(const FoldGeom& G, const double2* Yl, const SepTables& sep, const double2* W, double2* out,
                       const GammaTables& tabs, double cA, double shift, double inv_scale, double fwd_scale,
                       double* fit_partials, cudaStream_t st);
+// whether the pipelined sandwich covers the geometry (half spectrum, T = 1)
+bool tv_sandwich_pipe_ok(const FoldGeom& G);
+// fp32 mode: the same kernel on float2 rows, the transforms in fp32
+// arithmetic and the fold in fp64.  W / out are float2 half spectra.
+bool tv_sandwich_pipe_f32(const FoldGeom& G, const double2* Yl, const SepTables& sep, const float2* W, float2* out,
+                          const GammaTables& tabs, double cA, double shift, double inv_scale, double fwd_scale,
+                          double* fit_partials, cudaStream_t st);
 // The tiles (g2, g3) of the half-spectrum axis-1 sandwich that do work (one
 // of each conjugate pair of alias sets; tile = one LR (g2, g3)), g3-major.
 std::vector<int2> tv_sandwich1_active_tiles(const FoldGeom& G);

@@ -68,16 +68,18 @@ struct GroupSync {
     __device__ __forceinline__ void operator()() const { asm volatile("bar.sync %0, %1;" ::"r"(id), "n"(NT) : "memory"); }
 };
 
-template <int L, int A, int RM>
+template <int L, int A, int RM, class C = double2>
 struct SwShape {
     static constexpr int R = L < RM ? L : RM;
     static constexpr int P = L / R;          // threads per line
     static constexpr int GT = A * P;         // threads per group
     static constexpr int NG = 2;             // groups per CTA
     static constexpr int THREADS = NG * GT;
-    static constexpr int PITCH = L + 1;      // double2 units; bank-conflict free row <-> line-interleaved
+    // row pitch in elements: bank-conflict free row <-> line-interleaved, and
+    // every row start 16-B aligned for the bulk copies (float2: L + 2)
+    static constexpr int PITCH = sizeof(C) == 16 ? L + 1 : L + 2;
     static constexpr int NBUF = 3;
-    static constexpr size_t BUF = (size_t)A * PITCH * sizeof(double2);
+    static constexpr size_t BUF = (size_t)A * PITCH * sizeof(C);
     // the per-position tables a[f1], |e^{2 pi i f1/m} - 1|^2 stay in shared
     // memory unless the three buffers leave no room (L = 1024: read from L1)
     static constexpr bool TAB_SMEM = L <= 512;
@@ -87,7 +89,7 @@ struct SwShape {
     static constexpr size_t META = (size_t)NBUF * A * 80;  // LineMeta per line of each buffer
     // the twiddle table too, where it fits (L <= 512)
     static constexpr bool TW_SMEM = L <= 512;
-    static constexpr size_t TWB = TW_SMEM ? (size_t)L * sizeof(double2) : 0;
+    static constexpr size_t TWB = TW_SMEM ? (size_t)L * sizeof(C) : 0;
     static constexpr size_t SMEM = 64 + NBUF * BUF + META + TAB + TWB + NG * ROWS + NG * 32 * sizeof(double);
     static_assert(SMEM <= 232448, "shared memory budget");
 };
@@ -143,11 +145,11 @@ struct SwArgs {
     FoldGeom G;
     const double2* Yl;
     SepTables sep;
-    const double2* W;
-    double2* out;
+    const void* W;  // C rows (double2, or float2 in fp32 mode)
+    void* out;
     GammaTables tabs;
     double cA, shift, inv_scale, invsqrtd, fwd_scale;
-    const double2* tw;
+    const void* tw;  // C twiddles
     double* fit;
 };
 
@@ -167,9 +169,12 @@ __device__ __forceinline__ double group_sum(double v, double* red, int gt, int b
     return t;
 }
 
-template <int L, int A, int DR, int RM, bool FIT>
-__global__ void __launch_bounds__(SwShape<L, A, RM>::THREADS, 1) tv_sandwich_pipe_kernel(SwArgs args) {
-    using Sh = SwShape<L, A, RM>;
+// C = double2: the reference precision.  C = float2 (fp32 mode): rows and
+// the axis-1 transforms in fp32, the fold in fp64 (see the fold below).
+template <int L, int A, int DR, int RM, bool FIT, class C>
+__global__ void __launch_bounds__(SwShape<L, A, RM, C>::THREADS, 1) tv_sandwich_pipe_kernel(SwArgs args) {
+    using Sh = SwShape<L, A, RM, C>;
+    using RT = typename CplxT<C>::real;
     using Pl = fftc::Plan<L, RM>;
     constexpr int R = Pl::R, P = Pl::P, GT = Sh::GT, NLN = A;
     constexpr int RD = R / DR;  // r = rr + RD * br: alias br of g1 = t + P rr
@@ -177,7 +182,9 @@ __global__ void __launch_bounds__(SwShape<L, A, RM>::THREADS, 1) tv_sandwich_pip
     static_assert(R % DR == 0, "dr must divide the radix");
     static_assert(GT % 32 == 0, "a group is whole warps");
     static_assert(A <= 32, "one row per lane of the issuing warp");
-    constexpr unsigned ROWB = (unsigned)(L * sizeof(double2));
+    constexpr unsigned ROWB = (unsigned)(L * sizeof(C));
+    const C* __restrict__ Wc = static_cast<const C*>(args.W);
+    C* __restrict__ outc = static_cast<C*>(args.out);
     const FoldGeom& G = args.G;
     const GammaTables& tb = args.tabs;
 
@@ -188,14 +195,14 @@ __global__ void __launch_bounds__(SwShape<L, A, RM>::THREADS, 1) tv_sandwich_pip
     // tile k's rows have even landed)
     unsigned long long* full = reinterpret_cast<unsigned long long*>(smraw);
     unsigned long long* issued = full + 3;
-    double2* bufs = reinterpret_cast<double2*>(smraw + 64);
+    C* bufs = reinterpret_cast<C*>(smraw + 64);
     unsigned char* tail = smraw + 64 + Sh::NBUF * Sh::BUF;
     LineMeta* meta = reinterpret_cast<LineMeta*>(tail);
     tail += Sh::META;
     double2* sa_s = reinterpret_cast<double2*>(tail);
     double* nr_s = reinterpret_cast<double*>(sa_s + L);
     tail += Sh::TAB;
-    double2* tw_s = reinterpret_cast<double2*>(tail);
+    C* tw_s = reinterpret_cast<C*>(tail);
     tail += Sh::TWB;
     double* red_s = reinterpret_cast<double*>(tail);
     tail += Sh::NG * 32 * sizeof(double);
@@ -243,7 +250,7 @@ __global__ void __launch_bounds__(SwShape<L, A, RM>::THREADS, 1) tv_sandwich_pip
                          : "memory");
         __syncwarp();
         if (role != 2 && lane < A)
-            bulk_g2s(bufs + ((size_t)b * A + lane) * Sh::PITCH, args.W + meta[b * A + lane].rd, ROWB, full + b);
+            bulk_g2s(bufs + ((size_t)b * A + lane) * Sh::PITCH, Wc + meta[b * A + lane].rd, ROWB, full + b);
         if (lane == 0) {
             mbar_arrive(full + b);
             mbar_arrive(issued + b);
@@ -263,13 +270,13 @@ __global__ void __launch_bounds__(SwShape<L, A, RM>::THREADS, 1) tv_sandwich_pip
             nr_s[i] = __ldg(tb.nr + i);
         }
     if constexpr (Sh::TW_SMEM)
-        for (int i = tid; i < L; i += Sh::THREADS) tw_s[i] = __ldg(args.tw + i);
-    using TwT = std::conditional_t<Sh::TW_SMEM, fftc::TwShared, const double2*>;
+        for (int i = tid; i < L; i += Sh::THREADS) tw_s[i] = __ldg(static_cast<const C*>(args.tw) + i);
+    using TwT = std::conditional_t<Sh::TW_SMEM, fftc::TwShared<C>, const C*>;
     TwT twp;
     if constexpr (Sh::TW_SMEM)
-        twp = fftc::TwShared{tw_s};
+        twp = fftc::TwShared<C>{tw_s};
     else
-        twp = args.tw;
+        twp = static_cast<const C*>(args.tw);
     __syncthreads();
     if (tid < 32)
         for (int k = 0; k < Sh::NBUF; ++k) {
@@ -288,7 +295,7 @@ __global__ void __launch_bounds__(SwShape<L, A, RM>::THREADS, 1) tv_sandwich_pip
         const int tile = blockIdx.x + k * gridDim.x;
         if (tile >= ntiles) break;
         const int b = k % Sh::NBUF;
-        double2* sm = bufs + (size_t)b * A * Sh::PITCH;
+        C* sm = bufs + (size_t)b * A * Sh::PITCH;
         const LineMeta* mt = meta + b * A + ln;
         const int2 tt = __ldg(tiles + tile);
         const int role = tile_role(G, tt.x, tt.y);
@@ -304,7 +311,7 @@ __global__ void __launch_bounds__(SwShape<L, A, RM>::THREADS, 1) tv_sandwich_pip
         }
         mbar_wait(issued + b, (unsigned)((k / Sh::NBUF) & 1));
         mbar_wait(full + b, (unsigned)((k / Sh::NBUF) & 1));
-        double2 v[R];
+        C v[R];
         double tfit = 0.0;
         long long wr = -1, sec = -1;
         int flip = 0;
@@ -320,25 +327,31 @@ __global__ void __launch_bounds__(SwShape<L, A, RM>::THREADS, 1) tv_sandwich_pip
             fftc::stockham<L, false, decltype(sidx), RM, GroupSync<GT>, TwT>(v, t, sm, sidx, twp, gsync);
             fftc::to_natural<L, RM>(v);
             // fold: S = sum_b Lambda_b g_b, g_b = Gamma_b k_b; w = S / (Gw + mu d);
-            // x̂_b = (g_b - Gamma_b conj(Lambda_b) w) / mu; data fit from S and w
+            // x̂_b = (g_b - Gamma_b conj(Lambda_b) w) / mu; data fit from S and w.
+            // One LR position group rr of this thread, in arithmetic type T.
             const double2 bc_ = cmul(mt->b, mt->c);
             const double base_g = mt->nc + mt->ns;
-#pragma unroll
-            for (int rr = 0; rr < RD; ++rr) {
+            auto fold_rr = [&](auto zero, const int rr) {
+                using T = decltype(zero);
+                using CT = std::conditional_t<std::is_same<T, double>::value, double2, float2>;
                 const double2 yraw = yrow_s[t + P * rr];
                 const double gwv = gwrow_s[t + P * rr];
-                const double2 yv = cscale(yraw, args.invsqrtd);
-                double Gg[DR];
-                double2 Lr[DR];
-                double Sx = 0.0, Sy = 0.0;
+                const CT yv = from_d2<CT>(cscale(yraw, args.invsqrtd));
+                T Gg[DR];
+                CT Lr[DR], gv[DR];  // g_b kept in T between the two loops (it is up to 1/tau large)
+                T Sx = 0, Sy = 0;
 #pragma unroll
                 for (int br = 0; br < DR; ++br) {
                     const int r = rr + RD * br;
                     const int q = t + P * r;
-                    Lr[br] = cmul(sa_t[q], bc_);
-                    Gg[br] = rcp_pos((nr_t[q] + base_g) + tb.tau);
-                    v[r] = cscale(cadd(cmulc(Lr[br], yv), cscale(v[r], cAs)), Gg[br]);
-                    const double2 pr = cmul(Lr[br], v[r]);
+                    Lr[br] = from_d2<CT>(cmul(sa_t[q], bc_));
+                    if constexpr (std::is_same<T, double>::value)
+                        Gg[br] = rcp_pos((nr_t[q] + base_g) + tb.tau);
+                    else
+                        Gg[br] = __frcp_rn((float)((nr_t[q] + base_g) + tb.tau));
+                    const CT vr = from_d2<CT>(to_d2(v[r]));
+                    gv[br] = cscale(cadd(cmulc(Lr[br], yv), cscale(vr, (T)cAs)), Gg[br]);
+                    const CT pr = cmul(Lr[br], gv[br]);
                     Sx += pr.x;
                     Sy += pr.y;
                 }
@@ -347,23 +360,34 @@ __global__ void __launch_bounds__(SwShape<L, A, RM>::THREADS, 1) tv_sandwich_pip
                     Sx += __shfl_xor_sync(0xffffffffu, Sx, o);
                     Sy += __shfl_xor_sync(0xffffffffu, Sy, o);
                 }
-                const double iden = rcp_pos(gwv + args.shift);
-                const double2 w = make_double2(Sx * iden, Sy * iden);
+                T iden;
+                if constexpr (std::is_same<T, double>::value)
+                    iden = rcp_pos(gwv + args.shift);
+                else
+                    iden = __frcp_rn((float)(gwv + args.shift));
+                const CT w = cmake<CT>(Sx * iden, Sy * iden);
 #pragma unroll
                 for (int br = 0; br < DR; ++br) {
                     const int r = rr + RD * br;
-                    const double2 c = cmul(make_double2(Gg[br] * Lr[br].x, -(Gg[br] * Lr[br].y)), w);
-                    v[r] = cscale(csub(v[r], c), args.inv_scale);
+                    const CT c = cmul(cmake<CT>(Gg[br] * Lr[br].x, -(Gg[br] * Lr[br].y)), w);
+                    v[r] = from_d2<C>(to_d2(cscale(csub(gv[br], c), (T)args.inv_scale)));
                 }
                 if constexpr (FIT) {
                     if (ln == 0) {
-                        const double ax = (Sx - gwv * w.x) * args.inv_scale,
-                                     ay = (Sy - gwv * w.y) * args.inv_scale;
+                        const double ax = ((double)Sx - gwv * (double)w.x) * args.inv_scale,
+                                     ay = ((double)Sy - gwv * (double)w.y) * args.inv_scale;
                         const double rx = yraw.x - args.invsqrtd * ax, ry = yraw.y - args.invsqrtd * ay;
                         tfit += rx * rx + ry * ry;
                     }
                 }
-            }
+            };
+            // fp32 mode too folds in fp64: the naive Woodbury form cancels
+            // g_b against Gamma_b conj(Lambda_b) w and so amplifies rounding by
+            // ~Gamma_b |Lambda_b|^2 / (mu d) -- 1/tau at DC, hundreds at the
+            // lowest non-zero frequencies -- while the map itself is well
+            // conditioned in its inputs (fp32 spectra are fine)
+#pragma unroll
+            for (int rr = 0; rr < RD; ++rr) fold_rr(0.0, rr);
             // this line's store rows, read before the inverse transform's barriers
             // (after them, the issue below re-arms buffer b's metadata)
             wr = mt->wr, sec = mt->sec;
@@ -381,18 +405,22 @@ __global__ void __launch_bounds__(SwShape<L, A, RM>::THREADS, 1) tv_sandwich_pip
         if (role != 2) {
             // direct rows as computed; mirrored rows (role 1) conjugated into their mirror position
             if (wr >= 0) {
-                double2* dst = args.out + wr;
+                C* dst = outc + wr;
 #pragma unroll
                 for (int j = 0; j < R; ++j) {
-                    const double2 val = v[j];
-                    dst[Pl::out_q(t, j)] =
-                        make_double2(val.x, __hiloint2double(__double2hiint(val.y) ^ flip, __double2loint(val.y)));
+                    const C val = v[j];
+                    RT y;
+                    if constexpr (std::is_same<C, double2>::value)
+                        y = __hiloint2double(__double2hiint(val.y) ^ flip, __double2loint(val.y));
+                    else
+                        y = __int_as_float(__float_as_int(val.y) ^ flip);
+                    dst[Pl::out_q(t, j)] = cmake<C>(val.x, y);
                 }
             }
             if (sec >= 0) {  // planes 0 and s/2 only
-                double2* dst = args.out + sec;
+                C* dst = outc + sec;
 #pragma unroll
-                for (int j = 0; j < R; ++j) dst[Pl::out_q(t, j)] = make_double2(v[j].x, -v[j].y);
+                for (int j = 0; j < R; ++j) dst[Pl::out_q(t, j)] = cmake<C>(v[j].x, -v[j].y);
             }
             if constexpr (FIT) fit += role == 1 ? 2.0 * tfit : tfit;  // the skipped mirror set: same |residual|^2
         }
@@ -418,10 +446,10 @@ int sm_count() {
     return n;
 }
 
-template <int L, int A, int DR, int RM>
+template <int L, int A, int DR, int RM, class C>
 void launch_pipe(const SwArgs& a, cudaStream_t st) {
-    using Sh = SwShape<L, A, RM>;
-    auto kern = a.fit ? tv_sandwich_pipe_kernel<L, A, DR, RM, true> : tv_sandwich_pipe_kernel<L, A, DR, RM, false>;
+    using Sh = SwShape<L, A, RM, C>;
+    auto kern = a.fit ? tv_sandwich_pipe_kernel<L, A, DR, RM, true, C> : tv_sandwich_pipe_kernel<L, A, DR, RM, false, C>;
     VSR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Sh::SMEM));
     // two groups per CTA: at most ntiles / 2 CTAs, so every (CTA, group) partial slot is < ntiles
     const int grid = std::max(1, std::min(a.tabs.ntiles / 2, sm_count()));
@@ -436,11 +464,10 @@ void launch_pipe(const SwArgs& a, cudaStream_t st) {
     X(256, 16, 4) X(512, 8, 2) X(1024, 4, 2) X(64, 16, 4) X(128, 16, 4)               \
     X(64, 8, 2) X(128, 8, 2) X(256, 8, 2) X(128, 4, 2) X(256, 4, 2) X(512, 4, 2)
 
-}  // namespace
-
-bool tv_sandwich_pipe(const FoldGeom& G, const double2* Yl, const SepTables& sep, const double2* W, double2* out,
-                      const GammaTables& tabs, double cA, double shift, double inv_scale, double fwd_scale,
-                      double* fit_partials, cudaStream_t st) {
+template <class C>
+bool sandwich_pipe_t(const FoldGeom& G, const double2* Yl, const SepTables& sep, const void* W, void* out,
+                            const GammaTables& tabs, double cA, double shift, double inv_scale, double fwd_scale,
+                            double* fit_partials, cudaStream_t st) {
     if (!sep.a || !tabs.gw || !tabs.half3 || tabs.fit_only || !tabs.tiles || tabs.ntiles <= 0 || !out || out == W)
         return false;
     if (tv_sandwich1_tile_g2(G) != 1) return false;
@@ -449,13 +476,40 @@ bool tv_sandwich_pipe(const FoldGeom& G, const double2* Yl, const SepTables& sep
              nullptr, fit_partials};
 #define VSR_X(LL, AA, DD)                                                      \
     if (G.m == LL && A == AA && G.dr == DD) {                                  \
-        a.tw = fft_engine().twiddles((size_t)LL);                              \
-        launch_pipe<LL, AA, DD, 16>(a, st);                                    \
+        if constexpr (std::is_same<C, double2>::value)                         \
+            a.tw = fft_engine().twiddles((size_t)LL);                          \
+        else                                                                   \
+            a.tw = fft_engine().twiddles_f((size_t)LL);                        \
+        launch_pipe<LL, AA, DD, 16, C>(a, st);                                 \
         return true;                                                           \
     }
     VSR_PIPE_TABLE(VSR_X)
 #undef VSR_X
     return false;
+}
+
+}  // namespace
+
+bool tv_sandwich_pipe_ok(const FoldGeom& G) {
+    if (tv_sandwich1_tile_g2(G) != 1) return false;
+    const int A = G.dc * G.ds;
+#define VSR_X(LL, AA, DD) \
+    if (G.m == LL && A == AA && G.dr == DD) return true;
+    VSR_PIPE_TABLE(VSR_X)
+#undef VSR_X
+    return false;
+}
+
+bool tv_sandwich_pipe(const FoldGeom& G, const double2* Yl, const SepTables& sep, const double2* W, double2* out,
+                      const GammaTables& tabs, double cA, double shift, double inv_scale, double fwd_scale,
+                      double* fit_partials, cudaStream_t st) {
+    return sandwich_pipe_t<double2>(G, Yl, sep, W, out, tabs, cA, shift, inv_scale, fwd_scale, fit_partials, st);
+}
+
+bool tv_sandwich_pipe_f32(const FoldGeom& G, const double2* Yl, const SepTables& sep, const float2* W, float2* out,
+                          const GammaTables& tabs, double cA, double shift, double inv_scale, double fwd_scale,
+                          double* fit_partials, cudaStream_t st) {
+    return sandwich_pipe_t<float2>(G, Yl, sep, W, out, tabs, cA, shift, inv_scale, fwd_scale, fit_partials, st);
 }
 
 std::vector<int2> tv_sandwich1_active_tiles(const FoldGeom& G) {

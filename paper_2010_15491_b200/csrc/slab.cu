@@ -729,6 +729,8 @@ int vsr_slab_tv_create(vsr_comm* comm, const size_t hr_dims[3], const size_t rat
             throw std::invalid_argument("lambda must be positive, got " + std::to_string(cfg->lambda));
         if (!(cfg->mu > 0.0)) throw std::invalid_argument("mu must be positive, got " + std::to_string(cfg->mu));
         if (cfg->max_iters < 1) throw std::invalid_argument("admm_tv: max_iters must be >= 1");
+        if (cfg->precision != VSR_PRECISION_F64)
+            throw std::invalid_argument("admm_tv: the slab-sharded path runs in fp64 only");
         auto* h = new vsr_slab_tv();
         try {
             h->t0 = std::chrono::steady_clock::now();

@@ -275,14 +275,24 @@ __host__ __device__ constexpr size_t fast_smem_doubles() {
     return (size_t)3 * FXS + 2 * FDS + TY * (TX + 1) + (TY + 1) * TX;
 }
 
-template <bool INIT, bool RELCHG>
+// pair loads of the storage type (double, or float in fp32 mode) as double2
+__device__ __forceinline__ double2 ld_pair(const double* p) { return __ldg(reinterpret_cast<const double2*>(p)); }
+__device__ __forceinline__ double2 ld_pair(const float* p) {
+    const float2 v = __ldg(reinterpret_cast<const float2*>(p));
+    return make_double2(v.x, v.y);
+}
+
+// S = double: the reference precision.  S = float (fp32 mode): x, dual,
+// dual' and theta are stored in fp32 (half the HBM bytes); the stencil
+// arithmetic, the shared-memory planes and the reductions stay fp64.
+template <bool INIT, bool RELCHG, class S = double>
 __global__ void __launch_bounds__(STH)
-    tv_stencil_fast_kernel(int m, int n, int s, int KC, const double* __restrict__ x,
-                           const double* __restrict__ dual_in, double* __restrict__ dual_out,
-                           double* __restrict__ theta, double thr, const double* __restrict__ xprev,
+    tv_stencil_fast_kernel(int m, int n, int s, int KC, const S* __restrict__ x,
+                           const S* __restrict__ dual_in, S* __restrict__ dual_out,
+                           S* __restrict__ theta, double thr, const S* __restrict__ xprev,
                            double* __restrict__ partials, int halo, long long dsi, long long dso,
-                           const double* __restrict__ ylo_x = nullptr, const double* __restrict__ yhi_x = nullptr,
-                           const double* __restrict__ ylo_d = nullptr) {
+                           const S* __restrict__ ylo_x = nullptr, const S* __restrict__ yhi_x = nullptr,
+                           const S* __restrict__ ylo_d = nullptr) {
     extern __shared__ double sm[];
     double* rx = sm + 3 * FXS + 2 * FDS;  // [TY][TX+1]
     double* ry = rx + TY * (TX + 1);       // [TY+1][TX]
@@ -306,7 +316,7 @@ __global__ void __launch_bounds__(STH)
     // in place over NVLink peer memory (row n-1 of the lower one, row 0 of the
     // upper one; same plane stride)
     const bool yslab = ylo_x != nullptr;
-    auto yrow = [&](int jr, const double*& base, const double* lo, const double* hi) {
+    auto yrow = [&](int jr, const S*& base, const S* lo, const S* hi) {
         if (!yslab) return wrap(jr, n);
         if (jr < 0) {
             base = lo;
@@ -321,7 +331,7 @@ __global__ void __launch_bounds__(STH)
     // load assignments: one x pair (tid < FXP), up to two dual pairs
     const bool xa = tid < FXP;
     int xoff = 0, xsm = 0;
-    const double* xsrc = x;
+    const S* xsrc = x;
     if (xa) {
         const int row = tid / (FXW / 2), pc = tid % (FXW / 2);
         xoff = wrap(i0 - 2 + 2 * pc, m) + m * yrow(j0 - 1 + row, xsrc, ylo_x, yhi_x);
@@ -330,7 +340,7 @@ __global__ void __launch_bounds__(STH)
     bool da[2];
     long long doff[2];
     int dsm[2];
-    const double* dsrc[2] = {dual_in, dual_in};
+    const S* dsrc[2] = {dual_in, dual_in};
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
         const int e = tid + q * STH;
@@ -352,23 +362,22 @@ __global__ void __launch_bounds__(STH)
 
     double2 rxv = make_double2(0.0, 0.0), rdv[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
     // prologue: x(k0-1), x(k0), dual(k0-1) resident; x(k0+1), dual(k0) in registers
-    if (xa) *reinterpret_cast<double2*>(xsl[0] + xsm) = __ldg(reinterpret_cast<const double2*>(xsrc + zp(k0 - 1) + xoff));
+    if (xa) *reinterpret_cast<double2*>(xsl[0] + xsm) = ld_pair(xsrc + zp(k0 - 1) + xoff);
     if (!INIT) {
         const long long zo = zp(k0 - 1);
 #pragma unroll
         for (int q = 0; q < 2; ++q)
-            if (da[q]) *reinterpret_cast<double2*>(dsl[0] + dsm[q]) =
-                __ldg(reinterpret_cast<const double2*>(dsrc[q] + zo + doff[q]));
+            if (da[q]) *reinterpret_cast<double2*>(dsl[0] + dsm[q]) = ld_pair(dsrc[q] + zo + doff[q]);
     }
-    if (xa) *reinterpret_cast<double2*>(xsl[1] + xsm) = __ldg(reinterpret_cast<const double2*>(xsrc + zp(k0) + xoff));
-    const double* xnext = xsrc + xoff;    // advanced below; holds plane k+3 at step k
-    const double* dnext[2] = {dsrc[0] + doff[0], dsrc[1] + doff[1]};  // plane k+2 at step k
+    if (xa) *reinterpret_cast<double2*>(xsl[1] + xsm) = ld_pair(xsrc + zp(k0) + xoff);
+    const S* xnext = xsrc + xoff;    // advanced below; holds plane k+3 at step k
+    const S* dnext[2] = {dsrc[0] + doff[0], dsrc[1] + doff[1]};  // plane k+2 at step k
     long long zx = zp(k0 + 1), zd = zp(k0);
-    if (xa && k0 + 1 <= k1) rxv = __ldg(reinterpret_cast<const double2*>(xnext + zx));
+    if (xa && k0 + 1 <= k1) rxv = ld_pair(xnext + zx);
     if (!INIT && k0 < k1) {
 #pragma unroll
         for (int q = 0; q < 2; ++q)
-            if (da[q]) rdv[q] = __ldg(reinterpret_cast<const double2*>(dnext[q] + zd));
+            if (da[q]) rdv[q] = ld_pair(dnext[q] + zd);
     }
     // halo points (rho_x at ii = -1 for TY rows, rho_y at jj = -1 for TX columns)
     // packed into whole warps: warp 0 takes the TX row points, warp 1 the TY
@@ -404,14 +413,14 @@ __global__ void __launch_bounds__(STH)
         if (k + 3 <= k1) {
             zx += plane;
             if (!halo && zx >= plane * s) zx -= plane * s;
-            if (xa) rxv = __ldg(reinterpret_cast<const double2*>(xnext + zx));
+            if (xa) rxv = ld_pair(xnext + zx);
         }
         if (!INIT && k + 2 <= k1 - 1) {
             zd += plane;
             if (!halo && zd >= plane * s) zd -= plane * s;
 #pragma unroll
             for (int q = 0; q < 2; ++q)
-                if (da[q]) rdv[q] = __ldg(reinterpret_cast<const double2*>(dnext[q] + zd));
+                if (da[q]) rdv[q] = ld_pair(dnext[q] + zd);
         }
         __syncthreads();
         const bool warm = k < k0;
@@ -430,9 +439,9 @@ __global__ void __launch_bounds__(STH)
             r2 = l2;
             if (!warm && valid) {
                 const long long idx = col + zo;
-                dual_out[idx] = 0.0;
-                dual_out[dso + idx] = 0.0;
-                dual_out[2 * dso + idx] = 0.0;
+                dual_out[idx] = (S)0;
+                dual_out[dso + idx] = (S)0;
+                dual_out[2 * dso + idx] = (S)0;
                 {
                     double inv_;
                     acc_tv += norm3(l0, l1, l2, &inv_);
@@ -445,9 +454,9 @@ __global__ void __launch_bounds__(STH)
             r2 = o.r2;
             if (!warm && valid) {
                 const long long idx = col + zo;
-                dual_out[idx] = o.dn0;
-                dual_out[dso + idx] = o.dn1;
-                dual_out[2 * dso + idx] = o.dn2;
+                dual_out[idx] = (S)o.dn0;
+                dual_out[dso + idx] = (S)o.dn1;
+                dual_out[2 * dso + idx] = (S)o.dn2;
                 const double e0 = l0 - o.u0, e1 = l1 - o.u1, e2 = l2 - o.u2;
                 acc_res += e0 * e0 + e1 * e1 + e2 * e2;
                 {
@@ -458,7 +467,7 @@ __global__ void __launch_bounds__(STH)
         }
         if constexpr (RELCHG) {
             if (!warm && valid) {
-                const double xp = __ldg(xprev + col + zo);
+                const double xp = (double)__ldg(xprev + col + zo);
                 const double dd = xc - xp;
                 acc_dx += dd * dd;
                 acc_xp += xp * xp;
@@ -494,7 +503,7 @@ __global__ void __launch_bounds__(STH)
             const double ax = rx[ty * (TX + 1) + tx] - rx[ty * (TX + 1) + tx + 1];
             const double ay = ry[ty * TX + tx] - ry[(ty + 1) * TX + tx];
             const double az = rz_prev - r2;
-            theta[col + zo] = (ax + ay) + az;
+            theta[col + zo] = (S)((ax + ay) + az);
         }
         rz_prev = r2;
         // rotate the rings: x slots (k, k+1, k+2) -> (k+1, k+2, k+3); dual (k, k+1) -> (k+1, k+2)
@@ -705,6 +714,26 @@ void launch_tv_stencil(const Dims& d, bool init, const double* x, const double* 
         tv_stencil_kernel<false, false><<<g.grid, STH, smem, st>>>(m, n, s, g.kc, x, dual_in, dual_out,
                                                                    theta, thr, xprev, partials);
     }
+    VSR_LAUNCH_CHECK();
+}
+
+void launch_tv_stencil_f32(const Dims& d, bool init, const float* x, const float* dual_in, float* dual_out,
+                           float* theta, double thr, const float* xprev, double* partials, cudaStream_t st) {
+    const StencilGeom g = stencil_geom(d);
+    const int m = (int)d.m, n = (int)d.n, s = (int)d.s;
+    if (m % 2) throw std::logic_error("tv stencil (fp32 mode): axis 1 must be even");
+    const size_t smem = fast_smem_doubles() * sizeof(double);
+    const long long N = (long long)d.count();
+#define VSR_FAST(I, R)                                                                                      \
+    tv_stencil_fast_kernel<I, R, float><<<g.grid, STH, smem, st>>>(m, n, s, g.kc, x, dual_in, dual_out, theta, \
+                                                                   thr, xprev, partials, 0, N, N)
+    if (init)
+        VSR_FAST(true, false);
+    else if (xprev)
+        VSR_FAST(false, true);
+    else
+        VSR_FAST(false, false);
+#undef VSR_FAST
     VSR_LAUNCH_CHECK();
 }
 

@@ -37,6 +37,11 @@ void launch_tv_stencil_yslab(const Dims& loc, bool init, const double* x, const 
                              double* theta, double thr, const double* xprev, double* partials, const double* ylo_x,
                              const double* yhi_x, const double* ylo_d, cudaStream_t st);
 
+// fp32 mode: the same fused stencil with x, dual, dual' and theta stored in
+// fp32 (arithmetic and reductions in fp64); axis 1 must be even.
+void launch_tv_stencil_f32(const Dims& d, bool init, const float* x, const float* dual_in, float* dual_out,
+                           float* theta, double thr, const float* xprev, double* partials, cudaStream_t st);
+
 // Per-iteration scalar reduction for admm_tv (fixed order, single CTA):
 // report[iter] objective / primal residual / rel change, residue check.
 struct TvIterScalars {

@@ -89,6 +89,43 @@ __device__ __forceinline__ double2 cmulc(double2 a, double2 b) {
 __device__ __forceinline__ double2 cscale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
 __device__ __forceinline__ double cnorm(double2 a) { return a.x * a.x + a.y * a.y; }
 
+// fp32 (float2) overloads for the optional fp32 mode
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+    return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ float2 cmulc(float2 a, float2 b) {
+    return make_float2(a.x * b.x + a.y * b.y, a.x * b.y - a.y * b.x);
+}
+__device__ __forceinline__ float2 cscale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
+__device__ __forceinline__ float cnorm(float2 a) { return a.x * a.x + a.y * a.y; }
+
+// complex-type traits: the FFT core and the fp32-capable kernels are
+// templated on C = double2 (reference precision) or float2 (fp32 mode)
+template <class C>
+struct CplxT;
+template <>
+struct CplxT<double2> {
+    using real = double;
+    __host__ __device__ static __forceinline__ double2 make(double x, double y) { return make_double2(x, y); }
+};
+template <>
+struct CplxT<float2> {
+    using real = float;
+    __host__ __device__ static __forceinline__ float2 make(float x, float y) { return make_float2(x, y); }
+};
+template <class C>
+__device__ __forceinline__ C cmake(typename CplxT<C>::real x, typename CplxT<C>::real y) {
+    return CplxT<C>::make(x, y);
+}
+__device__ __forceinline__ double2 to_d2(double2 a) { return a; }
+__device__ __forceinline__ double2 to_d2(float2 a) { return make_double2(a.x, a.y); }
+template <class C>
+__device__ __forceinline__ C from_d2(double2 a) {
+    return cmake<C>((typename CplxT<C>::real)a.x, (typename CplxT<C>::real)a.y);
+}
+
 // ------------------------------------------------- deterministic block reduce
 // Fixed-order tree: warp shuffle tree, then warp 0 reduces the per-warp sums in
 // warp order.  Same launch geometry => bit-identical result run to run.

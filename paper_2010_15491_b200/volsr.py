@@ -72,7 +72,7 @@ _vp = C.c_void_p
 class _TvConfig(C.Structure):
     _fields_ = [("lambda_", C.c_double), ("mu", C.c_double), ("max_iters", C.c_size_t),
                 ("rel_tol", C.c_double), ("has_tau", C.c_int), ("tau", C.c_double),
-                ("init", C.c_int), ("init_volume", _dp)]
+                ("init", C.c_int), ("init_volume", _dp), ("precision", C.c_int)]
 
 
 class _Report(C.Structure):
@@ -601,6 +601,9 @@ class TvAdmmConfig:
     tau: Optional[float] = None
     init: int = INIT_ZERO
     init_volume: Optional[np.ndarray] = None
+    # "f64" (reference precision) or "f32": fp32 iteration state and fp32
+    # transforms / fold (LR frequency 0 in fp64); not a reference field
+    precision: str = "f64"
 
 
 @dataclass
@@ -623,6 +626,9 @@ def _tv_cfg(cfg: TvAdmmConfig, init_ptr=None) -> _TvConfig:
     c.tau = 0.0 if cfg.tau is None else float(cfg.tau)
     c.init = int(cfg.init)
     c.init_volume = init_ptr
+    if cfg.precision not in ("f64", "f32"):
+        raise ValueError("admm_tv: unknown precision")
+    c.precision = 1 if cfg.precision == "f32" else 0
     return c
 
 

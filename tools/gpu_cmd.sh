@@ -1,2 +1,3 @@
 mkdir -p gpurun_out
-for e in 0 1 2 4 5 7; do VSR_PIPE_EXP=$e timeout 600 python bench.py --steps 10 --warmup 3 --no-config4 --no-cpu --no-sharded --no-fft-path > gpurun_out/bench_e$e.json 2> gpurun_out/bench_e$e.err; done
+timeout 900 python -m pytest tests/test_fp32.py tests/test_acceptance.py -q -s > gpurun_out/t_fp32.log 2>&1; echo rc=$? >> gpurun_out/t_fp32.log
+timeout 600 python tools/diag_fp32.py > gpurun_out/diag.log 2>&1
