@@ -161,6 +161,12 @@ int vsr_tikhonov_solve(vsr_tikhonov* t, const double* y_r, double* x_r);
  * reported by the next vsr_tikhonov_check (which synchronizes). */
 int vsr_tikhonov_solve_d(vsr_tikhonov* t, const double* y_r_dev, double* x_r_dev);
 int vsr_tikhonov_check(vsr_tikhonov* t);
+/* fp32 mode (no reference analogue; BASELINE north_star's optional fp32 mode):
+ * y and x in fp32, the LR stage in fp64, the expansion in fp32 arithmetic.
+ * Only on the spatial path (vsr_tikhonov_fp32_ok); VSR_ERR_INVALID otherwise. */
+int vsr_tikhonov_solve_f32(vsr_tikhonov* t, const float* y_r, float* x_r);
+int vsr_tikhonov_solve_f32_d(vsr_tikhonov* t, const float* y_dev, float* x_dev);
+int vsr_tikhonov_fp32_ok(vsr_tikhonov* t);
 int vsr_tikhonov_fast(vsr_ctx* ctx, const size_t hr_dims[3], const size_t rates[3],
                       const double* y_r, const double* lambda_c, double reg, const double* xbar_r,
                       double* x_r);

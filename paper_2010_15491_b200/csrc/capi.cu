@@ -986,8 +986,8 @@ struct vsr_tikhonov {
     bool half = false;                // LR stage on the Hermitian half spectrum
     // CUDA graph of one solve for a given (y, x) pair (replayed while they repeat)
     cudaGraphExec_t gexec = nullptr;
-    const double* g_y = nullptr;
-    double* g_x = nullptr;
+    const void* g_y = nullptr;
+    void* g_x = nullptr;
     uint64_t g_kernels = 0;
     uint64_t solves = 0;
     ~vsr_tikhonov() {
@@ -995,6 +995,9 @@ struct vsr_tikhonov {
     }
     DevBuf<double2> sp_s1, U;
     DevBuf<unsigned long long> lrbad;
+    // fp32 solves (vsr_tikhonov_solve_f32*): fp32 y staging / x, and the graph's precision
+    DevBuf<float> yf, xf;
+    bool g_f32 = false;
 };
 
 static void tik_reset_status(vsr_tikhonov* t) {
@@ -1211,9 +1214,20 @@ int vsr_tikhonov_destroy(vsr_tikhonov* t) {
 // Enqueue one solve: LR FFT of y (== F D^H y up to the alias replication and
 // 1/sqrt(d)) -> fused fold -> inverse FFT to real x with
 // the residue / finiteness reductions.
-static void tik_enqueue(vsr_tikhonov* t, const double* y_dev, double* x_dev) {
+static bool tik_fp32_ok(const vsr_tikhonov* t) {
+    return t->spl.ok && t->half && spatial_march_ok(t->sp.hr, t->sp.rates, t->spl);
+}
+
+// xf_dev / yf_dev (fp32 solves, spatial half-spectrum path only): y arrives
+// as fp32 and is widened for the fp64 LR stage; the expansion writes fp32 x.
+static void tik_enqueue(vsr_tikhonov* t, const double* y_dev, double* x_dev, const float* yf_dev = nullptr,
+                        float* xf_dev = nullptr) {
     cudaStream_t st = t->ctx->stream;
     Profiler* prof = t->ctx->prof();
+    if (yf_dev) {
+        launch_widen(yf_dev, t->y.p, t->y.n, st);
+        y_dev = t->y.p;
+    }
     if (t->spl.ok && t->half) {
         // half-spectrum LR stage: r2c rows, axis 2, filter sandwich on axis 3,
         // inverse axis 2, c2r rows minus the constant prior term -> u
@@ -1245,10 +1259,14 @@ static void tik_enqueue(vsr_tikhonov* t, const double* y_dev, double* x_dev) {
         ++g_inv;
         {
             ProfScope ps(prof, "spatial_expand", st);
-            launch_spatial_expand(t->sp.hr, t->sp.rates, t->spl, t->u.p, t->zlat.p, 1.0, x_dev, t->bad.p, st);
+            if (xf_dev)
+                launch_spatial_expand_f32(t->sp.hr, t->sp.rates, t->spl, t->u.p, t->zlat.p, xf_dev, t->bad.p, st);
+            else
+                launch_spatial_expand(t->sp.hr, t->sp.rates, t->spl, t->u.p, t->zlat.p, 1.0, x_dev, t->bad.p, st);
         }
         return;  // real by construction: no imaginary residue to reduce
     }
+    if (xf_dev) throw std::logic_error("tikhonov fp32: not the spatial path");
     if (t->spl.ok && t->U.p == nullptr) {
         ProfScope ps(prof, "lr_fft12", st);
         fft_engine().forward12(t->sp.lr, y_dev, IN_REAL, t->Yl.p, st);
@@ -1333,7 +1351,8 @@ static void tik_enqueue(vsr_tikhonov* t, const double* y_dev, double* x_dev) {
 // operator runs eagerly (lazy twiddle tables, attribute setup); the next one is
 // captured for its (y, x) pair and replayed while the pair repeats.  The event
 // profiler and VSR_NO_GRAPH=1 keep the eager path.
-static void tik_run(vsr_tikhonov* t, const double* y_dev, double* x_dev) {
+static void tik_run(vsr_tikhonov* t, const double* y_dev, double* x_dev, const float* yf_dev = nullptr,
+                    float* xf_dev = nullptr) {
     static const bool off = [] {
         const char* e = std::getenv("VSR_NO_GRAPH");
         return e && e[0] == '1';
@@ -1341,10 +1360,13 @@ static void tik_run(vsr_tikhonov* t, const double* y_dev, double* x_dev) {
     cudaStream_t st = t->ctx->stream;
     const bool eager = off || t->ctx->prof() != nullptr || t->solves++ == 0;
     if (eager) {
-        tik_enqueue(t, y_dev, x_dev);
+        tik_enqueue(t, y_dev, x_dev, yf_dev, xf_dev);
         return;
     }
-    if (!(t->gexec && t->g_y == y_dev && t->g_x == x_dev)) {
+    const bool f32 = xf_dev != nullptr;
+    const void* gy = f32 ? (const void*)yf_dev : (const void*)y_dev;
+    void* gx = f32 ? (void*)xf_dev : (void*)x_dev;
+    if (!(t->gexec && t->g_y == gy && t->g_x == gx && t->g_f32 == f32)) {
         if (t->gexec) {
             cudaGraphExecDestroy(t->gexec);
             t->gexec = nullptr;
@@ -1354,7 +1376,7 @@ static void tik_run(vsr_tikhonov* t, const double* y_dev, double* x_dev) {
         cudaGraph_t graph = nullptr;
         VSR_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
         try {
-            tik_enqueue(t, y_dev, x_dev);
+            tik_enqueue(t, y_dev, x_dev, yf_dev, xf_dev);
         } catch (...) {
             cudaStreamEndCapture(st, &graph);
             if (graph) cudaGraphDestroy(graph);
@@ -1368,8 +1390,9 @@ static void tik_run(vsr_tikhonov* t, const double* y_dev, double* x_dev) {
         g_launches.fetch_sub(t->g_kernels);  // counted when the graph runs
         g_fwd.fetch_sub(g_fwd.load() - f0);
         g_inv.fetch_sub(g_inv.load() - i0);
-        t->g_y = y_dev;
-        t->g_x = x_dev;
+        t->g_y = gy;
+        t->g_x = gx;
+        t->g_f32 = f32;
     }
     VSR_CUDA(cudaGraphLaunch(t->gexec, st));
     g_launches.fetch_add(t->g_kernels);
@@ -1409,6 +1432,39 @@ int vsr_tikhonov_solve_d(vsr_tikhonov* t, const double* y_dev, double* x_dev) {
         tik_run(t, y_dev, x_dev);
     });
 }
+
+// fp32 solves (BASELINE north_star's optional fp32 mode): y and x in fp32,
+// the LR stage in fp64, the expansion in fp32 arithmetic
+static void tik_require_fp32(vsr_tikhonov* t) {
+    if (!t) throw std::invalid_argument("vsr_tikhonov_solve_f32: null operator");
+    if (!tik_fp32_ok(t))
+        throw std::invalid_argument(
+            "tikhonov_fast: fp32 mode needs the spatial path (separable compact PSF, lattice prior, "
+            "rates (2, 2, 2|4), tile-aligned LR grid)");
+}
+
+int vsr_tikhonov_solve_f32(vsr_tikhonov* t, const float* y_r, float* x_r) {
+    return guarded([&] {
+        tik_require_fp32(t);
+        vsr_ctx::Guard g(t->ctx->device);
+        if (!t->yf.p) t->yf.alloc(t->sp.lr.count());
+        if (!t->xf.p) t->xf.alloc(t->sp.hr.count());
+        h2d(t->ctx, t->yf.p, y_r, t->yf.bytes());
+        tik_run(t, nullptr, nullptr, t->yf.p, t->xf.p);
+        d2h(t->ctx, x_r, t->xf.p, t->xf.bytes());
+        tik_check(t);
+    });
+}
+
+int vsr_tikhonov_solve_f32_d(vsr_tikhonov* t, const float* y_dev, float* x_dev) {
+    return guarded([&] {
+        tik_require_fp32(t);
+        vsr_ctx::Guard g(t->ctx->device);
+        tik_run(t, nullptr, nullptr, y_dev, x_dev);
+    });
+}
+
+int vsr_tikhonov_fp32_ok(vsr_tikhonov* t) { return t && tik_fp32_ok(t) ? 1 : 0; }
 
 int vsr_tikhonov_check(vsr_tikhonov* t) {
     return guarded([&] {

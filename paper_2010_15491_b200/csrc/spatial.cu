@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <cmath>
 #include <complex>
+#include <type_traits>
 #include <vector>
 
 #include "fft.cuh"
@@ -376,14 +377,27 @@ struct MarchArgs {
     int dmin1, dmin2, dmin3;
     int zc;  // LR planes per CTA
     double k1[MX_KMAX], k2[MX_KMAX], k3[MX_KMAX];
+    float f1[MX_KMAX], f2[MX_KMAX], f3[MX_KMAX];  // the same taps for the fp32 march
     const double* u;
     const double* z;
-    double* x;
+    void* x;  // double (reference precision) or float (fp32 mode)
     unsigned long long* bad;
 };
 
-template <int DM, int R1, int R2, int R3, int CY>
+template <class T>
+__device__ __forceinline__ T march_tap(const MarchArgs& A, int axis, int i) {
+    if constexpr (std::is_same<T, double>::value)
+        return axis == 0 ? A.k1[i] : (axis == 1 ? A.k2[i] : A.k3[i]);
+    else
+        return axis == 0 ? A.f1[i] : (axis == 1 ? A.f2[i] : A.f3[i]);
+}
+
+// T = double: the reference precision.  T = float (fp32 mode): the LR tile
+// and prior arrive as fp64 and are rounded on use; the three correlation
+// stages, the register ring and x run in fp32 (half the HBM bytes of x).
+template <int DM, int R1, int R2, int R3, int CY, class T = double>
 __global__ void __launch_bounds__(MX_THREADS, 4) spatial_march_kernel(const __grid_constant__ MarchArgs A) {
+    using T2 = std::conditional_t<std::is_same<T, double>::value, double2, float2>;
     static_assert(R1 == 2, "stage z pairs (2c, 2c + 1) assume the lattice column is the even one");
     constexpr int CX = MX_CX, NT = MX_THREADS;
     constexpr int LX = CX + DM - 1, LY = CY + DM - 1;
@@ -398,8 +412,8 @@ __global__ void __launch_bounds__(MX_THREADS, 4) spatial_march_kernel(const __gr
     __shared__ __align__(16) double lt[NB][LTB];
     constexpr int NZB = MX_PD + 4;  // prior ring: fetched PD phases before plane q lands, read 3 after
     __shared__ __align__(16) double zs[NZB][CY * CX];
-    __shared__ __align__(16) double ex[2][LY * W];
-    __shared__ __align__(16) double ey[2][H * W];
+    __shared__ __align__(16) T ex[2][LY * W];
+    __shared__ __align__(16) T ey[2][H * W];
     __shared__ int xoff[LX], yoff[LY];
 
     const int tid = threadIdx.x;
@@ -431,8 +445,8 @@ __global__ void __launch_bounds__(MX_THREADS, 4) spatial_march_kernel(const __gr
     int zq = wrap_idx(c30 + A.dmin3, A.sl);  // LR z of the next plane to fetch
     const int cp = tid % CPR, rg = tid / CPR;
     const int X0 = cx0 * R1, Y0 = cy0 * R2;
-    double2 ring[RPT][DM];
-    double chk = 0.0;
+    T2 ring[RPT][DM];
+    T chk = 0;
     // LR plane tiles: cp.async ring of NB buffers, MX_PD planes in flight
     // per-element shared addresses of buffer 0 and global pointers of LR z = 0
     unsigned lsa[NLD];
@@ -467,7 +481,7 @@ __global__ void __launch_bounds__(MX_THREADS, 4) spatial_march_kernel(const __gr
     };
     for (int q = 0; q < MX_PD; ++q) fetch(q);
     const long long hplane = (long long)A.n * A.m;
-    double* const xrow = A.x + (long long)(Y0 + rg * RPT) * A.m + X0 + 2 * cp;
+    T* const xrow = static_cast<T*>(A.x) + (long long)(Y0 + rg * RPT) * A.m + X0 + 2 * cp;
     for (int pb = 0; pb < jend + 3; pb += DM) {
 #pragma unroll
         for (int s = 0; s < DM; ++s) {
@@ -479,35 +493,38 @@ __global__ void __launch_bounds__(MX_THREADS, 4) spatial_march_kernel(const __gr
             //    overlap the smem work of stages x and y below)
             const int jz = p - 3;
             if (jz >= 0) {
-                const double* eb = ey[jz & 1];
+                const T* eb = ey[jz & 1];
                 const int slot = ((s - 3) % DM + DM) % DM;  // compile-time after the unroll
 #pragma unroll
                 for (int rr = 0; rr < RPT; ++rr)
-                    ring[rr][slot] = *reinterpret_cast<const double2*>(eb + (rg * RPT + rr) * W + 2 * cp);
+                    ring[rr][slot] = *reinterpret_cast<const T2*>(eb + (rg * RPT + rr) * W + 2 * cp);
                 if (jz >= DM - 1) {
                     const int c3 = c30 + jz - (DM - 1);  // LR plane of the outputs
-                    double zv[RPT];
+                    T zv[RPT];
 #pragma unroll
                     for (int rr = 0; rr < RPT; ++rr) {
                         const int row = rg * RPT + rr;
-                        zv[rr] = (A.z && row % R2 == 0) ? zs[(c3 - c30) % NZB][(row / R2) * CX + cp] : 0.0;
+                        zv[rr] = (A.z && row % R2 == 0) ? (T)zs[(c3 - c30) % NZB][(row / R2) * CX + cp] : (T)0;
                     }
 #pragma unroll
                     for (int ph = 0; ph < R3; ++ph) {
-                        double* xp = xrow + (long long)(R3 * c3 + ph) * hplane;
+                        T* xp = xrow + (long long)(R3 * c3 + ph) * hplane;
 #pragma unroll
                         for (int rr = 0; rr < RPT; ++rr) {
-                            double ax = 0.0, ay = 0.0;
+                            T ax = 0, ay = 0;
 #pragma unroll
                             for (int i = 0; i < DM; ++i) {
-                                const double2 v = ring[rr][(slot + 1 + i) % DM];
-                                ax = fma(A.k3[ph * DM + i], v.x, ax);
-                                ay = fma(A.k3[ph * DM + i], v.y, ay);
+                                const T2 v = ring[rr][(slot + 1 + i) % DM];
+                                ax = fma(march_tap<T>(A, 2, ph * DM + i), v.x, ax);
+                                ay = fma(march_tap<T>(A, 2, ph * DM + i), v.y, ay);
                             }
                             if (ph == 0) ax += zv[rr];
-                            chk = fma(ax, 0.0, chk);
-                            chk = fma(ay, 0.0, chk);
-                            __stcs(reinterpret_cast<double2*>(xp + (long long)rr * A.m), make_double2(ax, ay));  // streaming: x must not evict u
+                            chk = fma(ax, (T)0, chk);
+                            chk = fma(ay, (T)0, chk);
+                            T2 o;
+                            o.x = ax;
+                            o.y = ay;
+                            __stcs(reinterpret_cast<T2*>(xp + (long long)rr * A.m), o);  // streaming: x must not evict u
                         }
                     }
                 }
@@ -516,50 +533,54 @@ __global__ void __launch_bounds__(MX_THREADS, 4) spatial_march_kernel(const __gr
             const int jx = p - 1;
             if (jx >= 0 && jx < jend) {
                 const double* lb = lt[jx % NB];
-                double* xb = ex[jx & 1];
+                T* xb = ex[jx & 1];
                 for (int it = tid; it < NXI; it += NT) {
                     const int qy = it / (CX / 2), c = 2 * (it - qy * (CX / 2));
                     const double* row = lb + qy * LXP + c;
-                    double in[2 * NPAIR];
+                    T in[2 * NPAIR];
 #pragma unroll
                     for (int i = 0; i < NPAIR; ++i) {
                         const double2 v = *reinterpret_cast<const double2*>(row + 2 * i);
-                        in[2 * i] = v.x;
-                        in[2 * i + 1] = v.y;
+                        in[2 * i] = (T)v.x;
+                        in[2 * i + 1] = (T)v.y;
                     }
-                    double o[2 * R1];
+                    T o[2 * R1];
 #pragma unroll
                     for (int cell = 0; cell < 2; ++cell)
 #pragma unroll
                         for (int ph = 0; ph < R1; ++ph) {
-                            double acc = 0.0;
+                            T acc = 0;
 #pragma unroll
-                            for (int i = 0; i < DM; ++i) acc = fma(A.k1[ph * DM + i], in[cell + i], acc);
+                            for (int i = 0; i < DM; ++i) acc = fma(march_tap<T>(A, 0, ph * DM + i), in[cell + i], acc);
                             o[cell * R1 + ph] = acc;
                         }
-                    double* dst = xb + qy * W + R1 * c;
+                    T* dst = xb + qy * W + R1 * c;
 #pragma unroll
-                    for (int i = 0; i < 2 * R1; i += 2)
-                        *reinterpret_cast<double2*>(dst + i) = make_double2(o[i], o[i + 1]);
+                    for (int i = 0; i < 2 * R1; i += 2) {
+                        T2 w2;
+                        w2.x = o[i];
+                        w2.y = o[i + 1];
+                        *reinterpret_cast<T2*>(dst + i) = w2;
+                    }
                 }
             }
             // c. stage y on plane p - 2
             const int jy = p - 2;
             if (jy >= 0 && jy < jend) {
-                const double* xb = ex[jy & 1];
-                double* yb = ey[jy & 1];
+                const T* xb = ex[jy & 1];
+                T* yb = ey[jy & 1];
                 for (int it = tid; it < NYI; it += NT) {
                     const int cy = 2 * (it / W), n = it % W;
-                    double in[DM + 1];
+                    T in[DM + 1];
 #pragma unroll
                     for (int i = 0; i < DM + 1; ++i) in[i] = xb[(cy + i) * W + n];
 #pragma unroll
                     for (int cell = 0; cell < 2; ++cell)
 #pragma unroll
                         for (int ph = 0; ph < R2; ++ph) {
-                            double acc = 0.0;
+                            T acc = 0;
 #pragma unroll
-                            for (int i = 0; i < DM; ++i) acc = fma(A.k2[ph * DM + i], in[cell + i], acc);
+                            for (int i = 0; i < DM; ++i) acc = fma(march_tap<T>(A, 1, ph * DM + i), in[cell + i], acc);
                             yb[(R2 * (cy + cell) + ph) * W + n] = acc;
                         }
                 }
@@ -576,15 +597,15 @@ __global__ void __launch_bounds__(MX_THREADS, 4) spatial_march_kernel(const __gr
                     for (int e = 0; e < 2; ++e) {
                         const unsigned long long idx =
                             ((unsigned long long)(R3 * c3 + ph) * A.n + Y0 + rg * RPT + rr) * A.m + X0 + 2 * cp + e;
-                        if (!isfinite(A.x[idx]) && idx < best) best = idx;
+                        if (!isfinite(static_cast<const T*>(A.x)[idx]) && idx < best) best = idx;
                     }
         atomicMin(A.bad, best);
     }
 }
 
-template <int DM, int R3, int CY>
+template <int DM, int R3, int CY, class T>
 static void launch_march_cy(MarchArgs& A, unsigned tx, unsigned ty, cudaStream_t st) {
-    auto kern = spatial_march_kernel<DM, 2, 2, R3, CY>;
+    auto kern = spatial_march_kernel<DM, 2, 2, R3, CY, T>;
     int dev = 0, sms = 0;
     VSR_CUDA(cudaGetDevice(&dev));
     VSR_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -615,16 +636,16 @@ static void launch_march_cy(MarchArgs& A, unsigned tx, unsigned ty, cudaStream_t
     VSR_LAUNCH_CHECK();
 }
 
-template <int DM, int R3>
+template <int DM, int R3, class T>
 static void launch_march_k(MarchArgs& A, unsigned tx, unsigned ty, cudaStream_t st) {
     static const bool cy8 = [] {
         const char* e = std::getenv("VSR_MARCH_CY");  // 8-row column tiles unless VSR_MARCH_CY=4
         return !(e && e[0] == '4');
     }();
     if (cy8 && ty % 2 == 0)
-        launch_march_cy<DM, R3, 8>(A, tx, ty / 2, st);
+        launch_march_cy<DM, R3, 8, T>(A, tx, ty / 2, st);
     else
-        launch_march_cy<DM, R3, 4>(A, tx, ty, st);
+        launch_march_cy<DM, R3, 4, T>(A, tx, ty, st);
 }
 
 // The march kernel serves rates (2, 2, 2|4) with a tile-aligned LR grid.
@@ -680,6 +701,41 @@ static void launch_expand_dm(const ExpandArgs& A, size_t smem, dim3 blocks, cuda
     }
 }
 
+bool spatial_march_ok(const Dims& hr, const int rates[3], const SpatialPlan& p) {
+    const int dm = spatial_tile(p, rates);
+    return dm && dm == p.dm && march_ok(hr, rates, dm) &&
+           p.kp_host.size() == (size_t)(rates[0] + rates[1] + rates[2]) * dm;
+}
+
+template <class T>
+static void march_dispatch(const Dims& hr, const int rates[3], const SpatialPlan& p, const double* u,
+                           const double* z, T* x, unsigned long long* bad, cudaStream_t st) {
+    const int dm = p.dm;
+    MarchArgs M{};
+    M.m = (int)hr.m, M.n = (int)hr.n, M.s = (int)hr.s;
+    M.ml = M.m / 2, M.nl = M.n / 2, M.sl = M.s / rates[2];
+    M.dmin1 = p.dmin[0], M.dmin2 = p.dmin[1], M.dmin3 = p.dmin[2];
+    const double* kp = p.kp_host.data();
+    for (int i = 0; i < 2 * dm; ++i) M.k1[i] = kp[i], M.f1[i] = (float)kp[i];
+    for (int i = 0; i < 2 * dm; ++i) M.k2[i] = kp[2 * dm + i], M.f2[i] = (float)kp[2 * dm + i];
+    for (int i = 0; i < rates[2] * dm; ++i) M.k3[i] = kp[4 * dm + i], M.f3[i] = (float)kp[4 * dm + i];
+    M.u = u, M.z = z, M.x = x, M.bad = bad;
+    const unsigned tx = (unsigned)(M.ml / MX_CX), ty = (unsigned)(M.nl / MX_CY);
+    const bool r4 = rates[2] == 4;
+    switch (dm) {
+        case 4: r4 ? launch_march_k<4, 4, T>(M, tx, ty, st) : launch_march_k<4, 2, T>(M, tx, ty, st); break;
+        case 5: r4 ? launch_march_k<5, 4, T>(M, tx, ty, st) : launch_march_k<5, 2, T>(M, tx, ty, st); break;
+        case 7: r4 ? launch_march_k<7, 4, T>(M, tx, ty, st) : launch_march_k<7, 2, T>(M, tx, ty, st); break;
+        default: r4 ? launch_march_k<8, 4, T>(M, tx, ty, st) : launch_march_k<8, 2, T>(M, tx, ty, st); break;
+    }
+}
+
+void launch_spatial_expand_f32(const Dims& hr, const int rates[3], const SpatialPlan& p, const double* u,
+                               const double* z, float* x, unsigned long long* bad, cudaStream_t st) {
+    if (!spatial_march_ok(hr, rates, p)) throw std::logic_error("spatial_expand (fp32): no z-march geometry");
+    march_dispatch<float>(hr, rates, p, u, z, x, bad, st);
+}
+
 void launch_spatial_expand(const Dims& hr, const int rates[3], const SpatialPlan& p, const double* u,
                            const double* z, double c0, double* x, unsigned long long* bad, cudaStream_t st) {
     (void)c0;  // folded into u's inverse-FFT scale by the caller
@@ -687,23 +743,7 @@ void launch_spatial_expand(const Dims& hr, const int rates[3], const SpatialPlan
     if (!dm) throw std::logic_error("spatial_expand: support too wide for the tile budget");
     if (dm != p.dm) throw std::logic_error("spatial_expand: plan taps built for another width");
     if (march_ok(hr, rates, dm) && p.kp_host.size() == (size_t)(rates[0] + rates[1] + rates[2]) * dm) {
-        MarchArgs M{};
-        M.m = (int)hr.m, M.n = (int)hr.n, M.s = (int)hr.s;
-        M.ml = M.m / 2, M.nl = M.n / 2, M.sl = M.s / rates[2];
-        M.dmin1 = p.dmin[0], M.dmin2 = p.dmin[1], M.dmin3 = p.dmin[2];
-        const double* kp = p.kp_host.data();
-        for (int i = 0; i < 2 * dm; ++i) M.k1[i] = kp[i];
-        for (int i = 0; i < 2 * dm; ++i) M.k2[i] = kp[2 * dm + i];
-        for (int i = 0; i < rates[2] * dm; ++i) M.k3[i] = kp[4 * dm + i];
-        M.u = u, M.z = z, M.x = x, M.bad = bad;
-        const unsigned tx = (unsigned)(M.ml / MX_CX), ty = (unsigned)(M.nl / MX_CY);
-        const bool r4 = rates[2] == 4;
-        switch (dm) {
-            case 4: r4 ? launch_march_k<4, 4>(M, tx, ty, st) : launch_march_k<4, 2>(M, tx, ty, st); break;
-            case 5: r4 ? launch_march_k<5, 4>(M, tx, ty, st) : launch_march_k<5, 2>(M, tx, ty, st); break;
-            case 7: r4 ? launch_march_k<7, 4>(M, tx, ty, st) : launch_march_k<7, 2>(M, tx, ty, st); break;
-            default: r4 ? launch_march_k<8, 4>(M, tx, ty, st) : launch_march_k<8, 2>(M, tx, ty, st); break;
-        }
+        march_dispatch<double>(hr, rates, p, u, z, x, bad, st);
         return;
     }
     ExpandArgs A;

@@ -64,5 +64,10 @@ void launch_spatial_sandwich(const Dims& lr, int d, const SpatialPlan& p, double
 // x = D^H z + c0 * H^T D^H v   (hr grid, rates); non-finite index -> bad (atomicMin)
 void launch_spatial_expand(const Dims& hr, const int rates[3], const SpatialPlan& p, const double* v,
                            const double* z, double c0, double* x, unsigned long long* bad, cudaStream_t st);
+// fp32 mode: the z-march expansion in fp32 arithmetic writing fp32 x (u and
+// the lattice prior stay fp64); only for the geometries the z march serves.
+bool spatial_march_ok(const Dims& hr, const int rates[3], const SpatialPlan& p);
+void launch_spatial_expand_f32(const Dims& hr, const int rates[3], const SpatialPlan& p, const double* u,
+                               const double* z, float* x, unsigned long long* bad, cudaStream_t st);
 
 }  // namespace vsr

@@ -125,6 +125,10 @@ _sig("vsr_tikhonov_create_d", [_vp, _szp, _szp, _vp, C.c_double, _vp, C.POINTER(
 _sig("vsr_tikhonov_destroy", [_vp])
 _sig("vsr_tikhonov_solve", [_vp, _dp, _dp])
 _sig("vsr_tikhonov_solve_d", [_vp, _vp, _vp])
+_sig("vsr_tikhonov_solve_f32", [_vp, _vp, _vp])
+_sig("vsr_tikhonov_solve_f32_d", [_vp, _vp, _vp])
+_sig("vsr_tikhonov_fp32_ok", [_vp])
+_sig("vsr_tv_x_f32_d", [_vp, C.POINTER(C.c_void_p)])
 _sig("vsr_tikhonov_check", [_vp])
 _sig("vsr_tikhonov_algorithmic_bytes", [_szp, _szp], C.c_double)
 _sig("vsr_make_gamma", [_vp, _szp, C.c_double, _dp])
@@ -516,6 +520,18 @@ class TikhonovOperator:
         check(_lib.vsr_tikhonov_solve(self.handle, _p(a), _p(out)))
         return out
 
+    def solve_f32(self, y) -> np.ndarray:
+        """fp32 mode (not a reference entry point): y and x in fp32, the LR
+        stage in fp64, the expansion in fp32; spatial path only (fp32_ok())."""
+        a = np.ascontiguousarray(y, dtype=np.float32)
+        require_same_dims(dims_of(a), self.spec.lr, "TikhonovOperator::solve")
+        out = np.empty(shape_of(self.spec.hr), dtype=np.float32)
+        check(_lib.vsr_tikhonov_solve_f32(self.handle, a.ctypes.data, out.ctypes.data))
+        return out
+
+    def fp32_ok(self) -> bool:
+        return bool(_lib.vsr_tikhonov_fp32_ok(self.handle))
+
     def path(self) -> dict:
         """Which specialisations the device solve uses (vsr_tikhonov_separable /
         _lattice_prior / _spatial)."""
@@ -835,6 +851,12 @@ class TikhonovDevice:
 
     def solve_host(self, y: np.ndarray, x_out: np.ndarray):
         check(_lib.vsr_tikhonov_solve(self.handle, _p(y), _p(x_out)))
+
+    def solve_f32_d(self, y_dev, x_dev):
+        check(_lib.vsr_tikhonov_solve_f32_d(self.handle, y_dev.ptr, x_dev.ptr))
+
+    def solve_f32_host(self, y: np.ndarray, x_out: np.ndarray):
+        check(_lib.vsr_tikhonov_solve_f32(self.handle, y.ctypes.data, x_out.ctypes.data))
 
     def check(self):
         check(_lib.vsr_tikhonov_check(self.handle))

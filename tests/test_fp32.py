@@ -1,11 +1,15 @@
 """fp32 mode (BASELINE north_star: relative L2 <= 1e-5 and PSNR within 0.01 dB
 of the fp64 result, which is itself pinned to the reference at <= 1e-10).
 
-ADMM-TV with TvAdmmConfig.precision = "f32": the iteration state in fp32,
-the half-spectrum transforms and the fold in fp32 arithmetic, the alias group
-of LR frequency 0 (Gamma_DC = 1/tau) folded in fp64.  The
+ADMM-TV with TvAdmmConfig.precision = "f32": the iteration state in fp32 and
+the half-spectrum transforms in fp32 arithmetic; the fold stays fp64 because
+its Woodbury form cancels g_b against Gamma_b conj(Lambda_b) w, amplifying
+rounding by ~Gamma_b |Lambda_b|^2 / (mu d) (1/tau at DC).  The
 cases are the BASELINE configs' recipes (synth.py) on grids with the configs'
-row geometries (m, dc*ds, dr) = (256, 16, 4), (512, 8, 2), (1024, 4, 2)."""
+row geometries (m, dc*ds, dr) = (256, 16, 4), (512, 8, 2), (1024, 4, 2).
+
+Tikhonov: TikhonovOperator.solve_f32 on the spatial path (fp64 LR stage,
+fp32 expansion and x).  The default-tau TV cases exercise the DC bin."""
 import numpy as np
 import pytest
 
@@ -89,3 +93,46 @@ def test_fp32_mode_rejections(V, O):
     with pytest.raises(ValueError, match="precision"):
         V.admm_tv(y, O.make_gaussian_psf((5, 5, 5), (1, 1, 1), hr), spec,
                   V.TvAdmmConfig(lambda_=2e-3, mu=0.05, max_iters=2, precision="f16"))
+
+
+# ------------------------------------------------------------------ Tikhonov
+TIK_CASES = [(0, (64, 64, 64)), (1, (256, 256, 256)), (1, (256, 128, 64)), (3, (128, 128, 64))]
+
+
+@pytest.mark.parametrize("cfg_idx,hr", TIK_CASES)
+def test_tikhonov_fp32_vs_fp64(V, cfg_idx, hr):
+    """TikhonovOperator::solve_f32 (spatial path: fp64 LR stage, fp32 expansion)
+    against the fp64 solve, on the configs' recipes; config 3's rates (2, 2, 4)
+    exercise the R3 = 4 expansion."""
+    cfg = synth.scaled(synth.CONFIGS[cfg_idx], hr)
+    inp = synth.make_inputs(cfg)
+    spec = V.DecimationSpec(cfg.hr, cfg.rates)
+    lam = V.psf_to_spectrum(inp.psf)
+    op = V.TikhonovOperator(lam, spec, V.TikhonovConfig(cfg.reg, V.zero_fill_upsample(inp.y, spec)))
+    assert op.fp32_ok()
+    x64 = op.solve(inp.y)
+    x32 = op.solve_f32(inp.y)
+    assert x32.dtype == np.float32
+    e = rel_err(x32.astype(np.float64), x64)
+    dp = abs(_psnr(inp.truth, x32.astype(np.float64)) - _psnr(inp.truth, x64))
+    print(f"tikhonov config {cfg_idx} {hr}: rel L2 {e:.2e}, PSNR gap {dp:.2e} dB")
+    assert e <= FP32_TOL and dp < PSNR_TOL
+    # graph replay of fp32 solves on new y, interleaved with fp64 solves
+    rng = np.random.default_rng(3)
+    for _ in range(3):
+        y2 = inp.y * rng.uniform(0.5, 1.5)
+        assert rel_err(op.solve_f32(y2).astype(np.float64), op.solve(y2)) <= FP32_TOL
+    op.close()
+
+
+def test_tikhonov_fp32_rejects_general_path(V):
+    rng = np.random.default_rng(2)
+    hr, rates = (64, 64, 32), (2, 2, 2)
+    spec = V.DecimationSpec(hr, rates)
+    psf = V.make_gaussian_psf((5, 5, 5), (1.2, 1.2, 1.2), hr)
+    xbar = rng.uniform(0, 1, V.shape_of(hr))  # not on the decimation lattice: no spatial path
+    op = V.TikhonovOperator(V.psf_to_spectrum(psf), spec, V.TikhonovConfig(1e-3, xbar))
+    assert not op.fp32_ok()
+    with pytest.raises(ValueError, match="fp32 mode"):
+        op.solve_f32(rng.uniform(0, 1, V.shape_of(spec.lr)))
+    op.close()
