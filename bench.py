@@ -403,9 +403,14 @@ def run_b200(args, rank, world, local):
                       "runs the user path (CUDA-graph replay), stage table from a second profiled pass"}
 
     line["config0"] = bench_tik_config(args, ctx, V, synth, torch, stream, local, hbm, 0)
+    if not args.no_fp32:
+        line["fp32"] = bench_tik_fp32(args, ctx, V, op, inp, cfg, torch, stream, flush, hbm)
     if not args.no_tv:
         line["tv"] = bench_tv(args, ctx, V, synth, torch, stream, local, hbm, 2)
         line["config3"] = bench_tv(args, ctx, V, synth, torch, stream, local, hbm, 3)
+        if not args.no_fp32:
+            line["fp32"]["tv_config2"] = bench_tv(args, ctx, V, synth, torch, stream, local, hbm, 2, "f32")
+            line["fp32"]["tv_config3"] = bench_tv(args, ctx, V, synth, torch, stream, local, hbm, 3, "f32")
         if rank == 0 and world == 1 and not args.no_cpu:
             line["tv"]["cpu_baseline"] = cpu_baseline_tv(synth.CONFIGS[2], synth.make_inputs(synth.CONFIGS[2],
                                                                                           with_truth=False))
@@ -603,9 +608,54 @@ def bench_config4(args, ctx, V, synth, torch, stream, local, hbm):
     return out
 
 
-def bench_tv(args, ctx, V, synth, torch, stream, local, hbm, idx=2):
+def bench_tik_fp32(args, ctx, V, op, inp, cfg, torch, stream, flush, hbm):
+    """fp32 mode on the headline workload (config 1): TikhonovOperator solve_f32
+    (fp64 LR stage, fp32 expansion and x), device-resident and end to end with
+    pinned fp32 host buffers; timed like the headline (per-solve events, L2
+    flushed between solves).  Not the headline: the reference precision is fp64."""
+    N = cfg.voxels
+    y32 = inp.y.astype(np.float32)
+    yd = V.DeviceBuffer(ctx, y32.nbytes)
+    yd.upload(y32)
+    xd = V.DeviceBuffer(ctx, N * 4)
+    for _ in range(max(args.warmup, 3)):
+        op.solve_f32_d(yd, xd)
+    op.check()
+    ctx.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for i in range(args.steps):
+        with torch.cuda.stream(stream):
+            flush.fill_(float(i))
+        evs[i][0].record(stream)
+        op.solve_f32_d(yd, xd)
+        evs[i][1].record(stream)
+    evs[-1][1].synchronize()
+    op.check()
+    ms = sum(a.elapsed_time(b) for a, b in evs) / args.steps
+    yp = V.PinnedBuffer(y32.shape, np.float32)
+    yp.array[...] = y32
+    xp = V.PinnedBuffer(V.shape_of(cfg.hr), np.float32)
+    for _ in range(2):
+        op.solve_f32_host(yp.array, xp.array)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        op.solve_f32_host(yp.array, xp.array)
+    e2e_s = (time.perf_counter() - t0) / args.steps
+    comp = 4 * N + 4 * (N // cfg.d)
+    return {"workload": "config1 Tikhonov solve in fp32 mode (y, x fp32; LR stage fp64; expansion fp32)",
+            "value": N / (ms * 1e-3), "unit": UNIT, "ms_per_solve": ms,
+            "path_compulsory": {"bytes": comp, "frac": comp / (ms * 1e-3) / 1e9 / hbm,
+                                "model": "(4 N + 4 N/d) bytes: fp32 y in, fp32 x out"},
+            "e2e": {"value": N / e2e_s, "unit": UNIT, "ms_per_step": e2e_s * 1e3,
+                    "h2d_bytes_per_step": int(y32.nbytes), "d2h_bytes_per_step": int(N * 4),
+                    "api": "vsr_tikhonov_solve_f32 (pinned fp32 host y, x)"},
+            "accuracy": "rel L2 vs the fp64 solve ~5e-8 (tests/test_fp32.py)"}
+
+
+def bench_tv(args, ctx, V, synth, torch, stream, local, hbm, idx=2, precision="f64"):
     """ADMM-TV iteration throughput on configs[2] (256^3, d = 64) or configs[3]
-    (512x512x256, d = (2,2,4)) through the single-GPU path."""
+    (512x512x256, d = (2,2,4)) through the single-GPU path (precision "f32":
+    the fp32 mode)."""
     cfg = synth.CONFIGS[idx]
     inp = synth.make_inputs(cfg, with_truth=False)
     N = cfg.voxels
@@ -621,7 +671,8 @@ def bench_tv(args, ctx, V, synth, torch, stream, local, hbm, idx=2):
     k = max(args.steps, 10)
     iters = 2 * k + max(args.warmup, 3)
     tcfg = V.TvAdmmConfig(lambda_=cfg.tv_lambda, mu=cfg.tv_mu, max_iters=iters, rel_tol=0.0,
-                          tau=1e-3 * cfg.tv_mu, init=V.INIT_PROVIDED if x0_d is not None else V.INIT_UPSAMPLED)
+                          tau=1e-3 * cfg.tv_mu, init=V.INIT_PROVIDED if x0_d is not None else V.INIT_UPSAMPLED,
+                          precision=precision)
     tv = V.TvDevice(ctx, spec, y_d, p_d, tcfg, x0_d)
     tv.iterate(max(args.warmup, 3))
     ctx.synchronize()
@@ -643,7 +694,11 @@ def bench_tv(args, ctx, V, synth, torch, stream, local, hbm, idx=2):
     rep = tv.report()
     tv_sep = tv.separable()
     tv.close()
+    f32 = precision == "f32"
+    # fp32 mode: every HR volume / spectrum term halves; the LR tables stay fp64
     path = V.tv_algorithmic_bytes(cfg.hr, cfg.rates)
+    if f32:
+        path = 80 * N + 16 * (N // cfg.d)
     rows = {}
     sep = tv_sep
     for name, (tot, cnt) in stages.items():
@@ -653,16 +708,20 @@ def bench_tv(args, ctx, V, synth, torch, stream, local, hbm, idx=2):
             a, b = STAGE_BYTES[name]
             if sep and name in SEP_STAGES:
                 a -= 16
+            if f32:
+                a = a / 2
             byts = a * N + b * (N // cfg.d)
             r["gbs"] = byts / (avg * 1e-3) / 1e9
             r["frac"] = r["gbs"] / hbm
         rows[name] = r
     hr, lr = cfg.hr, cfg.lr
-    return {"workload": f"config{idx}: ADMM-TV fp64 {hr[0]}x{hr[1]}x{hr[2]} -> {lr[0]}x{lr[1]}x{lr[2]} "
-                        f"(d={cfg.d}), lambda {cfg.tv_lambda:g}, mu {cfg.tv_mu:g}, tau 1e-3*mu, single GPU",
+    return {"workload": f"config{idx}: ADMM-TV {'fp32 mode' if f32 else 'fp64'} {hr[0]}x{hr[1]}x{hr[2]} -> "
+                        f"{lr[0]}x{lr[1]}x{lr[2]} (d={cfg.d}), lambda {cfg.tv_lambda:g}, mu {cfg.tv_mu:g}, "
+                        f"tau 1e-3*mu, single GPU",
             "value": N / (ms * 1e-3), "unit": "HR voxels/s per ADMM-TV iteration", "ms_per_iter": ms,
             "iters_timed": k, "path_frac": path / (ms * 1e-3) / 1e9 / hbm, "lambda_separable": tv_sep,
-            "path_model": "(160 + 16/d) N bytes per iteration", "objective_last": rep.objective[-1],
+            "path_model": "(80 + 16/d) N bytes per iteration (fp32 state)" if f32
+                          else "(160 + 16/d) N bytes per iteration", "objective_last": rep.objective[-1],
             "stages": rows, "stages_ms_per_iter": ms_prof}
 
 
@@ -803,6 +862,7 @@ def main():
     ap.add_argument("--no-tv", action="store_true")
     ap.add_argument("--no-config4", action="store_true", help="skip the 1024^3 single-GPU config-4 timing")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-fp32", action="store_true", help="skip the fp32-mode blocks")
     ap.add_argument("--no-fft-path", action="store_true", help="skip timing the general FFT-path solve")
     ap.add_argument("--no-sharded", action="store_true", help="skip the slab-sharded config-3/4 timings")
     args = ap.parse_args()

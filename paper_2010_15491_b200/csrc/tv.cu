@@ -50,6 +50,41 @@ __device__ __forceinline__ double norm3(double a, double b, double c, double* in
     return m2 * r;
 }
 
+// fp32 mode (the fast stencil with S = float): the same shrink in fp32
+struct ShrunkF {
+    float u0, u1, u2, dn0, dn1, dn2, r0, r1, r2;
+};
+__device__ __forceinline__ float norm3(float a, float b, float c, float* inv) {
+    const float m2 = a * a + b * b + c * c;
+    float r;
+    if (m2 > 1e-30f && m2 < 1e30f) {
+        r = rsqrtf(m2);
+        r = r * fmaf(-0.5f * m2 * r, r, 1.5f);  // one Newton step: ~1 ulp
+    } else {
+        r = m2 > 0.0f ? rsqrtf(m2) : 0.0f;
+    }
+    *inv = r;
+    return m2 * r;
+}
+__device__ __forceinline__ ShrunkF shrink_point(float l0, float l1, float l2, float d0, float d1, float d2,
+                                                float thr) {
+    ShrunkF o;
+    const float n0 = l0 + d0, n1 = l1 + d1, n2 = l2 + d2;
+    float inv;
+    const float mag = norm3(n0, n1, n2, &inv);
+    const float f = mag > thr ? 1.0f - thr * inv : 0.0f;
+    o.u0 = f * n0;
+    o.u1 = f * n1;
+    o.u2 = f * n2;
+    o.dn0 = n0 - o.u0;
+    o.dn1 = n1 - o.u1;
+    o.dn2 = n2 - o.u2;
+    o.r0 = o.u0 - o.dn0;
+    o.r1 = o.u1 - o.dn1;
+    o.r2 = o.u2 - o.dn2;
+    return o;
+}
+
 // solvers.cpp:286-301 (factor = mag > t ? 1 - t/mag : 0) and :387-390;
 // t/mag evaluated as t * rsqrt(mag^2).
 __device__ __forceinline__ Shrunk shrink_point(double l0, double l1, double l2, double d0, double d1,
@@ -275,12 +310,6 @@ __host__ __device__ constexpr size_t fast_smem_doubles() {
     return (size_t)3 * FXS + 2 * FDS + TY * (TX + 1) + (TY + 1) * TX;
 }
 
-// pair loads of the storage type (double, or float in fp32 mode) as double2
-__device__ __forceinline__ double2 ld_pair(const double* p) { return __ldg(reinterpret_cast<const double2*>(p)); }
-__device__ __forceinline__ double2 ld_pair(const float* p) {
-    const float2 v = __ldg(reinterpret_cast<const float2*>(p));
-    return make_double2(v.x, v.y);
-}
 
 // S = double: the reference precision.  S = float (fp32 mode): x, dual,
 // dual' and theta are stored in fp32 (half the HBM bytes); the stencil
@@ -293,9 +322,11 @@ __global__ void __launch_bounds__(STH)
                            double* __restrict__ partials, int halo, long long dsi, long long dso,
                            const S* __restrict__ ylo_x = nullptr, const S* __restrict__ yhi_x = nullptr,
                            const S* __restrict__ ylo_d = nullptr) {
-    extern __shared__ double sm[];
-    double* rx = sm + 3 * FXS + 2 * FDS;  // [TY][TX+1]
-    double* ry = rx + TY * (TX + 1);       // [TY+1][TX]
+    using S2 = std::conditional_t<std::is_same<S, double>::value, double2, float2>;
+    extern __shared__ double sm_raw[];
+    S* sm = reinterpret_cast<S*>(sm_raw);
+    S* rx = sm + 3 * FXS + 2 * FDS;  // [TY][TX+1]
+    S* ry = rx + TY * (TX + 1);       // [TY+1][TX]
     __shared__ double red[32 * 4];
 
     const int tid = threadIdx.x;
@@ -357,19 +388,20 @@ __global__ void __launch_bounds__(STH)
         return plane * (long long)(halo ? z : (z < 0 ? z + s : (z >= s ? z - s : z)));
     };
     // smem ring: x slots rotate through three buffers, dual through two
-    double* xsl[3] = {sm, sm + FXS, sm + 2 * FXS};
-    double* dsl[2] = {sm + 3 * FXS, sm + 3 * FXS + FDS};
+    S* xsl[3] = {sm, sm + FXS, sm + 2 * FXS};
+    S* dsl[2] = {sm + 3 * FXS, sm + 3 * FXS + FDS};
+    auto ld_pair = [](const S* p) { return __ldg(reinterpret_cast<const S2*>(p)); };
 
-    double2 rxv = make_double2(0.0, 0.0), rdv[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
+    S2 rxv{}, rdv[2] = {S2{}, S2{}};
     // prologue: x(k0-1), x(k0), dual(k0-1) resident; x(k0+1), dual(k0) in registers
-    if (xa) *reinterpret_cast<double2*>(xsl[0] + xsm) = ld_pair(xsrc + zp(k0 - 1) + xoff);
+    if (xa) *reinterpret_cast<S2*>(xsl[0] + xsm) = ld_pair(xsrc + zp(k0 - 1) + xoff);
     if (!INIT) {
         const long long zo = zp(k0 - 1);
 #pragma unroll
         for (int q = 0; q < 2; ++q)
-            if (da[q]) *reinterpret_cast<double2*>(dsl[0] + dsm[q]) = ld_pair(dsrc[q] + zo + doff[q]);
+            if (da[q]) *reinterpret_cast<S2*>(dsl[0] + dsm[q]) = ld_pair(dsrc[q] + zo + doff[q]);
     }
-    if (xa) *reinterpret_cast<double2*>(xsl[1] + xsm) = ld_pair(xsrc + zp(k0) + xoff);
+    if (xa) *reinterpret_cast<S2*>(xsl[1] + xsm) = ld_pair(xsrc + zp(k0) + xoff);
     const S* xnext = xsrc + xoff;    // advanced below; holds plane k+3 at step k
     const S* dnext[2] = {dsrc[0] + doff[0], dsrc[1] + doff[1]};  // plane k+2 at step k
     long long zx = zp(k0 + 1), zd = zp(k0);
@@ -393,22 +425,23 @@ __global__ void __launch_bounds__(STH)
     const int di = (ty + 1) * FDW + tx + 2;
 
     double acc_res = 0.0, acc_tv = 0.0, acc_dx = 0.0, acc_xp = 0.0;
-    double rz_prev = 0.0;
+    S rz_prev = 0;
+    const S thr_s = (S)thr;
     long long zo = zp(k0 - 1);
     // The march is unrolled by 6 (lcm of the x ring of 3 slots and the dual ring
     // of 2), so every slot is a compile-time offset of the shared-memory base.
     auto step = [&](int k, auto x0, auto x1, auto x2, auto d0, auto d1) {
-        double* const XS0 = sm + decltype(x0)::value * FXS;
-        double* const XS1 = sm + decltype(x1)::value * FXS;
-        double* const XS2 = sm + decltype(x2)::value * FXS;
-        double* const DS0 = sm + 3 * FXS + decltype(d0)::value * FDS;
-        double* const DS1 = sm + 3 * FXS + decltype(d1)::value * FDS;
+        S* const XS0 = sm + decltype(x0)::value * FXS;
+        S* const XS1 = sm + decltype(x1)::value * FXS;
+        S* const XS2 = sm + decltype(x2)::value * FXS;
+        S* const DS0 = sm + 3 * FXS + decltype(d0)::value * FDS;
+        S* const DS1 = sm + 3 * FXS + decltype(d1)::value * FDS;
         // registers -> smem for step k+1, then request x(k+3), dual(k+2)
-        if (k + 2 <= k1 && xa) *reinterpret_cast<double2*>(XS2 + xsm) = rxv;
+        if (k + 2 <= k1 && xa) *reinterpret_cast<S2*>(XS2 + xsm) = rxv;
         if (!INIT && k + 1 <= k1 - 1) {
 #pragma unroll
             for (int q = 0; q < 2; ++q)
-                if (da[q]) *reinterpret_cast<double2*>(DS1 + dsm[q]) = rdv[q];
+                if (da[q]) *reinterpret_cast<S2*>(DS1 + dsm[q]) = rdv[q];
         }
         if (k + 3 <= k1) {
             zx += plane;
@@ -424,15 +457,15 @@ __global__ void __launch_bounds__(STH)
         }
         __syncthreads();
         const bool warm = k < k0;
-        const double* X0 = XS0;
-        const double* X1 = XS1;
-        [[maybe_unused]] const double* D0 = DS0;
+        const S* X0 = XS0;
+        const S* X1 = XS1;
+        [[maybe_unused]] const S* D0 = DS0;
 
-        const double xc = X0[xi];
-        const double l0 = X0[xi + 1] - xc;
-        const double l1 = X0[xi + FXW] - xc;
-        const double l2 = X1[xi] - xc;
-        double r0, r1, r2;
+        const S xc = X0[xi];
+        const S l0 = X0[xi + 1] - xc;
+        const S l1 = X0[xi + FXW] - xc;
+        const S l2 = X1[xi] - xc;
+        S r0, r1, r2;
         if constexpr (INIT) {
             r0 = l0;
             r1 = l1;
@@ -443,25 +476,25 @@ __global__ void __launch_bounds__(STH)
                 dual_out[dso + idx] = (S)0;
                 dual_out[2 * dso + idx] = (S)0;
                 {
-                    double inv_;
-                    acc_tv += norm3(l0, l1, l2, &inv_);
+                    S inv_;
+                    acc_tv += (double)norm3(l0, l1, l2, &inv_);
                 }
             }
         } else {
-            const Shrunk o = shrink_point(l0, l1, l2, D0[di], D0[FDH * FDW + di], D0[2 * FDH * FDW + di], thr);
+            const auto o = shrink_point(l0, l1, l2, D0[di], D0[FDH * FDW + di], D0[2 * FDH * FDW + di], thr_s);
             r0 = o.r0;
             r1 = o.r1;
             r2 = o.r2;
             if (!warm && valid) {
                 const long long idx = col + zo;
-                dual_out[idx] = (S)o.dn0;
-                dual_out[dso + idx] = (S)o.dn1;
-                dual_out[2 * dso + idx] = (S)o.dn2;
+                dual_out[idx] = o.dn0;
+                dual_out[dso + idx] = o.dn1;
+                dual_out[2 * dso + idx] = o.dn2;
                 const double e0 = l0 - o.u0, e1 = l1 - o.u1, e2 = l2 - o.u2;
                 acc_res += e0 * e0 + e1 * e1 + e2 * e2;
                 {
-                    double inv_;
-                    acc_tv += norm3(l0, l1, l2, &inv_);
+                    S inv_;
+                    acc_tv += (double)norm3(l0, l1, l2, &inv_);
                 }
             }
         }
@@ -477,17 +510,17 @@ __global__ void __launch_bounds__(STH)
             rx[ty * (TX + 1) + tx + 1] = r0;
             ry[(ty + 1) * TX + tx] = r1;
             if (hwork) {  // halo: rho_x at ii = -1, rho_y at jj = -1
-                const double hc = X0[hx];
-                const double h0 = X0[hx + 1] - hc;
-                const double h1 = X0[hx + FXW] - hc;
-                [[maybe_unused]] const double h2 = X1[hx] - hc;
-                double q0, q1;
+                const S hc = X0[hx];
+                const S h0 = X0[hx + 1] - hc;
+                const S h1 = X0[hx + FXW] - hc;
+                [[maybe_unused]] const S h2 = X1[hx] - hc;
+                S q0, q1;
                 if constexpr (INIT) {
                     q0 = h0;
                     q1 = h1;
                 } else {
-                    const Shrunk o =
-                        shrink_point(h0, h1, h2, D0[hd], D0[FDH * FDW + hd], D0[2 * FDH * FDW + hd], thr);
+                    const auto o =
+                        shrink_point(h0, h1, h2, D0[hd], D0[FDH * FDW + hd], D0[2 * FDH * FDW + hd], thr_s);
                     q0 = o.r0;
                     q1 = o.r1;
                 }
@@ -500,10 +533,10 @@ __global__ void __launch_bounds__(STH)
         __syncthreads();
         if (!warm && valid) {
             // diff_adjoint sum in axis order (solvers.cpp:367-373): ((adj_x) + adj_y) + adj_z
-            const double ax = rx[ty * (TX + 1) + tx] - rx[ty * (TX + 1) + tx + 1];
-            const double ay = ry[ty * TX + tx] - ry[(ty + 1) * TX + tx];
-            const double az = rz_prev - r2;
-            theta[col + zo] = (S)((ax + ay) + az);
+            const S ax = rx[ty * (TX + 1) + tx] - rx[ty * (TX + 1) + tx + 1];
+            const S ay = ry[ty * TX + tx] - ry[(ty + 1) * TX + tx];
+            const S az = rz_prev - r2;
+            theta[col + zo] = (ax + ay) + az;
         }
         rz_prev = r2;
         // rotate the rings: x slots (k, k+1, k+2) -> (k+1, k+2, k+3); dual (k, k+1) -> (k+1, k+2)
@@ -722,7 +755,7 @@ void launch_tv_stencil_f32(const Dims& d, bool init, const float* x, const float
     const StencilGeom g = stencil_geom(d);
     const int m = (int)d.m, n = (int)d.n, s = (int)d.s;
     if (m % 2) throw std::logic_error("tv stencil (fp32 mode): axis 1 must be even");
-    const size_t smem = fast_smem_doubles() * sizeof(double);
+    const size_t smem = fast_smem_doubles() * sizeof(float);
     const long long N = (long long)d.count();
 #define VSR_FAST(I, R)                                                                                      \
     tv_stencil_fast_kernel<I, R, float><<<g.grid, STH, smem, st>>>(m, n, s, g.kc, x, dual_in, dual_out, theta, \

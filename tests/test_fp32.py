@@ -136,3 +136,30 @@ def test_tikhonov_fp32_rejects_general_path(V):
     with pytest.raises(ValueError, match="fp32 mode"):
         op.solve_f32(rng.uniform(0, 1, V.shape_of(spec.lr)))
     op.close()
+
+
+# ------------------------------------------------------------------ full size
+@pytest.mark.parametrize("cfg_idx", [1, 2, 3])
+def test_fp32_full_size_configs(V, cfg_idx):
+    """The BASELINE configs at full size and full iteration counts: fp32 mode
+    against the fp64 path (itself pinned to the reference binary at full size,
+    profiles/r02_fullsize_parity.md)."""
+    cfg = synth.CONFIGS[cfg_idx]
+    inp = synth.make_inputs(cfg)
+    spec = V.DecimationSpec(cfg.hr, cfg.rates)
+    if cfg.solver == "tikhonov":
+        op = V.TikhonovOperator(V.psf_to_spectrum(inp.psf), spec, V.TikhonovConfig(cfg.reg, inp.xbar))
+        x64, x32 = op.solve(inp.y), op.solve_f32(inp.y).astype(np.float64)
+        op.close()
+    else:
+        x = {}
+        for prec in ("f64", "f32"):
+            init = V.INIT_PROVIDED if inp.x0 is not None else V.INIT_ZERO
+            c = V.TvAdmmConfig(lambda_=cfg.tv_lambda, mu=cfg.tv_mu, max_iters=cfg.tv_iters, rel_tol=0.0,
+                               tau=1e-3 * cfg.tv_mu, init=init, init_volume=inp.x0, precision=prec)
+            x[prec] = V.admm_tv(inp.y, inp.psf, spec, c)[0]
+        x64, x32 = x["f64"], x["f32"]
+    e = rel_err(x32, x64)
+    dp = abs(_psnr(inp.truth, x32) - _psnr(inp.truth, x64))
+    print(f"full-size config {cfg_idx}: rel L2 {e:.2e}, PSNR gap {dp:.2e} dB")
+    assert e <= FP32_TOL and dp < PSNR_TOL
