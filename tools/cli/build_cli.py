@@ -11,6 +11,9 @@ library, so `volsr tikhonov|tv|bench|...` runs the hot path on the GPU.
   tests/cpp/_build/ref_test_cli
                             the reference's CLI test suite (proj/tests/test_cli.cpp)
                             compiled unchanged; it runs the binary named by $VOLSR_CLI
+  tests/cpp/_build/ref_acceptance
+                            the reference's acceptance suite (proj/tests/acceptance_main.cpp)
+                            compiled unchanged against the mirror
 
 Needs /root/reference (this container, __graft_entry__.build()); the
 binaries travel to the GPU box with the repo.
@@ -59,6 +62,10 @@ def build() -> bool:
     _run(["g++", *flags, *shim, f"-I{REF / 'tests'}", str(REF / "tests" / "test_cli.cpp"), objs[1], objs[0],
           f"-L{LIB}", "-lvsr_b200", "-Wl,-rpath,$ORIGIN/../../../paper_2010_15491_b200/_lib",
           "-o", str(CPP_BUILD / "ref_test_cli")])
+    # the reference's acceptance suite (proj/tests/acceptance_main.cpp), unchanged
+    _run(["g++", *flags, *shim, f"-I{REF / 'tests'}", str(REF / "tests" / "acceptance_main.cpp"), *objs,
+          f"-L{LIB}", "-lvsr_b200", "-Wl,-rpath,$ORIGIN/../../../paper_2010_15491_b200/_lib",
+          "-o", str(CPP_BUILD / "ref_acceptance")])
     # the same CLI on the reference library (oracle/_ref, built by oracle/Makefile)
     ref_objs = [REF_OBJ / f"{n}.o" for n in ("volume", "fft", "operators", "spectral", "solvers", "dense", "sim",
                                              "metrics", "volume_io", "fftw_shim")]
