@@ -26,12 +26,13 @@ def main(mode="all", reps=2):
         for _ in range(reps):
             op.solve(y)
         op.close()
-    if mode in ("all", "tv", "bench"):
+    if mode in ("all", "tv", "bench", "tv32"):
         hr, rates = (256, 256, 256), (4, 4, 4)
         spec = V.DecimationSpec(hr, rates)
         psf = V.make_gaussian_psf((13, 13, 13), (1.5, 1.5, 1.5), hr)
         y = rng.uniform(0, 1, V.shape_of(spec.lr))
-        cfg = V.TvAdmmConfig(lambda_=2e-3, mu=0.05, max_iters=reps, rel_tol=0.0, tau=5e-5)
+        cfg = V.TvAdmmConfig(lambda_=2e-3, mu=0.05, max_iters=reps, rel_tol=0.0, tau=5e-5,
+                             precision="f32" if mode == "tv32" else "f64")
         V.admm_tv(y, psf, spec, cfg)
     ctx.synchronize()
     print("prof_step ok", V.launch_count())
