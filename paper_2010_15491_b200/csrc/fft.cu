@@ -159,7 +159,10 @@ struct RPairShape {
     static constexpr int R = Pl::R, P = Pl::P, T = kRPairCols, TP = T / 2;
     static constexpr int TG = (TP * P) >= 128 ? 1 : 128 / (TP * P);  // tiles per CTA
     static constexpr int THREADS = TG * TP * P;
-    static constexpr int SMEM = TG * TP * L;
+    // per tile: the exchange (TP lines of L) or, in the inverse, the staged
+    // half-spectrum planes 0..L/2 (2 complex per pair each)
+    static constexpr int GREG = TP * (L + 2);
+    static constexpr int SMEM = TG * GREG;
 };
 
 template <int L, class C = double2>
@@ -175,7 +178,7 @@ __global__ void __launch_bounds__(RPairShape<L>::THREADS)
     const long long tile = (long long)blockIdx.x * Sh::TG + g;
     const bool active = tile < tiles;
     const long long tpo = S / T, o = active ? tile / tpo : 0, c = active ? (tile % tpo) * T + 2 * lp : 0;
-    auto sidx = [&](int q) { return g * (L * TP) + q * TP + lp; };
+    auto sidx = [&](int q) { return g * Sh::GREG + q * TP + lp; };
     const C* src = reinterpret_cast<const C*>(in + c + S * (long long)L * o);
     const long long S2 = S / 2;
     C v[R];
@@ -220,20 +223,49 @@ __global__ void __launch_bounds__(RPairShape<L>::THREADS)
     const long long tile = (long long)blockIdx.x * Sh::TG + g;
     const bool active = tile < tiles;
     const long long tpo = S / T, o = active ? tile / tpo : 0, c = active ? (tile % tpo) * T + 2 * lp : 0;
-    auto sidx = [&](int q) { return g * (L * TP) + q * TP + lp; };
+    auto sidx = [&](int q) { return g * Sh::GREG + q * TP + lp; };
     const C* src = in + c + S * (long long)(L / 2 + 1) * o;
+    // each half-spectrum plane q <= L/2 is loaded ONCE (by the thread holding
+    // position q) and staged as [q][A | B][pair]; positions q > L/2 read the
+    // conjugate mirror plane L - q back from shared memory
+    // (fp64; the fp32 mode keeps the direct mirror loads, measured faster there)
+    C* stg = sm + g * Sh::GREG;
     C v[R];
+    if constexpr (!std::is_same<C, double2>::value) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int q = t + P * r;
+            const bool lo = q <= L / 2;
+            const C* p = src + S * (lo ? q : L - q);
+            C A = active ? __ldg(p) : cmake<C>((RT)0, (RT)0), B = active ? __ldg(p + 1) : cmake<C>((RT)0, (RT)0);
+            if (!lo) A.y = -A.y, B.y = -B.y;
+            v[r] = cmake<C>(A.x - B.y, A.y + B.x);
+        }
+    } else {
 #pragma unroll
     for (int r = 0; r < R; ++r) {
         const int q = t + P * r;
-        const bool lo = q <= L / 2;
-        const int pq = lo ? q : L - q;
-        const C* p = src + S * pq;
-        if constexpr (std::is_same<C, double2>::value)
-            if (rp.peer) p = rp.peer[rp.owner[pq]] + rp.off[pq] + c;
-        C A = active ? __ldg(p) : cmake<C>((RT)0, (RT)0), B = active ? __ldg(p + 1) : cmake<C>((RT)0, (RT)0);
-        if (!lo) A.y = -A.y, B.y = -B.y;
-        v[r] = cmake<C>(A.x - B.y, A.y + B.x);  // A + i B
+        if (q <= L / 2) {
+            const C* p = src + S * q;
+            if constexpr (std::is_same<C, double2>::value)
+                if (rp.peer) p = rp.peer[rp.owner[q]] + rp.off[q] + c;
+            const C A = active ? __ldg(p) : cmake<C>((RT)0, (RT)0), B = active ? __ldg(p + 1) : cmake<C>((RT)0, (RT)0);
+            stg[q * 2 * TP + lp] = A;
+            stg[q * 2 * TP + TP + lp] = B;
+            v[r] = cmake<C>(A.x - B.y, A.y + B.x);  // A + i B
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int q = t + P * r;
+        if (q > L / 2) {
+            C A = stg[(L - q) * 2 * TP + lp], B = stg[(L - q) * 2 * TP + TP + lp];
+            A.y = -A.y, B.y = -B.y;
+            v[r] = cmake<C>(A.x - B.y, A.y + B.x);
+        }
+    }
+    __syncthreads();  // the staging area becomes the exchange buffer
     }
     fftc::stockham<L, true>(v, t, sm, sidx, tw);
     C* dst = reinterpret_cast<C*>(out + c + S * (long long)L * o);

@@ -1,4 +1,3 @@
 mkdir -p gpurun_out
-python tools/prof_cfg4.py 2 > gpurun_out/plain.log 2>&1 && \
-ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/cfg4_launches.csv python tools/prof_cfg4.py 2 > gpurun_out/ncu.log 2>&1
-echo rc=$? >> gpurun_out/ncu.log
+timeout 1200 python -m pytest tests/test_gpu_parity.py tests/test_dist.py tests/test_fp32.py -q -x -k "admm_tv or slab or fft or tv_" > gpurun_out/t_inv.log 2>&1; echo rc=$? >> gpurun_out/t_inv.log
+timeout 900 python bench.py --steps 20 --warmup 5 --no-cpu --no-sharded --no-fft-path > gpurun_out/bench_inv.json 2> gpurun_out/bench.err
