@@ -457,6 +457,8 @@ __global__ void __launch_bounds__(MX_THREADS, 4) spatial_march_kernel(const __gr
         lgp[k] = A.u + loff[k];
     }
     int qb = 0;  // ring buffer of the next fetch
+    int zfs = NZB - (DM - 1) % NZB;  // prior slot of the next fetch: (q - (DM - 1)) mod NZB, q = 0
+    if (zfs == NZB) zfs = 0;
     auto fetch = [&](int q) {
         if (q < jend) {
             const long long zo = zq * plane;
@@ -474,14 +476,31 @@ __global__ void __launch_bounds__(MX_THREADS, 4) spatial_march_kernel(const __gr
         if (A.z && oz >= 0 && oz < nz && tid < CY * (CX / 2)) {
             const int h = tid % (CX / 2), y = tid / (CX / 2);
             const double* g = A.z + ((long long)(c30 + oz) * A.nl + cy0 + y) * A.ml + cx0 + 2 * h;
-            const unsigned sa = (unsigned)__cvta_generic_to_shared(&zs[oz % NZB][2 * tid]);
+            const unsigned sa = (unsigned)__cvta_generic_to_shared(&zs[zfs][2 * tid]);
             asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(g) : "memory");
         }
+        zfs = zfs + 1 == NZB ? 0 : zfs + 1;
         asm volatile("cp.async.commit_group;" ::: "memory");  // (empty past the chunk: uniform counting)
     };
     for (int q = 0; q < MX_PD; ++q) fetch(q);
     const long long hplane = (long long)A.n * A.m;
     T* const xrow = static_cast<T*>(A.x) + (long long)(Y0 + rg * RPT) * A.m + X0 + 2 * cp;
+    // loop-invariant per-thread offsets of the x and y stages (one item each
+    // when the stage fits the CTA) and rotating slot counters instead of the
+    // runtime modulos: the march is issue-bound
+    static_assert(NXI <= NT && NYI <= NT, "one stage-x / stage-y item per thread");
+    const bool xact = tid < NXI;
+    const int sxq = xact ? tid / (CX / 2) : 0, sxc = xact ? 2 * (tid - sxq * (CX / 2)) : 0;
+    const int sx_in = sxq * LXP + sxc, sx_out = sxq * W + R1 * sxc;
+    const bool yact = tid < NYI;
+    const int syc = yact ? 2 * (tid / W) : 0, syn = yact ? tid % W : 0;
+    const int sy_in = syc * W + syn, sy_out = R2 * syc * W + syn;
+    const long long xrs = A.m;
+    // advanced at the top of each phase p: lslot = (p - 1) mod NB (stage x's
+    // LR tile), zslot = (p - 3 - (DM - 1)) mod NZB (stage z's prior plane)
+    int lslot = NB - 2;
+    int zslot = ((-DM - 3) % NZB + NZB) % NZB;
+    T* xz = xrow + (long long)R3 * c30 * hplane;  // output plane R3 * c3 of the next stage-z plane
     for (int pb = 0; pb < jend + 3; pb += DM) {
 #pragma unroll
         for (int s = 0; s < DM; ++s) {
@@ -492,6 +511,8 @@ __global__ void __launch_bounds__(MX_THREADS, 4) spatial_march_kernel(const __gr
             // d. stage z on plane p - 3 (issued first: its loads and stores
             //    overlap the smem work of stages x and y below)
             const int jz = p - 3;
+            zslot = zslot + 1 == NZB ? 0 : zslot + 1;
+            lslot = lslot + 1 == NB ? 0 : lslot + 1;
             if (jz >= 0) {
                 const T* eb = ey[jz & 1];
                 const int slot = ((s - 3) % DM + DM) % DM;  // compile-time after the unroll
@@ -499,16 +520,15 @@ __global__ void __launch_bounds__(MX_THREADS, 4) spatial_march_kernel(const __gr
                 for (int rr = 0; rr < RPT; ++rr)
                     ring[rr][slot] = *reinterpret_cast<const T2*>(eb + (rg * RPT + rr) * W + 2 * cp);
                 if (jz >= DM - 1) {
-                    const int c3 = c30 + jz - (DM - 1);  // LR plane of the outputs
                     T zv[RPT];
 #pragma unroll
                     for (int rr = 0; rr < RPT; ++rr) {
                         const int row = rg * RPT + rr;
-                        zv[rr] = (A.z && row % R2 == 0) ? (T)zs[(c3 - c30) % NZB][(row / R2) * CX + cp] : (T)0;
+                        zv[rr] = (A.z && row % R2 == 0) ? (T)zs[zslot][(row / R2) * CX + cp] : (T)0;
                     }
+                    T* xp = xz;
 #pragma unroll
-                    for (int ph = 0; ph < R3; ++ph) {
-                        T* xp = xrow + (long long)(R3 * c3 + ph) * hplane;
+                    for (int ph = 0; ph < R3; ++ph, xp += hplane) {
 #pragma unroll
                         for (int rr = 0; rr < RPT; ++rr) {
                             T ax = 0, ay = 0;
@@ -524,19 +544,19 @@ __global__ void __launch_bounds__(MX_THREADS, 4) spatial_march_kernel(const __gr
                             T2 o;
                             o.x = ax;
                             o.y = ay;
-                            __stcs(reinterpret_cast<T2*>(xp + (long long)rr * A.m), o);  // streaming: x must not evict u
+                            __stcs(reinterpret_cast<T2*>(xp + rr * xrs), o);  // streaming: x must not evict u
                         }
                     }
+                    xz += R3 * hplane;
                 }
             }
             // b. stage x on plane p - 1
             const int jx = p - 1;
             if (jx >= 0 && jx < jend) {
-                const double* lb = lt[jx % NB];
+                const double* lb = lt[lslot];
                 T* xb = ex[jx & 1];
-                for (int it = tid; it < NXI; it += NT) {
-                    const int qy = it / (CX / 2), c = 2 * (it - qy * (CX / 2));
-                    const double* row = lb + qy * LXP + c;
+                if (xact) {
+                    const double* row = lb + sx_in;
                     T in[2 * NPAIR];
 #pragma unroll
                     for (int i = 0; i < NPAIR; ++i) {
@@ -554,7 +574,7 @@ __global__ void __launch_bounds__(MX_THREADS, 4) spatial_march_kernel(const __gr
                             for (int i = 0; i < DM; ++i) acc = fma(march_tap<T>(A, 0, ph * DM + i), in[cell + i], acc);
                             o[cell * R1 + ph] = acc;
                         }
-                    T* dst = xb + qy * W + R1 * c;
+                    T* dst = xb + sx_out;
 #pragma unroll
                     for (int i = 0; i < 2 * R1; i += 2) {
                         T2 w2;
@@ -569,11 +589,10 @@ __global__ void __launch_bounds__(MX_THREADS, 4) spatial_march_kernel(const __gr
             if (jy >= 0 && jy < jend) {
                 const T* xb = ex[jy & 1];
                 T* yb = ey[jy & 1];
-                for (int it = tid; it < NYI; it += NT) {
-                    const int cy = 2 * (it / W), n = it % W;
+                if (yact) {
                     T in[DM + 1];
 #pragma unroll
-                    for (int i = 0; i < DM + 1; ++i) in[i] = xb[(cy + i) * W + n];
+                    for (int i = 0; i < DM + 1; ++i) in[i] = xb[sy_in + i * W];
 #pragma unroll
                     for (int cell = 0; cell < 2; ++cell)
 #pragma unroll
@@ -581,7 +600,7 @@ __global__ void __launch_bounds__(MX_THREADS, 4) spatial_march_kernel(const __gr
                             T acc = 0;
 #pragma unroll
                             for (int i = 0; i < DM; ++i) acc = fma(march_tap<T>(A, 1, ph * DM + i), in[cell + i], acc);
-                            yb[(R2 * (cy + cell) + ph) * W + n] = acc;
+                            yb[sy_out + (R2 * cell + ph) * W] = acc;
                         }
                 }
             }
