@@ -234,6 +234,14 @@ SEP_STAGES = {"tik_fold_ifft_axis3", "tv_fft3_fold_ifft3", "tik_fold_ifft_axis1"
               "tv_fft1_fold_ifft1_half"}
 
 
+def _guarded(fn):
+    """A side block that fails reports its error instead of losing the headline line."""
+    try:
+        return fn()
+    except Exception as e:  # noqa: BLE001
+        return {"error": f"{type(e).__name__}: {e}"[:400]}
+
+
 def run_b200(args, rank, world, local):
     import torch
     from paper_2010_15491_b200 import synth
@@ -417,14 +425,15 @@ def run_b200(args, rank, world, local):
     if not args.no_fft_path:
         line["fft3_vs_cufft"] = bench_fft_compare(args, ctx, V, torch, stream, local, hbm)
     if not args.no_sharded:
-        line["sharded"] = bench_sharded(args, ctx, V, synth, torch, rank, world, local, 3)
+        line["sharded"] = _guarded(lambda: bench_sharded(args, ctx, V, synth, torch, rank, world, local, 3))
     if rank == 0 and world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(cfg, inp)
     op.close()
     if world == 1 and not args.no_config4:
         line["config4"] = bench_config4(args, ctx, V, synth, torch, stream, local, hbm)
     if not args.no_sharded and not args.no_config4:
-        line["sharded_config4"] = bench_sharded(args, ctx, V, synth, torch, rank, world, local, 4, iters=3)
+        line["sharded_config4"] = _guarded(lambda: bench_sharded(args, ctx, V, synth, torch, rank, world, local, 4,
+                                                                 iters=3))
     if rank == 0:
         print(json.dumps(line), flush=True)
     return 0
