@@ -78,7 +78,9 @@ struct SwShape {
     // row pitch in elements: bank-conflict free row <-> line-interleaved, and
     // every row start 16-B aligned for the bulk copies (float2: L + 2)
     static constexpr int PITCH = sizeof(C) == 16 ? L + 1 : L + 2;
-    static constexpr int NBUF = 3;
+    // tile buffers: 3 fit at fp64 (64 KB tiles); the fp32 mode's 33 KB tiles
+    // allow 4, so each group's next tile is issued a whole tile-time ahead
+    static constexpr int NBUF = sizeof(C) == 16 ? 3 : 4;
     static constexpr size_t BUF = (size_t)A * PITCH * sizeof(C);
     // the per-position tables a[f1], |e^{2 pi i f1/m} - 1|^2 stay in shared
     // memory unless the three buffers leave no room (L = 1024: read from L1)
@@ -92,6 +94,7 @@ struct SwShape {
     static constexpr size_t TWB = TW_SMEM ? (size_t)L * sizeof(C) : 0;
     static constexpr size_t SMEM = 64 + NBUF * BUF + META + TAB + TWB + NG * ROWS + NG * 32 * sizeof(double);
     static_assert(SMEM <= 232448, "shared memory budget");
+    static_assert(2 * NBUF * 8 <= 64, "mbarrier header");
 };
 
 // per-line placement of a tile's alias row (the half-spectrum mirror rules of
@@ -194,7 +197,7 @@ __global__ void __launch_bounds__(SwShape<L, A, RM, C>::THREADS, 1) tv_sandwich_
     // within one phase, and the consumer of tile k + 3 may get there before
     // tile k's rows have even landed)
     unsigned long long* full = reinterpret_cast<unsigned long long*>(smraw);
-    unsigned long long* issued = full + 3;
+    unsigned long long* issued = full + Sh::NBUF;  // 2 NBUF <= 8 mbarriers in the 64-byte header
     C* bufs = reinterpret_cast<C*>(smraw + 64);
     unsigned char* tail = smraw + 64 + Sh::NBUF * Sh::BUF;
     LineMeta* meta = reinterpret_cast<LineMeta*>(tail);
