@@ -556,6 +556,15 @@ public:
         return x;
     }
     const DecimationSpec& spec() const { return spec_; }
+    // B200 extension: the fp32 mode on the spatial path (fp32 y / x, lexicographic);
+    // fp32_ok() tells whether this operator's path allows it
+    bool fp32_ok() const { return vsr_tikhonov_fp32_ok(h_) != 0; }
+    std::vector<float> solve_f32(const std::vector<float>& y) const {
+        if (y.size() != spec_.lr().count()) throw shape_error("TikhonovOperator::solve_f32: dims mismatch");
+        std::vector<float> x(spec_.hr().count());
+        detail::check(vsr_tikhonov_solve_f32(h_, y.data(), x.data()));
+        return x;
+    }
 
 private:
     DecimationSpec spec_;
@@ -620,6 +629,10 @@ struct TvAdmmConfig {
     enum class Init { Zero, UpsampledObservation, Provided };
     Init init = Init::Zero;
     Volume3D init_volume;
+    // B200 extension (not in the reference): the optional fp32 mode
+    // (include/vsr.h VSR_PRECISION_F32); the default keeps the reference precision
+    enum class Precision { F64, F32 };
+    Precision precision = Precision::F64;
 };
 
 // solvers.hpp:117 make_gamma(const DiffSpectra&, double)
@@ -678,7 +691,8 @@ inline std::pair<Volume3D, SolveReport> admm_tv(const Volume3D& y, const Volume3
         require_same_dims(cfg.init_volume.dims(), spec.hr(), "admm_tv: init volume");
     vsr_tv_config c{cfg.lambda, cfg.mu, cfg.max_iters, cfg.rel_tol, cfg.tau.has_value() ? 1 : 0,
                     cfg.tau.value_or(0.0), static_cast<int>(cfg.init),
-                    cfg.init == TvAdmmConfig::Init::Provided ? cfg.init_volume.data().data() : nullptr};
+                    cfg.init == TvAdmmConfig::Init::Provided ? cfg.init_volume.data().data() : nullptr,
+                    cfg.precision == TvAdmmConfig::Precision::F32 ? VSR_PRECISION_F32 : VSR_PRECISION_F64};
     SolveReport rep;
     rep.objective.resize(cfg.max_iters);
     rep.primal_residual.resize(cfg.max_iters);
@@ -694,4 +708,112 @@ inline std::pair<Volume3D, SolveReport> admm_tv(const Volume3D& y, const Volume3
     return {std::move(x), std::move(rep)};
 }
 
+// ---------------------------------------------------------------- B200 extensions
+// Slab-sharded solvers over P ranks (include/vsr.h vsr_comm_* / vsr_slab_*,
+// SURVEY §8(e)): rank p owns the HR rows y in [p n/P, (p+1) n/P) of every
+// plane; y and the PSF / Lambda are full volumes on every rank.  Slab results
+// come back as one (m, n/P, s) Volume3D per LOCAL rank (P for a local comm,
+// 1 for an NCCL comm).  Not part of the reference API.
+namespace b200 {
+
+class SlabComm {
+public:
+    // P virtual ranks in this process on the context's device
+    static SlabComm local(int nranks) {
+        vsr_comm* c = nullptr;
+        detail::check(vsr_comm_local(detail::ctx(), nranks, &c));
+        return SlabComm(c);
+    }
+    // one process per GPU over NCCL; rank 0's id (vsr_nccl_unique_id) on every rank
+    static SlabComm nccl(int nranks, int rank, const unsigned char id[128]) {
+        vsr_comm* c = nullptr;
+        detail::check(vsr_comm_nccl(detail::ctx(), nranks, rank, id, &c));
+        return SlabComm(c);
+    }
+    SlabComm(SlabComm&& o) noexcept : c_(o.c_) { o.c_ = nullptr; }
+    SlabComm(const SlabComm&) = delete;
+    SlabComm& operator=(const SlabComm&) = delete;
+    ~SlabComm() {
+        if (c_) vsr_comm_destroy(c_);
+    }
+    int nranks() const { int n = 0, r = 0, l = 0; vsr_comm_info(c_, &n, &r, &l); return n; }
+    int local_ranks() const { int n = 0, r = 0, l = 0; vsr_comm_info(c_, &n, &r, &l); return l; }
+    vsr_comm* handle() const { return c_; }
+
+private:
+    explicit SlabComm(vsr_comm* c) : c_(c) {}
+    vsr_comm* c_ = nullptr;
+};
+
+inline Dims3 slab_dims(const DecimationSpec& spec, const SlabComm& comm) {
+    const Dims3 hr = spec.hr();
+    return Dims3{hr.m, hr.n / static_cast<std::size_t>(comm.nranks()), hr.s};
+}
+
+// admm_tv (solvers.hpp:106-107) over the ranks; cfg.init == Provided takes
+// init_slabs (one per local rank) instead of cfg.init_volume
+inline std::pair<std::vector<Volume3D>, SolveReport> admm_tv_sharded(
+    const SlabComm& comm, const Volume3D& y, const Volume3D& psf, const DecimationSpec& spec,
+    const TvAdmmConfig& cfg, const std::vector<Volume3D>& init_slabs = {}) {
+    require_same_dims(y.dims(), spec.lr(), "admm_tv");
+    require_same_dims(psf.dims(), spec.hr(), "admm_tv: psf");
+    const int L = comm.local_ranks();
+    std::vector<Volume3D> xs(L, Volume3D(slab_dims(spec, comm)));
+    std::vector<double*> xp(L);
+    for (int i = 0; i < L; ++i) xp[i] = xs[i].data().data();
+    std::vector<const double*> ip;
+    if (cfg.init == TvAdmmConfig::Init::Provided) {
+        if ((int)init_slabs.size() != L) throw shape_error("admm_tv: init volume: one slab per local rank");
+        for (const auto& v : init_slabs) ip.push_back(v.data().data());
+    }
+    vsr_tv_config c{cfg.lambda, cfg.mu, cfg.max_iters, cfg.rel_tol, cfg.tau.has_value() ? 1 : 0,
+                    cfg.tau.value_or(0.0), static_cast<int>(cfg.init), nullptr, VSR_PRECISION_F64};
+    SolveReport rep;
+    rep.objective.resize(cfg.max_iters);
+    rep.primal_residual.resize(cfg.max_iters);
+    vsr_report vr{0, 0.0, 0.0, rep.objective.data(), rep.primal_residual.data()};
+    detail::check(vsr_slab_admm_tv(comm.handle(), detail::D3(spec.hr()).v, spec.rates_ptr(), y.data().data(),
+                                   psf.data().data(), &c, ip.empty() ? nullptr : ip.data(), xp.data(), &vr));
+    rep.iterations = vr.iterations;
+    rep.initial_objective = vr.initial_objective;
+    rep.seconds = vr.seconds;
+    rep.objective.resize(vr.iterations);
+    rep.primal_residual.resize(vr.iterations);
+    return {std::move(xs), std::move(rep)};
+}
+
+// TikhonovOperator (solvers.hpp:27-43) over the ranks; xbar as slabs
+class SlabTikhonovOperator {
+public:
+    SlabTikhonovOperator(const SlabComm& comm, const SpectrumDiag& lambda, const DecimationSpec& spec,
+                         double reg, const std::vector<Volume3D>& xbar_slabs)
+        : spec_(spec), comm_(&comm) {
+        require_same_dims(lambda.dims(), spec.hr(), "TikhonovOperator");
+        if ((int)xbar_slabs.size() != comm.local_ranks())
+            throw shape_error("TikhonovOperator: xbar: one slab per local rank");
+        std::vector<const double*> xb;
+        for (const auto& v : xbar_slabs) xb.push_back(v.data().data());
+        detail::check(vsr_slab_tikhonov_create(comm.handle(), detail::D3(spec.hr()).v, spec.rates_ptr(),
+                                               detail::cp(lambda.values), reg, xb.data(), &h_));
+    }
+    SlabTikhonovOperator(const SlabTikhonovOperator&) = delete;
+    SlabTikhonovOperator& operator=(const SlabTikhonovOperator&) = delete;
+    ~SlabTikhonovOperator() { vsr_slab_tikhonov_destroy(h_); }
+    std::vector<Volume3D> solve(const Volume3D& y) const {
+        require_same_dims(y.dims(), spec_.lr(), "TikhonovOperator::solve");
+        const int L = comm_->local_ranks();
+        std::vector<Volume3D> xs(L, Volume3D(slab_dims(spec_, *comm_)));
+        std::vector<double*> xp(L);
+        for (int i = 0; i < L; ++i) xp[i] = xs[i].data().data();
+        detail::check(vsr_slab_tikhonov_solve(h_, y.data().data(), xp.data()));
+        return xs;
+    }
+
+private:
+    DecimationSpec spec_;
+    const SlabComm* comm_;
+    vsr_slab_tikhonov* h_ = nullptr;
+};
+
+}  // namespace b200
 }  // namespace volsr

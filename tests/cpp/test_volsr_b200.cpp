@@ -232,6 +232,74 @@ int main() {
         CHECK(rel_err(x1, xstar) < 1e-10);
         CHECK(throws<std::invalid_argument>([&] { admm_l2l2(y, lam, spec, cfg, 0); }));
     }
+    {  // B200 extensions: the fp32 mode and the slab-sharded solvers through the mirror
+        std::mt19937_64 rng(11);
+        const Dims3 d{256, 32, 32};
+        const DecimationSpec spec(d, {4, 4, 4});
+        const Volume3D psf = make_gaussian_psf(PsfSpec::gaussian({5, 5, 5}, {1.5, 1.5, 1.5}), d);
+        const Volume3D y = random_volume(spec.lr(), rng, 0.0, 1.0);
+        TvAdmmConfig cfg;
+        cfg.lambda = 2e-3;
+        cfg.mu = 0.05;
+        cfg.max_iters = 5;
+        cfg.rel_tol = 0.0;
+        cfg.tau = 5e-5;
+        auto [x64, r64] = admm_tv(y, psf, spec, cfg);
+        cfg.precision = TvAdmmConfig::Precision::F32;
+        auto [x32, r32] = admm_tv(y, psf, spec, cfg);
+        CHECK(r32.iterations == 5);
+        CHECK(rel_err(x32, x64) < 1e-5);
+        cfg.precision = TvAdmmConfig::Precision::F64;
+        // two virtual ranks: the y-slabs joined back are the single-GPU result, bit for bit
+        const b200::SlabComm comm = b200::SlabComm::local(2);
+        auto [slabs, rs] = b200::admm_tv_sharded(comm, y, psf, spec, cfg);
+        CHECK(slabs.size() == 2);
+        double maxdiff = 0.0;
+        for (int p = 0; p < 2; ++p)
+            for (std::size_t k = 0; k < d.s; ++k)
+                for (std::size_t j = 0; j < d.n / 2; ++j)
+                    for (std::size_t i = 0; i < d.m; ++i)
+                        maxdiff = std::max(maxdiff, std::abs(slabs[p].at(i, j, k) - x64.at(i, j + p * d.n / 2, k)));
+        CHECK(maxdiff == 0.0);
+        CHECK(rs.iterations == 5);
+        // Tikhonov: slabs and the fp32 solve on the spatial path
+        const Dims3 d2{64, 64, 64};
+        const DecimationSpec s2(d2, {2, 2, 2});
+        const Volume3D psf2 = make_gaussian_psf(PsfSpec::gaussian({5, 5, 5}, {1.2, 1.2, 1.2}), d2);
+        const SpectrumDiag lam = psf_to_spectrum(psf2);
+        const Volume3D y2 = random_volume(s2.lr(), rng, 0.0, 1.0);
+        TikhonovConfig tc;
+        tc.lambda = 1e-3;
+        tc.xbar = zero_fill_upsample(y2, s2);
+        const TikhonovOperator op(lam, s2, tc);
+        const Volume3D xt = op.solve(y2);
+        CHECK(op.fp32_ok());
+        std::vector<float> yf(y2.data().begin(), y2.data().end());
+        const std::vector<float> xf = op.solve_f32(yf);
+        double num = 0.0, den = 0.0;
+        for (std::size_t q = 0; q < xf.size(); ++q) {
+            num += (xf[q] - xt[q]) * (xf[q] - xt[q]);
+            den += xt[q] * xt[q];
+        }
+        CHECK(std::sqrt(num / den) < 1e-5);
+        std::vector<Volume3D> xb;
+        for (int p = 0; p < 2; ++p) {
+            Volume3D v(Dims3{d2.m, d2.n / 2, d2.s});
+            for (std::size_t k = 0; k < d2.s; ++k)
+                for (std::size_t j = 0; j < d2.n / 2; ++j)
+                    for (std::size_t i = 0; i < d2.m; ++i) v.at(i, j, k) = tc.xbar.at(i, j + p * d2.n / 2, k);
+            xb.push_back(std::move(v));
+        }
+        const b200::SlabTikhonovOperator sop(comm, lam, s2, tc.lambda, xb);
+        const std::vector<Volume3D> xs = sop.solve(y2);
+        double md = 0.0;
+        for (int p = 0; p < 2; ++p)
+            for (std::size_t k = 0; k < d2.s; ++k)
+                for (std::size_t j = 0; j < d2.n / 2; ++j)
+                    for (std::size_t i = 0; i < d2.m; ++i)
+                        md = std::max(md, std::abs(xs[p].at(i, j, k) - xt.at(i, j + p * d2.n / 2, k)));
+        CHECK(md < 1e-12);
+    }
     std::printf("checks: %d failed: %d\n", g_checks, g_fail);
     return g_fail ? 1 : 0;
 }
