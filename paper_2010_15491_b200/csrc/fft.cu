@@ -242,22 +242,38 @@ __global__ void __launch_bounds__(RPairShape<L>::THREADS)
             v[r] = cmake<C>(A.x - B.y, A.y + B.x);
         }
     } else {
+    // q = t + P r with 0 <= t < P: slots r < R/2 hold planes below L/2, slot
+    // R/2 holds plane L/2 only on t = 0, the rest are mirrors.  All the plane
+    // loads are issued before the first use (one HBM latency per tile, not one
+    // per plane); the slab path's per-plane peer addresses are resolved first.
+    constexpr int RH = R / 2;
+    const C* pl[RH + 1];
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
+    for (int r = 0; r <= RH; ++r) {
+        const int q = min(t + P * r, L / 2);
+        pl[r] = src + S * q;
+        if constexpr (std::is_same<C, double2>::value)
+            if (rp.peer) pl[r] = rp.peer[rp.owner[q]] + rp.off[q] + c;
+    }
+    const bool mid = t == 0;  // slot RH is plane L/2
+    C A[RH + 1], B[RH + 1];
+#pragma unroll
+    for (int r = 0; r <= RH; ++r) {
+        const bool ld = active && (r < RH || mid);
+        A[r] = ld ? __ldg(pl[r]) : cmake<C>((RT)0, (RT)0);
+        B[r] = ld ? __ldg(pl[r] + 1) : cmake<C>((RT)0, (RT)0);
+    }
+#pragma unroll
+    for (int r = 0; r <= RH; ++r) {
+        if (r == RH && !mid) break;
         const int q = t + P * r;
-        if (q <= L / 2) {
-            const C* p = src + S * q;
-            if constexpr (std::is_same<C, double2>::value)
-                if (rp.peer) p = rp.peer[rp.owner[q]] + rp.off[q] + c;
-            const C A = active ? __ldg(p) : cmake<C>((RT)0, (RT)0), B = active ? __ldg(p + 1) : cmake<C>((RT)0, (RT)0);
-            stg[q * 2 * TP + lp] = A;
-            stg[q * 2 * TP + TP + lp] = B;
-            v[r] = cmake<C>(A.x - B.y, A.y + B.x);  // A + i B
-        }
+        stg[q * 2 * TP + lp] = A[r];
+        stg[q * 2 * TP + TP + lp] = B[r];
+        v[r] = cmake<C>(A[r].x - B[r].y, A[r].y + B[r].x);  // A + i B
     }
     __syncthreads();
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
+    for (int r = RH; r < R; ++r) {
         const int q = t + P * r;
         if (q > L / 2) {
             C A = stg[(L - q) * 2 * TP + lp], B = stg[(L - q) * 2 * TP + TP + lp];

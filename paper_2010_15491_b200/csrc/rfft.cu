@@ -88,6 +88,12 @@ __global__ void __launch_bounds__(RowShape<M>::THREADS)
 #pragma unroll
     for (int j = 0; j < R; ++j) buf[t + P * j] = active ? __ldg(in + t + P * j) : make_double2(0.0, 0.0);
     if (t == 0) buf[M] = active ? __ldg(in + M) : make_double2(0.0, 0.0);
+    // the subtrahend (cold in HBM) is fetched now, its latency hidden under the transform
+    double2 qv[R];
+    const double2* subz = reinterpret_cast<const double2*>(sub) + row * M;
+#pragma unroll
+    for (int j = 0; j < R; ++j)
+        qv[j] = (sub && active) ? __ldg(subz + fftc::Plan<M, row_r<M>()>::out_q(t, j)) : make_double2(0.0, 0.0);
     __syncthreads();
     double2 v[R];
 #pragma unroll
@@ -105,16 +111,10 @@ __global__ void __launch_bounds__(RowShape<M>::THREADS)
     fftc::stockham<M, true, decltype(sidx_r), row_r<M>()>(v, t, smr, sidx_r, twM);
     if (!active) return;
     double2* outz = reinterpret_cast<double2*>(x) + row * M;
-    const double2* subz = reinterpret_cast<const double2*>(sub) + row * M;
 #pragma unroll
     for (int j = 0; j < R; ++j) {
         const int n = fftc::Plan<M, row_r<M>()>::out_q(t, j);
-        double2 r = cscale(v[j], scale);
-        if (sub) {
-            const double2 q = __ldg(subz + n);
-            r = csub(r, q);
-        }
-        outz[n] = r;
+        outz[n] = csub(cscale(v[j], scale), qv[j]);
     }
 }
 

@@ -89,18 +89,22 @@ __global__ void __launch_bounds__(SwShape<L>::THREADS, 512 / SwShape<L>::THREADS
 #pragma unroll
         for (int r = 0; r < R; ++r) asm volatile("prefetch.global.L2 [%0];" ::"l"(Zl + p + S * (t + P * r)));
     }
+    // the filter's table reads are issued before the transform (latency hidden under it)
+    const int g1 = (int)(p % pitch), g2 = (int)(p / pitch);
+    const double ab2 = __ldg(a2 + g1) * __ldg(b2 + g2);
+    double cz[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) cz[r] = __ldg(c2 + t + P * r);
     fftc::stockham<L, false, decltype(sidx), kSwR>(v, t, smw, sidx, tw);
     fftc::to_natural<L, kSwR>(v);
     // v[r] = F_l(y) at g3 = t + P r (times 1/fs)
-    const int g1 = (int)(p % pitch), g2 = (int)(p / pitch);
     const double2 ab1 = Zl ? cmul(__ldg(a1 + g1), __ldg(b1 + g2)) : make_double2(0.0, 0.0);
-    const double ab2 = __ldg(a2 + g1) * __ldg(b2 + g2);
 #pragma unroll
     for (int r = 0; r < R; ++r) {
         const int g3 = t + P * r;
         const double2 y = cscale(v[r], cy);
         const double2 num = Zl ? csub(y, cmul(__ldg(Zl + p + S * g3), cmul(ab1, __ldg(c1 + g3)))) : y;
-        v[r] = cscale(num, rcp_pos(ab2 * __ldg(c2 + g3) + shift));
+        v[r] = cscale(num, rcp_pos(ab2 * cz[r] + shift));
     }
     __syncthreads();  // the exchange buffer is reused by the inverse transform
     fftc::stockham<L, true, decltype(sidx), kSwR>(v, t, smw, sidx, tw);
