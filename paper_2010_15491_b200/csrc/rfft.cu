@@ -48,6 +48,9 @@ __global__ void __launch_bounds__(RowShape<M>::THREADS)
     double2 v[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) v[r] = active ? __ldg(z + t + P * r) : make_double2(0.0, 0.0);
+    double2 wl[R];  // split twiddles, fetched under the transform
+#pragma unroll
+    for (int j = 0; j < R; ++j) wl[j] = __ldg(twL + t + P * j);
     auto sidx_r = [&](int q) { return ls * Sh::LPAD + q + q / R; };
     fftc::stockham<M, false, decltype(sidx_r), row_r<M>()>(v, t, smr, sidx_r, twM);
     __syncthreads();  // exchange buffer -> split buffer
@@ -63,7 +66,7 @@ __global__ void __launch_bounds__(RowShape<M>::THREADS)
         const double2 a = buf[k], b = buf[(M - k) & (M - 1)];
         const double2 e = make_double2(0.5 * (a.x + b.x), 0.5 * (a.y - b.y));
         const double2 o = make_double2(0.5 * (a.y + b.y), -0.5 * (a.x - b.x));  // -i (a - conj b) / 2
-        out[k] = cadd(e, cmul(__ldg(twL + k), o));
+        out[k] = cadd(e, cmul(wl[j], o));
     }
     if (t == 0) {
         const double2 a = buf[0];
@@ -88,6 +91,9 @@ __global__ void __launch_bounds__(RowShape<M>::THREADS)
 #pragma unroll
     for (int j = 0; j < R; ++j) buf[t + P * j] = active ? __ldg(in + t + P * j) : make_double2(0.0, 0.0);
     if (t == 0) buf[M] = active ? __ldg(in + M) : make_double2(0.0, 0.0);
+    double2 wl[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) wl[r] = __ldg(twL + t + P * r);
     // the subtrahend (cold in HBM) is fetched now, its latency hidden under the transform
     double2 qv[R];
     const double2* subz = reinterpret_cast<const double2*>(sub) + row * M;
@@ -102,7 +108,7 @@ __global__ void __launch_bounds__(RowShape<M>::THREADS)
         const double2 a = buf[k], b = buf[M - k];
         const double2 s = make_double2(a.x + b.x, a.y - b.y);   // a + conj b
         const double2 d = make_double2(a.x - b.x, a.y + b.y);   // a - conj b
-        const double2 w = __ldg(twL + k);                       // e^{-2 pi i k / L}
+        const double2 w = wl[r];                                // e^{-2 pi i k / L}
         const double2 wd = cmulc(w, d);                         // e^{+2 pi i k / L} d
         v[r] = make_double2(s.x - wd.y, s.y + wd.x);            // s + i wd
     }

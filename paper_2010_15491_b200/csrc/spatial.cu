@@ -388,8 +388,12 @@ struct MarchArgs {
     unsigned long long* bad;
 };
 
-template <class T>
+// ISO: the three axes share one tap set (an isotropic PSF at equal rates, the
+// common case): the DFMAs' uniform-register operands then fit without the
+// spill / refill traffic three distinct sets cause (~12 % of the instructions)
+template <class T, bool ISO>
 __device__ __forceinline__ T march_tap(const MarchArgs& A, int axis, int i) {
+    if (ISO) axis = 0;
     if constexpr (std::is_same<T, double>::value)
         return axis == 0 ? A.k1[i] : (axis == 1 ? A.k2[i] : A.k3[i]);
     else
@@ -399,8 +403,9 @@ __device__ __forceinline__ T march_tap(const MarchArgs& A, int axis, int i) {
 // T = double: the reference precision.  T = float (fp32 mode): the LR tile
 // and prior arrive as fp64 and are rounded on use; the three correlation
 // stages, the register ring and x run in fp32 (half the HBM bytes of x).
-template <int DM, int R1, int R2, int R3, int CY, class T = double>
+template <int DM, int R1, int R2, int R3, int CY, class T = double, bool ISO = false>
 __global__ void __launch_bounds__(MX_THREADS, 4) spatial_march_kernel(const __grid_constant__ MarchArgs A) {
+    static_assert(!ISO || (R1 == R2 && R2 == R3), "one tap set needs equal rates");
     using T2 = std::conditional_t<std::is_same<T, double>::value, double2, float2>;
     static_assert(R1 == 2, "stage z pairs (2c, 2c + 1) assume the lattice column is the even one");
     constexpr int CX = MX_CX, NT = MX_THREADS;
@@ -539,8 +544,8 @@ __global__ void __launch_bounds__(MX_THREADS, 4) spatial_march_kernel(const __gr
 #pragma unroll
                             for (int i = 0; i < DM; ++i) {
                                 const T2 v = ring[rr][(slot + 1 + i) % DM];
-                                ax = fma(march_tap<T>(A, 2, ph * DM + i), v.x, ax);
-                                ay = fma(march_tap<T>(A, 2, ph * DM + i), v.y, ay);
+                                ax = fma(march_tap<T, ISO>(A, 2, ph * DM + i), v.x, ax);
+                                ay = fma(march_tap<T, ISO>(A, 2, ph * DM + i), v.y, ay);
                             }
                             if (ph == 0) ax += zv[rr];
                             chk = fma(ax, (T)0, chk);
@@ -575,7 +580,7 @@ __global__ void __launch_bounds__(MX_THREADS, 4) spatial_march_kernel(const __gr
                         for (int ph = 0; ph < R1; ++ph) {
                             T acc = 0;
 #pragma unroll
-                            for (int i = 0; i < DM; ++i) acc = fma(march_tap<T>(A, 0, ph * DM + i), in[cell + i], acc);
+                            for (int i = 0; i < DM; ++i) acc = fma(march_tap<T, ISO>(A, 0, ph * DM + i), in[cell + i], acc);
                             o[cell * R1 + ph] = acc;
                         }
                     T* dst = xb + sx_out;
@@ -603,7 +608,7 @@ __global__ void __launch_bounds__(MX_THREADS, 4) spatial_march_kernel(const __gr
                         for (int ph = 0; ph < R2; ++ph) {
                             T acc = 0;
 #pragma unroll
-                            for (int i = 0; i < DM; ++i) acc = fma(march_tap<T>(A, 1, ph * DM + i), in[cell + i], acc);
+                            for (int i = 0; i < DM; ++i) acc = fma(march_tap<T, ISO>(A, 1, ph * DM + i), in[cell + i], acc);
                             yb[sy_out + (R2 * cell + ph) * W] = acc;
                         }
                 }
@@ -626,9 +631,9 @@ __global__ void __launch_bounds__(MX_THREADS, 4) spatial_march_kernel(const __gr
     }
 }
 
-template <int DM, int R3, int CY, class T>
+template <int DM, int R3, int CY, class T, bool ISO = false>
 static void launch_march_cy(MarchArgs& A, unsigned tx, unsigned ty, cudaStream_t st) {
-    auto kern = spatial_march_kernel<DM, 2, 2, R3, CY, T>;
+    auto kern = spatial_march_kernel<DM, 2, 2, R3, CY, T, ISO>;
     int dev = 0, sms = 0;
     VSR_CUDA(cudaGetDevice(&dev));
     VSR_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -660,15 +665,18 @@ static void launch_march_cy(MarchArgs& A, unsigned tx, unsigned ty, cudaStream_t
 }
 
 template <int DM, int R3, class T>
-static void launch_march_k(MarchArgs& A, unsigned tx, unsigned ty, cudaStream_t st) {
+static void launch_march_k(MarchArgs& A, unsigned tx, unsigned ty, bool iso, cudaStream_t st) {
     static const bool cy8 = [] {
         const char* e = std::getenv("VSR_MARCH_CY");  // 8-row column tiles unless VSR_MARCH_CY=4
         return !(e && e[0] == '4');
     }();
-    if (cy8 && ty % 2 == 0)
+    if (cy8 && ty % 2 == 0) {
+        if constexpr (R3 == 2)
+            if (iso) return launch_march_cy<DM, R3, 8, T, true>(A, tx, ty / 2, st);
         launch_march_cy<DM, R3, 8, T>(A, tx, ty / 2, st);
-    else
+    } else {
         launch_march_cy<DM, R3, 4, T>(A, tx, ty, st);
+    }
 }
 
 // The march kernel serves rates (2, 2, 2|4) with a tile-aligned LR grid.
@@ -745,11 +753,18 @@ static void march_dispatch(const Dims& hr, const int rates[3], const SpatialPlan
     M.u = u, M.z = z, M.x = x, M.bad = bad;
     const unsigned tx = (unsigned)(M.ml / MX_CX), ty = (unsigned)(M.nl / MX_CY);
     const bool r4 = rates[2] == 4;
+    // one tap set for all axes (bitwise equal; VSR_MARCH_ISO=0 forces the general kernel)
+    static const bool iso_on = [] {
+        const char* e = std::getenv("VSR_MARCH_ISO");
+        return !(e && e[0] == '0');
+    }();
+    bool iso = iso_on && !r4;
+    for (int i = 0; iso && i < 2 * dm; ++i) iso = kp[i] == kp[2 * dm + i] && kp[i] == kp[4 * dm + i];
     switch (dm) {
-        case 4: r4 ? launch_march_k<4, 4, T>(M, tx, ty, st) : launch_march_k<4, 2, T>(M, tx, ty, st); break;
-        case 5: r4 ? launch_march_k<5, 4, T>(M, tx, ty, st) : launch_march_k<5, 2, T>(M, tx, ty, st); break;
-        case 7: r4 ? launch_march_k<7, 4, T>(M, tx, ty, st) : launch_march_k<7, 2, T>(M, tx, ty, st); break;
-        default: r4 ? launch_march_k<8, 4, T>(M, tx, ty, st) : launch_march_k<8, 2, T>(M, tx, ty, st); break;
+        case 4: r4 ? launch_march_k<4, 4, T>(M, tx, ty, false, st) : launch_march_k<4, 2, T>(M, tx, ty, iso, st); break;
+        case 5: r4 ? launch_march_k<5, 4, T>(M, tx, ty, false, st) : launch_march_k<5, 2, T>(M, tx, ty, iso, st); break;
+        case 7: r4 ? launch_march_k<7, 4, T>(M, tx, ty, false, st) : launch_march_k<7, 2, T>(M, tx, ty, iso, st); break;
+        default: r4 ? launch_march_k<8, 4, T>(M, tx, ty, false, st) : launch_march_k<8, 2, T>(M, tx, ty, iso, st); break;
     }
 }
 

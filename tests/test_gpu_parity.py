@@ -163,7 +163,10 @@ SPATIAL_CASES = [((64, 64, 64), (2, 2, 2), (9, 9, 9), (1.0, 1.0, 1.0)),
                  ((96, 16, 8), (3, 2, 2), (9, 7, 7), (1.4, 1.0, 1.0)),
                  # z-march expand kernel: 13-tap (DM 7) at rate 2, config-3-like (DM 8, r3 = 4)
                  ((64, 32, 48), (2, 2, 2), (13, 13, 13), (1.5, 1.5, 1.5)),
-                 ((32, 16, 40), (2, 2, 4), (15, 15, 21), (1.2, 1.2, 2.0))]
+                 ((32, 16, 40), (2, 2, 4), (15, 15, 21), (1.2, 1.2, 2.0)),
+                 # z march with three distinct tap sets (the isotropic cases above share one)
+                 ((64, 32, 32), (2, 2, 2), (13, 11, 9), (1.5, 1.3, 1.1)),
+                 ((64, 32, 32), (2, 2, 2), (13, 13, 13), (1.5, 1.5, 1.4))]
 
 
 @pytest.mark.parametrize("dims,rates,ksz,sigma", SPATIAL_CASES)
@@ -599,6 +602,7 @@ print("ok", op.path())
     ({"VSR_MARCH_ZC": "5"}, (64, 64, 32), (2, 2, 2)),
     ({"VSR_MARCH_ZC": "1"}, (64, 64, 32), (2, 2, 2)),
     ({"VSR_MARCH_CY": "4"}, (64, 64, 32), (2, 2, 2)),
+    ({"VSR_MARCH_ISO": "0"}, (64, 64, 32), (2, 2, 2)),
     ({"VSR_NO_PIPE": "1"}, (256, 32, 32), (4, 4, 4)),
     ({"VSR_NO_PIPE": "1"}, (512, 16, 32), (2, 2, 4)),
 ])
