@@ -340,21 +340,24 @@ __global__ void __launch_bounds__(SwShape<L, A, RM, C>::THREADS, 1) tv_sandwich_
                 const double2 yraw = yrow_s[t + P * rr];
                 const double gwv = gwrow_s[t + P * rr];
                 const CT yv = from_d2<CT>(cscale(yraw, args.invsqrtd));
-                T Gg[DR];
-                CT Lr[DR], gv[DR];  // g_b kept in T between the two loops (it is up to 1/tau large)
+                // g_b kept in T between the two loops (it is up to 1/tau large);
+                // Gamma_b conj(Lambda_b) formed in the first loop (fewer live registers)
+                CT gl[DR], gv[DR];
                 T Sx = 0, Sy = 0;
 #pragma unroll
                 for (int br = 0; br < DR; ++br) {
                     const int r = rr + RD * br;
                     const int q = t + P * r;
-                    Lr[br] = from_d2<CT>(cmul(sa_t[q], bc_));
+                    const CT Lr = from_d2<CT>(cmul(sa_t[q], bc_));
+                    T Gg;
                     if constexpr (std::is_same<T, double>::value)
-                        Gg[br] = rcp_pos((nr_t[q] + base_g) + tb.tau);
+                        Gg = rcp_pos((nr_t[q] + base_g) + tb.tau);
                     else
-                        Gg[br] = __frcp_rn((float)((nr_t[q] + base_g) + tb.tau));
+                        Gg = __frcp_rn((float)((nr_t[q] + base_g) + tb.tau));
                     const CT vr = from_d2<CT>(to_d2(v[r]));
-                    gv[br] = cscale(cadd(cmulc(Lr[br], yv), cscale(vr, (T)cAs)), Gg[br]);
-                    const CT pr = cmul(Lr[br], gv[br]);
+                    gv[br] = cscale(cadd(cmulc(Lr, yv), cscale(vr, (T)cAs)), Gg);
+                    gl[br] = cmake<CT>(Gg * Lr.x, -(Gg * Lr.y));
+                    const CT pr = cmul(Lr, gv[br]);
                     Sx += pr.x;
                     Sy += pr.y;
                 }
@@ -372,7 +375,7 @@ __global__ void __launch_bounds__(SwShape<L, A, RM, C>::THREADS, 1) tv_sandwich_
 #pragma unroll
                 for (int br = 0; br < DR; ++br) {
                     const int r = rr + RD * br;
-                    const CT c = cmul(cmake<CT>(Gg[br] * Lr[br].x, -(Gg[br] * Lr[br].y)), w);
+                    const CT c = cmul(gl[br], w);
                     v[r] = from_d2<C>(to_d2(cscale(csub(gv[br], c), (T)args.inv_scale)));
                 }
                 if constexpr (FIT) {
