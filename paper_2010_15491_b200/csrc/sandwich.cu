@@ -89,10 +89,11 @@ struct SwShape {
     // per group: the tile's LR row of Y and of Gw (ml = L / dr entries, dr >= 2)
     static constexpr size_t ROWS = (size_t)(L / 2) * (sizeof(double2) + sizeof(double));
     static constexpr size_t META = (size_t)NBUF * A * 80;  // LineMeta per line of each buffer
-    // the twiddle table too, where it fits (L <= 512)
-    static constexpr bool TW_SMEM = L <= 512;
+    // the twiddle table too, where it fits (L <= 256; measured neutral at 512)
+    static constexpr bool TW_SMEM = L <= 256;
     static constexpr size_t TWB = TW_SMEM ? (size_t)L * sizeof(C) : 0;
-    static constexpr size_t SMEM = 64 + NBUF * BUF + META + TAB + TWB + NG * ROWS + NG * 32 * sizeof(double);
+    static constexpr size_t STASH = (size_t)NG * A * 24;  // per group: each line's store rows (LineStore)
+    static constexpr size_t SMEM = 64 + NBUF * BUF + META + TAB + TWB + NG * ROWS + NG * 32 * sizeof(double) + STASH;
     static_assert(SMEM <= 232448, "shared memory budget");
     static_assert(2 * NBUF * 8 <= 64, "mbarrier header");
 };
@@ -142,6 +143,26 @@ __device__ __forceinline__ LineInfo line_info(const FoldGeom& G, const int* __re
     const long long mrow = G.m * (nf2 + G.n * wpl(f3));
     li.sec = (role == 1 && !li.mir && (f3 == 0 || 2 * f3 == G.s) && mrow != li.wr) ? mrow : -1;
     return li;
+}
+
+// a line's store rows, copied out of its LineMeta before the inverse
+// transform (the issue after it re-arms the metadata) so they need not stay
+// in registers across the transform
+struct LineStore {
+    long long wr, sec;
+    int flip, pad;
+};
+static_assert(sizeof(LineStore) == 24, "LineStore layout");
+
+__device__ __forceinline__ double2 lds_d2(unsigned a) {
+    double2 v;
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ double lds_d(unsigned a) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+    return v;
 }
 
 struct SwArgs {
@@ -209,8 +230,11 @@ __global__ void __launch_bounds__(SwShape<L, A, RM, C>::THREADS, 1) tv_sandwich_
     tail += Sh::TWB;
     double* red_s = reinterpret_cast<double*>(tail);
     tail += Sh::NG * 32 * sizeof(double);
-    double2* yrow_s = reinterpret_cast<double2*>(tail + (threadIdx.x / Sh::GT) * Sh::ROWS);
-    double* gwrow_s = reinterpret_cast<double*>(yrow_s + ML);
+    LineStore* stash = reinterpret_cast<LineStore*>(tail + Sh::NG * Sh::ROWS) + (threadIdx.x / Sh::GT) * A;
+    // this group's LR rows of Y and Gw, by 32-bit shared address (a generic
+    // pointer here costs two registers across the whole tile loop)
+    const unsigned yrow_a = smem_u32(tail) + (threadIdx.x / Sh::GT) * (unsigned)Sh::ROWS;
+    const unsigned gwrow_a = yrow_a + ML * (unsigned)sizeof(double2);
     const double2* __restrict__ sa_t = Sh::TAB_SMEM ? sa_s : args.sep.a;
     const double* __restrict__ nr_t = Sh::TAB_SMEM ? nr_s : tb.nr;
 
@@ -292,9 +316,8 @@ __global__ void __launch_bounds__(SwShape<L, A, RM, C>::THREADS, 1) tv_sandwich_
     double fit = 0.0;  // this thread's data-fit terms over all its tiles (fixed order)
     const double cAs = args.cA * args.fwd_scale;  // theta_hat enters only as mu * fwd_scale * FFT(...)
 
-    // kk is CTA-uniform (a uniform register); k is recomputed from it
-    for (int kk = 0;; ++kk) {
-        const int k = Sh::NG * kk + (int)(threadIdx.x / GT);
+    // this group's tiles k = g, g + NG, ... (one loop-carried register)
+    for (int k = (int)(threadIdx.x / GT);; k += Sh::NG) {
         const int tile = blockIdx.x + k * gridDim.x;
         if (tile >= ntiles) break;
         const int b = k % Sh::NBUF;
@@ -305,10 +328,10 @@ __global__ void __launch_bounds__(SwShape<L, A, RM, C>::THREADS, 1) tv_sandwich_
         if (role != 2) {  // the tile's LR rows of Y and Gw -> this group's staging (cp.async)
             const long long lr = G.ml * (tt.x + G.nl * (long long)tt.y);
             for (int i = gt; i < ML; i += GT)
-                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(yrow_s + i)),
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(yrow_a + 16u * i),
                              "l"(args.Yl + lr + i) : "memory");
             for (int i = gt; i < ML / 2; i += GT)
-                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(gwrow_s + 2 * i)),
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(gwrow_a + 16u * i),
                              "l"(tb.gw + lr + 2 * i) : "memory");
             asm volatile("cp.async.commit_group;" ::: "memory");
         }
@@ -316,8 +339,6 @@ __global__ void __launch_bounds__(SwShape<L, A, RM, C>::THREADS, 1) tv_sandwich_
         mbar_wait(full + b, (unsigned)((k / Sh::NBUF) & 1));
         C v[R];
         double tfit = 0.0;
-        long long wr = -1, sec = -1;
-        int flip = 0;
         if (role != 2) {
             const bool mir = mt->mir;
 #pragma unroll
@@ -337,8 +358,8 @@ __global__ void __launch_bounds__(SwShape<L, A, RM, C>::THREADS, 1) tv_sandwich_
             auto fold_rr = [&](auto zero, const int rr) {
                 using T = decltype(zero);
                 using CT = std::conditional_t<std::is_same<T, double>::value, double2, float2>;
-                const double2 yraw = yrow_s[t + P * rr];
-                const double gwv = gwrow_s[t + P * rr];
+                const double2 yraw = lds_d2(yrow_a + 16u * (t + P * rr));
+                const double gwv = lds_d(gwrow_a + 8u * (t + P * rr));
                 const CT yv = from_d2<CT>(cscale(yraw, args.invsqrtd));
                 // g_b kept in T between the two loops (it is up to 1/tau large);
                 // Gamma_b conj(Lambda_b) formed in the first loop (fewer live registers)
@@ -396,8 +417,7 @@ __global__ void __launch_bounds__(SwShape<L, A, RM, C>::THREADS, 1) tv_sandwich_
             for (int rr = 0; rr < RD; ++rr) fold_rr(0.0, rr);
             // this line's store rows, read before the inverse transform's barriers
             // (after them, the issue below re-arms buffer b's metadata)
-            wr = mt->wr, sec = mt->sec;
-            flip = mir ? (int)0x80000000 : 0;
+            if (t == 0) stash[ln] = LineStore{mt->wr, mt->sec, mir ? (int)0x80000000 : 0, 0};
             fftc::stockham<L, true, decltype(sidx), RM, GroupSync<GT>, TwT>(v, t, sm, sidx, twp, gsync);
         } else {
             gsync();  // every thread of the group has seen this phase before it is re-armed
@@ -410,6 +430,8 @@ __global__ void __launch_bounds__(SwShape<L, A, RM, C>::THREADS, 1) tv_sandwich_
         }
         if (role != 2) {
             // direct rows as computed; mirrored rows (role 1) conjugated into their mirror position
+            const long long wr = stash[ln].wr, sec = stash[ln].sec;
+            const int flip = stash[ln].flip;
             if (wr >= 0) {
                 C* dst = outc + wr;
 #pragma unroll
