@@ -458,36 +458,36 @@ __global__ void __launch_bounds__(MX_THREADS, 4) spatial_march_kernel(const __gr
     T chk = 0;
     // LR plane tiles: cp.async ring of NB buffers, MX_PD planes in flight
     // per-element shared addresses of buffer 0 and global pointers of LR z = 0
+    // per-element shared addresses of buffer 0; 32-bit in-plane offsets
+    // against a running plane pointer (one wide add per element per fetch)
     unsigned lsa[NLD];
-    const double* lgp[NLD];
 #pragma unroll
-    for (int k = 0; k < NLD; ++k) {
-        lsa[k] = (unsigned)__cvta_generic_to_shared(&lt[0][lsm[k]]);
-        lgp[k] = A.u + loff[k];
-    }
-    int qb = 0;  // ring buffer of the next fetch
+    for (int k = 0; k < NLD; ++k) lsa[k] = (unsigned)__cvta_generic_to_shared(&lt[0][lsm[k]]);
+    const double* uz = A.u + zq * plane;  // LR plane zq
+    unsigned bo = 0;                      // byte offset of the next fetch's ring buffer
     int zfs = NZB - (DM - 1) % NZB;  // prior slot of the next fetch: (q - (DM - 1)) mod NZB, q = 0
     if (zfs == NZB) zfs = 0;
+    // the prior rows of this thread's (y, 2h) pair in output plane c3 = c30 + oz
+    const bool zact = A.z && tid < CY * (CX / 2);
+    const double* zp = A.z + ((long long)c30 * A.nl + cy0 + (zact ? tid / (CX / 2) : 0)) * A.ml + cx0 +
+                       2 * (zact ? tid % (CX / 2) : 0) - (long long)(DM - 1) * plane;
+    const unsigned zsa = (unsigned)__cvta_generic_to_shared(&zs[0][2 * tid]);
     auto fetch = [&](int q) {
         if (q < jend) {
-            const long long zo = zq * plane;
-            const unsigned bo = (unsigned)(qb * LTB) * 8u;
 #pragma unroll
             for (int k = 0; k < NLD; ++k)
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(lsa[k] + bo), "l"(lgp[k] + zo)
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(lsa[k] + bo), "l"(uz + loff[k])
                              : "memory");
-            zq = zq + 1 == A.sl ? 0 : zq + 1;
-            qb = qb + 1 == NB ? 0 : qb + 1;
+            uz += plane;
+            if (++zq == A.sl) zq = 0, uz = A.u;
+            bo = bo + LTB * 8u == NB * LTB * 8u ? 0u : bo + LTB * 8u;
         }
         // the lattice prior of output plane c3 (its last LR plane is q): cold in
         // HBM, so it rides in the same group, DM + 2 phases before stage z reads it
         const int oz = q - (DM - 1);
-        if (A.z && oz >= 0 && oz < nz && tid < CY * (CX / 2)) {
-            const int h = tid % (CX / 2), y = tid / (CX / 2);
-            const double* g = A.z + ((long long)(c30 + oz) * A.nl + cy0 + y) * A.ml + cx0 + 2 * h;
-            const unsigned sa = (unsigned)__cvta_generic_to_shared(&zs[zfs][2 * tid]);
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(g) : "memory");
-        }
+        if (zact && oz >= 0 && oz < nz)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(zsa + zfs * (unsigned)(CY * CX * 8)),
+                         "l"(zp + (long long)q * plane) : "memory");
         zfs = zfs + 1 == NZB ? 0 : zfs + 1;
         asm volatile("cp.async.commit_group;" ::: "memory");  // (empty past the chunk: uniform counting)
     };
@@ -758,8 +758,23 @@ static void march_dispatch(const Dims& hr, const int rates[3], const SpatialPlan
         const char* e = std::getenv("VSR_MARCH_ISO");
         return !(e && e[0] == '0');
     }();
+    // The per-axis factors of an isotropic PSF come out of three different
+    // lines of Lambda and differ in the last bits, so "equal" is within
+    // 1e-14 of the largest tap (an output error below 1e-14 relative, the
+    // same order as the 1e-14 support cut above); the shared set is the mean.
     bool iso = iso_on && !r4;
-    for (int i = 0; iso && i < 2 * dm; ++i) iso = kp[i] == kp[2 * dm + i] && kp[i] == kp[4 * dm + i];
+    double kmax = 0;
+    for (int i = 0; i < 2 * dm; ++i) kmax = std::max(kmax, std::fabs(kp[i]));
+    for (int i = 0; iso && i < 2 * dm; ++i)
+        iso = std::fabs(kp[i] - kp[2 * dm + i]) <= 1e-14 * kmax && std::fabs(kp[i] - kp[4 * dm + i]) <= 1e-14 * kmax;
+    if (iso)
+        for (int i = 0; i < 2 * dm; ++i) {
+            const double k = (kp[i] + kp[2 * dm + i] + kp[4 * dm + i]) / 3.0;
+            M.k1[i] = M.k2[i] = M.k3[i] = k;
+            M.f1[i] = M.f2[i] = M.f3[i] = (float)k;
+        }
+    if (const char* e = std::getenv("VSR_MARCH_DEBUG"))
+        if (e[0] == '1') std::fprintf(stderr, "vsr: z-march dm=%d r3=%d iso=%d\n", dm, rates[2], (int)iso);
     switch (dm) {
         case 4: r4 ? launch_march_k<4, 4, T>(M, tx, ty, false, st) : launch_march_k<4, 2, T>(M, tx, ty, iso, st); break;
         case 5: r4 ? launch_march_k<5, 4, T>(M, tx, ty, false, st) : launch_march_k<5, 2, T>(M, tx, ty, iso, st); break;

@@ -39,4 +39,4 @@ def main(mode="all", reps=2):
 
 
 if __name__ == "__main__":
-    main(*(sys.argv[1:2] or ["all"]))
+    main(sys.argv[1] if len(sys.argv) > 1 else "all", int(sys.argv[2]) if len(sys.argv) > 2 else 2)
