@@ -593,7 +593,7 @@ def bench_config4(args, ctx, V, synth, torch, stream, local, hbm):
     torch.cuda.empty_cache()
     # ADMM-TV: construction timed separately (setup: Lambda, tables, init)
     iters = 20
-    tcfg = V.TvAdmmConfig(lambda_=cfg.tv_lambda, mu=cfg.tv_mu, max_iters=iters + 4, rel_tol=0.0,
+    tcfg = V.TvAdmmConfig(lambda_=cfg.tv_lambda, mu=cfg.tv_mu, max_iters=iters + 6, rel_tol=0.0,
                           tau=1e-3 * cfg.tv_mu, init=V.INIT_UPSAMPLED)
     t0 = time.perf_counter()
     tv = V.TvDevice(ctx, spec, _Dev(y), _Dev(psf), tcfg)
@@ -602,6 +602,13 @@ def bench_config4(args, ctx, V, synth, torch, stream, local, hbm):
     tv.iterate(2)
     k = 4
     ms_it = ev_time(lambda: tv.iterate(k), 1) / k
+    # per-stage table from a second, profiled pass (as the config-2/3 blocks)
+    V.profile_enable(ctx, True)
+    tv.iterate(2)
+    ctx.synchronize()
+    st4 = V.profile_read(ctx)
+    V.profile_enable(ctx, False)
+    out["tv_stages_us"] = {name: tot / max(cnt, 1) * 1e3 for name, (tot, cnt) in st4.items()}
     rep = tv.report()
     tv.close()
     out["tv_ms_per_iter"] = ms_it

@@ -165,6 +165,11 @@ __device__ __forceinline__ double lds_d(unsigned a) {
     return v;
 }
 
+#ifndef VSR_RCP_FREE
+#define VSR_RCP_FREE 4
+#endif
+constexpr int kRcpFree = VSR_RCP_FREE;
+
 struct SwArgs {
     FoldGeom G;
     const double2* Yl;
@@ -355,66 +360,72 @@ __global__ void __launch_bounds__(SwShape<L, A, RM, C>::THREADS, 1) tv_sandwich_
             // One LR position group rr of this thread, in arithmetic type T.
             const double2 bc_ = cmul(mt->b, mt->c);
             const double base_g = mt->nc + mt->ns;
-            auto fold_rr = [&](auto zero, const int rr) {
-                using T = decltype(zero);
-                using CT = std::conditional_t<std::is_same<T, double>::value, double2, float2>;
+            // DR = 4: branch-free reciprocals interleave (115 vs 121 us at config 2).
+            // DR = 2 (8 position groups per thread): the freer schedule spills
+            // 200-750 B at the 128-register cap, so the branch stays as a fence.
+            auto rcp_fold = [](double x) { return DR >= kRcpFree ? rcp_pos_normal(x) : rcp_pos(x); };
+            // With t_b = Gamma_b Lambda_b and Gw = sum_b Gamma_b |Lambda_b|^2 (the gw
+            // table), S = Gw y + mu' sum_b t_b theta_b, and
+            //   x̂_b = (conj(t_b) (y - w) + Gamma_b mu' theta_b) / mu,
+            //   y - w = (mu d y - mu' sum_b t_b theta_b) / (Gw + mu d):
+            // the same map as g_b - Gamma_b conj(Lambda_b) w with 13 fewer fp64
+            // operations per element, fewer values live across the alias sum, and
+            // y - w formed without cancelling two O(Gw y) terms.
+            const double gcs = cAs * args.inv_scale;
+            auto fold_rr = [&](const int rr) {
                 const double2 yraw = lds_d2(yrow_a + 16u * (t + P * rr));
                 const double gwv = lds_d(gwrow_a + 8u * (t + P * rr));
-                const CT yv = from_d2<CT>(cscale(yraw, args.invsqrtd));
-                // g_b kept in T between the two loops (it is up to 1/tau large);
-                // Gamma_b conj(Lambda_b) formed in the first loop (fewer live registers)
-                CT gl[DR], gv[DR];
-                T Sx = 0, Sy = 0;
+                const double2 yv = cscale(yraw, args.invsqrtd);
+                // (early: with the branching reciprocal it would otherwise sit behind the shuffles)
+                const double us = rcp_fold(gwv + args.shift) * args.inv_scale;  // >= shift >= DBL_MIN (host check)
+                double2 tb_[DR], pv[DR];  // t_b and Gamma_b mu' theta_b / mu (v[r] itself dies in the first loop)
+                double Sx = 0, Sy = 0;
 #pragma unroll
                 for (int br = 0; br < DR; ++br) {
                     const int r = rr + RD * br;
                     const int q = t + P * r;
-                    const CT Lr = from_d2<CT>(cmul(sa_t[q], bc_));
-                    T Gg;
-                    if constexpr (std::is_same<T, double>::value)
-                        Gg = rcp_pos((nr_t[q] + base_g) + tb.tau);
-                    else
-                        Gg = __frcp_rn((float)((nr_t[q] + base_g) + tb.tau));
-                    const CT vr = from_d2<CT>(to_d2(v[r]));
-                    gv[br] = cscale(cadd(cmulc(Lr, yv), cscale(vr, (T)cAs)), Gg);
-                    gl[br] = cmake<CT>(Gg * Lr.x, -(Gg * Lr.y));
-                    const CT pr = cmul(Lr, gv[br]);
-                    Sx += pr.x;
-                    Sy += pr.y;
+                    const double2 Lr = cmul(sa_t[q], bc_);
+                    const double gg = rcp_fold((nr_t[q] + base_g) + tb.tau);  // >= tau >= DBL_MIN (host check)
+                    tb_[br] = cscale(Lr, gg);
+                    const double2 vr = to_d2(v[r]);
+                    pv[br] = cscale(vr, gg * gcs);
+                    Sx = fma(tb_[br].x, vr.x, Sx);
+                    Sx = fma(-tb_[br].y, vr.y, Sx);
+                    Sy = fma(tb_[br].x, vr.y, Sy);
+                    Sy = fma(tb_[br].y, vr.x, Sy);
                 }
 #pragma unroll
                 for (int o = 1; o < A; o <<= 1) {
                     Sx += __shfl_xor_sync(0xffffffffu, Sx, o);
                     Sy += __shfl_xor_sync(0xffffffffu, Sy, o);
                 }
-                T iden;
-                if constexpr (std::is_same<T, double>::value)
-                    iden = rcp_pos(gwv + args.shift);
-                else
-                    iden = __frcp_rn((float)(gwv + args.shift));
-                const CT w = cmake<CT>(Sx * iden, Sy * iden);
+                // (y - w) / mu
+                const double2 u = cmake<double2>(fma(args.shift, yv.x, -cAs * Sx) * us, fma(args.shift, yv.y, -cAs * Sy) * us);
 #pragma unroll
                 for (int br = 0; br < DR; ++br) {
                     const int r = rr + RD * br;
-                    const CT c = cmul(gl[br], w);
-                    v[r] = from_d2<C>(to_d2(cscale(csub(gv[br], c), (T)args.inv_scale)));
+                    double ox = fma(tb_[br].x, u.x, pv[br].x), oy = fma(tb_[br].x, u.y, pv[br].y);
+                    ox = fma(tb_[br].y, u.y, ox);
+                    oy = fma(-tb_[br].y, u.x, oy);
+                    v[r] = from_d2<C>(cmake<double2>(ox, oy));
                 }
                 if constexpr (FIT) {
                     if (ln == 0) {
-                        const double ax = ((double)Sx - gwv * (double)w.x) * args.inv_scale,
-                                     ay = ((double)Sy - gwv * (double)w.y) * args.inv_scale;
+                        // A x̂ folded: (S - Gw w) / mu with S = Gw y + mu' sum, w = S / (Gw + mu d)
+                        const double Stx = fma(gwv, yv.x, cAs * Sx), Sty = fma(gwv, yv.y, cAs * Sy);
+                        const double ax = Stx * args.inv_scale - gwv * (Stx * us),
+                                     ay = Sty * args.inv_scale - gwv * (Sty * us);
                         const double rx = yraw.x - args.invsqrtd * ax, ry = yraw.y - args.invsqrtd * ay;
                         tfit += rx * rx + ry * ry;
                     }
                 }
             };
-            // fp32 mode too folds in fp64: the naive Woodbury form cancels
-            // g_b against Gamma_b conj(Lambda_b) w and so amplifies rounding by
-            // ~Gamma_b |Lambda_b|^2 / (mu d) -- 1/tau at DC, hundreds at the
-            // lowest non-zero frequencies -- while the map itself is well
-            // conditioned in its inputs (fp32 spectra are fine)
+            // fp32 mode too folds in fp64: the Woodbury form cancels at low
+            // frequencies and amplifies rounding by ~Gamma_b |Lambda_b|^2 / (mu d)
+            // -- 1/tau at DC, hundreds at the lowest non-zero frequencies -- while
+            // the map itself is well conditioned in its inputs (fp32 spectra are fine)
 #pragma unroll
-            for (int rr = 0; rr < RD; ++rr) fold_rr(0.0, rr);
+            for (int rr = 0; rr < RD; ++rr) fold_rr(rr);
             // this line's store rows, read before the inverse transform's barriers
             // (after them, the issue below re-arms buffer b's metadata)
             if (t == 0) stash[ln] = LineStore{mt->wr, mt->sec, mir ? (int)0x80000000 : 0, 0};
@@ -499,6 +510,9 @@ bool sandwich_pipe_t(const FoldGeom& G, const double2* Yl, const SepTables& sep,
     if (!sep.a || !tabs.gw || !tabs.half3 || tabs.fit_only || !tabs.tiles || tabs.ntiles <= 0 || !out || out == W)
         return false;
     if (tv_sandwich1_tile_g2(G) != 1) return false;
+    // the fold's reciprocals skip the subnormal-denominator branch: both
+    // denominators are bounded below by these two (Gamma's tau, mu d)
+    if (!(tabs.tau >= 2.2250738585072014e-308) || !(shift >= 2.2250738585072014e-308)) return false;
     const int A = G.dc * G.ds;
     SwArgs a{G, Yl, sep, W, out, tabs, cA, shift, inv_scale, 1.0 / std::sqrt((double)G.d), fwd_scale,
              nullptr, fit_partials};

@@ -168,5 +168,14 @@ __device__ __forceinline__ double rcp_pos(double x) {
     y = y * fma(-x, y, 2.0);
     return y;
 }
+// The same for x known to be normal (>= DBL_MIN, checked by the caller on the
+// host): no slow-path branch, so independent reciprocals interleave.
+__device__ __forceinline__ double rcp_pos_normal(double x) {
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    y = y * fma(-x, y, 2.0);
+    y = y * fma(-x, y, 2.0);
+    return y;
+}
 
 }  // namespace vsr
