@@ -173,6 +173,80 @@ __device__ __forceinline__ void stockham(C* v, int t, C* sm, const SIdx& sidx, T
     }
 }
 
+// The same transform with the exchanges split into a real and an imaginary
+// round through a buffer of REALS (half the shared memory of stockham(), four
+// barriers per exchange instead of two).  sidx(q) maps a line position to this
+// thread's line slot in smr.  Used by the wide-tile passes of long lines, where
+// the full complex exchange buffer would leave no room for the prefetch stage.
+template <int L, bool INV, class SIdx, int RMAX = 16, class Sync = CtaSync, class Tw = const double2*, class C>
+__device__ __forceinline__ void stockham_split(C* v, int t, typename CplxT<C>::real* smr, const SIdx& sidx, Tw tw,
+                                               const Sync& sync = Sync()) {
+    using Pl = Plan<L, RMAX>;
+    constexpr int R = Pl::R, P = Pl::P;
+    int Ns = 1;
+#pragma unroll
+    for (int stage = 0; stage < Pl::NSTAGE; ++stage) {
+        const bool last = stage == Pl::NSTAGE - 1;
+        const int RS = (stage < Pl::K) ? R : Pl::RL;
+        const int NB = R / RS;
+#pragma unroll
+        for (int vv = 0; vv < NB; ++vv) {
+            const int u = t + P * vv;
+            const int k = u & (Ns - 1);
+            if (stage > 0) {
+                const int tstride = L / (Ns * RS);
+#pragma unroll
+                for (int r = 1; r < R; ++r) {
+                    if (r < RS) {
+                        const C w = tw_at(tw, (r * k * tstride) & (L - 1));
+                        const C a = v[vv * RS + r];
+                        v[vv * RS + r] = INV ? cmulc(w, a) : cmul(w, a);
+                    }
+                }
+            }
+            if (RS == R)
+                dft_reg<R, INV>(v);
+            else if (RS == Pl::RL)
+                dft_reg<(Pl::RL > 1 ? Pl::RL : 1), INV>(v + vv * RS);
+        }
+        if (!last) {
+            const int RSn = (stage + 1 < Pl::K) ? R : Pl::RL;
+            const int NBn = R / RSn;
+#pragma unroll
+            for (int comp = 0; comp < 2; ++comp) {
+#pragma unroll
+                for (int vv = 0; vv < NB; ++vv) {
+                    const int u = t + P * vv;
+                    const int k = u & (Ns - 1);
+                    const int ob = (u - k) * RS + k;
+#pragma unroll
+                    for (int r = 0; r < R; ++r)
+                        if (r < RS) smr[sidx(ob + r * Ns)] = comp ? v[vv * RS + r].y : v[vv * RS + r].x;
+                }
+                sync();
+#pragma unroll
+                for (int vv = 0; vv < NBn; ++vv) {
+                    const int u = t + P * vv;
+#pragma unroll
+                    for (int r = 0; r < R; ++r)
+                        if (r < RSn) {
+                            // (the other component of this slot still holds its
+                            // pre-exchange value until its own round)
+                            if (comp)
+                                v[vv * RSn + r].y = smr[sidx(u + (L / RSn) * r)];
+                            else
+                                v[vv * RSn + r].x = smr[sidx(u + (L / RSn) * r)];
+                        }
+                }
+                sync();
+            }
+            Ns *= RS;
+        } else {
+            Ns *= RS;
+        }
+    }
+}
+
 // Output order -> natural order (v[k] = X[t + P k]); compile-time permutation.
 template <int L, int RMAX = 16, class C>
 __device__ __forceinline__ void to_natural(C* v) {

@@ -469,6 +469,8 @@ TV_CASES = [((8, 8, 8), (2, 2, 2), 6), ((16, 16, 16), (4, 4, 4), 10), ((32, 32, 
             ((64, 48, 32), (4, 4, 4), 5), ((64, 64, 16), (4, 4, 4), 5), ((128, 64, 32), (4, 4, 2), 4),
             # 1024-point axis-3 lines (paired real passes with 16-column tiles, as at config 4)
             ((64, 8, 1024), (2, 2, 2), 3),
+            # 1024-point axis-2 lines (the wide strided pass, as at config 4)
+            ((16, 1024, 8), (2, 2, 2), 3),
             # the pipelined half-spectrum sandwich (sandwich.cu) at the configs' row geometries:
             # (m, dc*ds, dr) = (256, 16, 4) config 2, (512, 8, 2) config 3, (1024, 4, 2) config 4
             ((256, 32, 32), (4, 4, 4), 3), ((512, 16, 32), (2, 2, 4), 3), ((1024, 16, 8), (2, 2, 2), 3),
@@ -605,6 +607,9 @@ print("ok", op.path())
     ({"VSR_MARCH_ISO": "0"}, (64, 64, 32), (2, 2, 2)),
     ({"VSR_NO_PIPE": "1"}, (256, 32, 32), (4, 4, 4)),
     ({"VSR_NO_PIPE": "1"}, (512, 16, 32), (2, 2, 4)),
+    # 1024-point axis-2 / axis-3 lines on the narrow one-tile-per-CTA passes (default: the wide persistent ones)
+    ({"VSR_NO_WIDE": "1"}, (64, 8, 1024), (2, 2, 2)),
+    ({"VSR_NO_WIDE": "1"}, (16, 1024, 8), (2, 2, 2)),
 ])
 def test_env_variants(env, dims, rates):
     import os
