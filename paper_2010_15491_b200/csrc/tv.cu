@@ -306,8 +306,9 @@ constexpr int FXP = FXH * (FXW / 2);        // 180 x pairs per plane
 constexpr int FDP = FDH * (FDW / 2);        // 153 dual pairs per component
 constexpr int FXS = FXH * FXW, FDS = 3 * FDH * FDW;
 
+constexpr int FRS = TY * (TX + 1) + (TY + 1) * TX;  // one rho_x + rho_y exchange set
 __host__ __device__ constexpr size_t fast_smem_doubles() {
-    return (size_t)3 * FXS + 2 * FDS + TY * (TX + 1) + (TY + 1) * TX;
+    return (size_t)3 * FXS + 2 * FDS + 2 * FRS;  // two exchange sets, alternating by step
 }
 
 
@@ -325,8 +326,7 @@ __global__ void __launch_bounds__(STH)
     using S2 = std::conditional_t<std::is_same<S, double>::value, double2, float2>;
     extern __shared__ double sm_raw[];
     S* sm = reinterpret_cast<S*>(sm_raw);
-    S* rx = sm + 3 * FXS + 2 * FDS;  // [TY][TX+1]
-    S* ry = rx + TY * (TX + 1);       // [TY+1][TX]
+    S* const rxy = sm + 3 * FXS + 2 * FDS;  // two sets of rx [TY][TX+1], ry [TY+1][TX]
     __shared__ double red[32 * 4];
 
     const int tid = threadIdx.x;
@@ -432,8 +432,15 @@ __global__ void __launch_bounds__(STH)
     // of 2), so every slot is a compile-time offset of the shared-memory base.
     // steady steps (k0 <= k, k + 4 <= k1: planes k-1 .. k+3 inside [0, s), no
     // warm-up, every look-ahead load due) drop the per-plane bounds and wrap tests
-    auto step = [&](int k, auto x0, auto x1, auto x2, auto d0, auto d1, auto steady) {
+    // ONE barrier per step.  Plane k + 2 (x) / k + 1 (dual) goes into the slot
+    // nobody reads during step k, and is first read in step k + 1, after this
+    // step's barrier; the slot's previous plane was last read before the previous
+    // step's barrier.  The rho exchange set alternates by step parity, so step
+    // k + 1's writes cannot overtake step k's reads after the barrier.
+    auto step = [&](int k, auto x0, auto x1, auto x2, auto d0, auto d1, auto par, auto steady) {
         constexpr bool ST = decltype(steady)::value;
+        S* const rx = rxy + decltype(par)::value * FRS;
+        S* const ry = rx + TY * (TX + 1);
         S* const XS0 = sm + decltype(x0)::value * FXS;
         S* const XS1 = sm + decltype(x1)::value * FXS;
         S* const XS2 = sm + decltype(x2)::value * FXS;
@@ -458,7 +465,6 @@ __global__ void __launch_bounds__(STH)
             for (int q = 0; q < 2; ++q)
                 if (da[q]) rdv[q] = ld_pair(dnext[q] + zd);
         }
-        __syncthreads();
         const bool warm = !ST && k < k0;
         const S* X0 = XS0;
         const S* X1 = XS1;
@@ -552,19 +558,20 @@ __global__ void __launch_bounds__(STH)
     // (fp32 only: at fp64 the second step body costs spills at the 64-register
     // allocation, 229 vs 219 us; fp32 160 -> 154 us)
     constexpr bool kSteady = std::is_same<S, float>::value;
-    auto any_step = [&](int k, auto x0, auto x1, auto x2, auto d0, auto d1) {
+    auto any_step = [&](int k, auto x0, auto x1, auto x2, auto d0, auto d1, auto par) {
         if (kSteady && k >= k0 && k + 4 <= k1)
-            step(k, x0, x1, x2, d0, d1, std::true_type{});
+            step(k, x0, x1, x2, d0, d1, par, std::true_type{});
         else if (k < k1)
-            step(k, x0, x1, x2, d0, d1, std::false_type{});
+            step(k, x0, x1, x2, d0, d1, par, std::false_type{});
     };
+    __syncthreads();  // the prologue's planes
     for (int k = k0 - 1; k < k1; k += 6) {
-        any_step(k, I0{}, I1{}, I2{}, I0{}, I1{});
-        any_step(k + 1, I1{}, I2{}, I0{}, I1{}, I0{});
-        any_step(k + 2, I2{}, I0{}, I1{}, I0{}, I1{});
-        any_step(k + 3, I0{}, I1{}, I2{}, I1{}, I0{});
-        any_step(k + 4, I1{}, I2{}, I0{}, I0{}, I1{});
-        any_step(k + 5, I2{}, I0{}, I1{}, I1{}, I0{});
+        any_step(k, I0{}, I1{}, I2{}, I0{}, I1{}, I0{});
+        any_step(k + 1, I1{}, I2{}, I0{}, I1{}, I0{}, I1{});
+        any_step(k + 2, I2{}, I0{}, I1{}, I0{}, I1{}, I0{});
+        any_step(k + 3, I0{}, I1{}, I2{}, I1{}, I0{}, I1{});
+        any_step(k + 4, I1{}, I2{}, I0{}, I0{}, I1{}, I0{});
+        any_step(k + 5, I2{}, I0{}, I1{}, I1{}, I0{}, I1{});
     }
 
     double v[4] = {acc_res, acc_tv, acc_dx, acc_xp};
