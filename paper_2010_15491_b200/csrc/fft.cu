@@ -186,18 +186,24 @@ __global__ void __launch_bounds__(RPairShape<L>::THREADS)
     C v[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) v[r] = active ? __ldg(src + S2 * (t + P * r)) : cmake<C>((RT)0, (RT)0);
-    fftc::stockham<L, false>(v, t, sm, sidx, tw);
-    __syncthreads();
+    fftc::stockham<L, false>(v, t, sm, sidx, tw);  // (its last exchange ends with a barrier)
+    // Hermitian split: position k <= L/2 needs Z[k], which this thread holds,
+    // and Z[L - k], a position above L/2 (or k itself at k = 0, L/2): only the
+    // upper half goes through shared memory
 #pragma unroll
-    for (int j = 0; j < R; ++j) sm[sidx(fftc::Plan<L>::out_q(t, j))] = v[j];
+    for (int j = 0; j < R; ++j) {
+        const int q = fftc::Plan<L>::out_q(t, j);
+        if (q > L / 2) sm[sidx(q)] = v[j];
+    }
     __syncthreads();
     C* dst = out + c + S * (long long)(L / 2 + 1) * o;
     const RT half = (RT)0.5;
 #pragma unroll
     for (int j = 0; j < R; ++j) {
-        const int k = t + P * j;
+        const int k = fftc::Plan<L>::out_q(t, j);
         if (k > L / 2 || !active) continue;
-        const C a = sm[sidx(k)], b = sm[sidx((L - k) & (L - 1))];
+        const C a = v[j];
+        const C b = (k == 0 || k == L / 2) ? a : sm[sidx(L - k)];
         const C xa = cmake<C>(half * (a.x + b.x), half * (a.y - b.y));
         const C xb = cmake<C>(half * (a.y + b.y), -half * (a.x - b.x));
         // slab-sharded: plane k goes straight to its owner's spectral buffer
@@ -396,34 +402,38 @@ __global__ void __launch_bounds__(WideShape<L>::THREADS, 1)
             for (int j = 0; j < R; ++j) dst[S * (long long)fftc::Plan<L>::out_q(t, j)] = cscale(v[j], scale);
         } else {
             // Hermitian split X_c[k] = (Z[k] + conj Z[L-k]) / 2, X_{c+1}[k] = (Z[k] - conj Z[L-k]) / 2i,
-            // k <= L/2, through the real exchange buffer: real parts, then imaginary parts
-            constexpr int NK = R / 2 + 1;
-            double sx[NK], dx[NK];
+            // k <= L/2: Z[k] is in this thread's registers, Z[L-k] (a position above
+            // L/2, or k itself at k = 0, L/2) comes through the real exchange buffer,
+            // real parts first, then imaginary parts
+            double bx[R];
 #pragma unroll
-            for (int j = 0; j < R; ++j) xch[sidx(fftc::Plan<L>::out_q(t, j))] = v[j].x;
-            __syncthreads();
-#pragma unroll
-            for (int j = 0; j < NK; ++j) {
-                const int k = t + P * j;
-                if (k <= L / 2) {
-                    const double a = xch[sidx(k)], b = xch[sidx((L - k) & (L - 1))];
-                    sx[j] = a + b;
-                    dx[j] = a - b;
-                }
+            for (int j = 0; j < R; ++j) {
+                const int q = fftc::Plan<L>::out_q(t, j);
+                if (q > L / 2) xch[sidx(q)] = v[j].x;
             }
             __syncthreads();
 #pragma unroll
-            for (int j = 0; j < R; ++j) xch[sidx(fftc::Plan<L>::out_q(t, j))] = v[j].y;
+            for (int j = 0; j < R; ++j) {
+                const int k = fftc::Plan<L>::out_q(t, j);
+                if (k <= L / 2) bx[j] = (k == 0 || k == L / 2) ? v[j].x : xch[sidx(L - k)];
+            }
+            __syncthreads();
+#pragma unroll
+            for (int j = 0; j < R; ++j) {
+                const int q = fftc::Plan<L>::out_q(t, j);
+                if (q > L / 2) xch[sidx(q)] = v[j].y;
+            }
             __syncthreads();
             double2* dst = static_cast<double2*>(out_) + 2 * (c0 + lt) + S * (long long)(L / 2 + 1) * o;
 #pragma unroll
-            for (int j = 0; j < NK; ++j) {
-                const int k = t + P * j;
+            for (int j = 0; j < R; ++j) {
+                const int k = fftc::Plan<L>::out_q(t, j);
                 if (k <= L / 2) {
-                    const double a = xch[sidx(k)], b = xch[sidx((L - k) & (L - 1))];
+                    const double2 a = v[j];
+                    const double by = (k == 0 || k == L / 2) ? a.y : xch[sidx(L - k)];
                     double2* d = dst + S * (long long)k;
-                    d[0] = make_double2(0.5 * sx[j], 0.5 * (a - b));
-                    d[1] = make_double2(0.5 * (a + b), -0.5 * dx[j]);
+                    d[0] = make_double2(0.5 * (a.x + bx[j]), 0.5 * (a.y - by));
+                    d[1] = make_double2(0.5 * (a.y + by), -0.5 * (a.x - bx[j]));
                 }
             }
             __syncthreads();  // the buffer is read out before the next tile's first exchange
