@@ -234,8 +234,8 @@ __global__ void __launch_bounds__(RPairShape<L>::THREADS)
     auto sidx = [&](int q) { return g * Sh::GREG + q * TP + lp; };
     const C* src = in + c + S * (long long)(L / 2 + 1) * o;
     // each half-spectrum plane q <= L/2 is loaded ONCE (by the thread holding
-    // position q) and staged as [q][A | B][pair]; positions q > L/2 read the
-    // conjugate mirror plane L - q back from shared memory
+    // position q), which also stages the combined value its conjugate mirror
+    // position L - q needs; positions q > L/2 read that back from shared memory
     // (fp64; the fp32 mode keeps the direct mirror loads, measured faster there)
     C* stg = sm + g * Sh::GREG;
     C v[R];
@@ -275,19 +275,15 @@ __global__ void __launch_bounds__(RPairShape<L>::THREADS)
     for (int r = 0; r <= RH; ++r) {
         if (r == RH && !mid) break;
         const int q = t + P * r;
-        stg[q * 2 * TP + lp] = A[r];
-        stg[q * 2 * TP + TP + lp] = B[r];
+        // what the mirror position L - q needs is conj(A) + i conj(B): one value per plane
+        stg[q * TP + lp] = cmake<C>(A[r].x + B[r].y, B[r].x - A[r].y);
         v[r] = cmake<C>(A[r].x - B[r].y, A[r].y + B[r].x);  // A + i B
     }
     __syncthreads();
 #pragma unroll
     for (int r = RH; r < R; ++r) {
         const int q = t + P * r;
-        if (q > L / 2) {
-            C A = stg[(L - q) * 2 * TP + lp], B = stg[(L - q) * 2 * TP + TP + lp];
-            A.y = -A.y, B.y = -B.y;
-            v[r] = cmake<C>(A.x - B.y, A.y + B.x);
-        }
+        if (q > L / 2) v[r] = stg[(L - q) * TP + lp];
     }
     __syncthreads();  // the staging area becomes the exchange buffer
     }
