@@ -50,10 +50,10 @@ __global__ void __launch_bounds__(RowShape<M>::THREADS)
     for (int r = 0; r < R; ++r) v[r] = active ? __ldg(z + t + P * r) : make_double2(0.0, 0.0);
     double2 wl[R];  // split twiddles, fetched under the transform
 #pragma unroll
-    for (int j = 0; j < R; ++j) wl[j] = __ldg(twL + t + P * j);
+    for (int j = 0; j < R; ++j) wl[j] = __ldg(twL + fftc::Plan<M, row_r<M>()>::out_q(t, j));
     auto sidx_r = [&](int q) { return ls * Sh::LPAD + q + q / R; };
     fftc::stockham<M, false, decltype(sidx_r), row_r<M>()>(v, t, smr, sidx_r, twM);
-    __syncthreads();  // exchange buffer -> split buffer
+    // (the transform's last exchange ends with a barrier: the buffer is free)
     double2* buf = smr + ls * Sh::XPITCH;
 #pragma unroll
     for (int j = 0; j < R; ++j) buf[fftc::Plan<M, row_r<M>()>::out_q(t, j)] = v[j];
@@ -62,14 +62,14 @@ __global__ void __launch_bounds__(RowShape<M>::THREADS)
     double2* out = X + row * Mp;
 #pragma unroll
     for (int j = 0; j < R; ++j) {
-        const int k = t + P * j;
-        const double2 a = buf[k], b = buf[(M - k) & (M - 1)];
+        const int k = fftc::Plan<M, row_r<M>()>::out_q(t, j);
+        const double2 a = v[j], b = buf[(M - k) & (M - 1)];  // Z[k] is still in registers
         const double2 e = make_double2(0.5 * (a.x + b.x), 0.5 * (a.y - b.y));
         const double2 o = make_double2(0.5 * (a.y + b.y), -0.5 * (a.x - b.x));  // -i (a - conj b) / 2
         out[k] = cadd(e, cmul(wl[j], o));
     }
     if (t == 0) {
-        const double2 a = buf[0];
+        const double2 a = v[0];  // position 0 (out_q(0, 0) = 0)
         out[M] = make_double2(a.x - a.y, 0.0);  // E[0] - O[0] with E[0] = Re a, O[0] = Im a
     }
     for (int k = M + 1 + t; k < Mp; k += P) out[k] = make_double2(0.0, 0.0);
