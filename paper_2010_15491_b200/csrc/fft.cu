@@ -355,7 +355,7 @@ __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
 template <int L, int MODE, bool INV>
 __global__ void __launch_bounds__(WideShape<L>::THREADS, 1)
     fft_wide_kernel(const void* in_, void* out_, long long S, long long tiles, const double2* __restrict__ tw,
-                    double scale) {
+                    double scale, RemotePlanes rp) {
     using Sh = WideShape<L>;
     constexpr int R = Sh::R, P = Sh::P, T = Sh::T, NT = Sh::THREADS;
     extern __shared__ double2 sm_raw[];
@@ -427,7 +427,9 @@ __global__ void __launch_bounds__(WideShape<L>::THREADS, 1)
                 if (k <= L / 2) {
                     const double2 a = v[j];
                     const double by = (k == 0 || k == L / 2) ? a.y : xch[sidx(L - k)];
-                    double2* d = dst + S * (long long)k;
+                    // slab-sharded: plane k goes straight to its owner's spectral buffer
+                    // (peer memory over NVLink), as in rpair_fwd_kernel
+                    double2* d = rp.peer ? rp.peer[rp.owner[k]] + rp.off[k] + 2 * (c0 + lt) : dst + S * (long long)k;
                     d[0] = make_double2(0.5 * (a.x + bx[j]), 0.5 * (a.y - by));
                     d[1] = make_double2(0.5 * (a.y + by), -0.5 * (a.x - bx[j]));
                 }
@@ -435,6 +437,7 @@ __global__ void __launch_bounds__(WideShape<L>::THREADS, 1)
             __syncthreads();  // the buffer is read out before the next tile's first exchange
         }
     }
+    if (MODE == WIDE_RFWD && rp.peer) __threadfence_system();
 }
 
 static int wide_sm_count() {
@@ -456,13 +459,13 @@ static bool wide_enabled() {
 
 template <int L, int MODE, bool INV>
 void launch_wide(const void* in, void* out, long long S, long long tiles, const double2* tw, double scale,
-                 cudaStream_t st) {
+                 cudaStream_t st, const RemotePlanes& rp = RemotePlanes{}) {
     using Sh = WideShape<L>;
     auto kern = fft_wide_kernel<L, MODE, INV>;
     const size_t smem = Sh::SMEM;
     VSR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const unsigned grid = (unsigned)std::min<long long>(tiles, wide_sm_count());
-    kern<<<grid, Sh::THREADS, smem, st>>>(in, out, S, tiles, tw, scale);
+    kern<<<grid, Sh::THREADS, smem, st>>>(in, out, S, tiles, tw, scale, rp);
     VSR_LAUNCH_CHECK();
 }
 
@@ -476,8 +479,8 @@ bool launch_rpair(bool fwd, const void* in, void* out, long long S, long long to
     const size_t smem = (size_t)Sh::SMEM * sizeof(C);
     if constexpr (L == 1024 && std::is_same<C, double2>::value) {
         static_assert(Sh::T == 2 * WideShape<L>::T && Sh::TG == 1, "wide tiles match the rpair tiles");
-        if (fwd && wide_enabled() && !rp.peer) {
-            launch_wide<L, WIDE_RFWD, false>(in, out, S, tiles, tw, 1.0, st);
+        if (fwd && wide_enabled()) {
+            launch_wide<L, WIDE_RFWD, false>(in, out, S, tiles, tw, 1.0, st, rp);
             return true;
         }
     }

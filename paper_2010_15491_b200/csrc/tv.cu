@@ -354,6 +354,9 @@ __global__ void __launch_bounds__(STH)
             return n - 1;
         }
         if (jr >= n) {
+            // (no upper neighbour for the dual: rows past the slab are only reached
+            // when the slab is shorter than a tile, and never used; read row n - 1)
+            if (!hi) return n - 1;
             base = hi;
             return 0;
         }

@@ -178,7 +178,9 @@ def test_numpy_decomposition_two_gloo_processes(tmp_path, hr, rates):
 
 
 # ------------------------------------------------------------------ GPU: local comm (P virtual ranks)
-GPU_CASES = [((64, 32, 32), (2, 2, 2)), ((64, 64, 64), (4, 4, 4)), ((64, 32, 64), (2, 2, 4))]
+GPU_CASES = [((64, 32, 32), (2, 2, 2)), ((64, 64, 64), (4, 4, 4)), ((64, 32, 64), (2, 2, 4)),
+             # 1024-point axis-3 lines: the wide forward paired pass storing into the owners' buffers
+             ((64, 16, 1024), (2, 2, 2))]
 
 
 @pytest.mark.gpu
@@ -200,8 +202,12 @@ def test_slab_admm_tv_local_ranks(V, hr, rates, P):
     np.testing.assert_allclose(rep.primal_residual, wrep.primal_residual, rtol=1e-9)
     assert abs(rep.initial_objective - wrep.initial_objective) <= TOL * abs(wrep.initial_objective)
     # the per-voxel work is the single-GPU path's kernels on the same tiles: x is bit-identical
+    # (slabs shorter than the stencil's 8-row tile are covered by the oracle bound above only)
     one, _ = V.admm_tv(y, psf, spec, cfg)
-    assert x.tobytes() == one.tobytes()
+    if (hr[1] // P) % 8 == 0:
+        assert x.tobytes() == one.tobytes()
+    else:
+        assert rel_err(x, one) < 1e-13
 
 
 @pytest.mark.gpu
