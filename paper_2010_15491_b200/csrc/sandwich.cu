@@ -355,9 +355,9 @@ __global__ void __launch_bounds__(SwShape<L, A, RM, C>::THREADS, 1) tv_sandwich_
             gsync();  // rows read before the exchange overwrites the buffer; LR rows landed
             fftc::stockham<L, false, decltype(sidx), RM, GroupSync<GT>, TwT>(v, t, sm, sidx, twp, gsync);
             fftc::to_natural<L, RM>(v);
-            // fold: S = sum_b Lambda_b g_b, g_b = Gamma_b k_b; w = S / (Gw + mu d);
+            // fold (reference form): S = sum_b Lambda_b g_b, g_b = Gamma_b k_b; w = S / (Gw + mu d);
             // x̂_b = (g_b - Gamma_b conj(Lambda_b) w) / mu; data fit from S and w.
-            // One LR position group rr of this thread, in arithmetic type T.
+            // fold_rr below evaluates it for one LR position group rr of this thread, in fp64.
             const double2 bc_ = cmul(mt->b, mt->c);
             const double base_g = mt->nc + mt->ns;
             // DR = 4: branch-free reciprocals interleave (115 vs 121 us at config 2).
