@@ -83,9 +83,12 @@ struct SwShape {
     static constexpr int NBUF = sizeof(C) == 16 ? 3 : 4;
     static constexpr size_t BUF = (size_t)A * PITCH * sizeof(C);
     // the per-position tables a[f1], |e^{2 pi i f1/m} - 1|^2 stay in shared
-    // memory unless the three buffers leave no room (L = 1024: read from L1)
-    static constexpr bool TAB_SMEM = L <= 512;
-    static constexpr size_t TAB = TAB_SMEM ? (size_t)L * (sizeof(double2) + sizeof(double)) : 0;
+    // memory unless the three buffers leave no room
+    // (L = 1024: the fp32 mode's smaller buffers leave room for both tables; at fp64
+    // the 8 KB Gamma row table still fits beside the three buffers, a[f1] does not)
+    static constexpr bool TAB_SMEM = L <= 512 || sizeof(C) == 8;
+    static constexpr bool NR_SMEM = TAB_SMEM || (L == 1024 && sizeof(C) == 16);
+    static constexpr size_t TAB = (TAB_SMEM ? (size_t)L * sizeof(double2) : 0) + (NR_SMEM ? (size_t)L * sizeof(double) : 0);
     // per group: the tile's LR row of Y and of Gw (ml = L / dr entries, dr >= 2)
     static constexpr size_t ROWS = (size_t)(L / 2) * (sizeof(double2) + sizeof(double));
     static constexpr size_t META = (size_t)NBUF * A * 80;  // LineMeta per line of each buffer
@@ -229,7 +232,7 @@ __global__ void __launch_bounds__(SwShape<L, A, RM, C>::THREADS, 1) tv_sandwich_
     LineMeta* meta = reinterpret_cast<LineMeta*>(tail);
     tail += Sh::META;
     double2* sa_s = reinterpret_cast<double2*>(tail);
-    double* nr_s = reinterpret_cast<double*>(sa_s + L);
+    double* nr_s = reinterpret_cast<double*>(sa_s + (Sh::TAB_SMEM ? L : 0));
     tail += Sh::TAB;
     C* tw_s = reinterpret_cast<C*>(tail);
     tail += Sh::TWB;
@@ -241,7 +244,7 @@ __global__ void __launch_bounds__(SwShape<L, A, RM, C>::THREADS, 1) tv_sandwich_
     const unsigned yrow_a = smem_u32(tail) + (threadIdx.x / Sh::GT) * (unsigned)Sh::ROWS;
     const unsigned gwrow_a = yrow_a + ML * (unsigned)sizeof(double2);
     const double2* __restrict__ sa_t = Sh::TAB_SMEM ? sa_s : args.sep.a;
-    const double* __restrict__ nr_t = Sh::TAB_SMEM ? nr_s : tb.nr;
+    const double* __restrict__ nr_t = Sh::NR_SMEM ? nr_s : tb.nr;
 
     const int tid = threadIdx.x;
     const int g = tid / GT, gt = tid % GT;
@@ -297,10 +300,9 @@ __global__ void __launch_bounds__(SwShape<L, A, RM, C>::THREADS, 1) tv_sandwich_
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if constexpr (Sh::TAB_SMEM)
-        for (int i = tid; i < L; i += Sh::THREADS) {
-            sa_s[i] = __ldg(args.sep.a + i);
-            nr_s[i] = __ldg(tb.nr + i);
-        }
+        for (int i = tid; i < L; i += Sh::THREADS) sa_s[i] = __ldg(args.sep.a + i);
+    if constexpr (Sh::NR_SMEM)
+        for (int i = tid; i < L; i += Sh::THREADS) nr_s[i] = __ldg(tb.nr + i);
     if constexpr (Sh::TW_SMEM)
         for (int i = tid; i < L; i += Sh::THREADS) tw_s[i] = __ldg(static_cast<const C*>(args.tw) + i);
     using TwT = std::conditional_t<Sh::TW_SMEM, fftc::TwShared<C>, const C*>;
