@@ -335,7 +335,9 @@ struct WideShape {
     static constexpr int THREADS = T * P;
     static constexpr size_t XCH = (size_t)T * L * sizeof(double);
     static constexpr size_t STAGE = (size_t)THREADS * R * sizeof(double2);  // [R][THREADS]
-    static constexpr size_t SMEM = XCH + STAGE;
+    static constexpr size_t TWS = (size_t)L * sizeof(double2);  // the twiddle table, staged once per CTA
+    static constexpr size_t SMEM = XCH + STAGE + TWS;
+    static_assert(SMEM <= 232448, "shared memory budget");
     // exchange slot of line position q, column lt: rows of T reals; the row
     // index is swizzled by its bit 4 so the four t of a warp (rows 16 apart in
     // the first exchange) do not land on the same 16 banks
@@ -361,7 +363,11 @@ __global__ void __launch_bounds__(WideShape<L>::THREADS, 1)
     extern __shared__ double2 sm_raw[];
     double* xch = reinterpret_cast<double*>(sm_raw);
     double2* stage = reinterpret_cast<double2*>(xch + (size_t)T * L);
+    double2* tw_s = stage + (size_t)NT * R;
     const int tid = threadIdx.x, lt = tid % T, t = tid / T;
+    for (int i = tid; i < L; i += NT) tw_s[i] = __ldg(tw + i);
+    __syncthreads();
+    const fftc::TwShared<double2> twp{tw_s};
     const long long tpo = S / (MODE == WIDE_PASS ? T : 2 * T);
     auto sidx = [&](int q) { return Sh::xidx(q, lt); };
 
@@ -389,7 +395,7 @@ __global__ void __launch_bounds__(WideShape<L>::THREADS, 1)
         const long long next = tile + gridDim.x;
         if (next < tiles) prefetch(next);  // lands while this tile is transformed and stored
 
-        fftc::stockham_split<L, INV>(v, t, xch, sidx, tw);
+        fftc::stockham_split<L, INV, decltype(sidx), 16, fftc::CtaSync, fftc::TwShared<double2>>(v, t, xch, sidx, twp);
 
         const long long o = tile / tpo, c0 = (tile % tpo) * T;
         if constexpr (MODE == WIDE_PASS) {
